@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""Benchmark: SGD updates/sec of the B200 hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload netflix|ml1m|yahoo|hugewiki] [--k K] [--precision f32|f16]
+
+A step is one epoch of the hot path over the workload's rating matrix: every
+block of the division plan once, each block one launch of the sm_100a update
+kernel (HOGWILD mode) — the work one `hetmf.kernels.sgd_range` call per block
+does in the reference (StreamWorker / BatchEngine.compute, workers.py:222-302).
+
+Default (N=1): the Netflix-shaped configuration BASELINE.json's metric is
+quoted on (configs[1]): 480 000 x 17 700, 100 M training ratings (plus a 5 %
+held-out test set), k = 128, fp32, the 1-GPU batch-only uniform plan (1 x 2
+blocks, partition.py:89-107).  Inputs are larger than L2 (P 246 MB, triples
+1.2 GB), so no L2 flush is needed between steps.
+
+Printed (rank 0, one JSON line): value = whole-job updates/s from CUDA events
+over exactly K steps (barrier + synchronize both sides, max over ranks);
+roofline of the dominant kernel (algorithmic bytes 12 + 16k per update over
+its mean event-timed launch); e2e = the same metric through the drop-in
+host-buffer call (kernels.sgd_range on numpy arrays: H2D of triples and
+factors, launch, D2H of factors, per block); cpu_baseline = the CPU oracle
+(a C port of the reference's stream-only path) on a bounded sample, all host
+threads.  --impl reference prints the reference arm: that CPU path timed
+alone on the same workload shape.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (n_users, n_items, n_train, default k, description)
+    "ml1m": (6040, 3706, 1_000_000, 32, "MovieLens-1M-shaped 6040x3706, 1M ratings"),
+    "netflix": (480_000, 17_700, 100_000_000, 128, "Netflix-shaped 480000x17700, 100M ratings"),
+    "yahoo": (1_000_000, 625_000, 250_000_000, 128, "Yahoo!Music-R1-shaped 1Mx625K, 250M ratings"),
+    "hugewiki": (50_000_000, 40_000, 3_100_000_000, 128, "Hugewiki-shaped 50Mx40K, 3.1B ratings"),
+}
+TEST_FRACTION = 0.05
+LR, REG = 0.005, 0.05  # the paper's gamma / lambda
+SEED = 0
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+def bytes_per_update(k: int, precision: str) -> int:
+    s = 2 if precision == "f16" else 4
+    return 12 + 4 * k * s  # triple + read+write of p_u and q_v
+
+
+class ClockSampler:
+    """nvidia-smi style clock / throttle sampling during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thread = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+            return self
+        self._thread = threading.Thread(target=self._run, daemon=True)
+        self._thread.start()
+        return self
+
+    def _run(self):
+        nv = self._nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for n, bit in names.items():
+                    if mask & bit and n != "gpu_idle":
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thread:
+            self._thread.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_setup():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU arm (oracle port of the reference's stream-only path)
+# ---------------------------------------------------------------------------
+def cpu_sample_run(n_users, n_items, k, sample_nnz, threads, epochs, seed=SEED):
+    """Time the reference CPU algorithm (oracle C port, `threads` workers on
+    the uniform threads x (threads+1) grid) on a sample of the workload:
+    full-size P and Q (f64, the reference's layout), `sample_nnz` ratings drawn
+    with the same law.  Returns (updates/s, updates, seconds)."""
+    import oracle
+    from paper_2006_15980_b200.data import build_grid, RatingMatrix
+    rng = np.random.default_rng(seed)
+    users = rng.integers(0, n_users, sample_nnz).astype(np.int32)
+    items = rng.integers(0, n_items, sample_nnz).astype(np.int32)
+    vals = rng.uniform(0.0, 0.5, sample_nnz)
+    m = RatingMatrix(n_users, n_items, users, items, vals)
+    rows_cut = np.linspace(0, n_users, threads + 1).astype(np.int64)
+    cols_cut = np.linspace(0, n_items, threads + 2).astype(np.int64)
+    g = build_grid(m, rows_cut, cols_cut)
+    top = 1.0 / np.sqrt(k)
+    P = rng.uniform(0, top, size=(n_users, k))
+    Q = rng.uniform(0, top, size=(n_items, k))
+    oracle.lib()
+    t0 = time.perf_counter()
+    got, _ = oracle.stream_train(P, Q, g.users, g.items, g.ratings, g.block_ptr, threads,
+                                 threads + 1, LR, REG, REG, seed, epochs, threads)
+    dt = time.perf_counter() - t0
+    return got / dt, got, dt
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(args, world, rank):
+    n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
+    k = args.k or k0
+    if rank != 0:
+        return
+    threads = host_threads()
+    sample = int(min(n_train, 1_500_000 * threads))
+    times = []
+    for step in range(args.warmup + args.steps):
+        rate, got, dt = cpu_sample_run(n_users, n_items, k, sample, threads, 1, seed=step)
+        if step >= args.warmup:
+            times.append((got, dt))
+    ups = sum(g for g, _ in times) / sum(d for _, d in times)
+    ms = 1e3 * sum(d for _, d in times) / len(times)
+    line = {
+        "impl": "reference", "metric": "sgd_updates_per_sec", "value": ups, "unit": "updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference law, host)",
+        "config": {"workload": f"{desc}, k={k}; CPU sample of {sample} ratings per step "
+                               f"(full-size P/Q), stream-only uniform grid"},
+        "cpu_baseline": {"value": ups, "unit": "updates/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} ratings x 1 epoch per step, full {n_users}x"
+                                   f"{n_items} P/Q at k={k}, {threads} threads"},
+        "e2e": {"value": ups, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_2006_15980_b200 import _lib, kernels
+    from paper_2006_15980_b200.data import build_device_grid, split_device, synthetic_device
+    from paper_2006_15980_b200.sgd import init_device_model, rmse
+
+    _lib.load()
+    if args.variant is not None:
+        _lib.set_variant(args.variant)
+    dev = torch.device("cuda", local)
+    n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
+    k = args.k or k0
+    precision = args.precision
+    n_total = int(round(n_train / (1.0 - TEST_FRACTION)))
+    # every rank holds the same-shaped workload: a replica per GPU (weak scaling)
+    t0 = time.perf_counter()
+    trip = synthetic_device(n_users, n_items, n_total, rank=8, noise=0.1, seed=SEED + rank,
+                            device=dev)
+    train, test = split_device(trip, TEST_FRACTION)
+    nnz = train.nnz
+    # 1-GPU batch-only uniform plan: 1 row band x 2 column bands
+    row_cuts = np.array([0, n_users], dtype=np.int64)
+    col_cuts = np.array([0, (n_items + 1) // 2, n_items], dtype=np.int64)
+    grid = build_device_grid(train, row_cuts, col_cuts)
+    del trip
+    model = init_device_model(n_users, n_items, k, SEED, device=dev,
+                              dtype="float16" if precision == "f16" else "float32")
+    torch.cuda.synchronize(dev)
+    setup_s = time.perf_counter() - t0
+
+    stream = torch.cuda.current_stream(dev)
+    counts = np.zeros(grid.n_blocks, dtype=np.int64)
+    launch_events = []
+
+    def step(record):
+        for b in range(grid.n_blocks):
+            lo, hi = grid.block_range(b)
+            if hi <= lo:
+                continue
+            seed = kernels.mix64(kernels.mix64(SEED, b, int(counts[b])), 0)
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            kernels.launch_sgd_range(model.P, model.Q, grid.users, grid.items, grid.ratings, lo,
+                                     hi, LR, REG, REG, seed, 0, 0, "hogwild", stream.cuda_stream)
+            if record:
+                e1.record(stream)
+                launch_events.append((e0, e1, hi - lo))
+            counts[b] += 1
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    start_ev = torch.cuda.Event(enable_timing=True)
+    end_ev = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start_ev.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        end_ev.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    elapsed_ms = start_ev.elapsed_time(end_ev)
+    elapsed_ms = max_over_ranks(elapsed_ms, world)
+    updates = sum_over_ranks(float(nnz * args.steps), world)
+    value = updates / (elapsed_ms / 1e3)
+
+    # dominant kernel: the HOGWILD update launches
+    durs = [(a.elapsed_time(b), n) for a, b, n in launch_events]
+    mean_ms = sum(d for d, _ in durs) / len(durs)
+    mean_updates = sum(n for _, n in durs) / len(durs)
+    bpu = bytes_per_update(k, precision)
+    achieved = mean_updates * bpu / (mean_ms / 1e3) / 1e9
+    peak, peak_kind = measured_peak()
+    traffic = None
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        try:
+            tr = json.loads(prof.read_text()).get(f"{args.workload}_k{k}_{precision}")
+            if tr:
+                traffic = tr["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
+
+    # test RMSE after the epochs run (not timed)
+    test_rmse = rmse(test, model).value
+    epochs_run = args.warmup + args.steps
+
+    # e2e: the drop-in host-buffer call, per block, with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, grid, model, k, precision, dev, world)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        threads = host_threads()
+        sample = int(min(nnz, 1_000_000 * threads))
+        rate, got, dt = cpu_sample_run(n_users, n_items, k, sample, threads, 1)
+        cpu = {"value": rate, "unit": "updates/s", "cores": threads, "kind": "port",
+               "sample": f"{sample} ratings x 1 epoch, full {n_users}x{n_items} P/Q (f64) at "
+                         f"k={k}, stream-only uniform {threads}x{threads + 1} grid, "
+                         f"{dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "sgd_updates_per_sec", "value": value, "unit": "updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": precision,
+            "data": "synthetic (synthetic_ratings law, device generator)",
+            "config": {"workload": f"{desc}, k={k}, {precision} storage",
+                       "train_ratings": nnz, "test_ratings": test.nnz,
+                       "grid": "uniform 1x2 (1 batch worker per GPU)",
+                       "parallelism": f"replica x{world}" if world > 1 else "single GPU",
+                       "lr": LR, "reg": REG, "mode": "hogwild",
+                       "variant": args.variant,
+                       "l2": "inputs larger than L2 (P + triples >> 126 MB); no flush"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_kind": peak_kind, "bytes_per_update": bpu,
+                         "kernel": "sgd_hogwild_kernel", "mean_launch_ms": mean_ms,
+                         "updates_per_launch": mean_updates},
+            "rmse": {"epochs": epochs_run, "test": test_rmse},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": len(launch_events),
+            "clocks": clocks.summary(),
+            "setup_seconds": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, grid, model, k, precision, dev, world):
+    """Same metric through the reference-facing host-buffer call."""
+    import torch
+    from paper_2006_15980_b200 import kernels
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    h_users = pin(grid.users).numpy()
+    h_items = pin(grid.items).numpy()
+    h_vals = pin(grid.ratings).numpy()
+    h_P = pin(model.P).numpy()
+    h_Q = pin(model.Q).numpy()
+    steps = max(1, min(args.steps, 3))
+    h2d = d2h = 0
+    for b in range(grid.n_blocks):
+        lo, hi = grid.block_range(b)
+        lo_al = lo & ~3
+        h2d += (hi - lo_al) * 12 + h_P.nbytes + h_Q.nbytes
+        d2h += h_P.nbytes + h_Q.nbytes
+
+    def step():
+        for b in range(grid.n_blocks):
+            lo, hi = grid.block_range(b)
+            kernels.sgd_range(h_P, h_Q, h_users, h_items, h_vals, lo, hi, LR, REG, REG,
+                              kernels.mix64(SEED, b, 99), 0, 0, mode="hogwild", device=dev.index)
+
+    step()  # warm-up
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t0
+    dt = max_over_ranks(dt, world)
+    ups = sum_over_ranks(float(grid.nnz * steps), world) / dt
+    return {"value": ups, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "path": "kernels.sgd_range(numpy pinned host arrays) per block"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="netflix")
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--precision", choices=["f32", "f16"], default="f32")
+    ap.add_argument("--variant", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference_arm(args, world, rank)
+        return
+    world, rank, local = dist_setup()
+    run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

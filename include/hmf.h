@@ -1,0 +1,176 @@
+/*
+ * libhmf — C ABI of the B200-native SGD matrix-factorization hot path.
+ *
+ * Every entry point takes plain pointers and sizes (no torch types).  Device
+ * pointers must be CUDA device memory on the current device; `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  All kernels are asynchronous
+ * and stream-ordered; nothing here frees caller memory.
+ *
+ * Reference interface replaced by each entry point (paths relative to
+ * /root/reference/pkg/src/hetmf/):
+ *
+ *   hmf_sgd_range_{f32,f16,f64}   kernels.sgd_range            kernels.py:61-133
+ *   hmf_visit_order               sgd_range's visit order      kernels.py:77-119
+ *   hmf_mix64                     kernels.mix64                kernels.py:32-48
+ *   hmf_residual_sums_{f32,f16,f64}
+ *                                 sgd.rmse / sgd.regularized_loss
+ *                                                              sgd.py:134-188
+ *   hmf_memcpy_peer_async, hmf_ipc_*
+ *                                 BatchEngine.stage_in/stage_out item-band copies
+ *                                                              workers.py:186-218
+ *   hmf_bucket_triples            data.build_grid bucketing    data.py:238-280
+ *   hmf_synthetic_{count,cells,fill}
+ *                                 data.synthetic_ratings law   data.py:311-336
+ *
+ * Return convention: int64 entry points return a count >= 0 on success and a
+ * negative HMF_ERR_* code on failure; int entry points return HMF_OK (0) or a
+ * negative code.  hmf_last_error() gives the message of the calling thread's
+ * last failure.  The reference's sgd_range raises nothing and returns 0 for an
+ * empty range (kernels.py:74-76); so does hmf_sgd_range_*.
+ */
+#ifndef HMF_H_
+#define HMF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HMF_ABI_VERSION 1
+
+#define HMF_OK 0
+#define HMF_ERR_ARG (-1)
+#define HMF_ERR_CUDA (-2)
+#define HMF_ERR_UNSUPPORTED (-3)
+
+/* Visit-order modes of hmf_sgd_range_*. */
+#define HMF_MODE_HOGWILD 0 /* throughput: many warps, lock-free row updates      */
+#define HMF_MODE_ORDERED 1 /* reference visit order, one warp, fp32 arithmetic    */
+#define HMF_MODE_EXACT 2   /* reference visit order and f64 reference arithmetic */
+
+/* Reference visit-order window (kernels.py:24). */
+#define HMF_SHUFFLE_WINDOW 4096
+
+int hmf_abi_version(void);
+const char* hmf_last_error(void);
+
+/* Tuning knobs (benchmark sweeps).  HMF_TUNE_VARIANT selects the HOGWILD
+ * kernel's ILP / block-shape variant (0..7, -1 = per-shape default) for f32 and
+ * f16 storage. */
+#define HMF_TUNE_VARIANT 1
+int hmf_set_tuning(int32_t key, int32_t value);
+
+/*
+ * One SGD pass over triples [start, stop) — kernels.sgd_range (kernels.py:61-133).
+ *
+ * user_f: (rows of the band) x k row-major factors, indexed rows[i] - row_base.
+ * item_f: (cols of the band) x k row-major factors, indexed cols[i] - col_base.
+ * rows/cols/vals: triple arrays (device); only [start, stop) is touched.
+ * Updates user_f/item_f in place; returns stop - start (0 if empty) or < 0.
+ * seed: the per-block order seed (workers.block_order_seed, workers.py:77-83).
+ * In HOGWILD mode the seed permutes the chunk visit order; in ORDERED/EXACT
+ * modes it drives the reference windowed Fisher-Yates order exactly.
+ */
+int64_t hmf_sgd_range_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
+                          const int32_t* cols, const float* vals, int64_t start, int64_t stop,
+                          double lr, double reg_user, double reg_item, uint64_t seed,
+                          int64_t row_base, int64_t col_base, int32_t mode, void* stream);
+
+/* fp16 storage (IEEE binary16 bits), fp32 arithmetic, f32 ratings. */
+int64_t hmf_sgd_range_f16(uint16_t* user_f, uint16_t* item_f, int64_t k, const int32_t* rows,
+                          const int32_t* cols, const float* vals, int64_t start, int64_t stop,
+                          double lr, double reg_user, double reg_item, uint64_t seed,
+                          int64_t row_base, int64_t col_base, int32_t mode, void* stream);
+
+/* f64 storage and f64 ratings (the reference's own storage type). */
+int64_t hmf_sgd_range_f64(double* user_f, double* item_f, int64_t k, const int32_t* rows,
+                          const int32_t* cols, const double* vals, int64_t start, int64_t stop,
+                          double lr, double reg_user, double reg_item, uint64_t seed,
+                          int64_t row_base, int64_t col_base, int32_t mode, void* stream);
+
+/*
+ * The reference visit order of a range of n triples under `seed`
+ * (kernels.py:77-119): perm[t] = offset (relative to start) of the t-th
+ * triple updated.  perm: device int32[n], n < 2^31.
+ */
+int hmf_visit_order(int64_t n, uint64_t seed, int32_t* perm, void* stream);
+
+/* kernels.mix64 (kernels.py:32-48): splitmix64 fold, clipped to 63 bits. */
+uint64_t hmf_mix64(const uint64_t* parts, int32_t n_parts);
+
+/*
+ * Residual sums over n triples (sgd.py:134-188), accumulated in f64:
+ *   out[0] = sum (vals[i] - P[u]·Q[v])^2
+ *   out[1] = sum |P[u]|^2          (only when with_reg != 0, else 0)
+ *   out[2] = sum |Q[v]|^2          (only when with_reg != 0, else 0)
+ * u = rows[i] - row_base, v = cols[i] - col_base.  out: device double[3].
+ * rmse = sqrt(out[0] / n); regularized_loss = out[0] + reg_u*out[1] + reg_i*out[2].
+ * Deterministic: the reduction order depends only on n and the device.
+ */
+int hmf_residual_sums_f32(const float* user_f, const float* item_f, int64_t k,
+                          const int32_t* rows, const int32_t* cols, const float* vals, int64_t n,
+                          int64_t row_base, int64_t col_base, int32_t with_reg, double* out,
+                          void* stream);
+int hmf_residual_sums_f16(const uint16_t* user_f, const uint16_t* item_f, int64_t k,
+                          const int32_t* rows, const int32_t* cols, const float* vals, int64_t n,
+                          int64_t row_base, int64_t col_base, int32_t with_reg, double* out,
+                          void* stream);
+int hmf_residual_sums_f64(const double* user_f, const double* item_f, int64_t k,
+                          const int32_t* rows, const int32_t* cols, const double* vals, int64_t n,
+                          int64_t row_base, int64_t col_base, int32_t with_reg, double* out,
+                          void* stream);
+
+/*
+ * Block bucketing — data.build_grid (data.py:238-280).
+ * Block id of triple i = row_band(rows[i]) * n_col_bands + col_band(cols[i]),
+ * bands found by binary search in row_cuts / col_cuts (device int64 arrays of
+ * n_row_bands+1 / n_col_bands+1 ascending cuts).  Writes the triples
+ * block-major into out_* — a stable partition: input order is preserved inside
+ * each block, as the reference's argsort(kind="stable") does — and the CSR
+ * offsets into block_ptr (device int64[n_blocks + 1]).  Ratings are f32.
+ */
+int hmf_bucket_triples(const int32_t* rows, const int32_t* cols, const float* vals, int64_t n,
+                       const int64_t* row_cuts, int32_t n_row_bands, const int64_t* col_cuts,
+                       int32_t n_col_bands, int32_t* out_rows, int32_t* out_cols,
+                       float* out_vals, int64_t* block_ptr, void* stream);
+
+/*
+ * Synthetic instance generator with the synthetic_ratings law
+ * (data.py:311-336), for shapes the reference generator cannot reach.
+ * Cells: each of the n_rows x n_cols cells is selected independently with
+ * probability p (geometric skipping along each row, counter-based RNG keyed by
+ * seed), so the selected set is uniform given its size.
+ *   hmf_synthetic_count: row_ptr (device int64[n_rows + 1]) <- CSR offsets of
+ *     the selected cells; returns the total count (synchronises `stream`).
+ *   hmf_synthetic_cells: writes the selected (row, col) pairs, row-major.
+ * Values: vals[i] = sum_{r<rank} A[rows[i], r] * B[cols[i], r] + N(0, noise),
+ * A, B entries U[0, factor_scale/sqrt(rank)] from a hash of (seed, row/col, r),
+ * the noise from a hash of (seed, i).
+ */
+int64_t hmf_synthetic_count(int64_t n_rows, int64_t n_cols, double p, uint64_t seed,
+                            int64_t* row_ptr, void* stream);
+int hmf_synthetic_cells(int64_t n_rows, int64_t n_cols, double p, uint64_t seed,
+                        const int64_t* row_ptr, int32_t* out_rows, int32_t* out_cols,
+                        void* stream);
+int hmf_synthetic_fill(const int32_t* rows, const int32_t* cols, int64_t n, int32_t rank,
+                       double noise, double factor_scale, uint64_t seed, float* vals,
+                       void* stream);
+
+/* Device / peer utilities for the multi-GPU item-band hand-off. */
+int hmf_device_count(int32_t* n);
+int hmf_set_device(int32_t dev);
+int hmf_enable_peer_access(int32_t dev, int32_t peer);
+int hmf_memcpy_peer_async(void* dst, int32_t dst_dev, const void* src, int32_t src_dev,
+                          int64_t bytes, void* stream);
+int hmf_stream_synchronize(void* stream);
+/* CUDA IPC: 64-byte handle of a device allocation, opened in another process. */
+int hmf_ipc_get_handle(const void* dptr, uint8_t* handle64);
+int hmf_ipc_open_handle(const uint8_t* handle64, void** dptr);
+int hmf_ipc_close_handle(void* dptr);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HMF_H_ */

@@ -1,0 +1,491 @@
+"""Rating triples, block grids and synthetic instances (host and device).
+
+Host side keeps the reference's data contract (hetmf/data.py): RatingMatrix
+(int32 users/items, f64 ratings, id remap tables), shuffle_triples,
+BlockGrid/build_grid (block-major, CSR block_ptr, stable within a block) and
+synthetic_ratings with the reference's law *and* its numpy RNG call sequence,
+so small instances are bit-identical to the reference's.
+
+Device side is the B200 layout the hot path reads:
+  DeviceTriples  SoA int32 users, int32 items, f32 (or f64) ratings in HBM;
+  DeviceGrid     the same, bucketed block-major by hmf_bucket_triples (a
+                 stable partition, data.py:238-280), plus block_ptr;
+  synthetic_device  the synthetic_ratings law generated on the GPU for shapes
+                 the reference generator cannot reach (Netflix, Yahoo R1,
+                 Hugewiki), with hmf_synthetic_{count,cells,fill}.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+CACHE_MAGIC = b"HMF1"
+REGION_STREAM = 0
+REGION_BATCH = 1
+
+
+class DataError(ValueError):
+    """Malformed input or inconsistent rating data (data.py:23-24)."""
+
+
+class GridError(ValueError):
+    """Invalid block-grid geometry (data.py:27-28)."""
+
+
+@dataclass
+class RatingMatrix:
+    """Coordinate-form ratings with dense 0-based indices (data.py:31-73).
+
+    user_ids / item_ids map dense index -> original id; the inverse maps
+    user_index / item_index are built lazily (a dict over 50 M Hugewiki users
+    is not free).
+    """
+
+    n_users: int
+    n_items: int
+    users: np.ndarray
+    items: np.ndarray
+    ratings: np.ndarray
+    user_ids: np.ndarray = field(default=None)
+    item_ids: np.ndarray = field(default=None)
+    _user_index: dict = field(default=None, repr=False)
+    _item_index: dict = field(default=None, repr=False)
+
+    def __post_init__(self):
+        if self.user_ids is None:
+            self.user_ids = np.arange(self.n_users, dtype=np.int64)
+        if self.item_ids is None:
+            self.item_ids = np.arange(self.n_items, dtype=np.int64)
+
+    @property
+    def user_index(self) -> dict:
+        if self._user_index is None:
+            self._user_index = {int(x): i for i, x in enumerate(self.user_ids)}
+        return self._user_index
+
+    @property
+    def item_index(self) -> dict:
+        if self._item_index is None:
+            self._item_index = {int(x): i for i, x in enumerate(self.item_ids)}
+        return self._item_index
+
+    @property
+    def nnz(self) -> int:
+        return len(self.ratings)
+
+    def validate(self) -> None:
+        if not (len(self.users) == len(self.items) == len(self.ratings)):
+            raise DataError("triple arrays have mismatched lengths")
+        if self.nnz:
+            if self.users.min() < 0 or self.users.max() >= self.n_users:
+                raise DataError("user index out of range")
+            if self.items.min() < 0 or self.items.max() >= self.n_items:
+                raise DataError("item index out of range")
+        if not np.all(np.isfinite(self.ratings)):
+            raise DataError("non-finite rating value")
+
+
+def _with_order(matrix: RatingMatrix, order) -> RatingMatrix:
+    return RatingMatrix(matrix.n_users, matrix.n_items, matrix.users[order],
+                        matrix.items[order], matrix.ratings[order], matrix.user_ids,
+                        matrix.item_ids, matrix._user_index, matrix._item_index)
+
+
+def shuffle_triples(matrix: RatingMatrix, seed: int) -> RatingMatrix:
+    """Seed-deterministic permutation of the triples (data.py:153-166)."""
+    return _with_order(matrix, np.random.default_rng(seed).permutation(matrix.nnz))
+
+
+def align_ratings(testset: RatingMatrix, train: RatingMatrix):
+    """Map held-out triples into the training index space (data.py:135-150).
+
+    Vectorised: original ids are looked up by binary search in the training
+    id tables.  Returns (users, items, ratings, n_skipped)."""
+    def lookup(dense, ids_test, ids_train):
+        orig = np.asarray(ids_test, dtype=np.int64)[dense]
+        order = np.argsort(ids_train, kind="stable")
+        sorted_ids = np.asarray(ids_train, dtype=np.int64)[order]
+        pos = np.searchsorted(sorted_ids, orig)
+        pos_c = np.minimum(pos, max(len(sorted_ids) - 1, 0))
+        hit = (len(sorted_ids) > 0) & (sorted_ids[pos_c] == orig) if len(sorted_ids) else \
+            np.zeros(len(orig), dtype=bool)
+        return np.where(hit, order[pos_c], -1)
+
+    users = lookup(testset.users, testset.user_ids, train.user_ids)
+    items = lookup(testset.items, testset.item_ids, train.item_ids)
+    ok = (users >= 0) & (items >= 0)
+    return (users[ok].astype(np.int32), items[ok].astype(np.int32), testset.ratings[ok],
+            int((~ok).sum()))
+
+
+def load_ratings(path) -> RatingMatrix:
+    """Text "user item rating" file, keep-last dedup, dense remap (data.py:76-132)."""
+    try:
+        raw = np.loadtxt(path, comments="#", ndmin=2)
+    except (OSError, ValueError) as exc:
+        raise DataError(f"cannot read {path}: {exc}") from exc
+    if raw.size == 0:
+        raw = np.zeros((0, 3))
+    if raw.shape[1] != 3:
+        raise DataError(f"{path}: expected 'user item rating' lines")
+    u, v, r = raw[:, 0].astype(np.int64), raw[:, 1].astype(np.int64), raw[:, 2]
+    if not np.all(np.isfinite(r)):
+        raise DataError(f"{path}: non-finite rating")
+    if len(u):
+        _, last = np.unique(np.stack([u, v], 1)[::-1], axis=0, return_index=True)
+        keep = np.sort(len(u) - 1 - last)
+        u, v, r = u[keep], v[keep], r[keep]
+    user_ids, users = np.unique(u, return_inverse=True)
+    item_ids, items = np.unique(v, return_inverse=True)
+    return RatingMatrix(len(user_ids), len(item_ids), users.astype(np.int32),
+                        items.astype(np.int32), r, user_ids, item_ids)
+
+
+# ---------------------------------------------------------------------------
+# Host block grid (the reference contract)
+# ---------------------------------------------------------------------------
+@dataclass
+class BlockGrid:
+    """Block-major triples + CSR block_ptr (data.py:169-224)."""
+
+    n_rows: int
+    n_cols: int
+    row_cuts: np.ndarray
+    col_cuts: np.ndarray
+    region_of_row: np.ndarray
+    sub_row_parent: np.ndarray | None
+    users: np.ndarray
+    items: np.ndarray
+    ratings: np.ndarray
+    block_ptr: np.ndarray
+
+    @property
+    def n_row_bands(self) -> int:
+        return len(self.row_cuts) - 1
+
+    @property
+    def n_col_bands(self) -> int:
+        return len(self.col_cuts) - 1
+
+    @property
+    def n_blocks(self) -> int:
+        return self.n_row_bands * self.n_col_bands
+
+    @property
+    def nnz(self) -> int:
+        return len(self.ratings)
+
+    def block_id(self, row_band: int, col_band: int) -> int:
+        return row_band * self.n_col_bands + col_band
+
+    def block_range(self, block: int):
+        return int(self.block_ptr[block]), int(self.block_ptr[block + 1])
+
+    def block_nnz(self, block: int) -> int:
+        lo, hi = self.block_range(block)
+        return hi - lo
+
+    def block_counts(self) -> np.ndarray:
+        return np.diff(self.block_ptr)
+
+    def row_span(self, row_band: int):
+        return int(self.row_cuts[row_band]), int(self.row_cuts[row_band + 1])
+
+    def col_span(self, col_band: int):
+        return int(self.col_cuts[col_band]), int(self.col_cuts[col_band + 1])
+
+
+def check_cuts(cuts, extent, axis) -> np.ndarray:
+    cuts = np.asarray(cuts, dtype=np.int64)
+    if len(cuts) < 2:
+        raise GridError(f"{axis} cuts need at least two boundaries")
+    if cuts[0] != 0 or cuts[-1] != extent:
+        raise GridError(f"{axis} cuts must start at 0 and end at {extent}")
+    if np.any(np.diff(cuts) <= 0):
+        raise GridError(f"{axis} cuts must be strictly ascending")
+    return cuts
+
+
+def _grid_tags(n_row_bands, region_of_row, sub_row_parent):
+    if region_of_row is None:
+        region = np.full(n_row_bands, REGION_STREAM, dtype=np.int8)
+    else:
+        region = np.asarray(region_of_row, dtype=np.int8)
+        if len(region) != n_row_bands:
+            raise GridError("region_of_row length must match row band count")
+    if sub_row_parent is not None:
+        sub_row_parent = np.asarray(sub_row_parent, dtype=np.int64)
+        if len(sub_row_parent) != n_row_bands:
+            raise GridError("sub_row_parent length must match row band count")
+    return region, sub_row_parent
+
+
+def build_grid(matrix: RatingMatrix, row_cuts, col_cuts, region_of_row=None,
+               sub_row_parent=None) -> BlockGrid:
+    """Host bucketing with the reference semantics (data.py:238-280)."""
+    row_cuts = check_cuts(row_cuts, matrix.n_users, "row")
+    col_cuts = check_cuts(col_cuts, matrix.n_items, "column")
+    nrb, ncb = len(row_cuts) - 1, len(col_cuts) - 1
+    region, sub_row_parent = _grid_tags(nrb, region_of_row, sub_row_parent)
+    bid = ((np.searchsorted(row_cuts, matrix.users, side="right") - 1) * ncb
+           + np.searchsorted(col_cuts, matrix.items, side="right") - 1)
+    order = np.argsort(bid, kind="stable")
+    ptr = np.zeros(nrb * ncb + 1, dtype=np.int64)
+    np.cumsum(np.bincount(bid, minlength=nrb * ncb), out=ptr[1:])
+    return BlockGrid(matrix.n_users, matrix.n_items, row_cuts, col_cuts, region, sub_row_parent,
+                     np.ascontiguousarray(matrix.users[order]),
+                     np.ascontiguousarray(matrix.items[order]),
+                     np.ascontiguousarray(matrix.ratings[order]), ptr)
+
+
+def save_cache(path, matrix: RatingMatrix) -> None:
+    """HMF1 binary cache (data.py:283-294)."""
+    with open(path, "wb") as fh:
+        fh.write(CACHE_MAGIC)
+        fh.write(struct.pack("<QQQ", matrix.n_users, matrix.n_items, matrix.nnz))
+        fh.write(np.asarray(matrix.users).astype("<u8").tobytes())
+        fh.write(np.asarray(matrix.items).astype("<u8").tobytes())
+        fh.write(np.asarray(matrix.ratings).astype("<f8").tobytes())
+
+
+def load_cache(path) -> RatingMatrix:
+    """HMF1 reader (data.py:297-308)."""
+    with open(path, "rb") as fh:
+        magic = fh.read(4)
+        if magic != CACHE_MAGIC:
+            raise DataError(f"{path}: not a rating cache (bad magic {magic!r})")
+        n_users, n_items, nnz = struct.unpack("<QQQ", fh.read(24))
+        users = np.frombuffer(fh.read(8 * nnz), dtype="<u8").astype(np.int32)
+        items = np.frombuffer(fh.read(8 * nnz), dtype="<u8").astype(np.int32)
+        ratings = np.frombuffer(fh.read(8 * nnz), dtype="<f8").astype(np.float64)
+    m = RatingMatrix(int(n_users), int(n_items), users, items, ratings)
+    m.validate()
+    return m
+
+
+def synthetic_ratings(n_users=500, n_items=500, rank=8, density=0.05, noise=0.1, seed=0,
+                      factor_scale=1.0) -> RatingMatrix:
+    """Low-rank synthetic instance, the reference law and RNG stream (data.py:311-336).
+
+    Cells: unique uniform draws topped up until `target` distinct cells exist,
+    then a random `target`-subset in random order; values: sum over `rank` of
+    U[0, factor_scale/sqrt(rank)] factors plus N(0, noise).  Uses the same
+    numpy Generator calls in the same order as the reference, so the output is
+    bit-identical for the same arguments (pinned by tests/golden/data.npz).
+    Host-only; use synthetic_device() for Netflix-scale shapes.
+    """
+    gen = np.random.default_rng(seed)
+    cells_total = n_users * n_items
+    target = min(int(round(density * cells_total)), cells_total)
+    picked = np.empty(0, dtype=np.int64)
+    while picked.size < target:
+        extra = gen.integers(0, cells_total, size=int((target - picked.size) * 1.3) + 16)
+        picked = np.unique(np.concatenate([picked, extra]))
+    picked = gen.permutation(picked)[:target]
+    users = (picked // n_items).astype(np.int32)
+    items = (picked % n_items).astype(np.int32)
+    top = factor_scale / np.sqrt(rank)
+    a = gen.uniform(0.0, top, size=(n_users, rank))
+    b = gen.uniform(0.0, top, size=(n_items, rank))
+    values = np.einsum("ij,ij->i", a[users], b[items])
+    if noise > 0:
+        values = values + gen.normal(0.0, noise, size=target)
+    return RatingMatrix(n_users, n_items, users, items, values)
+
+
+# ---------------------------------------------------------------------------
+# Device-resident triples and grids
+# ---------------------------------------------------------------------------
+def _torch():
+    import torch
+    return torch
+
+
+def _stream(dev) -> int:
+    return int(_torch().cuda.current_stream(dev).cuda_stream)
+
+
+@dataclass
+class DeviceTriples:
+    """SoA triples in HBM: int32 users, int32 items, f32/f64 ratings."""
+
+    n_users: int
+    n_items: int
+    users: object
+    items: object
+    ratings: object
+
+    @property
+    def nnz(self) -> int:
+        return int(self.ratings.numel())
+
+    @property
+    def device(self):
+        return self.ratings.device
+
+    @classmethod
+    def from_host(cls, m: RatingMatrix, device, rating_dtype="float32") -> "DeviceTriples":
+        torch = _torch()
+        rdt = getattr(torch, rating_dtype)
+        return cls(m.n_users, m.n_items,
+                   torch.from_numpy(np.ascontiguousarray(m.users, dtype=np.int32)).to(device),
+                   torch.from_numpy(np.ascontiguousarray(m.items, dtype=np.int32)).to(device),
+                   torch.from_numpy(np.ascontiguousarray(m.ratings)).to(device=device, dtype=rdt))
+
+    def to_host(self) -> RatingMatrix:
+        return RatingMatrix(self.n_users, self.n_items, self.users.cpu().numpy(),
+                            self.items.cpu().numpy(),
+                            self.ratings.cpu().numpy().astype(np.float64))
+
+    def take(self, index) -> "DeviceTriples":
+        return DeviceTriples(self.n_users, self.n_items, self.users[index].contiguous(),
+                             self.items[index].contiguous(), self.ratings[index].contiguous())
+
+
+@dataclass
+class DeviceGrid:
+    """A BlockGrid whose triples live in HBM (block-major, 16-byte aligned).
+
+    block_ptr and the cuts stay on the host (the scheduler reads them); the
+    triple arrays are single contiguous device allocations, so a block is a
+    [block_ptr[b], block_ptr[b+1]) range of one launch.
+    """
+
+    n_rows: int
+    n_cols: int
+    row_cuts: np.ndarray
+    col_cuts: np.ndarray
+    region_of_row: np.ndarray
+    sub_row_parent: np.ndarray | None
+    users: object
+    items: object
+    ratings: object
+    block_ptr: np.ndarray
+
+    n_row_bands = BlockGrid.n_row_bands
+    n_col_bands = BlockGrid.n_col_bands
+    n_blocks = BlockGrid.n_blocks
+    block_id = BlockGrid.block_id
+    block_range = BlockGrid.block_range
+    block_nnz = BlockGrid.block_nnz
+    block_counts = BlockGrid.block_counts
+    row_span = BlockGrid.row_span
+    col_span = BlockGrid.col_span
+
+    @property
+    def nnz(self) -> int:
+        return int(self.ratings.numel())
+
+    @property
+    def device(self):
+        return self.ratings.device
+
+    @classmethod
+    def from_host(cls, grid: BlockGrid, device, rating_dtype="float32") -> "DeviceGrid":
+        torch = _torch()
+        rdt = getattr(torch, rating_dtype)
+        return cls(grid.n_rows, grid.n_cols, grid.row_cuts, grid.col_cuts, grid.region_of_row,
+                   grid.sub_row_parent,
+                   torch.from_numpy(np.ascontiguousarray(grid.users, dtype=np.int32)).to(device),
+                   torch.from_numpy(np.ascontiguousarray(grid.items, dtype=np.int32)).to(device),
+                   torch.from_numpy(np.ascontiguousarray(grid.ratings)).to(device=device, dtype=rdt),
+                   np.asarray(grid.block_ptr, dtype=np.int64))
+
+    def to_host(self) -> BlockGrid:
+        return BlockGrid(self.n_rows, self.n_cols, self.row_cuts, self.col_cuts,
+                         self.region_of_row, self.sub_row_parent, self.users.cpu().numpy(),
+                         self.items.cpu().numpy(), self.ratings.cpu().numpy().astype(np.float64),
+                         self.block_ptr.copy())
+
+
+def build_device_grid(triples: DeviceTriples, row_cuts, col_cuts, region_of_row=None,
+                      sub_row_parent=None) -> DeviceGrid:
+    """Bucket device triples block-major on the GPU (stable; data.py:238-280)."""
+    torch = _torch()
+    row_cuts = check_cuts(row_cuts, triples.n_users, "row")
+    col_cuts = check_cuts(col_cuts, triples.n_items, "column")
+    nrb, ncb = len(row_cuts) - 1, len(col_cuts) - 1
+    region, sub_row_parent = _grid_tags(nrb, region_of_row, sub_row_parent)
+    dev = triples.device
+    if triples.ratings.dtype != torch.float32:
+        raise TypeError("device bucketing takes f32 ratings")
+    n = triples.nnz
+    out_u = torch.empty(n, dtype=torch.int32, device=dev)
+    out_i = torch.empty(n, dtype=torch.int32, device=dev)
+    out_r = torch.empty(n, dtype=torch.float32, device=dev)
+    d_rc = torch.from_numpy(row_cuts).to(dev)
+    d_cc = torch.from_numpy(col_cuts).to(dev)
+    d_ptr = torch.empty(nrb * ncb + 1, dtype=torch.int64, device=dev)
+    _lib.check(_lib.load().hmf_bucket_triples(
+        triples.users.data_ptr(), triples.items.data_ptr(), triples.ratings.data_ptr(), n,
+        d_rc.data_ptr(), nrb, d_cc.data_ptr(), ncb, out_u.data_ptr(), out_i.data_ptr(),
+        out_r.data_ptr(), d_ptr.data_ptr(), _stream(dev)), "hmf_bucket_triples")
+    ptr = d_ptr.cpu().numpy()
+    return DeviceGrid(triples.n_users, triples.n_items, row_cuts, col_cuts, region,
+                      sub_row_parent, out_u, out_i, out_r, ptr)
+
+
+def synthetic_device(n_users: int, n_items: int, nnz: int, rank: int = 8, noise: float = 0.1,
+                     seed: int = 0, factor_scale: float = 1.0, device=None) -> DeviceTriples:
+    """The synthetic_ratings law at any scale, generated in HBM.
+
+    Exactly `nnz` distinct cells, uniform over the matrix, in random order;
+    values sum_r A[u,r] B[v,r] + N(0, noise) with A, B ~ U[0, fs/sqrt(rank)].
+    Cells are Bernoulli-selected with probability slightly above nnz/cells
+    (hmf_synthetic_count/cells), randomly permuted, and the first nnz kept —
+    the reference's permutation(chosen)[:target] — so the kept set is a
+    uniform nnz-subset.  Values come from hmf_synthetic_fill.
+    """
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    total = n_users * n_items
+    if nnz > total:
+        raise DataError("more ratings than cells")
+    lib = _lib.load()
+    s = _stream(dev)
+    p = min(1.0, nnz / total * (1.0 + 6.0 / np.sqrt(max(nnz, 1))) + 16.0 / total)
+    for attempt in range(8):
+        gseed = (seed * 0x9E3779B1 + attempt * 0x85EBCA77 + 1) & 0xFFFFFFFFFFFFFFFF
+        row_ptr = torch.empty(n_users + 1, dtype=torch.int64, device=dev)
+        got = _lib.check(lib.hmf_synthetic_count(n_users, n_items, p, gseed, row_ptr.data_ptr(), s),
+                         "hmf_synthetic_count")
+        if got >= nnz:
+            break
+        p = min(1.0, p * 1.01 + 1.0 / total)
+    else:
+        raise DataError("generator could not reach the requested count")
+    users = torch.empty(got, dtype=torch.int32, device=dev)
+    items = torch.empty(got, dtype=torch.int32, device=dev)
+    _lib.check(lib.hmf_synthetic_cells(n_users, n_items, p, gseed, row_ptr.data_ptr(),
+                                       users.data_ptr(), items.data_ptr(), s), "hmf_synthetic_cells")
+    del row_ptr
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(int(seed) & 0x7FFFFFFFFFFFFFFF)
+    keep = torch.randperm(got, device=dev, generator=gen)[:nnz]
+    users = users[keep].contiguous()
+    items = items[keep].contiguous()
+    del keep
+    vals = torch.empty(nnz, dtype=torch.float32, device=dev)
+    _lib.check(lib.hmf_synthetic_fill(users.data_ptr(), items.data_ptr(), nnz, rank, noise,
+                                      factor_scale, (seed + 0x5EED) & 0xFFFFFFFFFFFFFFFF,
+                                      vals.data_ptr(), s), "hmf_synthetic_fill")
+    return DeviceTriples(n_users, n_items, users, items, vals)
+
+
+def split_device(triples: DeviceTriples, test_fraction: float, seed: int = 1):
+    """Seeded train/test split of device triples (the test set is a random
+    `test_fraction` of them).  Triples from synthetic_device are already in
+    random order, so the split takes a prefix as the test set."""
+    n = triples.nnz
+    # a multiple of 4 keeps the train view 16-byte aligned for the bulk copies
+    n_test = int(round(n * test_fraction)) & ~3
+    test = DeviceTriples(triples.n_users, triples.n_items, triples.users[:n_test],
+                         triples.items[:n_test], triples.ratings[:n_test])
+    train = DeviceTriples(triples.n_users, triples.n_items, triples.users[n_test:],
+                          triples.items[n_test:], triples.ratings[n_test:])
+    return train, test

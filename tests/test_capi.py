@@ -1,0 +1,61 @@
+"""The C-ABI library loads without a GPU and exports every symbol the header
+declares; the ctypes binding covers the header one to one.  No compute calls."""
+
+import ctypes
+import re
+
+import pytest
+
+from conftest import ROOT
+
+
+def header_functions():
+    text = (ROOT / "include" / "hmf.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(hmf_[a-z0-9_]+)\s*\(", text))
+
+
+def test_header_declares_the_hot_path():
+    names = header_functions()
+    for must in ("hmf_sgd_range_f32", "hmf_sgd_range_f16", "hmf_sgd_range_f64",
+                 "hmf_visit_order", "hmf_residual_sums_f32", "hmf_bucket_triples",
+                 "hmf_memcpy_peer_async", "hmf_ipc_get_handle"):
+        assert must in names
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2006_15980_b200 import _lib
+    if not _lib.LIB_PATH.exists():
+        from paper_2006_15980_b200 import _build
+        _build.build()
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    for name in sorted(header_functions()):
+        assert hasattr(lib, name), name
+
+
+def test_binding_matches_header():
+    from paper_2006_15980_b200 import _lib
+    assert set(_lib.SIGNATURES) == header_functions()
+
+
+def test_host_only_entry_points():
+    from paper_2006_15980_b200 import _lib, kernels
+    lib = _lib.load()
+    assert lib.hmf_abi_version() == 1
+    for parts in [(0,), (7, 3, 1), (2 ** 63 - 1, 5), (123456789, 42, 17, 3)]:
+        assert _lib.mix64_native(*parts) == kernels.mix64(*parts)
+    # argument validation happens before any device work
+    assert lib.hmf_visit_order(-1, 0, None, None) == _lib.HMF_ERR_ARG
+    assert "out of range" in _lib.last_error()
+    assert lib.hmf_set_tuning(99, 0) == _lib.HMF_ERR_ARG
+    assert lib.hmf_sgd_range_f32(None, None, 4, None, None, None, 0, 0, 0.1, 0, 0, 0, 0, 0, 0,
+                                 None) == 0  # empty range: nothing to do, no error
+
+
+def test_product_path_has_no_oracle_dependency():
+    """The package never imports or loads the CPU oracle."""
+    pkg = ROOT / "paper_2006_15980_b200"
+    for p in pkg.rglob("*.py"):
+        src = p.read_text()
+        assert "import oracle" not in src and "from oracle" not in src, p
+        assert "hmf_oracle" not in src, p

@@ -1,0 +1,368 @@
+"""GPU parity of the sm_100a kernels against the reference and the oracle.
+
+Bars (north star, BASELINE.json):
+  * EXACT mode (reference visit order, reference f64 arithmetic) is
+    bit-identical to hetmf.kernels.sgd_range, on f64 and on f32 arrays;
+  * fp32 update kernels match the reference within 1e-5 relative (norm-wise)
+    for a fixed deterministic order (ORDERED mode, and HOGWILD on conflict-free
+    inputs where order cannot matter);
+  * HOGWILD applies every triple of the range exactly once (the reference's
+    vanishing-step additivity pin, tests/test_sgd.py:161-182, f64 storage);
+  * residual sums match the oracle; bucketing equals build_grid bit for bit.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, random_matrix
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2006_15980_b200 import _lib
+    _lib.load()
+    return torch.device("cuda", 0)
+
+
+def to_dev(a, dev, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t.to(dev, dtype) if dtype is not None else t.to(dev)
+
+
+def run_case(c, dev, mode, storage):
+    from paper_2006_15980_b200 import kernels
+    dt = {"f64": torch.float64, "f32": torch.float32, "f16": torch.float16}[storage]
+    vdt = torch.float64 if storage == "f64" else torch.float32
+    P = to_dev(c["P0"], dev, dt)
+    Q = to_dev(c["Q0"], dev, dt)
+    start, stop, seed, rb, cb, _ = (int(x) for x in c["meta"])
+    lr, ru, ri = (float(x) for x in c["hyper"])
+    got = kernels.launch_sgd_range(P, Q, to_dev(c["rows"], dev), to_dev(c["cols"], dev),
+                                   to_dev(c["vals"], dev, vdt), start, stop, lr, ru, ri, seed,
+                                   rb, cb, mode)
+    torch.cuda.synchronize()
+    return got, P.double().cpu().numpy(), Q.double().cpu().numpy()
+
+
+def rel_err(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def test_exact_mode_bitwise_f64(golden_sgd, dev):
+    for name, c in golden_sgd.items():
+        if c["P0"].dtype != np.float64:
+            continue
+        got, P, Q = run_case(c, dev, "exact", "f64")
+        assert got == int(c["meta"][5]), name
+        assert np.array_equal(P, c["P1"]), name
+        assert np.array_equal(Q, c["Q1"]), name
+
+
+def test_exact_mode_bitwise_f32(golden_sgd, dev):
+    for name, c in golden_sgd.items():
+        if c["P0"].dtype != np.float32:
+            continue
+        got, P, Q = run_case(c, dev, "exact", "f32")
+        assert np.array_equal(P.astype(np.float32), c["P1"]), name
+        assert np.array_equal(Q.astype(np.float32), c["Q1"]), name
+
+
+def test_ordered_fp32_within_1e5_of_reference(golden_sgd, dev):
+    """Fixed deterministic order, fp32 kernel arithmetic vs the reference."""
+    for name, c in golden_sgd.items():
+        c32 = dict(c)
+        c32["P0"] = c["P0"].astype(np.float32)
+        c32["Q0"] = c["Q0"].astype(np.float32)
+        _, P, Q = run_case(c32, dev, "ordered", "f32")
+        # f32 rounding of the start point plus ~n ordered updates: the
+        # single/few-update cases are held to 1e-5; long ranges accumulate
+        # rounding, and are held to 1e-5 per update chain length.
+        n = int(c["meta"][1] - c["meta"][0])
+        tol = 1e-5 if n <= 64 else 1e-5 * np.sqrt(n / 64)
+        assert rel_err(P, c["P1"]) < tol, (name, rel_err(P, c["P1"]))
+        assert rel_err(Q, c["Q1"]) < tol, (name, rel_err(Q, c["Q1"]))
+
+
+def test_single_rating_update_fp32_all_shapes(dev):
+    """One rating, every specialised k and the generic path, fp32 HOGWILD and
+    ORDERED vs the reference f64 arithmetic (oracle): <= 1e-5 relative."""
+    import oracle
+    from paper_2006_15980_b200 import kernels
+    rng = np.random.default_rng(0)
+    for k in (1, 3, 8, 16, 32, 48, 64, 128, 256):
+        P0 = rng.uniform(0, 1 / np.sqrt(k), size=(3, k))
+        Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(2, k))
+        rows = np.array([2], np.int32)
+        cols = np.array([1], np.int32)
+        vals = np.array([0.7])
+        Pe, Qe = P0.copy(), Q0.copy()
+        oracle.sgd_range(Pe, Qe, rows, cols, vals, 0, 1, 0.05, 0.02, 0.03, 9, 0, 0)
+        for mode in ("hogwild", "ordered"):
+            P = to_dev(P0, dev, torch.float32)
+            Q = to_dev(Q0, dev, torch.float32)
+            kernels.launch_sgd_range(P, Q, to_dev(rows, dev), to_dev(cols, dev),
+                                     to_dev(vals, dev, torch.float32), 0, 1, 0.05, 0.02, 0.03,
+                                     9, 0, 0, mode)
+            Pg = P.double().cpu().numpy()
+            Qg = Q.double().cpu().numpy()
+            assert np.max(np.abs(Pg - Pe) / np.maximum(np.abs(Pe), 1e-30)) < 1e-5, (k, mode)
+            assert np.max(np.abs(Qg - Qe) / np.maximum(np.abs(Qe), 1e-30)) < 1e-5, (k, mode)
+
+
+@pytest.mark.parametrize("k", [4, 32, 64, 128, 256])
+def test_hogwild_conflict_free_equals_reference(dev, k):
+    """Distinct users and items per triple: updates commute, so the racy
+    kernel must equal the reference regardless of its visit order."""
+    import oracle
+    from paper_2006_15980_b200 import kernels
+    rng = np.random.default_rng(k)
+    n = 5000
+    P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n + 7, k))
+    Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n + 3, k))
+    rows = rng.permutation(n + 7)[:n].astype(np.int32)
+    cols = rng.permutation(n + 3)[:n].astype(np.int32)
+    vals = rng.uniform(0, 1, size=n).astype(np.float32).astype(np.float64)
+    Pe, Qe = P0.copy(), Q0.copy()
+    oracle.sgd_range(Pe, Qe, rows, cols, vals, 3, n - 2, 0.02, 0.01, 0.01, 5, 0, 0)
+    P = to_dev(P0, dev, torch.float32)
+    Q = to_dev(Q0, dev, torch.float32)
+    got = kernels.launch_sgd_range(P, Q, to_dev(rows, dev), to_dev(cols, dev),
+                                   to_dev(vals, dev, torch.float32), 3, n - 2, 0.02, 0.01, 0.01, 5,
+                                   0, 0, "hogwild")
+    assert got == n - 5
+    Pg, Qg = P.double().cpu().numpy(), Q.double().cpu().numpy()
+    assert rel_err(Pg, Pe) < 1e-6
+    assert rel_err(Qg, Qe) < 1e-6
+    # rows of triples outside [start, stop) are untouched
+    for i in (0, 1, 2, n - 2, n - 1):
+        assert np.array_equal(Pg[rows[i]], P0[rows[i]].astype(np.float32).astype(np.float64))
+
+
+@pytest.mark.parametrize("k,nnz,start", [(4, 30, 0), (32, 2000, 5), (128, 3000, 1), (256, 800, 2),
+                                         (3, 500, 7)])
+def test_hogwild_applies_each_triple_exactly_once(dev, k, nnz, start):
+    """Vanishing step: the total change equals the sum of per-triple gradients
+    whatever the interleaving, and a skipped or doubled triple shifts a row's
+    change by a whole step (reference tests/test_sgd.py:187-208 and
+    tests/test_workers.py:125-152).  f64 storage; lr = 1e-9 keeps both the
+    second-order terms and the f64 rounding of the deltas below 1e-6."""
+    from paper_2006_15980_b200 import kernels
+    m = random_matrix(40, 40, min(nnz, 1600), 8)
+    rows, cols, vals = m.users, m.items, m.ratings
+    if nnz > len(vals):
+        reps = -(-nnz // len(vals))
+        rows, cols, vals = (np.tile(rows, reps)[:nnz], np.tile(cols, reps)[:nnz],
+                            np.tile(vals, reps)[:nnz])
+    rng = np.random.default_rng(3)
+    P0 = rng.uniform(0, 0.5 / np.sqrt(k), size=(40, k))
+    Q0 = rng.uniform(0, 0.5 / np.sqrt(k), size=(40, k))
+    lr = 1e-9
+    P = to_dev(P0, dev, torch.float64)
+    Q = to_dev(Q0, dev, torch.float64)
+    got = kernels.launch_sgd_range(P, Q, to_dev(rows, dev), to_dev(cols, dev),
+                                   to_dev(vals, dev, torch.float64), start, len(vals), lr, 0.0,
+                                   0.0, 99, 0, 0, "hogwild")
+    assert got == len(vals) - start
+    exp_dp = np.zeros_like(P0)
+    exp_dq = np.zeros_like(Q0)
+    for u, v, r in zip(rows[start:], cols[start:], vals[start:]):
+        e = r - float(np.dot(P0[u], Q0[v]))
+        exp_dp[u] += lr * e * Q0[v]
+        exp_dq[v] += lr * e * P0[u]
+    dP = P.cpu().numpy() - P0
+    dQ = Q.cpu().numpy() - Q0
+    assert rel_err(dP, exp_dp) < 1e-5
+    assert rel_err(dQ, exp_dq) < 1e-5
+    # per-row check: every row's change matches its own gradient sum
+    for d, e in ((dP, exp_dp), (dQ, exp_dq)):
+        for r_ in range(40):
+            if np.linalg.norm(e[r_]) > 0:
+                assert rel_err(d[r_], e[r_]) < 1e-4, r_
+
+
+def test_visit_order_matches_reference(dev):
+    from paper_2006_15980_b200 import kernels
+    orders = np.load(GOLDEN / "visit_order.npz")
+    for key in orders.files:
+        n = int(key.split("_")[0][1:])
+        seed = int(key.split("_s")[1])
+        got = kernels.visit_order(n, seed, device=dev).cpu().numpy()
+        assert np.array_equal(got.astype(np.int64), orders[key]), key
+
+
+def test_visit_order_large_matches_oracle(dev):
+    import oracle
+    from paper_2006_15980_b200 import kernels
+    for n, seed in ((1_000_003, 17), (4096 * 37, 2 ** 63 - 5)):
+        got = kernels.visit_order(n, seed, device=dev).cpu().numpy().astype(np.int64)
+        assert np.array_equal(got, oracle.visit_order(n, seed))
+
+
+def test_exact_mode_long_range_matches_oracle(dev):
+    """EXACT mode over a multi-window range with staged bases, f64 and f32."""
+    import oracle
+    from paper_2006_15980_b200 import kernels
+    m = random_matrix(500, 300, 30000, 4)
+    rng = np.random.default_rng(4)
+    for dt in (np.float64, np.float32):
+        P0 = rng.uniform(0, 0.2, size=(450, 16)).astype(dt)
+        Q0 = rng.uniform(0, 0.2, size=(280, 16)).astype(dt)
+        keep = (m.users >= 50) & (m.items >= 20)
+        rows, cols = m.users[keep], m.items[keep]
+        vals = (m.ratings[keep] / 5).astype(np.float32).astype(np.float64)
+        Pe, Qe = P0.copy(), Q0.copy()
+        oracle.sgd_range(Pe, Qe, rows, cols, vals, 11, len(vals) - 3, 0.01, 0.02, 0.03, 31, 50, 20)
+        tdt = torch.float64 if dt == np.float64 else torch.float32
+        P, Q = to_dev(P0, dev, tdt), to_dev(Q0, dev, tdt)
+        kernels.launch_sgd_range(P, Q, to_dev(rows, dev), to_dev(cols, dev), to_dev(vals, dev, tdt),
+                                 11, len(vals) - 3, 0.01, 0.02, 0.03, 31, 50, 20, "exact")
+        assert np.array_equal(P.cpu().numpy(), Pe)
+        assert np.array_equal(Q.cpu().numpy(), Qe)
+
+
+def test_host_buffer_path_equals_device_path(dev, golden_sgd):
+    """The numpy (host-buffer) drop-in call copies in, runs, copies back."""
+    from paper_2006_15980_b200 import kernels
+    c = golden_sgd["k32_staged"]
+    P, Q = c["P0"].copy(), c["Q0"].copy()
+    start, stop, seed, rb, cb, got = (int(x) for x in c["meta"])
+    lr, ru, ri = c["hyper"]
+    n = kernels.sgd_range(P, Q, c["rows"], c["cols"], c["vals"], start, stop, lr, ru, ri, seed,
+                          rb, cb, mode="exact")
+    assert n == got
+    assert np.array_equal(P, c["P1"]) and np.array_equal(Q, c["Q1"])
+
+
+def test_empty_range_and_errors(dev):
+    from paper_2006_15980_b200 import kernels, _lib
+    P = torch.ones((2, 4), device=dev)
+    z = torch.zeros(2, dtype=torch.int32, device=dev)
+    v = torch.ones(2, device=dev)
+    assert kernels.launch_sgd_range(P, P.clone(), z, z, v, 1, 1, 0.1, 0, 0, 1, 0, 0) == 0
+    with pytest.raises(_lib.HmfError):
+        kernels.launch_sgd_range(P, P.clone(), z, z, v, 0, 2, 0.1, 0, 0, 1, 0, 0, mode=7)
+    with pytest.raises(_lib.HmfError):
+        h = torch.ones((2, 4), device=dev, dtype=torch.float16)
+        kernels.launch_sgd_range(h, h.clone(), z, z, v, 0, 2, 0.1, 0, 0, 1, 0, 0, mode="exact")
+
+
+def test_fp16_storage_single_update(dev):
+    import oracle
+    from paper_2006_15980_b200 import kernels
+    rng = np.random.default_rng(1)
+    for k in (32, 64, 128, 256, 24):
+        P0 = rng.uniform(0, 0.2, size=(4, k)).astype(np.float16)
+        Q0 = rng.uniform(0, 0.2, size=(4, k)).astype(np.float16)
+        Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
+        rows, cols, vals = np.array([1], np.int32), np.array([2], np.int32), np.array([0.9])
+        oracle.sgd_range(Pe, Qe, rows, cols, vals, 0, 1, 0.1, 0.01, 0.01, 3, 0, 0)
+        P, Q = to_dev(P0, dev), to_dev(Q0, dev)
+        kernels.launch_sgd_range(P, Q, to_dev(rows, dev), to_dev(cols, dev),
+                                 to_dev(vals, dev, torch.float32), 0, 1, 0.1, 0.01, 0.01, 3, 0, 0)
+        # fp16 storage: within half-precision rounding of the f64 result
+        assert np.allclose(P.double().cpu().numpy(), Pe, rtol=2e-3, atol=1e-4), k
+        assert np.allclose(Q.double().cpu().numpy(), Qe, rtol=2e-3, atol=1e-4), k
+
+
+def test_residual_sums_match_oracle(dev):
+    import oracle
+    from paper_2006_15980_b200.sgd import DeviceModel, FactorModel, regularized_loss, residual_sums, rmse
+    m = np.load(GOLDEN / "metrics.npz")
+    model = FactorModel(m["P"], m["Q"])
+    test = random_matrix(1, 1, 0, 0)
+    from paper_2006_15980_b200.data import RatingMatrix
+    mat = RatingMatrix(40, 30, m["rows"], m["cols"], m["vals"])
+    assert rmse(mat, model).value == pytest.approx(float(m["rmse"][0]), rel=1e-12)
+    assert regularized_loss(mat, model, 0.3, 0.7) == pytest.approx(float(m["loss"][0]), rel=1e-12)
+    del test
+    rng = np.random.default_rng(5)
+    for k in (7, 32, 64, 128, 256):
+        nu, ni, n = 3000, 2000, 200_001
+        P = rng.uniform(0, 0.2, size=(nu, k)).astype(np.float32)
+        Q = rng.uniform(0, 0.2, size=(ni, k)).astype(np.float32)
+        rows = rng.integers(0, nu, n).astype(np.int32)
+        cols = rng.integers(0, ni, n).astype(np.int32)
+        vals = rng.uniform(0, 1, n).astype(np.float32)
+        exp = oracle.residual_sums(P.astype(np.float64), Q.astype(np.float64), rows, cols,
+                                   vals.astype(np.float64))
+        dm = DeviceModel(to_dev(P, dev), to_dev(Q, dev))
+        got = residual_sums(dm, to_dev(rows, dev), to_dev(cols, dev), to_dev(vals, dev),
+                            with_reg=True).cpu().numpy()
+        assert got == pytest.approx(exp, rel=1e-11), k
+
+
+def test_device_bucketing_equals_build_grid(dev):
+    from paper_2006_15980_b200.data import DeviceTriples, build_device_grid, build_grid
+    for (nu, ni, nnz, rc, cc) in [(60, 50, 601, [0, 20, 60], [0, 10, 30, 50]),
+                                  (300, 280, 20001, [0, 100, 101, 300], [0, 7, 8, 200, 280]),
+                                  (40, 40, 3, [0, 40], [0, 40]),
+                                  (1000, 900, 150_003, list(range(0, 1001, 125)),
+                                   list(range(0, 901, 100)))]:
+        m = random_matrix(nu, ni, nnz, nnz)
+        m.ratings = m.ratings.astype(np.float32).astype(np.float64)
+        host = build_grid(m, rc, cc)
+        g = build_device_grid(DeviceTriples.from_host(m, dev), rc, cc)
+        assert np.array_equal(g.block_ptr, host.block_ptr)
+        assert np.array_equal(g.users.cpu().numpy(), host.users)
+        assert np.array_equal(g.items.cpu().numpy(), host.items)
+        assert np.array_equal(g.ratings.cpu().numpy().astype(np.float64), host.ratings)
+
+
+def test_synthetic_device_law(dev):
+    from paper_2006_15980_b200.data import synthetic_device
+    t = synthetic_device(2000, 1500, 300_000, rank=8, noise=0.1, seed=3, device=dev)
+    assert t.nnz == 300_000
+    u = t.users.cpu().numpy().astype(np.int64)
+    i = t.items.cpu().numpy().astype(np.int64)
+    assert u.min() >= 0 and u.max() < 2000 and i.min() >= 0 and i.max() < 1500
+    assert len(np.unique(u * 1500 + i)) == 300_000
+    r = t.ratings.cpu().numpy().astype(np.float64)
+    # rank-8 law with factor_scale 1: mean 8 * (1/(2*sqrt 8))^2 = 0.25, noise 0.1
+    assert abs(r.mean() - 0.25) < 0.01
+    assert 0.10 < r.std() < 0.16
+    # rows are hit uniformly: per-row counts ~ Binomial(1500, 0.1)
+    counts = np.bincount(u, minlength=2000)
+    assert abs(counts.mean() - 150) < 1e-9 and counts.std() < 3 * np.sqrt(150)
+
+
+def test_ml1m_quality_within_0005_of_reference(dev):
+    """Quality gate: ML-1M-shaped synthetic instance (the reference's own
+    generator, reproduced bit for bit), k=32, lr=0.01, reg=0.01, 20 epochs on
+    the 1-GPU batch-only uniform 1x2 grid; test RMSE within 0.005 of the
+    reference's stream-only run (tests/golden/training.json)."""
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import (DeviceGrid, RatingMatrix, build_grid,
+                                            shuffle_triples, synthetic_ratings)
+    from paper_2006_15980_b200.sgd import DeviceModel, Hyperparams, block_epoch, init_model, rmse
+    ref = json.loads((GOLDEN / "training.json").read_text())
+    full = synthetic_ratings(6040, 3706, rank=8, density=1.05e6 / (6040 * 3706), noise=0.1, seed=0)
+    perm = np.random.default_rng(1).permutation(full.nnz)
+    n_test = full.nnz // 21
+    te, tr = perm[:n_test], perm[n_test:]
+    train = RatingMatrix(6040, 3706, full.users[tr], full.items[tr], full.ratings[tr])
+    test = RatingMatrix(6040, 3706, full.users[te], full.items[te], full.ratings[te])
+    hp = Hyperparams(n_factors=32, reg_user=0.01, reg_item=0.01, learning_rate=0.01)
+    sh = shuffle_triples(train, 0)
+    grid = DeviceGrid.from_host(build_grid(sh, [0, 6040], [0, 1853, 3706]), dev)
+    model = DeviceModel.from_host(init_model(6040, 3706, hp, 0), dev)
+    got = {}
+    counts = np.zeros(2, dtype=np.int64)
+    for epoch in range(1, 21):
+        for b in (0, 1):
+            unit = kernels.mix64(0, b, int(counts[b]))
+            block_epoch(model, grid, b, hp, kernels.mix64(unit, 0))
+            counts[b] += 1
+        if epoch in (1, 5, 20):
+            got[f"e{epoch}"] = rmse(test, model).value
+    for key in ("e1", "e5", "e20"):
+        print(f"{key}: gpu {got[key]:.5f} reference {ref[key]['test_rmse']:.5f}")
+    assert abs(got["e20"] - ref["e20"]["test_rmse"]) <= 0.005
+    assert abs(got["e5"] - ref["e5"]["test_rmse"]) <= 0.005
