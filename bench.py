@@ -277,7 +277,7 @@ def run_ours(args, world, rank, local):
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
             kernels.launch_sgd_range(model.P, model.Q, grid.users, grid.items, grid.ratings, lo,
-                                     hi, LR, REG, REG, seed, 0, 0, "hogwild", stream.cuda_stream)
+                                     hi, LR, REG, REG, seed, 0, 0, args.mode, stream.cuda_stream)
             if record:
                 e1.record(stream)
                 launch_events.append((e0, e1, hi - lo))
@@ -349,7 +349,7 @@ def run_ours(args, world, rank, local):
                        "train_ratings": nnz, "test_ratings": test.nnz,
                        "grid": "uniform 1x2 (1 batch worker per GPU)",
                        "parallelism": f"replica x{world}" if world > 1 else "single GPU",
-                       "lr": LR, "reg": REG, "mode": "hogwild",
+                       "lr": LR, "reg": REG, "mode": args.mode,
                        "variant": args.variant,
                        "l2": "inputs larger than L2 (P + triples >> 126 MB); no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -389,7 +389,7 @@ def run_e2e(args, grid, model, k, precision, dev, world):
         for b in range(grid.n_blocks):
             lo, hi = grid.block_range(b)
             kernels.sgd_range(h_P, h_Q, h_users, h_items, h_vals, lo, hi, LR, REG, REG,
-                              kernels.mix64(SEED, b, 99), 0, 0, mode="hogwild", device=dev.index)
+                              kernels.mix64(SEED, b, 99), 0, 0, mode=args.mode, device=dev.index)
 
     step()  # warm-up
     torch.cuda.synchronize(dev)
@@ -416,6 +416,7 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--precision", choices=["f32", "f16"], default="f32")
     ap.add_argument("--variant", type=int, default=None)
+    ap.add_argument("--mode", choices=["hogwild", "hogwild_lww"], default="hogwild")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

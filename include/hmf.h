@@ -45,9 +45,10 @@ extern "C" {
 #define HMF_ERR_UNSUPPORTED (-3)
 
 /* Visit-order modes of hmf_sgd_range_*. */
-#define HMF_MODE_HOGWILD 0 /* throughput: many warps, lock-free row updates      */
-#define HMF_MODE_ORDERED 1 /* reference visit order, one warp, fp32 arithmetic    */
-#define HMF_MODE_EXACT 2   /* reference visit order and f64 reference arithmetic */
+#define HMF_MODE_HOGWILD 0     /* throughput: many warps, lock-free delta reductions */
+#define HMF_MODE_ORDERED 1     /* reference visit order, one warp, fp32 arithmetic   */
+#define HMF_MODE_EXACT 2       /* reference visit order, f64 reference arithmetic   */
+#define HMF_MODE_HOGWILD_LWW 3 /* HOGWILD with plain stores (last writer wins)      */
 
 /* Reference visit-order window (kernels.py:24). */
 #define HMF_SHUFFLE_WINDOW 4096

@@ -24,7 +24,9 @@ HMF_ERR_UNSUPPORTED = -3
 MODE_HOGWILD = 0
 MODE_ORDERED = 1
 MODE_EXACT = 2
-MODES = {"hogwild": MODE_HOGWILD, "ordered": MODE_ORDERED, "exact": MODE_EXACT}
+MODE_HOGWILD_LWW = 3
+MODES = {"hogwild": MODE_HOGWILD, "ordered": MODE_ORDERED, "exact": MODE_EXACT,
+         "hogwild_lww": MODE_HOGWILD_LWW}
 
 TUNE_VARIANT = 1
 

@@ -30,6 +30,15 @@ template <> struct Storage<float> {
   }
   __device__ static inline C load1(const float* p) { return __ldcg(p); }
   __device__ static inline void store1(float* p, C v) { __stcg(p, v); }
+  // p[0..3] += in[0..3], one vector reduction at L2 (REDG.E.ADD.F32x4)
+  __device__ static inline void red(float* p, const C* in) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(in[0]), "f"(in[1]),
+                 "f"(in[2]), "f"(in[3])
+                 : "memory");
+  }
+  __device__ static inline void red1(float* p, C v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+  }
 };
 
 template <> struct Storage<__half> {
@@ -58,6 +67,20 @@ template <> struct Storage<__half> {
   __device__ static inline void store1(__half* p, C v) {
     __stcg(reinterpret_cast<unsigned short*>(p), __half_as_ushort(__float2half_rn(v)));
   }
+  __device__ static inline void red(__half* p, const C* in) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2 h = __floats2half2_rn(in[2 * i], in[2 * i + 1]);
+      asm volatile("red.global.add.noftz.f16x2 [%0], %1;" ::"l"(p + 2 * i),
+                   "r"(*reinterpret_cast<uint32_t*>(&h))
+                   : "memory");
+    }
+  }
+  __device__ static inline void red1(__half* p, C v) {
+    asm volatile("red.global.add.noftz.f16 [%0], %1;" ::"l"(p),
+                 "h"(__half_as_ushort(__float2half_rn(v)))
+                 : "memory");
+  }
 };
 
 template <> struct Storage<double> {
@@ -72,6 +95,13 @@ template <> struct Storage<double> {
   }
   __device__ static inline C load1(const double* p) { return __ldcg(p); }
   __device__ static inline void store1(double* p, C v) { __stcg(p, v); }
+  __device__ static inline void red(double* p, const C* in) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(in[0]) : "memory");
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p + 1), "d"(in[1]) : "memory");
+  }
+  __device__ static inline void red1(double* p, C v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+  }
 };
 
 // Rating value type paired with each storage type (f64 storage keeps f64

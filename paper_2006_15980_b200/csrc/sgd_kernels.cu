@@ -7,10 +7,15 @@
 //   Q[v,f] = qv + lr * (err * pu - reg_item * qv)      (pu, qv pre-update)
 // with u = rows[i] - row_base, v = cols[i] - col_base (kernels.py:105-106).
 //
-// Three modes:
+// Modes:
 //   HOGWILD  many warps, each lane group owns one rating at a time; rows are
-//            updated lock-free (last writer wins), the B200 analogue of the
-//            reference's racing batch lanes (workers.py:222-266).  Triples are
+//            updated lock-free: each update's deltas are added with vector
+//            reductions at L2 (red.global.add.v4.f32), so concurrent updates
+//            of a row never overwrite each other (reads may be stale).  The
+//            B200 analogue of the reference's racing batch lanes
+//            (workers.py:222-266).
+//   HOGWILD_LWW  the same, written back with plain stores: last writer wins
+//            per component, exactly the reference lanes' race.  Triples are
 //            staged into per-warp shared-memory rings by cp.async.bulk (TMA)
 //            with mbarrier completion, P/Q rows move as 16-byte vectors and the
 //            dot product is a __shfl_xor butterfly.
@@ -22,6 +27,8 @@
 //            storage type on store.  Bit-identical to the reference.
 #include "hmf_common.cuh"
 #include "hmf_internal.h"
+
+#include <type_traits>
 
 namespace hmf {
 
@@ -54,6 +61,20 @@ template <int K, typename S> struct RowMath {
       p[e] = pu + lr * (err * qv - ru * pu);
       q[e] = qv + lr * (err * pu - ri * qv);
     }
+  }
+  // The same step as deltas (p, q overwritten with lr*(...)), for write-back
+  // by vector reductions.
+  __device__ static inline void delta(C* p, C* q, C err, C lr, C ru, C ri) {
+#pragma unroll
+    for (int e = 0; e < G::EPL; ++e) {
+      const C pu = p[e], qv = q[e];
+      p[e] = lr * (err * qv - ru * pu);
+      q[e] = lr * (err * pu - ri * qv);
+    }
+  }
+  __device__ static inline void red(S* row, int lane_g, const C* in) {
+#pragma unroll
+    for (int v = 0; v < G::NV; ++v) ST::red(row + (v * G::LPR + lane_g) * G::VE, in + v * G::VE);
   }
 };
 
@@ -135,7 +156,7 @@ __device__ inline void stage_chunk(const Stage<S>& st, uint64_t* bar, const int3
 // is computed.  Pb / Qb are the factor bases biased by -row_base*K and
 // -col_base*K so a row address is one wide multiply-add of the staged index.
 // ---------------------------------------------------------------------------
-template <int K, typename S, int U, int WPB, int MINB>
+template <int K, typename S, int U, int WPB, int MINB, bool ATOMIC>
 __global__ void __launch_bounds__(WPB * 32, MINB)
     sgd_hogwild_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const int32_t* __restrict__ rows,
                        const int32_t* __restrict__ cols,
@@ -226,9 +247,15 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
       for (int j = 0; j < U; ++j) {
         if (ui[j] >= 0) {
           const int i = base + j * G::RPW + grp;
-          M::update(p[j], q[j], C(st.vals[i]) - d[j], lr, ru, ri);
-          M::store(Pb + int64_t(ui[j]) * K, lane_g, p[j]);
-          M::store(Qb + int64_t(vi[j]) * K, lane_g, q[j]);
+          if constexpr (ATOMIC) {
+            M::delta(p[j], q[j], C(st.vals[i]) - d[j], lr, ru, ri);
+            M::red(Pb + int64_t(ui[j]) * K, lane_g, p[j]);
+            M::red(Qb + int64_t(vi[j]) * K, lane_g, q[j]);
+          } else {
+            M::update(p[j], q[j], C(st.vals[i]) - d[j], lr, ru, ri);
+            M::store(Pb + int64_t(ui[j]) * K, lane_g, p[j]);
+            M::store(Qb + int64_t(vi[j]) * K, lane_g, q[j]);
+          }
         }
       }
     }
@@ -240,7 +267,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
 // HOGWILD kernel, runtime k (any factor count): one rating per warp per step,
 // lane l owns elements l, l+32, ...; scalar loads.
 // ---------------------------------------------------------------------------
-template <typename S>
+template <typename S, bool ATOMIC>
 __global__ void __launch_bounds__(256)
     sgd_hogwild_generic_kernel(S* P, S* Q, const int32_t* __restrict__ rows,
                                const int32_t* __restrict__ cols,
@@ -262,8 +289,13 @@ __global__ void __launch_bounds__(256)
     const C err = C(vals[i]) - d;
     for (int f = lane; f < k; f += 32) {
       const C pu = ST::load1(prow + f), qv = ST::load1(qrow + f);
-      ST::store1(prow + f, pu + lr * (err * qv - ru * pu));
-      ST::store1(qrow + f, qv + lr * (err * pu - ri * qv));
+      if constexpr (ATOMIC) {
+        ST::red1(prow + f, lr * (err * qv - ru * pu));
+        ST::red1(qrow + f, lr * (err * pu - ri * qv));
+      } else {
+        ST::store1(prow + f, pu + lr * (err * qv - ru * pu));
+        ST::store1(qrow + f, qv + lr * (err * pu - ri * qv));
+      }
     }
   }
 }
@@ -409,14 +441,14 @@ static uint64_t gcd_u64(uint64_t a, uint64_t b) {
 
 static int g_variant_override = -1;
 
-template <int K, typename S, int U, int WPB, int MINB>
+template <int K, typename S, int U, int WPB, int MINB, bool ATOMIC>
 static cudaError_t launch_hogwild_v(S* P, S* Q, const int32_t* rows, const int32_t* cols,
                                     const typename RatingOf<S>::T* vals, int64_t start,
                                     int64_t stop, double lr, double ru, double ri, uint64_t seed,
                                     int64_t row_base, int64_t col_base, cudaStream_t stream) {
   using C = typename Storage<S>::C;
   constexpr int CH = ChunkOf<S>::CH;
-  auto kern = sgd_hogwild_kernel<K, S, U, WPB, MINB>;
+  auto kern = sgd_hogwild_kernel<K, S, U, WPB, MINB, ATOMIC>;
   const int smem = WPB * warp_smem_bytes<S>();
   static int per_sm = 0;
   if (per_sm == 0) {
@@ -447,51 +479,48 @@ static cudaError_t launch_hogwild_v(S* P, S* Q, const int32_t* rows, const int32
   return cudaGetLastError();
 }
 
-template <int K, typename S, int V>
+template <int K, typename S, int V, bool ATOMIC>
 static cudaError_t launch_variant(S* P, S* Q, const int32_t* rows, const int32_t* cols,
                                   const typename RatingOf<S>::T* vals, int64_t start, int64_t stop,
                                   double lr, double ru, double ri, uint64_t seed, int64_t row_base,
                                   int64_t col_base, cudaStream_t stream) {
   constexpr Variant v = kVariants[V];
-  return launch_hogwild_v<K, S, v.u, v.wpb, v.minb>(P, Q, rows, cols, vals, start, stop, lr, ru,
-                                                    ri, seed, row_base, col_base, stream);
+  return launch_hogwild_v<K, S, v.u, v.wpb, v.minb, ATOMIC>(P, Q, rows, cols, vals, start, stop,
+                                                            lr, ru, ri, seed, row_base, col_base,
+                                                            stream);
 }
 
-template <int K, typename S>
+template <int K, typename S, bool ATOMIC>
 static cudaError_t launch_hogwild_k(S* P, S* Q, const int32_t* rows, const int32_t* cols,
                                     const typename RatingOf<S>::T* vals, int64_t start,
                                     int64_t stop, double lr, double ru, double ri, uint64_t seed,
                                     int64_t row_base, int64_t col_base, cudaStream_t stream) {
-  // Tuning sweeps cover the fp32 / fp16 kernels; f64 storage stays on its default.
-  if constexpr (sizeof(S) > 4) {
-    return launch_variant<K, S, DefaultVariant<K, S>::index>(P, Q, rows, cols, vals, start, stop,
-                                                             lr, ru, ri, seed, row_base, col_base,
-                                                             stream);
+  constexpr int DV = DefaultVariant<K, S>::index;
+  // Tuning sweeps cover the fp32 kernels; other storages stay on their default.
+  if constexpr (!std::is_same<S, float>::value) {
+    return launch_variant<K, S, DV, ATOMIC>(P, Q, rows, cols, vals, start, stop, lr, ru, ri, seed,
+                                            row_base, col_base, stream);
   } else {
-  if (g_variant_override < 0)
-    return launch_variant<K, S, DefaultVariant<K, S>::index>(P, Q, rows, cols, vals, start, stop,
-                                                             lr, ru, ri, seed, row_base, col_base,
-                                                             stream);
-  switch (g_variant_override) {
-#define HMF_VARIANT_CASE(VV)                                                                 \
-  case VV:                                                                                   \
-    return launch_variant<K, S, VV>(P, Q, rows, cols, vals, start, stop, lr, ru, ri, seed,   \
-                                    row_base, col_base, stream);
-    HMF_VARIANT_CASE(0)
-    HMF_VARIANT_CASE(1)
-    HMF_VARIANT_CASE(2)
-    HMF_VARIANT_CASE(3)
-    HMF_VARIANT_CASE(4)
-    HMF_VARIANT_CASE(5)
-    HMF_VARIANT_CASE(6)
-    HMF_VARIANT_CASE(7)
+    switch (g_variant_override < 0 ? DV : g_variant_override) {
+#define HMF_VARIANT_CASE(VV)                                                                    \
+  case VV:                                                                                      \
+    return launch_variant<K, S, VV, ATOMIC>(P, Q, rows, cols, vals, start, stop, lr, ru, ri,    \
+                                            seed, row_base, col_base, stream);
+      HMF_VARIANT_CASE(0)
+      HMF_VARIANT_CASE(1)
+      HMF_VARIANT_CASE(2)
+      HMF_VARIANT_CASE(3)
+      HMF_VARIANT_CASE(4)
+      HMF_VARIANT_CASE(5)
+      HMF_VARIANT_CASE(6)
+      HMF_VARIANT_CASE(7)
 #undef HMF_VARIANT_CASE
-    default: return cudaErrorInvalidValue;
-  }
+      default: return cudaErrorInvalidValue;
+    }
   }
 }
 
-template <typename S>
+template <typename S, bool ATOMIC>
 static cudaError_t launch_hogwild(S* P, S* Q, int k, const int32_t* rows, const int32_t* cols,
                                   const typename RatingOf<S>::T* vals, int64_t start, int64_t stop,
                                   double lr, double ru, double ri, uint64_t seed, int64_t row_base,
@@ -500,10 +529,15 @@ static cudaError_t launch_hogwild(S* P, S* Q, int k, const int32_t* rows, const 
       ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) == 0;
   if (aligned_rows) {
     switch (k) {
-      case 32: return launch_hogwild_k<32, S>(P, Q, rows, cols, vals, start, stop, lr, ru, ri, seed, row_base, col_base, stream);
-      case 64: return launch_hogwild_k<64, S>(P, Q, rows, cols, vals, start, stop, lr, ru, ri, seed, row_base, col_base, stream);
-      case 128: return launch_hogwild_k<128, S>(P, Q, rows, cols, vals, start, stop, lr, ru, ri, seed, row_base, col_base, stream);
-      case 256: return launch_hogwild_k<256, S>(P, Q, rows, cols, vals, start, stop, lr, ru, ri, seed, row_base, col_base, stream);
+#define HMF_K_CASE(KK)                                                                          \
+  case KK:                                                                                      \
+    return launch_hogwild_k<KK, S, ATOMIC>(P, Q, rows, cols, vals, start, stop, lr, ru, ri, seed, \
+                                           row_base, col_base, stream);
+      HMF_K_CASE(32)
+      HMF_K_CASE(64)
+      HMF_K_CASE(128)
+      HMF_K_CASE(256)
+#undef HMF_K_CASE
       default: break;
     }
   }
@@ -511,7 +545,7 @@ static cudaError_t launch_hogwild(S* P, S* Q, int k, const int32_t* rows, const 
   const int64_t n = stop - start;
   const int64_t warps = n < int64_t(sm_count()) * 64 ? n : int64_t(sm_count()) * 64;
   const int64_t grid = (warps + 7) / 8;
-  sgd_hogwild_generic_kernel<S><<<unsigned(grid), 256, 0, stream>>>(
+  sgd_hogwild_generic_kernel<S, ATOMIC><<<unsigned(grid), 256, 0, stream>>>(
       P, Q, rows, cols, vals, start, stop, k, C(lr), C(ru), C(ri), row_base, col_base);
   return cudaGetLastError();
 }
@@ -571,8 +605,11 @@ int64_t sgd_range_impl(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t
   if (!P || !Q || !rows || !cols || !vals) return set_error(HMF_ERR_ARG, "null pointer");
   cudaError_t e = cudaSuccess;
   if (mode == HMF_MODE_HOGWILD) {
-    e = launch_hogwild<S>(P, Q, int(k), rows, cols, vals, start, stop, lr, ru, ri, seed,
-                          row_base, col_base, stream);
+    e = launch_hogwild<S, true>(P, Q, int(k), rows, cols, vals, start, stop, lr, ru, ri, seed,
+                                row_base, col_base, stream);
+  } else if (mode == HMF_MODE_HOGWILD_LWW) {
+    e = launch_hogwild<S, false>(P, Q, int(k), rows, cols, vals, start, stop, lr, ru, ri, seed,
+                                 row_base, col_base, stream);
   } else if (mode == HMF_MODE_ORDERED || mode == HMF_MODE_EXACT) {
     if (n > INT32_MAX) return set_error(HMF_ERR_ARG, "ordered modes take < 2^31 triples");
     if (mode == HMF_MODE_EXACT && sizeof(S) == 2)

@@ -144,7 +144,7 @@ def sgd_range(user_f, item_f, rows, cols, vals, start, stop, lr, reg_user, reg_i
 def visit_order(n: int, seed: int, device=None):
     """The reference visit order of n triples (offsets), computed on device."""
     torch = _torch()
-    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     out = torch.empty(max(int(n), 0), dtype=torch.int32, device=dev)
     if n > 0:
         _lib.check(_lib.load().hmf_visit_order(int(n), int(seed) & _MASK64, out.data_ptr(),
