@@ -235,7 +235,8 @@ def run_reference_arm(args, world, rank):
 def run_ours(args, world, rank, local):
     import torch
     from paper_2006_15980_b200 import _lib, kernels
-    from paper_2006_15980_b200.data import build_device_grid, split_device, synthetic_device
+    from paper_2006_15980_b200.data import (bucket_qbands, build_device_grid, split_device,
+                                            synthetic_device)
     from paper_2006_15980_b200.sgd import init_device_model, rmse
 
     _lib.load()
@@ -257,6 +258,8 @@ def run_ours(args, world, rank, local):
     col_cuts = np.array([0, (n_items + 1) // 2, n_items], dtype=np.int64)
     grid = build_device_grid(train, row_cuts, col_cuts)
     del trip
+    if args.kernel == "qband":
+        bucket_qbands(grid, k)
     model = init_device_model(n_users, n_items, k, SEED, device=dev,
                               dtype="float16" if precision == "f16" else "float32")
     torch.cuda.synchronize(dev)
@@ -276,8 +279,13 @@ def run_ours(args, world, rank, local):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            kernels.launch_sgd_range(model.P, model.Q, grid.users, grid.items, grid.ratings, lo,
-                                     hi, LR, REG, REG, seed, 0, 0, args.mode, stream.cuda_stream)
+            if args.kernel == "qband":
+                kernels.launch_block_qband(model.P, model.Q, grid, b, LR, REG, REG, seed,
+                                           stream=stream.cuda_stream)
+            else:
+                kernels.launch_sgd_range(model.P, model.Q, grid.users, grid.items, grid.ratings,
+                                         lo, hi, LR, REG, REG, seed, 0, 0, args.mode,
+                                         stream.cuda_stream)
             if record:
                 e1.record(stream)
                 launch_events.append((e0, e1, hi - lo))
@@ -313,7 +321,8 @@ def run_ours(args, world, rank, local):
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
-            tr = json.loads(prof.read_text()).get(f"{args.workload}_k{k}_{precision}")
+            tr = json.loads(prof.read_text()).get(
+                f"{args.workload}_k{k}_{precision}_{args.kernel}")
             if tr:
                 traffic = tr["dram_bytes_per_launch"]
         except Exception:
@@ -349,13 +358,15 @@ def run_ours(args, world, rank, local):
                        "train_ratings": nnz, "test_ratings": test.nnz,
                        "grid": "uniform 1x2 (1 batch worker per GPU)",
                        "parallelism": f"replica x{world}" if world > 1 else "single GPU",
-                       "lr": LR, "reg": REG, "mode": args.mode,
+                       "lr": LR, "reg": REG, "mode": args.mode, "kernel": args.kernel,
                        "variant": args.variant,
                        "l2": "inputs larger than L2 (P + triples >> 126 MB); no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "bytes_per_update": bpu,
-                         "kernel": "sgd_hogwild_kernel", "mean_launch_ms": mean_ms,
+                         "kernel": ("qband_kernel" if args.kernel == "qband"
+                                    else "sgd_hogwild_kernel"),
+                         "mean_launch_ms": mean_ms,
                          "updates_per_launch": mean_updates},
             "rmse": {"epochs": epochs_run, "test": test_rmse},
             "e2e": e2e,
@@ -417,6 +428,9 @@ def main():
     ap.add_argument("--precision", choices=["f32", "f16"], default="f32")
     ap.add_argument("--variant", type=int, default=None)
     ap.add_argument("--mode", choices=["hogwild", "hogwild_lww"], default="hogwild")
+    ap.add_argument("--kernel", choices=["qband", "hogwild"], default="qband",
+                    help="qband: Q band in shared memory (engine fast path); hogwild: "
+                         "global-Q kernel behind hmf_sgd_range")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

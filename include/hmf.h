@@ -10,6 +10,8 @@
  * /root/reference/pkg/src/hetmf/):
  *
  *   hmf_sgd_range_{f32,f16,f64}   kernels.sgd_range            kernels.py:61-133
+ *   hmf_sgd_block_qband_{f32,f16} BatchEngine.compute on a staged item band
+ *                                                              workers.py:186-255
  *   hmf_visit_order               sgd_range's visit order      kernels.py:77-119
  *   hmf_mix64                     kernels.mix64                kernels.py:32-48
  *   hmf_residual_sums_{f32,f16,f64}
@@ -89,6 +91,29 @@ int64_t hmf_sgd_range_f64(double* user_f, double* item_f, int64_t k, const int32
                           const int32_t* cols, const double* vals, int64_t start, int64_t stop,
                           double lr, double reg_user, double reg_item, uint64_t seed,
                           int64_t row_base, int64_t col_base, int32_t mode, void* stream);
+
+/*
+ * Q-band-stationary update of one block (the engine's fast path): the block's
+ * triples are bucketed into n_sub column sub-bands (stable), sub-band s being
+ * triples [sub_ptr[s], sub_ptr[s+1]) whose items lie in [sub_cuts[s],
+ * sub_cuts[s+1]) (absolute item ids; device arrays).  One warp owns a
+ * sub-band: its Q rows live in shared memory for the whole launch (exact
+ * sequential SGD on Q), P deltas go back by vector reductions.  Each
+ * sub-band may span at most hmf_qband_max_items(k) items; k in
+ * {32, 64, 128, 256}; ratings are f32.  Same update rule and indexing
+ * (row_base / col_base) as hmf_sgd_range_*.  Returns 0 or < 0.
+ */
+int32_t hmf_qband_max_items(int64_t k);
+int64_t hmf_sgd_block_qband_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
+                                const int32_t* cols, const float* vals, const int64_t* sub_ptr,
+                                const int32_t* sub_cuts, int64_t n_sub, double lr, double reg_user,
+                                double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
+                                void* stream);
+int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                                const int32_t* rows, const int32_t* cols, const float* vals,
+                                const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
+                                double lr, double reg_user, double reg_item, uint64_t seed,
+                                int64_t row_base, int64_t col_base, void* stream);
 
 /*
  * The reference visit order of a range of n triples under `seed`

@@ -1,0 +1,382 @@
+// Q-band-stationary block update: the staged item band of the reference's
+// BatchEngine (workers.py:186-202, "triples plus the touched item-factor
+// columns") held in shared memory on B200.
+//
+// A block of the division plan is split into S column sub-bands (equal item
+// width).  Its triples are bucketed by sub-band (stable), so sub-band s is the
+// contiguous range [sub_ptr[s], sub_ptr[s+1]) and touches only items
+// [sub_cuts[s], sub_cuts[s+1]).  Warp w owns sub-bands w, w + TW, ...:
+//   1. copy the sub-band's Q rows into its private shared-memory slice (fp32),
+//   2. stream the sub-band's triples through a 2-stage cp.async.bulk ring,
+//   3. per rating: P row from HBM (16-byte vectors, prefetched one group of U
+//      ratings ahead), Q row from shared memory, __shfl_xor dot, update; the Q
+//      row is rewritten in shared memory (exact sequential SGD for Q — no
+//      other warp can touch it), the P delta is added with a vector
+//      reduction (red.global.add.v4.f32; other warps may share the user),
+//   4. write the Q slice back (rounded to the storage type once).
+// Versus the global-Q HOGWILD kernel this removes the Q loads and Q
+// reductions from the SM->L2 path (half of its traffic, the binding unit in
+// the r01 ncu profile) and all races on Q.
+#include "hmf_common.cuh"
+#include "hmf_internal.h"
+
+namespace hmf {
+
+namespace qs {
+
+constexpr int kWarps = 16;           // warps per CTA
+constexpr int kChunk = 128;          // triples per staging stage
+constexpr int kSliceBytes = 4096;    // fp32 Q slice per warp
+
+// Lane layout of a K-row for one warp-owned rating: 32 lanes, EPL elements
+// each, interleaved by 16-byte vectors when a lane holds >= one vector,
+// interleaved by element otherwise (coalesced global, conflict-free shared).
+template <int K, typename S> struct Lay {
+  static constexpr int VE = Storage<S>::VE;
+  static constexpr int EPL = K / 32;
+  static constexpr bool VEC = (EPL % VE) == 0;
+  static constexpr int NV = VEC ? EPL / VE : 0;
+  static_assert(K % 32 == 0, "K must be a multiple of 32");
+  // element index of the lane's e-th element
+  __device__ static inline int elem(int lane, int e) {
+    if constexpr (VEC) return ((e / VE) * 32 + lane) * VE + (e % VE);
+    else return e * 32 + lane;
+  }
+};
+
+template <int K, typename S>
+__device__ inline void load_row(const S* row, int lane, float* out) {
+  using L = Lay<K, S>;
+  using ST = Storage<S>;
+  if constexpr (L::VEC) {
+#pragma unroll
+    for (int v = 0; v < L::NV; ++v) {
+      typename ST::C tmp[L::VE];
+      ST::load(row + (v * 32 + lane) * L::VE, tmp);
+#pragma unroll
+      for (int e = 0; e < L::VE; ++e) out[v * L::VE + e] = float(tmp[e]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < L::EPL; ++e) out[e] = float(ST::load1(row + e * 32 + lane));
+  }
+}
+
+template <int K, typename S>
+__device__ inline void red_row(S* row, int lane, const float* d) {
+  using L = Lay<K, S>;
+  using ST = Storage<S>;
+  if constexpr (L::VEC) {
+#pragma unroll
+    for (int v = 0; v < L::NV; ++v) {
+      typename ST::C tmp[L::VE];
+#pragma unroll
+      for (int e = 0; e < L::VE; ++e) tmp[e] = typename ST::C(d[v * L::VE + e]);
+      ST::red(row + (v * 32 + lane) * L::VE, tmp);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < L::EPL; ++e) ST::red1(row + e * 32 + lane, typename ST::C(d[e]));
+  }
+}
+
+// Shared-memory Q row access (fp32 slice, same element interleave).
+template <int K, typename S>
+__device__ inline void lds_row(const float* q, int lane, float* out) {
+  using L = Lay<K, S>;
+  if constexpr (L::VEC && (L::VE % 4 == 0)) {
+#pragma unroll
+    for (int v = 0; v < L::NV; ++v)
+#pragma unroll
+      for (int h = 0; h < L::VE / 4; ++h) {
+        const float4 t = *reinterpret_cast<const float4*>(q + (v * 32 + lane) * L::VE + 4 * h);
+        out[v * L::VE + 4 * h + 0] = t.x;
+        out[v * L::VE + 4 * h + 1] = t.y;
+        out[v * L::VE + 4 * h + 2] = t.z;
+        out[v * L::VE + 4 * h + 3] = t.w;
+      }
+  } else {
+#pragma unroll
+    for (int e = 0; e < L::EPL; ++e) out[e] = q[L::elem(lane, e)];
+  }
+}
+
+template <int K, typename S>
+__device__ inline void sts_row(float* q, int lane, const float* in) {
+  using L = Lay<K, S>;
+  if constexpr (L::VEC && (L::VE % 4 == 0)) {
+#pragma unroll
+    for (int v = 0; v < L::NV; ++v)
+#pragma unroll
+      for (int h = 0; h < L::VE / 4; ++h)
+        *reinterpret_cast<float4*>(q + (v * 32 + lane) * L::VE + 4 * h) =
+            make_float4(in[v * L::VE + 4 * h], in[v * L::VE + 4 * h + 1],
+                        in[v * L::VE + 4 * h + 2], in[v * L::VE + 4 * h + 3]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < L::EPL; ++e) q[L::elem(lane, e)] = in[e];
+  }
+}
+
+constexpr int stage_bytes = kChunk * 12;
+constexpr int warp_bytes = kSliceBytes + 2 * stage_bytes + 16;
+
+struct Ring {
+  int32_t* rows;
+  int32_t* cols;
+  float* vals;
+};
+
+__device__ inline Ring ring_at(unsigned char* base, int b) {
+  unsigned char* p = base + kSliceBytes + b * stage_bytes;
+  return Ring{reinterpret_cast<int32_t*>(p), reinterpret_cast<int32_t*>(p + kChunk * 4),
+              reinterpret_cast<float*>(p + kChunk * 8)};
+}
+
+__device__ inline void stage(const Ring& r, uint64_t* bar, const int32_t* rows,
+                             const int32_t* cols, const float* vals, int64_t beg, int64_t end,
+                             bool bulk_ok, int lane) {
+  const int n = int(end - beg);
+  const int n_bulk = bulk_ok ? (n & ~3) : 0;
+  if (lane == 0) {
+    fence_proxy_async();
+    mbar_arrive_expect_tx(bar, uint32_t(n_bulk) * 12u);
+    if (n_bulk > 0) {
+      bulk_g2s(r.rows, rows + beg, n_bulk * 4, bar);
+      bulk_g2s(r.cols, cols + beg, n_bulk * 4, bar);
+      bulk_g2s(r.vals, vals + beg, n_bulk * 4, bar);
+    }
+  }
+  for (int i = n_bulk + lane; i < n; i += 32) {
+    r.rows[i] = __ldg(rows + beg + i);
+    r.cols[i] = __ldg(cols + beg + i);
+    r.vals[i] = __ldg(vals + beg + i);
+  }
+}
+
+template <int K, typename S, int U>
+__global__ void __launch_bounds__(kWarps * 32, 2)
+    qband_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const int32_t* __restrict__ rows,
+                 const int32_t* __restrict__ cols, const float* __restrict__ vals,
+                 const int64_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_cuts,
+                 int n_sub, float lr, float ru, float ri, uint64_t seed) {
+  using L = Lay<K, S>;
+  constexpr int E = L::EPL;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wbase = smem + warp * warp_bytes;
+  float* qslice = reinterpret_cast<float*>(wbase);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kSliceBytes + 2 * stage_bytes);
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const int tw = gridDim.x * kWarps;
+  const bool bulk_ok = ((reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(cols) |
+                         reinterpret_cast<uintptr_t>(vals)) & 15u) == 0;
+  uint32_t phase[2] = {0u, 0u};
+
+  for (int s = blockIdx.x * kWarps + warp; s < n_sub; s += tw) {
+    const int c_lo = sub_cuts[s];
+    const int n_items = sub_cuts[s + 1] - c_lo;
+    if (n_items > kSliceBytes / (K * 4)) __trap();  // host contract: slice fits
+    S* qrow0 = Qb + int64_t(c_lo) * K;
+    // 1. Q slice -> shared memory (fp32)
+    for (int it = 0; it < n_items; ++it) {
+      float t[E];
+      load_row<K, S>(qrow0 + int64_t(it) * K, lane, t);
+      sts_row<K, S>(qslice + it * K, lane, t);
+    }
+    const int64_t beg = sub_ptr[s], end = sub_ptr[s + 1];
+    const int64_t a0 = beg & ~int64_t(3);
+    const int64_t n_chunks = (end - a0 + kChunk - 1) / kChunk;
+    // seeded rotation of the chunk visit order (fresh order every epoch)
+    const int64_t rot = n_chunks > 0 ? int64_t(splitmix_finalize(seed + uint64_t(s) * kGolden) %
+                                                uint64_t(n_chunks))
+                                     : 0;
+    auto chunk_begin = [&](int64_t x) -> int64_t {
+      int64_t c = x + rot;
+      if (c >= n_chunks) c -= n_chunks;
+      return a0 + c * kChunk;
+    };
+    if (n_chunks > 0) {
+      const int64_t cb = chunk_begin(0);
+      stage(ring_at(wbase, 0), &bars[0], rows, cols, vals, cb, min(cb + kChunk, end), bulk_ok,
+            lane);
+    }
+    __syncwarp();
+    for (int64_t x = 0; x < n_chunks; ++x) {
+      const int b = int(x & 1);
+      if (x + 1 < n_chunks) {
+        const int64_t nb = chunk_begin(x + 1);
+        stage(ring_at(wbase, b ^ 1), &bars[b ^ 1], rows, cols, vals, nb, min(nb + kChunk, end),
+              bulk_ok, lane);
+      }
+      const int64_t cb = chunk_begin(x);
+      const int lo = int(max(beg - cb, int64_t(0)));
+      const int hi = int(min(cb + kChunk, end) - cb);
+      mbar_wait(&bars[b], phase[b]);
+      phase[b] ^= 1u;
+      __syncwarp();
+      const Ring r = ring_at(wbase, b);
+
+      float pc[U][E], pn[U][E];
+      int32_t uc[U], un[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int i = lo + j;
+        uc[j] = i < hi ? r.rows[i] : -1;
+        if (uc[j] >= 0) load_row<K, S>(Pb + int64_t(uc[j]) * K, lane, pc[j]);
+      }
+      for (int base = lo; base < hi; base += U) {
+        // prefetch the next group's P rows
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int i = base + U + j;
+          un[j] = i < hi ? r.rows[i] : -1;
+          if (un[j] >= 0) load_row<K, S>(Pb + int64_t(un[j]) * K, lane, pn[j]);
+        }
+        // the current group, sequentially on the shared-memory Q slice
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          if (uc[j] >= 0) {
+            const int i = base + j;
+            float* qs_row = qslice + (r.cols[i] - c_lo) * K;
+            float q[E];
+            lds_row<K, S>(qs_row, lane, q);
+            float d = 0.f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) d += pc[j][e] * q[e];
+            d = group_sum<32>(d);
+            const float err = r.vals[i] - d;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const float pu = pc[j][e], qv = q[e];
+              pc[j][e] = lr * (err * qv - ru * pu);
+              q[e] = qv + lr * (err * pu - ri * qv);
+            }
+            sts_row<K, S>(qs_row, lane, q);
+            __syncwarp();
+            red_row<K, S>(Pb + int64_t(uc[j]) * K, lane, pc[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          uc[j] = un[j];
+#pragma unroll
+          for (int e = 0; e < E; ++e) pc[j][e] = pn[j][e];
+        }
+      }
+      __syncwarp();
+    }
+    // 4. Q slice back to HBM (rounded to the storage type once per lease)
+    for (int it = 0; it < n_items; ++it) {
+      float t[E];
+      lds_row<K, S>(qslice + it * K, lane, t);
+      using L2 = Lay<K, S>;
+      if constexpr (L2::VEC) {
+#pragma unroll
+        for (int v = 0; v < L2::NV; ++v) {
+          typename Storage<S>::C tmp[L2::VE];
+#pragma unroll
+          for (int e = 0; e < L2::VE; ++e) tmp[e] = typename Storage<S>::C(t[v * L2::VE + e]);
+          Storage<S>::store(qrow0 + int64_t(it) * K + (v * 32 + lane) * L2::VE, tmp);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          Storage<S>::store1(qrow0 + int64_t(it) * K + e * 32 + lane,
+                             typename Storage<S>::C(t[e]));
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int K, typename S>
+constexpr int max_items() {
+  return kSliceBytes / (K * 4);
+}
+
+template <int K, typename S>
+static cudaError_t launch(S* P, S* Q, const int32_t* rows, const int32_t* cols, const float* vals,
+                          const int64_t* sub_ptr, const int32_t* sub_cuts, int n_sub, double lr,
+                          double ru, double ri, uint64_t seed, int64_t row_base, int64_t col_base,
+                          cudaStream_t stream) {
+  // P rows prefetched one group ahead: 2 x U x (K/32) floats per lane in flight
+  constexpr int U = (K / 32) >= 4 ? 2 : 4;
+  auto kern = qband_kernel<K, S, U>;
+  const int smem = kWarps * warp_bytes;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int want = (n_sub + kWarps - 1) / kWarps;
+  const int cap = device_sm_count() * per_sm;
+  const int grid = want < cap ? want : cap;
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, kWarps * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
+                                            sub_ptr, sub_cuts, n_sub, float(lr), float(ru),
+                                            float(ri), seed);
+  return cudaGetLastError();
+}
+
+template <typename S>
+static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* cols,
+                   const float* vals, const int64_t* sub_ptr, const int32_t* sub_cuts,
+                   int64_t n_sub, double lr, double ru, double ri, uint64_t seed,
+                   int64_t row_base, int64_t col_base, cudaStream_t stream) {
+  if (n_sub <= 0) return 0;
+  if (!P || !Q || !rows || !cols || !vals || !sub_ptr || !sub_cuts)
+    return set_error(HMF_ERR_ARG, "null pointer");
+  if (((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) != 0)
+    return set_error(HMF_ERR_ARG, "factor arrays must be 16-byte aligned");
+  cudaError_t e;
+  switch (k) {
+    case 32: e = launch<32, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, seed, row_base, col_base, stream); break;
+    case 64: e = launch<64, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, seed, row_base, col_base, stream); break;
+    case 128: e = launch<128, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, seed, row_base, col_base, stream); break;
+    case 256: e = launch<256, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, seed, row_base, col_base, stream); break;
+    default: return set_error(HMF_ERR_UNSUPPORTED, "Q-band kernel needs k in {32,64,128,256}");
+  }
+  if (e != cudaSuccess) return set_cuda_error(e);
+  return 0;
+}
+
+}  // namespace qs
+}  // namespace hmf
+
+extern "C" {
+
+int32_t hmf_qband_max_items(int64_t k) {
+  if (k != 32 && k != 64 && k != 128 && k != 256) return 0;
+  return int32_t(hmf::qs::kSliceBytes / (k * 4));
+}
+
+int64_t hmf_sgd_block_qband_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
+                                const int32_t* cols, const float* vals, const int64_t* sub_ptr,
+                                const int32_t* sub_cuts, int64_t n_sub, double lr, double reg_user,
+                                double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
+                                void* stream) {
+  return hmf::qs::run<float>(user_f, item_f, k, rows, cols, vals, sub_ptr, sub_cuts, n_sub, lr,
+                             reg_user, reg_item, seed, row_base, col_base,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                                const int32_t* rows, const int32_t* cols, const float* vals,
+                                const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
+                                double lr, double reg_user, double reg_item, uint64_t seed,
+                                int64_t row_base, int64_t col_base, void* stream) {
+  return hmf::qs::run<__half>(reinterpret_cast<__half*>(user_f), reinterpret_cast<__half*>(item_f),
+                              k, rows, cols, vals, sub_ptr, sub_cuts, n_sub, lr, reg_user, reg_item,
+                              seed, row_base, col_base, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -367,6 +367,12 @@ class DeviceGrid:
     ratings: object
     block_ptr: np.ndarray
 
+    # Q-band sub-bucketing (optional): per block, device int64 sub_ptr[S+1]
+    # (absolute triple offsets) and int32 sub_cuts[S+1] (absolute item ids);
+    # see hmf_sgd_block_qband_* and bucket_qbands().
+    sub_ptr: list | None = None
+    sub_cuts: list | None = None
+
     n_row_bands = BlockGrid.n_row_bands
     n_col_bands = BlockGrid.n_col_bands
     n_blocks = BlockGrid.n_blocks
@@ -428,6 +434,60 @@ def build_device_grid(triples: DeviceTriples, row_cuts, col_cuts, region_of_row=
     ptr = d_ptr.cpu().numpy()
     return DeviceGrid(triples.n_users, triples.n_items, row_cuts, col_cuts, region,
                       sub_row_parent, out_u, out_i, out_r, ptr)
+
+
+def resident_warps(device) -> int:
+    """Warps the Q-band kernel keeps resident: 2 CTAs x 16 warps per SM."""
+    torch = _torch()
+    return int(torch.cuda.get_device_properties(device).multi_processor_count) * 32
+
+
+def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int) -> np.ndarray:
+    """Equal-width item sub-bands of [c_lo, c_hi): about `target` of them
+    (one per resident warp), never more than the items, and narrow enough
+    that each sub-band's Q slice fits the kernel's shared-memory slice."""
+    items = c_hi - c_lo
+    cap = int(_lib.load().hmf_qband_max_items(k))
+    if cap <= 0:
+        raise ValueError(f"Q-band kernel does not support k={k}")
+    n_sub = min(items, max(target, -(-items // cap)))
+    base, rem = divmod(items, n_sub)
+    widths = np.full(n_sub, base, dtype=np.int64)
+    widths[:rem] += 1
+    return np.concatenate([[c_lo], c_lo + np.cumsum(widths)]).astype(np.int64)
+
+
+def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None) -> DeviceGrid:
+    """Re-bucket every block of a device grid by item sub-band (stable), in
+    place, and attach sub_ptr / sub_cuts for the Q-band kernel."""
+    torch = _torch()
+    dev = grid.device
+    lib = _lib.load()
+    s = _stream(dev)
+    target = resident_warps(dev) if target is None else int(target)
+    out_u = torch.empty_like(grid.users)
+    out_i = torch.empty_like(grid.items)
+    out_r = torch.empty_like(grid.ratings)
+    row_cuts = torch.tensor([0, grid.n_rows], dtype=torch.int64, device=dev)
+    sub_ptrs, sub_cuts = [], []
+    for b in range(grid.n_blocks):
+        lo, hi = grid.block_range(b)
+        c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
+        cuts = qband_sub_cuts(c_lo, c_hi, k, target)
+        n_sub = len(cuts) - 1
+        d_cuts = torch.from_numpy(cuts).to(dev)
+        ptr = torch.zeros(n_sub + 1, dtype=torch.int64, device=dev)
+        if hi > lo:
+            _lib.check(lib.hmf_bucket_triples(
+                grid.users.data_ptr() + 4 * lo, grid.items.data_ptr() + 4 * lo,
+                grid.ratings.data_ptr() + 4 * lo, hi - lo, row_cuts.data_ptr(), 1,
+                d_cuts.data_ptr(), n_sub, out_u.data_ptr() + 4 * lo, out_i.data_ptr() + 4 * lo,
+                out_r.data_ptr() + 4 * lo, ptr.data_ptr(), s), "hmf_bucket_triples")
+        sub_ptrs.append(ptr + lo)
+        sub_cuts.append(d_cuts.to(torch.int32))
+    grid.users, grid.items, grid.ratings = out_u, out_i, out_r
+    grid.sub_ptr, grid.sub_cuts = sub_ptrs, sub_cuts
+    return grid
 
 
 def synthetic_device(n_users: int, n_items: int, nnz: int, rank: int = 8, noise: float = 0.1,

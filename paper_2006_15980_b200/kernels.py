@@ -105,6 +105,31 @@ def launch_sgd_range(user_f, item_f, rows, cols, vals, start, stop, lr, reg_user
     return _lib.check(got, f"hmf_sgd_range_{st}")
 
 
+def launch_block_qband(user_f, item_f, grid, block, lr, reg_user, reg_item, seed, row_base=0,
+                       col_base=0, stream=None) -> int:
+    """Q-band-stationary update of one block of a DeviceGrid bucketed by
+    data.bucket_qbands (the engine fast path).  Returns triples processed."""
+    _check_factor(user_f, "user_f")
+    _check_factor(item_f, "item_f")
+    if grid.sub_ptr is None:
+        raise ValueError("grid has no Q-band sub-bucketing (data.bucket_qbands)")
+    st = _storage_of(user_f.dtype)
+    if st == "f64":
+        raise TypeError("the Q-band kernel stores f32 or f16 factors")
+    lo, hi = grid.block_range(block)
+    if hi <= lo:
+        return 0
+    sp, sc = grid.sub_ptr[block], grid.sub_cuts[block]
+    s = current_stream_handle(user_f.device) if stream is None else int(stream)
+    fn = getattr(_lib.load(), f"hmf_sgd_block_qband_{st}")
+    _lib.check(fn(user_f.data_ptr(), item_f.data_ptr(), user_f.shape[1], grid.users.data_ptr(),
+                  grid.items.data_ptr(), grid.ratings.data_ptr(), sp.data_ptr(), sc.data_ptr(),
+                  int(sp.numel()) - 1, float(lr), float(reg_user), float(reg_item),
+                  int(seed) & _MASK64, int(row_base), int(col_base), s),
+               f"hmf_sgd_block_qband_{st}")
+    return hi - lo
+
+
 def sgd_range(user_f, item_f, rows, cols, vals, start, stop, lr, reg_user, reg_item, seed,
               row_base, col_base, *, mode="hogwild", stream=None, device=None) -> int:
     """Apply one SGD pass over triples[start:stop] (hetmf/kernels.py:61-133).

@@ -83,6 +83,11 @@ def netflix(args):
     h_test = test.to_host()
     out = {"config": dict(n_users=n_users, n_items=n_items, train=train.nnz, test=test.nnz, k=k,
                           lr=lr, reg=reg, epochs=args.epochs)}
+    qgrid = None
+    if "qband" in args.modes.split(","):
+        from paper_2006_15980_b200.data import bucket_qbands
+        qgrid = build_device_grid(train, [0, n_users], [0, (n_items + 1) // 2, n_items])
+        bucket_qbands(qgrid, k)
     for mode in args.modes.split(","):
         model = DeviceModel(torch.from_numpy(P0).to(dev), torch.from_numpy(Q0).to(dev))
         traj = []
@@ -91,8 +96,11 @@ def netflix(args):
             for b in (0, 1):
                 lo, hi = grid.block_range(b)
                 seed = kernels.mix64(kernels.mix64(0, b, int(counts[b])), 0)
-                kernels.launch_sgd_range(model.P, model.Q, grid.users, grid.items, grid.ratings,
-                                         lo, hi, lr, reg, reg, seed, 0, 0, mode)
+                if mode == "qband":
+                    kernels.launch_block_qband(model.P, model.Q, qgrid, b, lr, reg, reg, seed)
+                else:
+                    kernels.launch_sgd_range(model.P, model.Q, grid.users, grid.items,
+                                             grid.ratings, lo, hi, lr, reg, reg, seed, 0, 0, mode)
                 counts[b] += 1
             traj.append(rmse(test, model).value)
         out[f"gpu_{mode}"] = traj
@@ -168,6 +176,7 @@ def main():
     ap.add_argument("--variants", default="0-7")
     ap.add_argument("--k", type=int, default=128)
     ap.add_argument("--precision", default="f32")
+    ap.add_argument("--kernel", default="hogwild")
     args = ap.parse_args()
     {"ml1m": ml1m, "netflix": netflix, "sweep": sweep}[args.what](args)
 

@@ -366,3 +366,90 @@ def test_ml1m_quality_within_0005_of_reference(dev):
         print(f"{key}: gpu {got[key]:.5f} reference {ref[key]['test_rmse']:.5f}")
     assert abs(got["e20"] - ref["e20"]["test_rmse"]) <= 0.005
     assert abs(got["e5"] - ref["e5"]["test_rmse"]) <= 0.005
+
+
+# ---------------------------------------------------------------------------
+# Q-band-stationary kernel
+# ---------------------------------------------------------------------------
+def _qband_grid(dev, m, k, col_cuts, target):
+    from paper_2006_15980_b200.data import DeviceTriples, bucket_qbands, build_device_grid
+    g = build_device_grid(DeviceTriples.from_host(m, dev), [0, m.n_users], col_cuts)
+    return bucket_qbands(g, k, target=target)
+
+
+@pytest.mark.parametrize("k", [32, 64, 128, 256])
+def test_qband_bucketing_contract(dev, k):
+    m = random_matrix(700, 900, 40_000, k)
+    g = _qband_grid(dev, m, k, [0, 450, 900], target=100)
+    items = g.items.cpu().numpy()
+    for b in range(g.n_blocks):
+        ptr = g.sub_ptr[b].cpu().numpy()
+        cuts = g.sub_cuts[b].cpu().numpy()
+        lo, hi = g.block_range(b)
+        assert ptr[0] == lo and ptr[-1] == hi
+        from paper_2006_15980_b200 import _lib
+        assert np.max(np.diff(cuts)) <= _lib.load().hmf_qband_max_items(k)
+        for s in range(len(cuts) - 1):
+            seg = items[ptr[s]:ptr[s + 1]]
+            assert np.all((seg >= cuts[s]) & (seg < cuts[s + 1]))
+
+
+@pytest.mark.parametrize("k", [32, 64, 128, 256])
+def test_qband_equals_sequential_per_item(dev, k):
+    """Distinct users, <= 128 triples per sub-band: every Q row is updated
+    sequentially in storage order by its owner warp and no P row is shared,
+    so the result equals a sequential f64 replay within fp32 rounding."""
+    from paper_2006_15980_b200 import kernels
+    rng = np.random.default_rng(k)
+    n_users, n_items, n = 4000, 300, 3000
+    users = rng.permutation(n_users)[:n].astype(np.int32)
+    items = rng.integers(0, n_items, n).astype(np.int32)
+    vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
+    from paper_2006_15980_b200.data import RatingMatrix
+    m = RatingMatrix(n_users, n_items, users, items, vals)
+    g = _qband_grid(dev, m, k, [0, n_items], target=n_items)  # one item per sub-band
+    P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
+    Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
+    P, Q = to_dev(P0, dev), to_dev(Q0, dev)
+    got = kernels.launch_block_qband(P, Q, g, 0, 0.05, 0.02, 0.03, 11)
+    assert got == n
+    # sequential replay in the bucketed storage order
+    Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
+    for u, v, r in zip(g.users.cpu().numpy(), g.items.cpu().numpy(),
+                       g.ratings.cpu().numpy().astype(np.float64)):
+        pu, qv = Pe[u].copy(), Qe[v].copy()
+        e = r - pu @ qv
+        Pe[u] = pu + 0.05 * (e * qv - 0.02 * pu)
+        Qe[v] = qv + 0.05 * (e * pu - 0.03 * qv)
+    assert rel_err(P.double().cpu().numpy(), Pe) < 1e-5
+    assert rel_err(Q.double().cpu().numpy(), Qe) < 1e-5
+
+
+def test_qband_ml1m_quality_within_0005_of_reference(dev):
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import (DeviceGrid, RatingMatrix, bucket_qbands, build_grid,
+                                            shuffle_triples, synthetic_ratings)
+    from paper_2006_15980_b200.sgd import DeviceModel, Hyperparams, init_model, rmse
+    ref = json.loads((GOLDEN / "training.json").read_text())
+    full = synthetic_ratings(6040, 3706, rank=8, density=1.05e6 / (6040 * 3706), noise=0.1, seed=0)
+    perm = np.random.default_rng(1).permutation(full.nnz)
+    n_test = full.nnz // 21
+    te, tr = perm[:n_test], perm[n_test:]
+    train = RatingMatrix(6040, 3706, full.users[tr], full.items[tr], full.ratings[tr])
+    test = RatingMatrix(6040, 3706, full.users[te], full.items[te], full.ratings[te])
+    hp = Hyperparams(n_factors=32, reg_user=0.01, reg_item=0.01, learning_rate=0.01)
+    grid = DeviceGrid.from_host(build_grid(shuffle_triples(train, 0), [0, 6040], [0, 1853, 3706]),
+                                dev)
+    bucket_qbands(grid, 32)
+    model = DeviceModel.from_host(init_model(6040, 3706, hp, 0), dev)
+    got = {}
+    for epoch in range(1, 21):
+        for b in (0, 1):
+            kernels.launch_block_qband(model.P, model.Q, grid, b, 0.01, 0.01, 0.01,
+                                       kernels.mix64(0, b, epoch))
+        if epoch in (1, 5, 20):
+            got[f"e{epoch}"] = rmse(test, model).value
+    for key in ("e1", "e5", "e20"):
+        print(f"{key}: gpu qband {got[key]:.5f} reference {ref[key]['test_rmse']:.5f}")
+    assert abs(got["e20"] - ref["e20"]["test_rmse"]) <= 0.005
+    assert abs(got["e5"] - ref["e5"]["test_rmse"]) <= 0.005
