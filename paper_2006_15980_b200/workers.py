@@ -1,0 +1,538 @@
+"""Batch workers on B200: the reference's accelerator seam, real.
+
+Mirrors hetmf/workers.py's batch half (workers.py:45-369, 408-514):
+BatchWorkerConfig, block_order_seed, BatchEngine (stage_rows / flush_rows /
+stage_in / stage_in_async / stage_out / compute / close, `resident`,
+`staged`), BatchWorker (lease loop with P-band residency and a staged-ahead
+unit), time_batch_prefixes and throughput_sweep.  The reference emulates the
+GPU with sleeps and CPU lanes; here:
+
+* factors live in HBM.  A FactorStore shared by the engines of one run keeps a
+  full-size replica of P and Q per device and records, per user and per
+  item, which device holds the freshest copy and the CUDA event that
+  completes it.  Staging a band brings it from that home: nothing if it is
+  already local, a peer copy over NVLink (cudaMemcpyPeerAsync on the copy
+  stream) from another GPU, or an H2D copy from the host model.  The copy is
+  ordered before compute by a stream wait on the home's event — no host
+  round trip.  stage_out / flush_rows only move the home; the host model is
+  refreshed at barriers and at the end (FactorStore.sync_host), invisible to
+  callers that read the model afterwards (SURVEY §7 hard part 6);
+* triples are resident too: each device keeps one block-major copy of the
+  grid (f32 ratings), Q-band sub-bucketed for the shared-memory kernel;
+* compute launches one kernel per sub-block with the reference's seeds
+  (block_order_seed(unit_seed, i), workers.py:77-83 / 234-237).  Lanes are a
+  CPU notion: `lanes`, `launch_overhead` and `bandwidth` are accepted and
+  ignored.  `mode="exact"` runs the reference's visit order and arithmetic, so
+  a CUDA batch worker equals a reference stream worker bit for bit over the
+  same lease sequence (the reference's own degenerate-equivalence property,
+  workers.py:19-21);
+* stage methods return CUDA-event-timed seconds, which calibration fits.
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib, kernels
+from .data import BlockGrid, DeviceGrid, bucket_qbands
+from .scheduler import CLASS_BATCH, GridScheduler, Unit
+from .sgd import FactorModel, Hyperparams, init_model
+
+TRIPLE_BYTES = 12  # int32 row + int32 col + f32 rating on device (the reference: 16)
+HOST = -1
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class BatchWorkerConfig:
+    """workers.py:45-58, plus the B200 knobs."""
+
+    lanes: int = 4                  # accepted for compatibility; no CPU lanes on B200
+    launch_overhead: float = 0.002  # accepted; the real overhead is measured
+    bandwidth: float = 4e9          # accepted; the real copies are measured
+    pipeline_depth: int = 3
+    device: int | None = None       # CUDA device index (None: current device)
+    precision: str = "f32"          # factor storage on device: f32 | f16 | f64
+    kernel: str = "qband"           # qband (Q band in shared memory) | range (hmf_sgd_range)
+    mode: str = "hogwild"           # for kernel="range": hogwild | hogwild_lww | ordered | exact
+
+    def validate(self) -> None:
+        if self.lanes < 1:
+            raise ValueError("lanes must be >= 1")
+        if self.launch_overhead < 0:
+            raise ValueError("launch_overhead must be >= 0")
+        if self.bandwidth <= 0:
+            raise ValueError("bandwidth must be > 0")
+        if self.precision not in ("f32", "f16", "f64"):
+            raise ValueError(f"unknown precision {self.precision!r}")
+        if self.kernel not in ("qband", "range"):
+            raise ValueError(f"unknown kernel {self.kernel!r}")
+        if self.mode not in _lib.MODES:
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if self.kernel == "qband" and self.precision == "f64":
+            raise ValueError("the Q-band kernel stores f32 or f16 factors")
+
+    def device_name(self) -> str:
+        torch = _torch()
+        d = torch.cuda.current_device() if self.device is None else self.device
+        return torch.cuda.get_device_name(d).replace(" ", "_")
+
+
+def block_order_seed(unit_seed: int, index: int) -> int:
+    """Visit-order seed of sub-block `index` of a unit (workers.py:77-83)."""
+    return kernels.mix64(unit_seed, index)
+
+
+_DTYPES = {"f32": "float32", "f16": "float16", "f64": "float64"}
+
+
+class FactorStore:
+    """Per-device factor replicas and the home of every user / item row.
+
+    home_p[u] / home_q[v] is HOST or the device index holding the freshest
+    copy; ready_* maps a device to the CUDA event after which its copy is
+    complete.  All methods are called with the band leased to the caller, so
+    the rows they touch are not moving concurrently (the lease protocol's
+    conflict freedom); the lock only guards the bookkeeping itself.
+    """
+
+    def __init__(self, model: FactorModel, precision: str = "f32", grid=None):
+        self.model = model
+        self.precision = precision
+        self.k = model.n_factors
+        self.home_p = np.full(model.n_users, HOST, dtype=np.int16)
+        self.home_q = np.full(model.n_items, HOST, dtype=np.int16)
+        self.replicas: dict[int, tuple] = {}
+        self.events: dict[int, object] = {}
+        self.grids: dict[int, DeviceGrid] = {}
+        self.host_grid = grid
+        self.copy_streams: dict[int, object] = {}
+        self.lock = threading.RLock()
+
+    # -- device resources -----------------------------------------------------
+    def replica(self, dev: int):
+        torch = _torch()
+        with self.lock:
+            if dev not in self.replicas:
+                dt = getattr(torch, _DTYPES[self.precision])
+                d = torch.device("cuda", dev)
+                self.replicas[dev] = (torch.empty((self.model.n_users, self.k), dtype=dt, device=d),
+                                      torch.empty((self.model.n_items, self.k), dtype=dt, device=d))
+                self.copy_streams[dev] = torch.cuda.Stream(device=d)
+            return self.replicas[dev]
+
+    def copy_stream(self, dev: int):
+        self.replica(dev)
+        return self.copy_streams[dev]
+
+    def device_grid(self, dev: int, grid: BlockGrid, kernel: str) -> DeviceGrid:
+        torch = _torch()
+        with self.lock:
+            g = self.grids.get(dev)
+            if g is None or self.host_grid is not grid:
+                rd = "float64" if self.precision == "f64" else "float32"
+                with torch.cuda.device(dev):
+                    g = DeviceGrid.from_host(grid, torch.device("cuda", dev), rd)
+                    if kernel == "qband":
+                        bucket_qbands(g, self.k)
+                self.grids[dev] = g
+                self.host_grid = grid
+            return g
+
+    # -- moving rows to a device ------------------------------------------------
+    def _runs(self, home: np.ndarray, lo: int, hi: int):
+        """Maximal [a, b) runs of equal home inside [lo, hi)."""
+        seg = home[lo:hi]
+        if len(seg) == 0:
+            return []
+        edges = np.flatnonzero(np.diff(seg)) + 1
+        starts = np.concatenate([[0], edges])
+        ends = np.concatenate([edges, [len(seg)]])
+        return [(lo + int(a), lo + int(b), int(seg[a])) for a, b in zip(starts, ends)]
+
+    def bring(self, which: str, dev: int, lo: int, hi: int, stream) -> int:
+        """Make rows [lo, hi) of P ('p') or Q ('q') fresh on `dev`, enqueued on
+        `stream`; returns bytes moved."""
+        torch = _torch()
+        P, Q = self.replica(dev)
+        dst = P if which == "p" else Q
+        home = self.home_p if which == "p" else self.home_q
+        host = self.model.user_factors if which == "p" else self.model.item_factors
+        moved = 0
+        with self.lock:
+            runs = self._runs(home, lo, hi)
+        for a, b, h in runs:
+            if h == dev:
+                continue
+            with torch.cuda.stream(stream):
+                if h == HOST:
+                    src = torch.from_numpy(np.ascontiguousarray(host[a:b]))
+                    dst[a:b].copy_(src.to(dst.dtype), non_blocking=False)
+                else:
+                    ev = self.events.get(h)
+                    if ev is not None:
+                        stream.wait_event(ev)
+                    sp, sq = self.replicas[h]
+                    src = sp if which == "p" else sq
+                    _lib.check(_lib.load().hmf_memcpy_peer_async(
+                        dst[a:b].data_ptr(), dev, src[a:b].data_ptr(), h,
+                        (b - a) * self.k * dst.element_size(), stream.cuda_stream),
+                        "hmf_memcpy_peer_async")
+            moved += (b - a) * self.k * dst.element_size()
+            with self.lock:
+                home[a:b] = dev
+        return moved
+
+    def claim(self, which: str, dev: int, lo: int, hi: int, event) -> None:
+        """Record that `dev` holds the freshest rows [lo, hi), complete at `event`."""
+        with self.lock:
+            (self.home_p if which == "p" else self.home_q)[lo:hi] = dev
+            self.events[dev] = event
+
+    def sync_host(self) -> None:
+        """Copy every device-homed row back into the host model (f64)."""
+        torch = _torch()
+        for which in ("p", "q"):
+            home = self.home_p if which == "p" else self.home_q
+            host = self.model.user_factors if which == "p" else self.model.item_factors
+            with self.lock:
+                runs = self._runs(home, 0, len(home))
+            for a, b, h in runs:
+                if h == HOST:
+                    continue
+                torch.cuda.synchronize(h)
+                src = self.replicas[h][0 if which == "p" else 1]
+                host[a:b] = src[a:b].to(torch.float64).cpu().numpy()
+
+    def gather_on(self, dev: int):
+        """Bring every row to `dev` (for metrics at a barrier); returns (P, Q)."""
+        torch = _torch()
+        s = self.copy_stream(dev)
+        self.bring("p", dev, 0, self.model.n_users, s)
+        self.bring("q", dev, 0, self.model.n_items, s)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        return self.replicas[dev]
+
+
+class StagedBlock:
+    """A staged unit: its device grid, item span and sub-block count."""
+
+    __slots__ = ("unit", "grid", "col_lo", "col_hi", "offsets", "items")
+
+    def __init__(self, unit, grid, col_lo, col_hi, offsets, items=None):
+        self.unit = unit
+        self.grid = grid
+        self.col_lo = col_lo
+        self.col_hi = col_hi
+        self.offsets = offsets
+        self.items = items
+
+
+class BatchEngine:
+    """CUDA batch engine with the reference's method surface (workers.py:144-266)."""
+
+    def __init__(self, config: BatchWorkerConfig, model: FactorModel, hparams: Hyperparams,
+                 store: FactorStore | None = None):
+        torch = _torch()
+        config.validate()
+        _lib.load()
+        if not torch.cuda.is_available():
+            raise _lib.HmfError("no CUDA device: the B200 engine has no CPU fallback")
+        self.config = config
+        self.model = model
+        self.hparams = hparams
+        self.dev = torch.cuda.current_device() if config.device is None else int(config.device)
+        self.store = store if store is not None else FactorStore(model, config.precision)
+        self.stream = torch.cuda.Stream(device=torch.device("cuda", self.dev))
+        self.resident = None
+        self.staged: dict = {}
+        self._owns_store = store is None
+
+    def close(self):
+        if self._owns_store:
+            self.store.sync_host()
+
+    def _timed(self, fn, stream):
+        torch = _torch()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.device(self.dev):
+            e0.record(stream)
+            out = fn()
+            e1.record(stream)
+            e1.synchronize()
+        return out, e0.elapsed_time(e1) / 1e3
+
+    # -- staging ---------------------------------------------------------------
+    def stage_rows(self, row_lo: int, row_hi: int) -> float:
+        """Make a P band resident on this GPU (from host or a peer)."""
+        _, secs = self._timed(lambda: self.store.bring("p", self.dev, row_lo, row_hi, self.stream),
+                              self.stream)
+        P, _ = self.store.replica(self.dev)
+        self.resident = (row_lo, row_hi, P[row_lo:row_hi])
+        return secs
+
+    def flush_rows(self) -> float:
+        """Release the resident band: its home stays on this GPU; the host
+        copy is refreshed at barriers / close (sync_host)."""
+        if self.resident is None:
+            return 0.0
+        torch = _torch()
+        lo, hi, _ = self.resident
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        self.store.claim("p", self.dev, lo, hi, ev)
+        if self._owns_store:
+            self.store.sync_host()
+        self.resident = None
+        return 0.0
+
+    def _stage(self, key, grid, unit: Unit, stream) -> int:
+        g = self.store.device_grid(self.dev, grid, self.config.kernel)
+        col_lo, col_hi = grid.col_span(unit.col)
+        moved = self.store.bring("q", self.dev, col_lo, col_hi, stream)
+        spans = [grid.block_range(b) for b in unit.blocks]
+        offsets = np.concatenate([[0], np.cumsum([hi - lo for lo, hi in spans])])
+        _, Q = self.store.replica(self.dev)
+        self.staged[key] = StagedBlock(unit, g, col_lo, col_hi, offsets, Q[col_lo:col_hi])
+        return moved
+
+    def stage_in(self, key, grid, unit: Unit) -> float:
+        """Stage a unit: device triples (resident) plus its Q band."""
+        _, secs = self._timed(lambda: self._stage(key, grid, unit, self.stream), self.stream)
+        return secs
+
+    def stage_in_async(self, key, grid, unit: Unit):
+        """Stage on the copy stream; the returned join makes compute wait for it."""
+        torch = _torch()
+        cs = self.store.copy_stream(self.dev)
+        self._stage(key, grid, unit, cs)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+
+        def join():
+            self.stream.wait_event(ev)
+        return join
+
+    def stage_out(self, key) -> float:
+        """The Q band stays here; record the home (the host copy is refreshed
+        at barriers / close)."""
+        torch = _torch()
+        st = self.staged.pop(key)
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        self.store.claim("q", self.dev, st.col_lo, st.col_hi, ev)
+        if self._owns_store:
+            self.store.sync_host()
+        return 0.0
+
+    # -- compute ---------------------------------------------------------------
+    def compute(self, key, unit_seed: int) -> int:
+        """Run every staged block once, sub-blocks in order with the
+        reference's seeds (workers.py:222-255)."""
+        st = self.staged[key]
+        hp = self.hparams
+        P, Q = self.store.replica(self.dev)
+        g = st.grid
+        done = 0
+        for i, b in enumerate(st.unit.blocks):
+            seed = block_order_seed(unit_seed, i)
+            if self.config.kernel == "qband":
+                done += kernels.launch_block_qband(P, Q, g, b, hp.learning_rate, hp.reg_user,
+                                                   hp.reg_item, seed,
+                                                   stream=self.stream.cuda_stream)
+            else:
+                lo, hi = g.block_range(b)
+                done += kernels.launch_sgd_range(P, Q, g.users, g.items, g.ratings, lo, hi,
+                                                 hp.learning_rate, hp.reg_user, hp.reg_item, seed,
+                                                 0, 0, self.config.mode, self.stream.cuda_stream)
+        return done
+
+    def synchronize(self) -> None:
+        self.stream.synchronize()
+
+
+class BatchWorker(threading.Thread):
+    """Lease loop of one GPU (workers.py:305-369)."""
+
+    def __init__(self, worker_id: int, scheduler: GridScheduler, model: FactorModel,
+                 grid: BlockGrid, hparams: Hyperparams, config: BatchWorkerConfig,
+                 store: FactorStore | None = None):
+        super().__init__(name=f"batch-{worker_id}", daemon=True)
+        self.worker_id = worker_id
+        self.scheduler = scheduler
+        self.grid = grid
+        self.config = config
+        self.engine = None
+        self._model, self._hp, self._store = model, hparams, store
+        self.blocks_done = 0
+        self.error = None
+        self.kernel_seconds = 0.0
+
+    def _row_span(self, unit: Unit):
+        return self.grid.row_span(unit.rows[0])[0], self.grid.row_span(unit.rows[-1])[1]
+
+    def _ensure_resident(self, unit: Unit) -> None:
+        span = self._row_span(unit)
+        if self.engine.resident is None or self.engine.resident[:2] != span:
+            self.engine.flush_rows()
+            self.engine.stage_rows(*span)
+
+    def run(self):
+        torch = _torch()
+        try:
+            dev = self.config.device if self.config.device is not None else 0
+            torch.cuda.set_device(dev)
+            self.engine = BatchEngine(self.config, self._model, self._hp, self._store)
+            engine = self.engine
+            lease = self.scheduler.acquire(self.worker_id, CLASS_BATCH)
+            if lease is None:
+                return
+            self._ensure_resident(lease.unit)
+            engine.stage_in(id(lease.unit), self.grid, lease.unit)
+            while True:
+                unit = lease.unit
+                join = None
+                if lease.prefetch is not None and id(lease.prefetch) not in engine.staged:
+                    join = engine.stage_in_async(id(lease.prefetch), self.grid, lease.prefetch)
+                done = engine.compute(id(unit), unit.order_seed)
+                if join is not None:
+                    join()
+                engine.stage_out(id(unit))
+                self.blocks_done += len(unit.blocks)
+                if lease.prefetch is None:
+                    engine.flush_rows()
+                # the next owner of this unit's bands must see finished data:
+                # homes carry the completion event, so only the lease release
+                # (host bookkeeping) waits for the kernel here
+                engine.synchronize()
+                nxt = self.scheduler.release(lease, done)
+                if nxt is None:
+                    engine.staged.clear()
+                    nxt = self.scheduler.acquire(self.worker_id, CLASS_BATCH)
+                    if nxt is None:
+                        break
+                self._ensure_resident(nxt.unit)
+                if id(nxt.unit) not in engine.staged:
+                    engine.stage_in(id(nxt.unit), self.grid, nxt.unit)
+                lease = nxt
+        except BaseException as exc:  # re-raised by the driver (engine.py)
+            self.error = exc
+            self.scheduler.abort("worker error")
+        finally:
+            if self.engine is not None:
+                try:
+                    self.engine.flush_rows()
+                    self.engine.synchronize()
+                finally:
+                    self.engine.close()
+
+
+# -- calibration / benchmarking helpers ----------------------------------------
+
+
+class _PrefixWork:
+    """A triple prefix as a one-block grid (workers.py:396-405)."""
+
+    def __init__(self, matrix, size):
+        from .data import RatingMatrix, build_grid
+        sub = RatingMatrix(matrix.n_users, matrix.n_items, matrix.users[:size],
+                           matrix.items[:size], matrix.ratings[:size])
+        self.grid = build_grid(sub, [0, matrix.n_users], [0, matrix.n_items])
+        self.unit = Unit(blocks=(0,), rows=(0,), col=0, size=size)
+
+
+def time_batch_prefixes(matrix, prefixes, repeats, hparams: Hyperparams,
+                        config: BatchWorkerConfig, seed: int):
+    """Per-stage mean seconds of the CUDA engine on each prefix
+    (workers.py:408-444): transfer_in = stage_rows + stage_in (H2D of P, Q
+    band and triples), kernel = compute, transfer_out = stage_out + flush_rows
+    + the D2H write-back; CUDA events, stages timed separately."""
+    torch = _torch()
+    out = {"transfer_in": [], "kernel": [], "transfer_out": []}
+    for size in prefixes:
+        work = _PrefixWork(matrix, size)
+        t_in = t_k = t_out = 0.0
+        for rep in range(repeats):
+            model = init_model(matrix.n_users, matrix.n_items, hparams,
+                               kernels.mix64(seed, size, rep, 2))
+            store = FactorStore(model, config.precision)
+            eng = BatchEngine(config, model, hparams, store)
+            t0 = time.perf_counter()
+            eng.stage_rows(0, matrix.n_users)
+            eng.stage_in("cal", work.grid, work.unit)
+            torch.cuda.synchronize(eng.dev)
+            t_in += time.perf_counter() - t0
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(eng.stream)
+            eng.compute("cal", kernels.mix64(seed, size, rep, 3))
+            e1.record(eng.stream)
+            e1.synchronize()
+            t_k += e0.elapsed_time(e1) / 1e3
+            t0 = time.perf_counter()
+            eng.stage_out("cal")
+            eng.flush_rows()
+            store.sync_host()
+            t_out += time.perf_counter() - t0
+        out["transfer_in"].append(t_in / repeats)
+        out["kernel"].append(t_k / repeats)
+        out["transfer_out"].append(t_out / repeats)
+    return out
+
+
+def throughput_sweep(worker_class: str, sizes, repeats: int = 3, *,
+                     hparams: Hyperparams | None = None,
+                     batch_config: BatchWorkerConfig | None = None, n_rows: int = 4096,
+                     n_cols: int = 4096, seed: int = 0):
+    """Elements/second per workload size of the CUDA batch worker
+    (workers.py:447-514, batch branch); the fastest of `repeats`."""
+    from .data import RatingMatrix
+    if list(sizes) != sorted(sizes):
+        raise ValueError("sizes must be ascending")
+    if worker_class != CLASS_BATCH:
+        raise ValueError("the B200 engine provides batch workers only; stream workers are "
+                         "the reference's CPU path")
+    if batch_config is None:
+        raise ValueError("batch sweeps need a BatchWorkerConfig")
+    hparams = hparams or Hyperparams()
+    torch = _torch()
+    rng = np.random.default_rng(seed)
+    res = []
+    for size in sizes:
+        m = RatingMatrix(n_rows, n_cols, rng.integers(0, n_rows, size=size).astype(np.int32),
+                         rng.integers(0, n_cols, size=size).astype(np.int32),
+                         rng.normal(size=size))
+        work = _PrefixWork(m, size)
+        best = None
+        for rep in range(repeats):
+            model = init_model(n_rows, n_cols, hparams, kernels.mix64(seed, size, rep, 4))
+            eng = BatchEngine(batch_config, model, hparams, FactorStore(model, batch_config.precision))
+            t0 = time.perf_counter()
+            t_in = eng.stage_rows(0, n_rows) + eng.stage_in("s", work.grid, work.unit)
+            t1 = time.perf_counter()
+            eng.compute("s", kernels.mix64(rep, size, 5))
+            eng.synchronize()
+            t_kernel = time.perf_counter() - t1
+            t2 = time.perf_counter()
+            eng.stage_out("s")
+            eng.flush_rows()
+            eng.store.sync_host()
+            t_out = time.perf_counter() - t2
+            total = time.perf_counter() - t0
+            entry = {"size": size, "seconds": total, "elements_per_second": size / total,
+                     "stage_in_seconds": t_in, "kernel_seconds": t_kernel,
+                     "stage_out_seconds": t_out}
+            if best is None or total < best["seconds"]:
+                best = entry
+        res.append(best)
+    torch.cuda.synchronize()
+    return res

@@ -1,0 +1,140 @@
+"""The CUDA batch engine behind the reference's seams (workers / engine),
+modelled on the reference's tests/test_workers.py and test_acceptance.py."""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, random_matrix
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return 0
+
+
+def test_staging_round_trip_leaves_factors_unchanged(dev):
+    """workers.py stage_rows/stage_in/stage_out/flush_rows, f64 storage."""
+    from paper_2006_15980_b200.data import build_grid
+    from paper_2006_15980_b200.scheduler import Unit
+    from paper_2006_15980_b200.sgd import Hyperparams, init_model
+    from paper_2006_15980_b200.workers import BatchEngine, BatchWorkerConfig
+    m = random_matrix(20, 20, 133, 3)
+    grid = build_grid(m, [0, 20], [0, 20])
+    hp = Hyperparams(n_factors=4)
+    model = init_model(20, 20, hp, 3)
+    before = model.copy()
+    eng = BatchEngine(BatchWorkerConfig(device=dev, precision="f64", kernel="range"), model, hp)
+    assert eng.stage_rows(0, 20) >= 0
+    assert eng.stage_in("k", grid, Unit(blocks=(0,), rows=(0,), col=0)) >= 0
+    eng.stage_out("k")
+    eng.flush_rows()
+    eng.close()
+    assert np.array_equal(model.user_factors, before.user_factors)
+    assert np.array_equal(model.item_factors, before.item_factors)
+
+
+def test_batch_worker_exact_equals_reference_stream_replay(dev):
+    """A CUDA batch worker in EXACT mode over a real lease sequence equals the
+    reference algorithm replayed serially over the same leases, bit for bit
+    (reference tests/test_workers.py:43-70 and 155-183)."""
+    import oracle
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import build_grid
+    from paper_2006_15980_b200.scheduler import CLASS_BATCH, POLICY_QUOTA, GridScheduler
+    from paper_2006_15980_b200.sgd import Hyperparams, init_model
+    from paper_2006_15980_b200.workers import BatchWorker, BatchWorkerConfig, FactorStore
+    m = random_matrix(48, 48, 48 * 48 // 3, 7)
+    grid = build_grid(m, [0, 24, 48], [0, 16, 32, 48])
+    hp = Hyperparams(n_factors=4, reg_user=0.01, reg_item=0.01, learning_rate=0.02)
+    model = init_model(48, 48, hp, 7)
+    start = model.copy()
+    store = FactorStore(model, "f64", grid)
+    sched = GridScheduler(grid, POLICY_QUOTA, max_epochs=3, seed=7, trace=True)
+    cfg = BatchWorkerConfig(device=dev, precision="f64", kernel="range", mode="exact")
+    w = BatchWorker(0, sched, model, grid, hp, cfg, store)
+    w.start()
+    w.join(timeout=120)
+    assert w.error is None and sched.epoch == 3
+    store.sync_host()
+    P, Q = start.user_factors.copy(), start.item_factors.copy()
+    counts = np.zeros(grid.n_blocks, dtype=np.int64)
+    for ev in sched.trace:
+        b = ev.block
+        unit_seed = kernels.mix64(7, b, int(counts[b]))
+        lo, hi = grid.block_range(b)
+        oracle.sgd_range(P, Q, grid.users, grid.items, grid.ratings, lo, hi, 0.02, 0.01, 0.01,
+                         kernels.mix64(unit_seed, 0), 0, 0)
+        counts[b] += 1
+    assert np.array_equal(model.user_factors, P)
+    assert np.array_equal(model.item_factors, Q)
+
+
+def test_run_training_ml1m_quality(dev):
+    """run_training (batch-only, 1 GPU, Q-band kernel) on the ML-1M-shaped
+    instance: test RMSE within 0.005 of the reference's after 20 epochs, the
+    per-epoch metrics on device, and every block updated once per epoch."""
+    from paper_2006_15980_b200.data import RatingMatrix, synthetic_ratings
+    from paper_2006_15980_b200.engine import RunConfig, run_training
+    ref = json.loads((GOLDEN / "training.json").read_text())
+    full = synthetic_ratings(6040, 3706, rank=8, density=1.05e6 / (6040 * 3706), noise=0.1, seed=0)
+    perm = np.random.default_rng(1).permutation(full.nnz)
+    n_test = full.nnz // 21
+    te, tr = perm[:n_test], perm[n_test:]
+    train = RatingMatrix(6040, 3706, full.users[tr], full.items[tr], full.ratings[tr])
+    test = RatingMatrix(6040, 3706, full.users[te], full.items[te], full.ratings[te])
+    cfg = RunConfig(n_factors=32, learning_rate=0.01, reg_user=0.01, reg_item=0.01, epochs=20,
+                    seed=0, n_batch=1, devices=(dev,))
+    res = run_training(cfg, matrix=train, testset=test)
+    assert res.epochs_run == 20 and len(res.metrics) == 20
+    assert np.all(res.scheduler.counts == 20)
+    assert res.scheduler.total_updates == 20 * train.nnz
+    print("gpu", [round(r.test_rmse, 5) for r in res.metrics][:5], res.test_report.value,
+          "reference", ref["e20"]["test_rmse"])
+    assert abs(res.test_report.value - ref["e20"]["test_rmse"]) <= 0.005
+    assert abs(res.metrics[4].test_rmse - ref["e5"]["test_rmse"]) <= 0.005
+    assert res.metrics[-1].train_loss < res.metrics[0].train_loss
+    assert res.model.all_finite()
+
+
+def test_run_training_rejects_cpu_schedules():
+    from paper_2006_15980_b200.engine import ConfigError, RunConfig
+    with pytest.raises(ConfigError):
+        RunConfig(schedule="stream-only", n_stream=2, synthetic=True).validate()
+    with pytest.raises(ConfigError):
+        RunConfig(schedule="hsgd-star", division="nonuniform", n_stream=2, n_batch=1,
+                  synthetic=True).validate()
+
+
+def test_gpu_calibration_fits_profile(dev, tmp_path):
+    from paper_2006_15980_b200.costmodel import (DeviceTopology, calibrate_gpu, load_profile,
+                                                 save_profile)
+    from paper_2006_15980_b200.data import shuffle_triples, synthetic_ratings
+    from paper_2006_15980_b200.sgd import Hyperparams
+    from paper_2006_15980_b200.workers import BatchWorkerConfig
+    m = shuffle_triples(synthetic_ratings(2000, 1500, rank=8, density=0.1, seed=1), 1)
+    prof = calibrate_gpu(m, Hyperparams(n_factors=32), BatchWorkerConfig(device=dev),
+                         DeviceTopology(0, 1), segments=8, repeats=3)
+    for stage in (prof.transfer_in, prof.kernel, prof.transfer_out):
+        assert stage.eval(m.nnz) > 0
+    save_profile(tmp_path / "prof.txt", prof)
+    assert load_profile(tmp_path / "prof.txt").kernel == prof.kernel
+
+
+def test_throughput_sweep_reports_stages(dev):
+    from paper_2006_15980_b200.sgd import Hyperparams
+    from paper_2006_15980_b200.workers import BatchWorkerConfig, throughput_sweep
+    out = throughput_sweep("batch", [10_000, 400_000], repeats=2, hparams=Hyperparams(n_factors=32),
+                           batch_config=BatchWorkerConfig(device=dev), n_rows=2048, n_cols=2048)
+    assert [r["size"] for r in out] == [10_000, 400_000]
+    for r in out:
+        assert r["kernel_seconds"] > 0 and r["stage_in_seconds"] > 0
+        assert r["seconds"] >= r["kernel_seconds"]
+    with pytest.raises(ValueError):
+        throughput_sweep("batch", [2, 1], batch_config=BatchWorkerConfig(device=dev))
