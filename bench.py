@@ -130,11 +130,21 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
+        n_dev = torch.cuda.device_count()
+        local = local % n_dev            # several ranks may share a GPU (testing)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world <= n_dev:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
+
+
+def _reduce_device():
+    import torch.distributed as dist
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
 
 
 def barrier(world):
@@ -148,7 +158,7 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_reduce_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -158,7 +168,7 @@ def sum_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_reduce_device())
     dist.all_reduce(t)
     return float(t.item())
 
@@ -378,6 +388,78 @@ def run_ours(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def run_ours_multi(args, world, rank, local):
+    """N > 1: one process per GPU, weak scaling.  Every rank owns a Netflix-
+    shaped row band (480 000 users, 100 M training ratings) of one matrix with
+    shared items (17 700); Q column bands (2N+1) move between GPUs through the
+    lease table (distributed.LeaseTable) and CUDA IPC peer pulls; P bands stay
+    resident.  A step is one quota epoch of every GPU's blocks + a barrier."""
+    import torch
+    import torch.distributed as dist
+    from paper_2006_15980_b200 import _lib
+    from paper_2006_15980_b200.data import split_device, synthetic_device
+    from paper_2006_15980_b200.distributed import CudaRowBand, LeaseTable, RowBandTrainer
+    from paper_2006_15980_b200.sgd import DeviceModel, residual_sums
+
+    _lib.load()
+    dev = torch.device("cuda", local)
+    n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
+    k = args.k or k0
+    n_total = int(round(n_train / (1.0 - TEST_FRACTION)))
+    trip = synthetic_device(n_users, n_items, n_total, rank=8, noise=0.1, seed=SEED + rank,
+                            device=dev)
+    row_lo, row_hi = rank * n_users, (rank + 1) * n_users
+    trip.users += row_lo                       # global user ids of this rank's band
+    train, test = split_device(trip, TEST_FRACTION)
+    n_cols = 2 * world + 1
+    col_cuts = np.linspace(0, n_items, n_cols + 1).astype(np.int64)
+    band = CudaRowBand(dist, rank, world, dev, train, row_lo, row_hi, col_cuts, k, LR, REG, REG,
+                       init_seed=SEED, kernel=args.multi_kernel)
+    table = LeaseTable(dist.distributed_c10d._get_default_store(), n_cols, rank,
+                       f"bench{os.getpid() if world == 1 else 0}")
+    if rank == 0:
+        table.initialize()
+    dist.barrier()
+    trainer = RowBandTrainer(band, table, rank, seed=SEED)
+    for _ in range(args.warmup):
+        trainer.run_epoch()
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    upd0 = trainer.total_updates
+    with ClockSampler(local) as clocks:
+        e0.record(band.stream)
+        for _ in range(args.steps):
+            trainer.run_epoch()
+            dist.barrier()
+        e1.record(band.stream)
+        torch.cuda.synchronize(dev)
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    updates = sum_over_ranks(float(trainer.total_updates - upd0), world)
+    band.refresh_q(table)
+    sums = residual_sums(DeviceModel(band.P, band.Q), test.users, test.items, test.ratings,
+                         row_base=row_lo).to(_reduce_device())
+    dist.all_reduce(sums)
+    n_test = sum_over_ranks(float(test.nnz), world)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "sgd_updates_per_sec", "value": updates / (ms / 1e3), "unit": "updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (synthetic_ratings law, device generator)",
+            "config": {"workload": f"{desc} row band per GPU (weak scaling), k={k}",
+                       "grid": f"{world} row bands x {n_cols} column bands",
+                       "parallelism": f"dp{world} row bands, Q bands leased and pulled peer-to-peer",
+                       "kernel": band.kernel, "lr": LR, "reg": REG},
+            "rmse": {"epochs": args.warmup + args.steps,
+                     "test": float(np.sqrt(sums[0].item() / n_test))},
+            "lease_wait_seconds_rank0": trainer.wait_seconds,
+            "gpu_launches": None, "clocks": clocks.summary(), "e2e": None,
+        }), flush=True)
+
+
 def run_e2e(args, grid, model, k, precision, dev, world):
     """Same metric through the reference-facing host-buffer call."""
     import torch
@@ -431,6 +513,7 @@ def main():
     ap.add_argument("--kernel", choices=["qband", "hogwild"], default="qband",
                     help="qband: Q band in shared memory (engine fast path); hogwild: "
                          "global-Q kernel behind hmf_sgd_range")
+    ap.add_argument("--multi-kernel", choices=["auto", "qband", "range"], default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -442,7 +525,10 @@ def main():
         run_reference_arm(args, world, rank)
         return
     world, rank, local = dist_setup()
-    run_ours(args, world, rank, local)
+    if world > 1:
+        run_ours_multi(args, world, rank, local)
+    else:
+        run_ours(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

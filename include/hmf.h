@@ -190,8 +190,9 @@ int hmf_enable_peer_access(int32_t dev, int32_t peer);
 int hmf_memcpy_peer_async(void* dst, int32_t dst_dev, const void* src, int32_t src_dev,
                           int64_t bytes, void* stream);
 int hmf_stream_synchronize(void* stream);
-/* CUDA IPC: 64-byte handle of a device allocation, opened in another process. */
-int hmf_ipc_get_handle(const void* dptr, uint8_t* handle64);
+/* CUDA IPC: 64-byte handle of the allocation holding dptr (and dptr's byte
+ * offset inside it), to be opened in another process of the same node. */
+int hmf_ipc_get_handle(const void* dptr, uint8_t* handle64, int64_t* offset);
 int hmf_ipc_open_handle(const uint8_t* handle64, void** dptr);
 int hmf_ipc_close_handle(void* dptr);
 

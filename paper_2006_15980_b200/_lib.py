@@ -67,7 +67,7 @@ SIGNATURES = {
     "hmf_enable_peer_access": (C.c_int, [_i32, _i32]),
     "hmf_memcpy_peer_async": (C.c_int, [_p, _i32, _p, _i32, _i64, _p]),
     "hmf_stream_synchronize": (C.c_int, [_p]),
-    "hmf_ipc_get_handle": (C.c_int, [_p, C.POINTER(C.c_uint8)]),
+    "hmf_ipc_get_handle": (C.c_int, [_p, C.POINTER(C.c_uint8), C.POINTER(_i64)]),
     "hmf_ipc_open_handle": (C.c_int, [C.POINTER(C.c_uint8), C.POINTER(_p)]),
     "hmf_ipc_close_handle": (C.c_int, [_p]),
 }

@@ -179,8 +179,14 @@ int hmf_memcpy_peer_async(void* dst, int32_t dst_dev, const void* src, int32_t s
                           int64_t bytes, void* stream) {
   if (bytes < 0) return int(hmf::set_error(HMF_ERR_ARG, "negative byte count"));
   if (bytes == 0) return HMF_OK;
-  cudaError_t e = cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, size_t(bytes),
-                                      static_cast<cudaStream_t>(stream));
+  // a negative device means "locate by unified address" (e.g. an IPC-mapped
+  // peer allocation): the driver routes the copy over NVLink
+  cudaError_t e =
+      (dst_dev < 0 || src_dev < 0)
+          ? cudaMemcpyAsync(dst, src, size_t(bytes), cudaMemcpyDefault,
+                            static_cast<cudaStream_t>(stream))
+          : cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, size_t(bytes),
+                                static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? HMF_OK : int(hmf::set_cuda_error(e));
 }
 
@@ -189,12 +195,31 @@ int hmf_stream_synchronize(void* stream) {
   return e == cudaSuccess ? HMF_OK : int(hmf::set_cuda_error(e));
 }
 
-int hmf_ipc_get_handle(const void* dptr, uint8_t* handle64) {
+// IPC handles name whole allocations; a pointer from a caching allocator may
+// sit inside one.  The allocation base comes from the driver's
+// cuMemGetAddressRange (fetched through the runtime's entry-point query, so
+// the library keeps no link-time dependency on libcuda).
+typedef int (*MemGetAddressRangeFn)(unsigned long long*, size_t*, unsigned long long);
+
+int hmf_ipc_get_handle(const void* dptr, uint8_t* handle64, int64_t* offset) {
+  static MemGetAddressRangeFn range_fn = nullptr;
+  if (!range_fn) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !fn) return int(hmf::set_error(HMF_ERR_CUDA, "no cuMemGetAddressRange"));
+    range_fn = reinterpret_cast<MemGetAddressRangeFn>(fn);
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, reinterpret_cast<unsigned long long>(dptr)) != 0)
+    return int(hmf::set_error(HMF_ERR_CUDA, "cuMemGetAddressRange failed"));
   cudaIpcMemHandle_t h;
-  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dptr));
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
   if (e != cudaSuccess) return int(hmf::set_cuda_error(e));
   static_assert(sizeof(h) == 64, "IPC handle is 64 bytes");
   std::memcpy(handle64, &h, 64);
+  *offset = int64_t(reinterpret_cast<unsigned long long>(dptr) - base);
   return HMF_OK;
 }
 

@@ -1,0 +1,279 @@
+"""Multi-GPU block scheduling across processes: one process per GPU.
+
+The reference runs its workers as threads around one GridScheduler
+(scheduler.py:333-409) and moves item columns through shared host arrays
+(workers.py:186-218).  Across B200 processes the same protocol becomes:
+
+* rows are banded one band per GPU (partition.gpu_plan: mass proportional to
+  each GPU's fitted throughput) and each P band stays resident on its GPU —
+  the reference's P-band residency (workers.py:13-17, 324-328);
+* columns are 2*N+1 bands (a primary and a staged-ahead column per GPU plus a
+  spare, the reference's column rule for batch workers);
+* a column lease is a compare-and-set on a key of the torch.distributed store
+  (LeaseTable): at most one GPU holds a column band, so Q bands have a single
+  owner at a time, exactly the scheduler's independence rule;
+* each GPU pulls (RowBandTrainer) its undone blocks dynamically, least-updated
+  first with a seeded tie break, and keeps a staged-ahead column: while the
+  kernel runs on column c it tries to lease the next column and starts
+  pulling that Q band from its last owner on a copy stream (CUDA IPC +
+  cudaMemcpyPeerAsync over NVLink), the reference's prefetch unit
+  (scheduler.py:280-304, workers.py:338-361);
+* an epoch is the reference's quota epoch: every block once, then a barrier
+  where metrics are reduced (all_reduce of the residual sums).
+
+No process ever holds a column while waiting for another one, so the
+protocol cannot deadlock.  The transport and the compute are pluggable: the
+GPU implementation lives in CudaRowBand; tests drive the same trainer with a
+CPU transport over gloo (world size 2).
+"""
+
+from __future__ import annotations
+
+import time
+import uuid
+
+import numpy as np
+
+from .kernels import mix64
+
+FREE = b"free"
+
+
+class LeaseTable:
+    """Column-band leases over a torch.distributed Store (compare-and-set)."""
+
+    def __init__(self, store, n_cols: int, rank: int, run_id: str):
+        self.store = store
+        self.n_cols = n_cols
+        self.rank = rank
+        self.prefix = f"hmf/{run_id}"
+        self._me = str(rank).encode()
+
+    def _key(self, kind: str, c: int) -> str:
+        return f"{self.prefix}/{kind}/{c}"
+
+    def initialize(self) -> None:
+        """Rank 0, before the first barrier: every column free, no owner yet
+        (every replica of Q starts from the same seeded init)."""
+        for c in range(self.n_cols):
+            self.store.set(self._key("lease", c), FREE)
+            self.store.set(self._key("owner", c), b"-1")
+
+    def try_acquire(self, c: int) -> bool:
+        got = self.store.compare_set(self._key("lease", c), FREE, self._me)
+        return bytes(got) == self._me
+
+    def owner(self, c: int) -> int:
+        return int(bytes(self.store.get(self._key("owner", c))))
+
+    def release(self, c: int) -> None:
+        # publish the new owner first: whoever leases c next pulls from us
+        self.store.set(self._key("owner", c), self._me)
+        got = self.store.compare_set(self._key("lease", c), self._me, FREE)
+        if bytes(got) != FREE:
+            raise RuntimeError(f"rank {self.rank} released column {c} it did not hold")
+
+    def ticket(self) -> int:
+        """A global sequence number (lease order, for traces and tests)."""
+        return int(self.store.add(f"{self.prefix}/seq", 1))
+
+
+def new_run_id() -> str:
+    return uuid.uuid4().hex[:12]
+
+
+class RowBandTrainer:
+    """One GPU's lease loop over the blocks of its row band.
+
+    backend must provide:
+      n_cols                        column bands
+      pull(c, owner)                enqueue the Q band c copy from `owner`'s
+                                    replica (no-op when owner is self or -1)
+      compute(c, seed) -> int       enqueue the block's update; returns triples
+      finish(c)                     block until the compute of c completed
+    """
+
+    def __init__(self, backend, table: LeaseTable, rank: int, seed: int = 0,
+                 prefetch: bool = True, record: bool = False):
+        self.backend = backend
+        self.table = table
+        self.rank = rank
+        self.seed = seed
+        self.prefetch = prefetch
+        self.n_cols = backend.n_cols
+        self.counts = np.zeros(self.n_cols, dtype=np.int64)
+        self._rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(0xC1, rank)))
+        self.record = record
+        self.log = []            # (ticket, column, seed) per granted block
+        self.total_updates = 0
+        self.wait_seconds = 0.0
+
+    def _candidates(self, todo: set) -> list:
+        cols = sorted(todo)
+        ties = self._rng.permutation(len(cols))
+        return [c for _, _, c in sorted(zip((self.counts[c] for c in cols), ties, cols))]
+
+    def _grab(self, todo: set, blocking: bool):
+        delay = 2e-5
+        t0 = time.perf_counter()
+        while todo:
+            for c in self._candidates(todo):
+                if self.table.try_acquire(c):
+                    self.wait_seconds += time.perf_counter() - t0
+                    return c
+            if not blocking:
+                return None
+            time.sleep(delay)
+            delay = min(delay * 2, 1e-3)
+        return None
+
+    def _start(self, c: int) -> None:
+        """Lease granted: stamp the seed, pull the band, enqueue compute."""
+        block = self.rank * self.n_cols + c
+        unit_seed = mix64(self.seed, block, int(self.counts[c]))
+        if self.record:
+            self.log.append((self.table.ticket(), c, unit_seed))
+        self.backend.pull(c, self.table.owner(c))
+        self.total_updates += self.backend.compute(c, mix64(unit_seed, 0))
+
+    def run_epoch(self) -> None:
+        todo = set(range(self.n_cols))
+        cur = self._grab(todo, blocking=True)
+        todo.discard(cur)
+        self._start(cur)
+        while cur is not None:
+            nxt = None
+            if self.prefetch and todo:
+                nxt = self._grab(todo, blocking=False)
+                if nxt is not None:
+                    todo.discard(nxt)
+                    self._start(nxt)          # queued behind cur on the device
+            self.backend.finish(cur)
+            self.table.release(cur)
+            self.counts[cur] += 1
+            if nxt is None and todo:
+                nxt = self._grab(todo, blocking=True)
+                todo.discard(nxt)
+                self._start(nxt)
+            cur = nxt
+
+
+# ---------------------------------------------------------------------------
+# GPU backend
+# ---------------------------------------------------------------------------
+class CudaRowBand:
+    """One rank's device state: its P band, a full Q replica, its triples.
+
+    Q replicas of all ranks are mapped into every process with CUDA IPC, so a
+    pull is a one-sided peer copy from the band's last owner — the owner does
+    not participate.  Blocks use the Q-band kernel when the column bands are
+    wide enough to fill the GPU with one warp per item sub-band, else the
+    global-Q HOGWILD kernel.
+    """
+
+    def __init__(self, dist, rank: int, world: int, device, triples, row_lo: int, row_hi: int,
+                 col_cuts, k: int, lr: float, reg_user: float, reg_item: float,
+                 init_seed: int = 0, kernel: str = "auto", init=None):
+        import torch
+        from . import _lib
+        from .data import DeviceTriples, bucket_qbands, build_device_grid, resident_warps
+        self.torch = torch
+        self.lib = _lib
+        self.dev = torch.device(device)
+        self.rank, self.world = rank, world
+        self.k = k
+        self.lr, self.ru, self.ri = lr, reg_user, reg_item
+        self.row_lo, self.row_hi = row_lo, row_hi
+        self.col_cuts = np.asarray(col_cuts, dtype=np.int64)
+        self.n_cols = len(self.col_cuts) - 1
+        n_items = int(self.col_cuts[-1])
+        # P band (rows of this rank) and a full Q replica, same init law on
+        # every rank for Q (so owner -1 = "any replica is current")
+        if init is not None:   # explicit starting factors (host arrays: P band, Q)
+            self.P = torch.from_numpy(np.ascontiguousarray(init[0], dtype=np.float32)).to(self.dev)
+            self.Q = torch.from_numpy(np.ascontiguousarray(init[1], dtype=np.float32)).to(self.dev)
+        else:
+            g = torch.Generator(device=self.dev)
+            g.manual_seed(init_seed * 1_000_003 + rank + 1)
+            top = 1.0 / float(np.sqrt(k))
+            self.P = (torch.rand((row_hi - row_lo, k), generator=g, device=self.dev)
+                      * top).contiguous()
+            gq = torch.Generator(device=self.dev)
+            gq.manual_seed(init_seed * 1_000_003)
+            self.Q = (torch.rand((n_items, k), generator=gq, device=self.dev) * top).contiguous()
+        # local triples (users already global ids within [row_lo, row_hi))
+        local = DeviceTriples(row_hi, n_items, triples.users, triples.items, triples.ratings)
+        self.grid = build_device_grid(local, [0, row_hi], self.col_cuts)
+        self.block_of = list(range(self.n_cols))   # one row band: block c = column c
+        widest = int(np.max(np.diff(self.col_cuts)))
+        want = resident_warps(self.dev) // 2
+        self.kernel = kernel if kernel != "auto" else ("qband" if widest >= want else "range")
+        if self.kernel == "qband":
+            bucket_qbands(self.grid, k)
+        self.stream = torch.cuda.Stream(device=self.dev)
+        self.copy_stream = torch.cuda.Stream(device=self.dev)
+        self.done_events = {}
+        # exchange IPC handles of the Q replicas
+        import ctypes
+        handle = (ctypes.c_uint8 * 64)()
+        off = ctypes.c_int64(0)
+        _lib.check(_lib.load().hmf_ipc_get_handle(self.Q.data_ptr(), handle, ctypes.byref(off)),
+                   "hmf_ipc_get_handle")
+        mine = (bytes(handle), int(off.value), self.dev.index)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine)
+        self.peer_q = {}
+        for r, (hb, offset, pdev) in enumerate(allh):
+            if r == rank:
+                continue
+            buf = (ctypes.c_uint8 * 64).from_buffer_copy(hb)
+            ptr = ctypes.c_void_p()
+            _lib.check(_lib.load().hmf_ipc_open_handle(buf, ctypes.byref(ptr)),
+                       "hmf_ipc_open_handle")
+            self.peer_q[r] = (ptr.value + offset, pdev)
+
+    # -- backend protocol ------------------------------------------------------
+    def pull(self, c: int, owner: int) -> None:
+        if owner < 0 or owner == self.rank:
+            return
+        lo, hi = int(self.col_cuts[c]), int(self.col_cuts[c + 1])
+        nbytes = (hi - lo) * self.k * 4
+        src, _ = self.peer_q[owner]
+        _lib = self.lib
+        # IPC-mapped peer pointer: a UVA copy (device -1) over NVLink
+        _lib.check(_lib.load().hmf_memcpy_peer_async(
+            self.Q.data_ptr() + lo * self.k * 4, -1, src + lo * self.k * 4, -1,
+            nbytes, self.copy_stream.cuda_stream), "hmf_memcpy_peer_async")
+        ev = self.torch.cuda.Event()
+        ev.record(self.copy_stream)
+        self.stream.wait_event(ev)
+
+    def compute(self, c: int, seed: int) -> int:
+        from . import kernels
+        b = self.block_of[c]
+        lo, hi = self.grid.block_range(b)
+        if self.kernel == "qband":
+            n = kernels.launch_block_qband(self.P, self.Q, self.grid, b, self.lr, self.ru, self.ri,
+                                           seed, row_base=self.row_lo,
+                                           stream=self.stream.cuda_stream)
+        else:   # "range" (HOGWILD) or "exact" (reference order and arithmetic)
+            n = kernels.launch_sgd_range(self.P, self.Q, self.grid.users, self.grid.items,
+                                         self.grid.ratings, lo, hi, self.lr, self.ru, self.ri,
+                                         seed, self.row_lo, 0,
+                                         "exact" if self.kernel == "exact" else "hogwild",
+                                         self.stream.cuda_stream)
+        ev = self.torch.cuda.Event()
+        ev.record(self.stream)
+        self.done_events[c] = ev
+        return n
+
+    def finish(self, c: int) -> None:
+        ev = self.done_events.pop(c, None)
+        if ev is not None:
+            ev.synchronize()
+
+    def refresh_q(self, table: LeaseTable) -> None:
+        """Pull every band from its owner (metrics / end of run)."""
+        for c in range(self.n_cols):
+            self.pull(c, table.owner(c))
+        self.stream.synchronize()

@@ -1,0 +1,74 @@
+"""torchrun worker for tests/test_gpu_distributed.py (not collected by pytest).
+
+Each rank: one row band on a CUDA device (ranks may share a GPU), Q replicas
+exchanged by CUDA IPC, columns leased through the store, EXACT-mode kernel so
+the result can be compared with a serial replay bit for bit.
+"""
+
+import os
+import pickle
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+N_USERS, N_ITEMS, K, NNZ = 300, 260, 32, 12_000
+EPOCHS, SEED, LR, REG = 3, 9, 0.02, 0.01
+
+
+def problem():
+    rng = np.random.default_rng(21)
+    cells = rng.permutation(N_USERS * N_ITEMS)[:NNZ]
+    users = (cells // N_ITEMS).astype(np.int32)
+    items = (cells % N_ITEMS).astype(np.int32)
+    vals = rng.uniform(0, 1, NNZ).astype(np.float32).astype(np.float64)
+    P0 = rng.uniform(0, 0.3, size=(N_USERS, K)).astype(np.float32)
+    Q0 = rng.uniform(0, 0.3, size=(N_ITEMS, K)).astype(np.float32)
+    return users, items, vals, P0, Q0
+
+
+def main(out_dir):
+    import torch
+    import torch.distributed as dist
+    from paper_2006_15980_b200.data import DeviceTriples
+    from paper_2006_15980_b200.distributed import CudaRowBand, LeaseTable, RowBandTrainer
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"]) % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    users, items, vals, P0, Q0 = problem()
+    row_cuts = np.linspace(0, N_USERS, world + 1).astype(np.int64)
+    col_cuts = np.linspace(0, N_ITEMS, 2 * world + 2).astype(np.int64)
+    lo, hi = int(row_cuts[rank]), int(row_cuts[rank + 1])
+    keep = (users >= lo) & (users < hi)
+    dev = torch.device("cuda", local)
+    trip = DeviceTriples(hi, N_ITEMS, torch.from_numpy(users[keep]).to(dev),
+                         torch.from_numpy(items[keep]).to(dev),
+                         torch.from_numpy(vals[keep].astype(np.float32)).to(dev))
+    band = CudaRowBand(dist, rank, world, dev, trip, lo, hi, col_cuts, K, LR, REG, REG,
+                       kernel="exact", init=(P0[lo:hi], Q0))
+    table = LeaseTable(dist.distributed_c10d._get_default_store(), band.n_cols, rank, "gputest")
+    if rank == 0:
+        table.initialize()
+    dist.barrier()
+    trainer = RowBandTrainer(band, table, rank, seed=SEED, record=True)
+    for _ in range(EPOCHS):
+        trainer.run_epoch()
+        dist.barrier()
+    band.refresh_q(table)
+    torch.cuda.synchronize()
+    res = [None] * world
+    dist.all_gather_object(res, (trainer.log, band.P.cpu().numpy(), trainer.counts.tolist()))
+    if rank == 0:
+        with open(os.path.join(out_dir, "result.pkl"), "wb") as fh:
+            pickle.dump((res, band.Q.cpu().numpy(), row_cuts, col_cuts), fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
