@@ -252,6 +252,7 @@ def run_ours(args, world, rank, local):
     _lib.load()
     if args.variant is not None:
         _lib.set_variant(args.variant)
+    _lib.check(_lib.load().hmf_qband_set_impl(args.qband_impl), "hmf_qband_set_impl")
     dev = torch.device("cuda", local)
     n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
     k = args.k or k0
@@ -514,6 +515,8 @@ def main():
                     help="qband: Q band in shared memory (engine fast path); hogwild: "
                          "global-Q kernel behind hmf_sgd_range")
     ap.add_argument("--multi-kernel", choices=["auto", "qband", "range"], default="auto")
+    ap.add_argument("--qband-impl", type=int, choices=[0, 1], default=1,
+                    help="Q-band kernel: 1 = TMA pipeline, 0 = register prefetch")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

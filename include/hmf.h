@@ -104,6 +104,13 @@ int64_t hmf_sgd_range_f64(double* user_f, double* item_f, int64_t k, const int32
  * (row_base / col_base) as hmf_sgd_range_*.  Returns 0 or < 0.
  */
 int32_t hmf_qband_max_items(int64_t k);
+/* Warps per SM the Q-band kernel keeps resident (one sub-band each); needs a
+ * current CUDA device.  f16 != 0 for fp16 storage. */
+int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16);
+/* Q-band implementation: 1 = TMA pipeline (bulk P-row loads into a shared
+ * ring, bulk-reduce P deltas; default), 0 = register prefetch + per-lane
+ * vector reductions. */
+int hmf_qband_set_impl(int32_t impl);
 int64_t hmf_sgd_block_qband_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
                                 const int32_t* cols, const float* vals, const int64_t* sub_ptr,
                                 const int32_t* sub_cuts, int64_t n_sub, double lr, double reg_user,

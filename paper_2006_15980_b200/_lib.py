@@ -49,6 +49,8 @@ SIGNATURES = {
     "hmf_sgd_range_f64": (_i64, [_p, _p, _i64, _p, _p, _p, _i64, _i64, _f64, _f64, _f64, _u64,
                                  _i64, _i64, _i32, _p]),
     "hmf_qband_max_items": (_i32, [_i64]),
+    "hmf_qband_warps_per_sm": (_i32, [_i64, _i32]),
+    "hmf_qband_set_impl": (C.c_int, [_i32]),
     "hmf_sgd_block_qband_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _f64, _f64, _f64,
                                        _u64, _i64, _i64, _p]),
     "hmf_sgd_block_qband_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _f64, _f64, _f64,

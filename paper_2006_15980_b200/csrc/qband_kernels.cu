@@ -295,6 +295,317 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-pipelined variant.  Same ownership scheme (one warp per item sub-band,
+// Q slice in shared memory), but every global transfer is a bulk async copy
+// issued by one lane:
+//   * P rows are fetched D ratings ahead into a per-warp shared-memory ring
+//     (cp.async.bulk global->shared, one mbarrier per slot), so a warp keeps D
+//     rows in flight without holding them in registers;
+//   * P deltas are written to a small ring and added to HBM by TMA bulk
+//     reductions (cp.reduce.async.bulk .add.f32 -> UBLKRED), E in flight;
+//   * triples arrive through the 2-stage bulk ring as before.
+// Lanes only touch shared memory and registers: the per-lane LDG/RED traffic
+// of the register-prefetch variant (the SM->L2 request path bound in the r01
+// profile) moves to the TMA engine.
+// ---------------------------------------------------------------------------
+template <int K, typename S, int D, int E> struct TmaLayout {
+  static constexpr int ROWB = K * int(sizeof(S));
+  static constexpr int TRIP = 2 * stage_bytes;
+  static constexpr int PRING = D * ROWB;
+  static constexpr int DRING = E * ROWB;
+  static constexpr int O_TRIP = kSliceBytes;
+  static constexpr int O_PRING = O_TRIP + TRIP;
+  static constexpr int O_DRING = O_PRING + PRING;
+  static constexpr int O_BARS = O_DRING + DRING;
+  static constexpr int BYTES = ((O_BARS + (2 + D) * 8) + 127) / 128 * 128;
+};
+
+__device__ inline void bulk_reduce_add(float* dst, const void* src, uint32_t bytes) {
+  asm volatile(
+      "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+      "r"(smem_addr(src)), "r"(bytes)
+      : "memory");
+}
+__device__ inline void bulk_reduce_add(__half* dst, const void* src, uint32_t bytes) {
+  asm volatile(
+      "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.noftz.f16 [%0], [%1], %2;" ::"l"(
+          dst),
+      "r"(smem_addr(src)), "r"(bytes)
+      : "memory");
+}
+__device__ inline void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N> __device__ inline void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ inline void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// storage-typed row <-> lane floats, shared memory, same interleave as Lay
+template <int K, typename S>
+__device__ inline void lds_srow(const S* row, int lane, float* out) {
+  using L = Lay<K, S>;
+  if constexpr (L::VEC) {
+#pragma unroll
+    for (int v = 0; v < L::NV; ++v) {
+      if constexpr (sizeof(S) == 4) {
+        const float4 t = *reinterpret_cast<const float4*>(row + (v * 32 + lane) * L::VE);
+        out[v * 4 + 0] = t.x; out[v * 4 + 1] = t.y; out[v * 4 + 2] = t.z; out[v * 4 + 3] = t.w;
+      } else {
+        const uint4 t = *reinterpret_cast<const uint4*>(row + (v * 32 + lane) * L::VE);
+        const __half2* h = reinterpret_cast<const __half2*>(&t);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __half22float2(h[i]);
+          out[v * 8 + 2 * i] = f.x; out[v * 8 + 2 * i + 1] = f.y;
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < L::EPL; ++e) out[e] = float(row[e * 32 + lane]);
+  }
+}
+
+template <int K, typename S>
+__device__ inline void sts_srow(S* row, int lane, const float* in) {
+  using L = Lay<K, S>;
+  if constexpr (L::VEC) {
+#pragma unroll
+    for (int v = 0; v < L::NV; ++v) {
+      if constexpr (sizeof(S) == 4) {
+        *reinterpret_cast<float4*>(row + (v * 32 + lane) * L::VE) =
+            make_float4(in[v * 4], in[v * 4 + 1], in[v * 4 + 2], in[v * 4 + 3]);
+      } else {
+        uint4 t;
+        __half2* h = reinterpret_cast<__half2*>(&t);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(in[v * 8 + 2 * i], in[v * 8 + 2 * i + 1]);
+        *reinterpret_cast<uint4*>(row + (v * 32 + lane) * L::VE) = t;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < L::EPL; ++e) row[e * 32 + lane] = S(in[e]);
+  }
+}
+
+template <int K, typename S, int D, int E, int WPB, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB)
+    qtma_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const int32_t* __restrict__ rows,
+                const int32_t* __restrict__ cols, const float* __restrict__ vals,
+                const int64_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_cuts,
+                int n_sub, float lr, float ru, float ri, uint64_t seed) {
+  using T = TmaLayout<K, S, D, E>;
+  constexpr int EL = Lay<K, S>::EPL;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wbase = smem + warp * T::BYTES;
+  float* qslice = reinterpret_cast<float*>(wbase);
+  S* pring = reinterpret_cast<S*>(wbase + T::O_PRING);
+  S* dring = reinterpret_cast<S*>(wbase + T::O_DRING);
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(wbase + T::O_BARS);  // 2 triple stages
+  uint64_t* pbar = tbar + 2;                                         // D P slots
+  if (lane == 0) {
+    mbar_init(&tbar[0], 1);
+    mbar_init(&tbar[1], 1);
+    for (int i = 0; i < D; ++i) mbar_init(&pbar[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const int tw = gridDim.x * WPB;
+  const bool bulk_ok = ((reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(cols) |
+                         reinterpret_cast<uintptr_t>(vals)) & 15u) == 0;
+  uint32_t tpar[2] = {0u, 0u};  // wait parity per triple stage
+  uint32_t issued = 0, consumed = 0;
+
+  for (int s = blockIdx.x * WPB + warp; s < n_sub; s += tw) {
+    const int c_lo = sub_cuts[s];
+    const int n_items = sub_cuts[s + 1] - c_lo;
+    if (n_items > kSliceBytes / (K * 4)) __trap();
+    S* qrow0 = Qb + int64_t(c_lo) * K;
+    for (int it = 0; it < n_items; ++it) {
+      float t[EL];
+      load_row<K, S>(qrow0 + int64_t(it) * K, lane, t);
+      sts_row<K, S>(qslice + it * K, lane, t);
+    }
+    const int64_t beg = sub_ptr[s], end = sub_ptr[s + 1];
+    const int64_t a0 = beg & ~int64_t(3);
+    const int n_chunks = int((end - a0 + kChunk - 1) / kChunk);
+    if (n_chunks <= 0) continue;
+    const int rot = int(splitmix_finalize(seed + uint64_t(s) * kGolden) % uint64_t(n_chunks));
+    auto cbeg = [&](int x) -> int64_t {
+      int c = x + rot;
+      if (c >= n_chunks) c -= n_chunks;
+      return a0 + int64_t(c) * kChunk;
+    };
+    auto clo = [&](int x) -> int { return int(max(beg - cbeg(x), int64_t(0))); };
+    auto chi = [&](int x) -> int { return int(min(cbeg(x) + kChunk, end) - cbeg(x)); };
+    auto stage_x = [&](int x) {
+      const int64_t b0 = cbeg(x);
+      stage(ring_at(wbase, x & 1), &tbar[x & 1], rows, cols, vals, b0, min(b0 + kChunk, end),
+            bulk_ok, lane);
+    };
+    auto wait_x = [&](int x) {
+      mbar_wait(&tbar[x & 1], tpar[x & 1]);
+      tpar[x & 1] ^= 1u;
+      __syncwarp();
+    };
+    // prefetch cursor (px, pi) runs up to D ratings ahead of the consume
+    // cursor (cx, ci) and never more than one chunk ahead (only chunks cx and
+    // cx+1 are staged)
+    stage_x(0);
+    if (n_chunks > 1) stage_x(1);
+    __syncwarp();
+    wait_x(0);
+    int px = 0, pi = clo(0);
+    int cx = 0, ci = clo(0);
+    auto issue = [&]() {
+      if (lane == 0) {
+        const int slot = int(issued % D);
+        const int32_t u = ring_at(wbase, px & 1).rows[pi];
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&pbar[slot], uint32_t(T::ROWB));
+        bulk_g2s(pring + slot * K, Pb + int64_t(u) * K, uint32_t(T::ROWB), &pbar[slot]);
+      }
+      ++issued;
+      if (++pi >= chi(px)) {
+        ++px;
+        if (px < n_chunks) {
+          wait_x(px);
+          pi = clo(px);
+        }
+      }
+    };
+    while (px < n_chunks && px <= cx + 1 && issued - consumed < uint32_t(D)) issue();
+    while (cx < n_chunks) {
+      const Ring r = ring_at(wbase, cx & 1);
+      const int slot = int(consumed % D);
+      mbar_wait(&pbar[slot], (consumed / D) & 1u);
+      float p[EL], q[EL];
+      lds_srow<K, S>(pring + slot * K, lane, p);
+      const int vloc = r.cols[ci] - c_lo;
+      float* qs_row = qslice + vloc * K;
+      lds_row<K, S>(qs_row, lane, q);
+      float d = 0.f;
+#pragma unroll
+      for (int e = 0; e < EL; ++e) d += p[e] * q[e];
+      d = group_sum<32>(d);
+      const float err = r.vals[ci] - d;
+#pragma unroll
+      for (int e = 0; e < EL; ++e) {
+        const float pu = p[e], qv = q[e];
+        p[e] = lr * (err * qv - ru * pu);
+        q[e] = qv + lr * (err * pu - ri * qv);
+      }
+      sts_row<K, S>(qs_row, lane, q);
+      // delta ring slot: the reduction that last read it must be done reading
+      const int dslot = int(consumed % E);
+      if (lane == 0 && consumed >= uint32_t(E)) bulk_wait_read<E - 1>();
+      __syncwarp();
+      sts_srow<K, S>(dring + dslot * K, lane, p);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        bulk_reduce_add(Pb + int64_t(r.rows[ci]) * K, dring + dslot * K, uint32_t(T::ROWB));
+        bulk_commit();
+      }
+      ++consumed;
+      if (++ci >= chi(cx)) {
+        ++cx;
+        if (cx + 1 < n_chunks) {
+          __syncwarp();
+          stage_x(cx + 1);  // buffer (cx+1)&1 held chunk cx-1: fully consumed
+        }
+        if (cx < n_chunks) ci = clo(cx);
+      }
+      while (px < n_chunks && px <= cx + 1 && issued - consumed < uint32_t(D)) issue();
+    }
+    // Q slice back to HBM
+    for (int it = 0; it < n_items; ++it) {
+      float t[EL];
+      lds_row<K, S>(qslice + it * K, lane, t);
+      using L2 = Lay<K, S>;
+      if constexpr (L2::VEC) {
+#pragma unroll
+        for (int v = 0; v < L2::NV; ++v) {
+          typename Storage<S>::C tmp[L2::VE];
+#pragma unroll
+          for (int e = 0; e < L2::VE; ++e) tmp[e] = typename Storage<S>::C(t[v * L2::VE + e]);
+          Storage<S>::store(qrow0 + int64_t(it) * K + (v * 32 + lane) * L2::VE, tmp);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < EL; ++e)
+          Storage<S>::store1(qrow0 + int64_t(it) * K + e * 32 + lane, typename Storage<S>::C(t[e]));
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) bulk_wait_all();
+  __syncwarp();
+}
+
+// (D, E, WPB, MINB) per K: ~13-14 KB of shared memory per warp, 16 warps/SM
+template <int K, typename S> struct TmaCfg {
+  static constexpr int ROWB = K * int(sizeof(S));
+  static constexpr int D0 = 4096 / ROWB;
+  static constexpr int D = D0 < 4 ? 4 : (D0 > 16 ? 16 : D0);
+  static constexpr int E = D / 2;
+  static constexpr int WPB = 8, MINB = 2;
+};
+
+template <int K, typename S>
+static cudaError_t launch_tma(S* P, S* Q, const int32_t* rows, const int32_t* cols,
+                              const float* vals, const int64_t* sub_ptr, const int32_t* sub_cuts,
+                              int n_sub, double lr, double ru, double ri, uint64_t seed,
+                              int64_t row_base, int64_t col_base, cudaStream_t stream) {
+  using C = TmaCfg<K, S>;
+  using T = TmaLayout<K, S, C::D, C::E>;
+  auto kern = qtma_kernel<K, S, C::D, C::E, C::WPB, C::MINB>;
+  const int smem = C::WPB * T::BYTES;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPB * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int want = (n_sub + C::WPB - 1) / C::WPB;
+  const int cap = device_sm_count() * per_sm;
+  const int grid = want < cap ? want : cap;
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
+                                            sub_ptr, sub_cuts, n_sub, float(lr), float(ru),
+                                            float(ri), seed);
+  return cudaGetLastError();
+}
+
+template <int K, typename S>
+static int tma_warps_per_sm() {
+  using C = TmaCfg<K, S>;
+  using T = TmaLayout<K, S, C::D, C::E>;
+  auto kern = qtma_kernel<K, S, C::D, C::E, C::WPB, C::MINB>;
+  const int smem = C::WPB * T::BYTES;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPB * 32, smem);
+  return per_sm * C::WPB;
+}
+
+template <int K, typename S>
+static int reg_warps_per_sm() {
+  constexpr int U = (K / 32) >= 4 ? 2 : 4;
+  auto kern = qband_kernel<K, S, U>;
+  const int smem = kWarps * warp_bytes;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
+  return per_sm * kWarps;
+}
+
+static int g_qband_impl = 1;  // 0 = register prefetch, 1 = TMA pipeline
+
 template <int K, typename S>
 constexpr int max_items() {
   return kSliceBytes / (K * 4);
@@ -338,21 +649,52 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
   if (((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) != 0)
     return set_error(HMF_ERR_ARG, "factor arrays must be 16-byte aligned");
   cudaError_t e;
+  const bool tma = g_qband_impl == 1;
   switch (k) {
-    case 32: e = launch<32, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, seed, row_base, col_base, stream); break;
-    case 64: e = launch<64, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, seed, row_base, col_base, stream); break;
-    case 128: e = launch<128, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, seed, row_base, col_base, stream); break;
-    case 256: e = launch<256, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, seed, row_base, col_base, stream); break;
+#define HMF_QB_CASE(KK)                                                                       \
+  case KK:                                                                                    \
+    e = tma ? launch_tma<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, \
+                                ri, seed, row_base, col_base, stream)                         \
+            : launch<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, \
+                            seed, row_base, col_base, stream);                                \
+    break;
+    HMF_QB_CASE(32)
+    HMF_QB_CASE(64)
+    HMF_QB_CASE(128)
+    HMF_QB_CASE(256)
+#undef HMF_QB_CASE
     default: return set_error(HMF_ERR_UNSUPPORTED, "Q-band kernel needs k in {32,64,128,256}");
   }
   if (e != cudaSuccess) return set_cuda_error(e);
   return 0;
 }
 
+template <typename S>
+static int warps_per_sm(int64_t k) {
+  const bool tma = g_qband_impl == 1;
+  switch (k) {
+    case 32: return tma ? tma_warps_per_sm<32, S>() : reg_warps_per_sm<32, S>();
+    case 64: return tma ? tma_warps_per_sm<64, S>() : reg_warps_per_sm<64, S>();
+    case 128: return tma ? tma_warps_per_sm<128, S>() : reg_warps_per_sm<128, S>();
+    case 256: return tma ? tma_warps_per_sm<256, S>() : reg_warps_per_sm<256, S>();
+    default: return 0;
+  }
+}
+
 }  // namespace qs
 }  // namespace hmf
 
 extern "C" {
+
+int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16) {
+  return f16 ? hmf::qs::warps_per_sm<__half>(k) : hmf::qs::warps_per_sm<float>(k);
+}
+
+int hmf_qband_set_impl(int32_t impl) {
+  if (impl != 0 && impl != 1) return int(hmf::set_error(HMF_ERR_ARG, "impl must be 0 or 1"));
+  hmf::qs::g_qband_impl = impl;
+  return HMF_OK;
+}
 
 int32_t hmf_qband_max_items(int64_t k) {
   if (k != 32 && k != 64 && k != 128 && k != 256) return 0;

@@ -436,10 +436,13 @@ def build_device_grid(triples: DeviceTriples, row_cuts, col_cuts, region_of_row=
                       sub_row_parent, out_u, out_i, out_r, ptr)
 
 
-def resident_warps(device) -> int:
-    """Warps the Q-band kernel keeps resident: 2 CTAs x 16 warps per SM."""
+def resident_warps(device, k: int = 128, f16: bool = False) -> int:
+    """Warps the active Q-band kernel keeps resident on `device` (one item
+    sub-band each): SMs x the kernel's occupancy in warps."""
     torch = _torch()
-    return int(torch.cuda.get_device_properties(device).multi_processor_count) * 32
+    with torch.cuda.device(device):
+        per_sm = int(_lib.load().hmf_qband_warps_per_sm(int(k), 1 if f16 else 0))
+    return int(torch.cuda.get_device_properties(device).multi_processor_count) * max(per_sm, 1)
 
 
 def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int) -> np.ndarray:
@@ -464,7 +467,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None) -> Device
     dev = grid.device
     lib = _lib.load()
     s = _stream(dev)
-    target = resident_warps(dev) if target is None else int(target)
+    target = resident_warps(dev, k) if target is None else int(target)
     out_u = torch.empty_like(grid.users)
     out_i = torch.empty_like(grid.items)
     out_r = torch.empty_like(grid.ratings)

@@ -206,7 +206,7 @@ class CudaRowBand:
         self.grid = build_device_grid(local, [0, row_hi], self.col_cuts)
         self.block_of = list(range(self.n_cols))   # one row band: block c = column c
         widest = int(np.max(np.diff(self.col_cuts)))
-        want = resident_warps(self.dev) // 2
+        want = resident_warps(self.dev, k) // 2
         self.kernel = kernel if kernel != "auto" else ("qband" if widest >= want else "range")
         if self.kernel == "qband":
             bucket_qbands(self.grid, k)

@@ -394,8 +394,16 @@ def test_qband_bucketing_contract(dev, k):
             assert np.all((seg >= cuts[s]) & (seg < cuts[s + 1]))
 
 
+@pytest.fixture(params=[1, 0], ids=["tma", "regs"])
+def qband_impl(request):
+    from paper_2006_15980_b200 import _lib
+    _lib.check(_lib.load().hmf_qband_set_impl(request.param), "set_impl")
+    yield request.param
+    _lib.load().hmf_qband_set_impl(1)
+
+
 @pytest.mark.parametrize("k", [32, 64, 128, 256])
-def test_qband_equals_sequential_per_item(dev, k):
+def test_qband_equals_sequential_per_item(dev, k, qband_impl):
     """Distinct users, <= 128 triples per sub-band: every Q row is updated
     sequentially in storage order by its owner warp and no P row is shared,
     so the result equals a sequential f64 replay within fp32 rounding."""
@@ -425,7 +433,7 @@ def test_qband_equals_sequential_per_item(dev, k):
     assert rel_err(Q.double().cpu().numpy(), Qe) < 1e-5
 
 
-def test_qband_ml1m_quality_within_0005_of_reference(dev):
+def test_qband_ml1m_quality_within_0005_of_reference(dev, qband_impl):
     from paper_2006_15980_b200 import kernels
     from paper_2006_15980_b200.data import (DeviceGrid, RatingMatrix, bucket_qbands, build_grid,
                                             shuffle_triples, synthetic_ratings)
@@ -453,3 +461,69 @@ def test_qband_ml1m_quality_within_0005_of_reference(dev):
         print(f"{key}: gpu qband {got[key]:.5f} reference {ref[key]['test_rmse']:.5f}")
     assert abs(got["e20"] - ref["e20"]["test_rmse"]) <= 0.005
     assert abs(got["e5"] - ref["e5"]["test_rmse"]) <= 0.005
+
+
+@pytest.mark.parametrize("k", [64, 128])
+def test_qband_multi_chunk_subbands_match_sequential(dev, k, qband_impl):
+    """Sub-bands of several hundred triples (several staging chunks, rotated
+    per seed): with distinct users the result still equals a sequential
+    replay in the kernel's visit order (chunks rotated by the seed)."""
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import RatingMatrix
+    rng = np.random.default_rng(k + 1)
+    n_users, n_items, n = 20000, 24, 6000
+    users = rng.permutation(n_users)[:n].astype(np.int32)
+    items = rng.integers(0, n_items, n).astype(np.int32)
+    vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
+    m = RatingMatrix(n_users, n_items, users, items, vals)
+    g = _qband_grid(dev, m, k, [0, n_items], target=n_items)
+    P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
+    Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
+    P, Q = to_dev(P0, dev), to_dev(Q0, dev)
+    seed = 12345
+    kernels.launch_block_qband(P, Q, g, 0, 0.05, 0.02, 0.03, seed)
+    # replay: per sub-band, chunks of 128 from the 4-aligned base, rotated
+    from paper_2006_15980_b200.kernels import _MASK64
+    gu, gi = g.users.cpu().numpy(), g.items.cpu().numpy()
+    gr = g.ratings.cpu().numpy().astype(np.float64)
+    ptr = g.sub_ptr[0].cpu().numpy()
+    Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
+
+    def fin(z):
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9 & _MASK64
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EB & _MASK64
+        return z ^ (z >> 31)
+    for s_ in range(len(ptr) - 1):
+        beg, end = int(ptr[s_]), int(ptr[s_ + 1])
+        a0 = beg & ~3
+        nch = (end - a0 + 127) // 128
+        if nch == 0:
+            continue
+        rot = fin((seed + s_ * 0x9E3779B97F4A7C15) & _MASK64) % nch
+        for x in range(nch):
+            c = (x + rot) % nch
+            for i in range(max(beg, a0 + c * 128), min(a0 + (c + 1) * 128, end)):
+                u, v, r = gu[i], gi[i], gr[i]
+                pu, qv = Pe[u].copy(), Qe[v].copy()
+                e = r - pu @ qv
+                Pe[u] = pu + 0.05 * (e * qv - 0.02 * pu)
+                Qe[v] = qv + 0.05 * (e * pu - 0.03 * qv)
+    assert rel_err(Q.double().cpu().numpy(), Qe) < 1e-5
+    assert rel_err(P.double().cpu().numpy(), Pe) < 1e-5
+
+
+def test_qband_fp16_storage_tracks_fp32(dev, qband_impl):
+    from paper_2006_15980_b200 import kernels
+    m = random_matrix(3000, 800, 200_000, 5)
+    g = _qband_grid(dev, m, 128, [0, 800], target=400)
+    rng = np.random.default_rng(5)
+    P0 = rng.uniform(0, 0.09, size=(3000, 128)).astype(np.float32)
+    Q0 = rng.uniform(0, 0.09, size=(800, 128)).astype(np.float32)
+    out = {}
+    for dt in (torch.float32, torch.float16):
+        P, Q = to_dev(P0, dev, dt), to_dev(Q0, dev, dt)
+        for e in range(3):
+            kernels.launch_block_qband(P, Q, g, 0, 0.002, 0.01, 0.01, e)
+        out[dt] = (P.double().cpu().numpy(), Q.double().cpu().numpy())
+    assert rel_err(out[torch.float16][0], out[torch.float32][0]) < 5e-3
+    assert rel_err(out[torch.float16][1], out[torch.float32][1]) < 5e-3
