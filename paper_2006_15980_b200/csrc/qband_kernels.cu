@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     const int c_lo = sub_cuts[s];
     const int n_items = sub_cuts[s + 1] - c_lo;
     if (n_items > kSliceBytes / (K * 4)) __trap();
+    if (sub_ptr[s + 1] <= sub_ptr[s]) continue;  // no triples: nothing to stage
     S* qrow0 = Qb + int64_t(c_lo) * K;
     for (int it = 0; it < n_items; ++it) {
       float t[EL];
@@ -459,7 +460,14 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     wait_x(0);
     int px = 0, pi = clo(0);
     int cx = 0, ci = clo(0);
+    bool px_ready = true;  // chunk px's triples waited (chunk 0 just was)
     auto issue = [&]() {
+      // Wait for a chunk lazily, at its first issue: issues are guarded by
+      // px <= cx + 1, so the chunk has been staged by then.
+      if (!px_ready) {
+        wait_x(px);
+        px_ready = true;
+      }
       if (lane == 0) {
         const int slot = int(issued % D);
         const int32_t u = ring_at(wbase, px & 1).rows[pi];
@@ -470,10 +478,8 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
       ++issued;
       if (++pi >= chi(px)) {
         ++px;
-        if (px < n_chunks) {
-          wait_x(px);
-          pi = clo(px);
-        }
+        px_ready = false;
+        if (px < n_chunks) pi = clo(px);
       }
     };
     while (px < n_chunks && px <= cx + 1 && issued - consumed < uint32_t(D)) issue();
