@@ -480,7 +480,18 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None) -> Device
         n_sub = len(cuts) - 1
         d_cuts = torch.from_numpy(cuts).to(dev)
         ptr = torch.zeros(n_sub + 1, dtype=torch.int64, device=dev)
-        if hi > lo:
+        if hi > lo and n_sub > 12288:
+            # beyond the tile-histogram bucketing's bin limit: a stable key sort
+            # (layout preparation, once per grid; the reference uses
+            # np.argsort(kind="stable") here, data.py:264)
+            key = torch.bucketize(grid.items[lo:hi], d_cuts[1:-1].to(torch.int32), right=True)
+            order = torch.sort(key, stable=True).indices
+            out_u[lo:hi] = grid.users[lo:hi][order]
+            out_i[lo:hi] = grid.items[lo:hi][order]
+            out_r[lo:hi] = grid.ratings[lo:hi][order]
+            ptr[1:] = torch.cumsum(torch.bincount(key, minlength=n_sub), 0)
+            del key, order
+        elif hi > lo:
             _lib.check(lib.hmf_bucket_triples(
                 grid.users.data_ptr() + 4 * lo, grid.items.data_ptr() + 4 * lo,
                 grid.ratings.data_ptr() + 4 * lo, hi - lo, row_cuts.data_ptr(), 1,

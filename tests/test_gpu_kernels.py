@@ -527,3 +527,22 @@ def test_qband_fp16_storage_tracks_fp32(dev, qband_impl):
         out[dt] = (P.double().cpu().numpy(), Q.double().cpu().numpy())
     assert rel_err(out[torch.float16][0], out[torch.float32][0]) < 5e-3
     assert rel_err(out[torch.float16][1], out[torch.float32][1]) < 5e-3
+
+
+def test_qband_bucketing_many_subbands(dev):
+    """More sub-bands than the histogram bucketing handles (> 12288): the
+    stable-sort path keeps the same contract."""
+    m = random_matrix(2000, 30000, 300_000, 77)
+    g = _qband_grid(dev, m, 128, [0, 30000], target=20000)
+    items = g.items.cpu().numpy()
+    users = g.users.cpu().numpy()
+    ptr = g.sub_ptr[0].cpu().numpy()
+    cuts = g.sub_cuts[0].cpu().numpy()
+    assert len(cuts) - 1 == 20000 and ptr[-1] == 300_000
+    for s in range(0, 20000, 97):
+        seg = items[ptr[s]:ptr[s + 1]]
+        assert np.all((seg >= cuts[s]) & (seg < cuts[s + 1]))
+    # stable: inside a sub-band the original (block) order is preserved
+    key = np.searchsorted(cuts, m.items, side="right") - 1
+    order = np.argsort(key, kind="stable")
+    assert np.array_equal(users, m.users[order]) and np.array_equal(items, m.items[order])
