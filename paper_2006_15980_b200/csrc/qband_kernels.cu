@@ -610,7 +610,7 @@ static int reg_warps_per_sm() {
   return per_sm * kWarps;
 }
 
-static int g_qband_impl = 1;  // 0 = register prefetch, 1 = TMA pipeline
+static int g_qband_impl = 0;  // 0 = register prefetch (default, faster), 1 = TMA pipeline
 
 template <int K, typename S>
 constexpr int max_items() {

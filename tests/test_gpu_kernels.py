@@ -399,7 +399,7 @@ def qband_impl(request):
     from paper_2006_15980_b200 import _lib
     _lib.check(_lib.load().hmf_qband_set_impl(request.param), "set_impl")
     yield request.param
-    _lib.load().hmf_qband_set_impl(1)
+    _lib.load().hmf_qband_set_impl(0)
 
 
 @pytest.mark.parametrize("k", [32, 64, 128, 256])
