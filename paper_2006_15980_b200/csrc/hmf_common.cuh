@@ -67,14 +67,17 @@ template <> struct Storage<__half> {
   __device__ static inline void store1(__half* p, C v) {
     __stcg(reinterpret_cast<unsigned short*>(p), __half_as_ushort(__float2half_rn(v)));
   }
+  // p[0..7] += in[0..7]: one 16-byte vector reduction (REDG.E.ADD.F16x8)
   __device__ static inline void red(__half* p, const C* in) {
+    uint32_t w[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       __half2 h = __floats2half2_rn(in[2 * i], in[2 * i + 1]);
-      asm volatile("red.global.add.noftz.f16x2 [%0], %1;" ::"l"(p + 2 * i),
-                   "r"(*reinterpret_cast<uint32_t*>(&h))
-                   : "memory");
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
     }
+    asm volatile("red.global.add.noftz.v4.f16x2 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(w[0]),
+                 "r"(w[1]), "r"(w[2]), "r"(w[3])
+                 : "memory");
   }
   __device__ static inline void red1(__half* p, C v) {
     asm volatile("red.global.add.noftz.f16 [%0], %1;" ::"l"(p),

@@ -19,6 +19,7 @@
 // the r01 ncu profile) and all races on Q.
 #include "hmf_common.cuh"
 #include "hmf_internal.h"
+#include "lanevec.cuh"
 
 namespace hmf {
 
@@ -28,95 +29,10 @@ constexpr int kWarps = 16;           // warps per CTA
 constexpr int kChunk = 128;          // triples per staging stage
 constexpr int kSliceBytes = 4096;    // fp32 Q slice per warp
 
-// Lane layout of a K-row for one warp-owned rating: 32 lanes, EPL elements
-// each, interleaved by 16-byte vectors when a lane holds >= one vector,
-// interleaved by element otherwise (coalesced global, conflict-free shared).
-template <int K, typename S> struct Lay {
-  static constexpr int VE = Storage<S>::VE;
-  static constexpr int EPL = K / 32;
-  static constexpr bool VEC = (EPL % VE) == 0;
-  static constexpr int NV = VEC ? EPL / VE : 0;
-  static_assert(K % 32 == 0, "K must be a multiple of 32");
-  // element index of the lane's e-th element
-  __device__ static inline int elem(int lane, int e) {
-    if constexpr (VEC) return ((e / VE) * 32 + lane) * VE + (e % VE);
-    else return e * 32 + lane;
-  }
-};
-
-template <int K, typename S>
-__device__ inline void load_row(const S* row, int lane, float* out) {
-  using L = Lay<K, S>;
-  using ST = Storage<S>;
-  if constexpr (L::VEC) {
-#pragma unroll
-    for (int v = 0; v < L::NV; ++v) {
-      typename ST::C tmp[L::VE];
-      ST::load(row + (v * 32 + lane) * L::VE, tmp);
-#pragma unroll
-      for (int e = 0; e < L::VE; ++e) out[v * L::VE + e] = float(tmp[e]);
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < L::EPL; ++e) out[e] = float(ST::load1(row + e * 32 + lane));
-  }
-}
-
-template <int K, typename S>
-__device__ inline void red_row(S* row, int lane, const float* d) {
-  using L = Lay<K, S>;
-  using ST = Storage<S>;
-  if constexpr (L::VEC) {
-#pragma unroll
-    for (int v = 0; v < L::NV; ++v) {
-      typename ST::C tmp[L::VE];
-#pragma unroll
-      for (int e = 0; e < L::VE; ++e) tmp[e] = typename ST::C(d[v * L::VE + e]);
-      ST::red(row + (v * 32 + lane) * L::VE, tmp);
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < L::EPL; ++e) ST::red1(row + e * 32 + lane, typename ST::C(d[e]));
-  }
-}
-
-// Shared-memory Q row access (fp32 slice, same element interleave).
-template <int K, typename S>
-__device__ inline void lds_row(const float* q, int lane, float* out) {
-  using L = Lay<K, S>;
-  if constexpr (L::VEC && (L::VE % 4 == 0)) {
-#pragma unroll
-    for (int v = 0; v < L::NV; ++v)
-#pragma unroll
-      for (int h = 0; h < L::VE / 4; ++h) {
-        const float4 t = *reinterpret_cast<const float4*>(q + (v * 32 + lane) * L::VE + 4 * h);
-        out[v * L::VE + 4 * h + 0] = t.x;
-        out[v * L::VE + 4 * h + 1] = t.y;
-        out[v * L::VE + 4 * h + 2] = t.z;
-        out[v * L::VE + 4 * h + 3] = t.w;
-      }
-  } else {
-#pragma unroll
-    for (int e = 0; e < L::EPL; ++e) out[e] = q[L::elem(lane, e)];
-  }
-}
-
-template <int K, typename S>
-__device__ inline void sts_row(float* q, int lane, const float* in) {
-  using L = Lay<K, S>;
-  if constexpr (L::VEC && (L::VE % 4 == 0)) {
-#pragma unroll
-    for (int v = 0; v < L::NV; ++v)
-#pragma unroll
-      for (int h = 0; h < L::VE / 4; ++h)
-        *reinterpret_cast<float4*>(q + (v * 32 + lane) * L::VE + 4 * h) =
-            make_float4(in[v * L::VE + 4 * h], in[v * L::VE + 4 * h + 1],
-                        in[v * L::VE + 4 * h + 2], in[v * L::VE + 4 * h + 3]);
-  } else {
-#pragma unroll
-    for (int e = 0; e < L::EPL; ++e) q[L::elem(lane, e)] = in[e];
-  }
-}
+// Row layout: RowLay<K, S> (lanevec.cuh) — 32 lanes, K/32 elements each,
+// vectorised for every storage width; the fp32 Q slice uses the same
+// element interleave.
+template <int K, typename S> using Lay = RowLay<K, S>;
 
 constexpr int stage_bytes = kChunk * 12;
 constexpr int warp_bytes = kSliceBytes + 2 * stage_bytes + 16;
@@ -186,8 +102,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
     // 1. Q slice -> shared memory (fp32)
     for (int it = 0; it < n_items; ++it) {
       float t[E];
-      load_row<K, S>(qrow0 + int64_t(it) * K, lane, t);
-      sts_row<K, S>(qslice + it * K, lane, t);
+      Lay<K, S>::ldg(qrow0 + int64_t(it) * K, lane, t);
+      Lay<K, S>::stsf(qslice + it * K, lane, t);
     }
     const int64_t beg = sub_ptr[s], end = sub_ptr[s + 1];
     const int64_t a0 = beg & ~int64_t(3);
@@ -228,7 +144,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       for (int j = 0; j < U; ++j) {
         const int i = lo + j;
         uc[j] = i < hi ? r.rows[i] : -1;
-        if (uc[j] >= 0) load_row<K, S>(Pb + int64_t(uc[j]) * K, lane, pc[j]);
+        if (uc[j] >= 0) Lay<K, S>::ldg(Pb + int64_t(uc[j]) * K, lane, pc[j]);
       }
       for (int base = lo; base < hi; base += U) {
         // prefetch the next group's P rows
@@ -236,7 +152,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
         for (int j = 0; j < U; ++j) {
           const int i = base + U + j;
           un[j] = i < hi ? r.rows[i] : -1;
-          if (un[j] >= 0) load_row<K, S>(Pb + int64_t(un[j]) * K, lane, pn[j]);
+          if (un[j] >= 0) Lay<K, S>::ldg(Pb + int64_t(un[j]) * K, lane, pn[j]);
         }
         // the current group, sequentially on the shared-memory Q slice
 #pragma unroll
@@ -245,7 +161,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
             const int i = base + j;
             float* qs_row = qslice + (r.cols[i] - c_lo) * K;
             float q[E];
-            lds_row<K, S>(qs_row, lane, q);
+            Lay<K, S>::ldsf(qs_row, lane, q);
             float d = 0.f;
 #pragma unroll
             for (int e = 0; e < E; ++e) d += pc[j][e] * q[e];
@@ -257,9 +173,9 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
               pc[j][e] = lr * (err * qv - ru * pu);
               q[e] = qv + lr * (err * pu - ri * qv);
             }
-            sts_row<K, S>(qs_row, lane, q);
+            Lay<K, S>::stsf(qs_row, lane, q);
             __syncwarp();
-            red_row<K, S>(Pb + int64_t(uc[j]) * K, lane, pc[j]);
+            Lay<K, S>::red(Pb + int64_t(uc[j]) * K, lane, pc[j]);
           }
         }
 #pragma unroll
@@ -274,22 +190,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
     // 4. Q slice back to HBM (rounded to the storage type once per lease)
     for (int it = 0; it < n_items; ++it) {
       float t[E];
-      lds_row<K, S>(qslice + it * K, lane, t);
-      using L2 = Lay<K, S>;
-      if constexpr (L2::VEC) {
-#pragma unroll
-        for (int v = 0; v < L2::NV; ++v) {
-          typename Storage<S>::C tmp[L2::VE];
-#pragma unroll
-          for (int e = 0; e < L2::VE; ++e) tmp[e] = typename Storage<S>::C(t[v * L2::VE + e]);
-          Storage<S>::store(qrow0 + int64_t(it) * K + (v * 32 + lane) * L2::VE, tmp);
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e)
-          Storage<S>::store1(qrow0 + int64_t(it) * K + e * 32 + lane,
-                             typename Storage<S>::C(t[e]));
-      }
+      Lay<K, S>::ldsf(qslice + it * K, lane, t);
+      Lay<K, S>::stg(qrow0 + int64_t(it) * K, lane, t);
     }
     __syncwarp();
   }
@@ -340,55 +242,6 @@ template <int N> __device__ inline void bulk_wait_read() {
 }
 __device__ inline void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// storage-typed row <-> lane floats, shared memory, same interleave as Lay
-template <int K, typename S>
-__device__ inline void lds_srow(const S* row, int lane, float* out) {
-  using L = Lay<K, S>;
-  if constexpr (L::VEC) {
-#pragma unroll
-    for (int v = 0; v < L::NV; ++v) {
-      if constexpr (sizeof(S) == 4) {
-        const float4 t = *reinterpret_cast<const float4*>(row + (v * 32 + lane) * L::VE);
-        out[v * 4 + 0] = t.x; out[v * 4 + 1] = t.y; out[v * 4 + 2] = t.z; out[v * 4 + 3] = t.w;
-      } else {
-        const uint4 t = *reinterpret_cast<const uint4*>(row + (v * 32 + lane) * L::VE);
-        const __half2* h = reinterpret_cast<const __half2*>(&t);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 f = __half22float2(h[i]);
-          out[v * 8 + 2 * i] = f.x; out[v * 8 + 2 * i + 1] = f.y;
-        }
-      }
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < L::EPL; ++e) out[e] = float(row[e * 32 + lane]);
-  }
-}
-
-template <int K, typename S>
-__device__ inline void sts_srow(S* row, int lane, const float* in) {
-  using L = Lay<K, S>;
-  if constexpr (L::VEC) {
-#pragma unroll
-    for (int v = 0; v < L::NV; ++v) {
-      if constexpr (sizeof(S) == 4) {
-        *reinterpret_cast<float4*>(row + (v * 32 + lane) * L::VE) =
-            make_float4(in[v * 4], in[v * 4 + 1], in[v * 4 + 2], in[v * 4 + 3]);
-      } else {
-        uint4 t;
-        __half2* h = reinterpret_cast<__half2*>(&t);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(in[v * 8 + 2 * i], in[v * 8 + 2 * i + 1]);
-        *reinterpret_cast<uint4*>(row + (v * 32 + lane) * L::VE) = t;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < L::EPL; ++e) row[e * 32 + lane] = S(in[e]);
-  }
-}
-
 template <int K, typename S, int D, int E, int WPB, int MINB>
 __global__ void __launch_bounds__(WPB * 32, MINB)
     qtma_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const int32_t* __restrict__ rows,
@@ -426,8 +279,8 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     S* qrow0 = Qb + int64_t(c_lo) * K;
     for (int it = 0; it < n_items; ++it) {
       float t[EL];
-      load_row<K, S>(qrow0 + int64_t(it) * K, lane, t);
-      sts_row<K, S>(qslice + it * K, lane, t);
+      Lay<K, S>::ldg(qrow0 + int64_t(it) * K, lane, t);
+      Lay<K, S>::stsf(qslice + it * K, lane, t);
     }
     const int64_t beg = sub_ptr[s], end = sub_ptr[s + 1];
     const int64_t a0 = beg & ~int64_t(3);
@@ -488,10 +341,10 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
       const int slot = int(consumed % D);
       mbar_wait(&pbar[slot], (consumed / D) & 1u);
       float p[EL], q[EL];
-      lds_srow<K, S>(pring + slot * K, lane, p);
+      Lay<K, S>::lds(pring + slot * K, lane, p);
       const int vloc = r.cols[ci] - c_lo;
       float* qs_row = qslice + vloc * K;
-      lds_row<K, S>(qs_row, lane, q);
+      Lay<K, S>::ldsf(qs_row, lane, q);
       float d = 0.f;
 #pragma unroll
       for (int e = 0; e < EL; ++e) d += p[e] * q[e];
@@ -503,12 +356,12 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
         p[e] = lr * (err * qv - ru * pu);
         q[e] = qv + lr * (err * pu - ri * qv);
       }
-      sts_row<K, S>(qs_row, lane, q);
+      Lay<K, S>::stsf(qs_row, lane, q);
       // delta ring slot: the reduction that last read it must be done reading
       const int dslot = int(consumed % E);
       if (lane == 0 && consumed >= uint32_t(E)) bulk_wait_read<E - 1>();
       __syncwarp();
-      sts_srow<K, S>(dring + dslot * K, lane, p);
+      Lay<K, S>::sts(dring + dslot * K, lane, p);
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
@@ -529,21 +382,8 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     // Q slice back to HBM
     for (int it = 0; it < n_items; ++it) {
       float t[EL];
-      lds_row<K, S>(qslice + it * K, lane, t);
-      using L2 = Lay<K, S>;
-      if constexpr (L2::VEC) {
-#pragma unroll
-        for (int v = 0; v < L2::NV; ++v) {
-          typename Storage<S>::C tmp[L2::VE];
-#pragma unroll
-          for (int e = 0; e < L2::VE; ++e) tmp[e] = typename Storage<S>::C(t[v * L2::VE + e]);
-          Storage<S>::store(qrow0 + int64_t(it) * K + (v * 32 + lane) * L2::VE, tmp);
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < EL; ++e)
-          Storage<S>::store1(qrow0 + int64_t(it) * K + e * 32 + lane, typename Storage<S>::C(t[e]));
-      }
+      Lay<K, S>::ldsf(qslice + it * K, lane, t);
+      Lay<K, S>::stg(qrow0 + int64_t(it) * K, lane, t);
     }
     __syncwarp();
   }
