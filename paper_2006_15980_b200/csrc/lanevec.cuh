@@ -197,8 +197,21 @@ template <int K, typename S> struct RowLay {
     for (int v = 0; v < NV; ++v) V::stg(row + off(v, lane), i + v * W);
   }
   __device__ static void red(S* row, int lane, const float* d) {
+    if constexpr (W == 1 && sizeof(S) == 2) {
+      // one half per lane: pair neighbouring lanes into a 4-byte f16x2
+      // reduction instead of 2-byte atomics (must be called warp-uniformly)
 #pragma unroll
-    for (int v = 0; v < NV; ++v) V::red(row + off(v, lane), d + v * W);
+      for (int v = 0; v < NV; ++v) {
+        const float hi = __shfl_down_sync(0xffffffffu, d[v], 1);
+        if ((lane & 1) == 0) {
+          const float pair[2] = {d[v], hi};
+          Vec<S, 2>::red(row + off(v, lane), pair);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) V::red(row + off(v, lane), d + v * W);
+    }
   }
   // storage-typed row in shared memory
   __device__ static void lds(const S* row, int lane, float* o) {

@@ -504,6 +504,34 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None) -> Device
     return grid
 
 
+def stripe_layout(grid: DeviceGrid, n_stripes: int) -> DeviceGrid:
+    """Split every block into `n_stripes` index stripes and lay the grid out
+    stripe-major: stripe 0 of every block, then stripe 1, ...  The result is a
+    DeviceGrid with n_stripes row bands (all spanning every row) whose block
+    (r, c) is stripe r of the original column band c — each stripe a
+    contiguous slice holding part of every item, so a host->device stream can
+    upload stripe s+1 while the GPU updates stripe s with all warps busy.
+    Blocks keep their original relative order inside a stripe."""
+    torch = _torch()
+    if grid.n_row_bands != 1:
+        raise GridError("stripe_layout expects a single-row-band grid (one GPU's band)")
+    ncb = grid.n_col_bands
+    pieces, ptr = [], [0]
+    for r in range(n_stripes):
+        for c in range(ncb):
+            lo, hi = grid.block_range(c)
+            n = hi - lo
+            a, b = lo + (n * r) // n_stripes, lo + (n * (r + 1)) // n_stripes
+            pieces.append((a, b))
+            ptr.append(ptr[-1] + (b - a))
+    idx = torch.cat([torch.arange(a, b, device=grid.device) for a, b in pieces])
+    row_cuts = np.linspace(0, grid.n_rows, n_stripes + 1).astype(np.int64)
+    return DeviceGrid(grid.n_rows, grid.n_cols, row_cuts, grid.col_cuts,
+                      np.full(n_stripes, REGION_BATCH, dtype=np.int8), None,
+                      grid.users[idx].contiguous(), grid.items[idx].contiguous(),
+                      grid.ratings[idx].contiguous(), np.asarray(ptr, dtype=np.int64))
+
+
 def synthetic_device(n_users: int, n_items: int, nnz: int, rank: int = 8, noise: float = 0.1,
                      seed: int = 0, factor_scale: float = 1.0, device=None) -> DeviceTriples:
     """The synthetic_ratings law at any scale, generated in HBM.

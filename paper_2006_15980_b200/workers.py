@@ -436,6 +436,79 @@ class BatchWorker(threading.Thread):
                     self.engine.close()
 
 
+class StreamingEpoch:
+    """Epochs whose rating triples stream from pinned host memory.
+
+    The reference stages a unit's triples into the accelerator for every
+    lease (BatchEngine.stage_in, workers.py:186-202).  This is that pipeline
+    for data that is not kept resident: the grid is laid out stripe-major
+    (data.stripe_layout) and Q-band bucketed once, copied to pinned host
+    memory, and every epoch uploads stripe s+1 on a copy stream while the
+    Q-band kernel updates stripe s (double-buffered device staging, ordered by
+    CUDA events).  P and Q stay on the device.  Per epoch the host->device
+    traffic is exactly the triples (12 bytes per rating).
+    """
+
+    def __init__(self, grid: DeviceGrid, k: int, n_stripes: int = 8):
+        from .data import stripe_layout
+        torch = _torch()
+        self.dev = grid.device
+        sg = bucket_qbands(stripe_layout(grid, n_stripes), k)
+        self.k = k
+        self.n_blocks = sg.n_blocks
+        self.nnz = sg.nnz
+        # host copies (pinned) of the stripe-major, sub-band bucketed triples
+        self.h_users = sg.users.cpu().pin_memory()
+        self.h_items = sg.items.cpu().pin_memory()
+        self.h_vals = sg.ratings.cpu().pin_memory()
+        self.block_ptr = sg.block_ptr
+        # per block: sub_ptr relative to the block start (device) and sub_cuts
+        self.sub_rel = [(p - int(sg.block_ptr[b])).contiguous() for b, p in enumerate(sg.sub_ptr)]
+        self.sub_cuts = sg.sub_cuts
+        cap = int(np.max(np.diff(sg.block_ptr))) + 4
+        self.bufs = [tuple(torch.empty(cap, dtype=dt, device=self.dev)
+                           for dt in (torch.int32, torch.int32, torch.float32)) for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(device=self.dev)
+        self.freed = [None, None]
+        del sg
+
+    @property
+    def h2d_bytes(self) -> int:
+        return 12 * self.nnz
+
+    def run(self, P, Q, hparams: Hyperparams, seed: int, stream=None) -> int:
+        """One epoch over every block; returns triples processed (async)."""
+        torch = _torch()
+        comp = torch.cuda.current_stream(self.dev) if stream is None else stream
+        st = "f16" if P.dtype == torch.float16 else "f32"
+        fn = getattr(_lib.load(), f"hmf_sgd_block_qband_{st}")
+        done = 0
+        for b in range(self.n_blocks):
+            lo, hi = int(self.block_ptr[b]), int(self.block_ptr[b + 1])
+            if hi <= lo:
+                continue
+            buf = self.bufs[b & 1]
+            with torch.cuda.stream(self.copy_stream):
+                if self.freed[b & 1] is not None:
+                    self.copy_stream.wait_event(self.freed[b & 1])
+                for dst, src in zip(buf, (self.h_users, self.h_items, self.h_vals)):
+                    dst[:hi - lo].copy_(src[lo:hi], non_blocking=True)
+                up = torch.cuda.Event()
+                up.record(self.copy_stream)
+            comp.wait_event(up)
+            sp, sc = self.sub_rel[b], self.sub_cuts[b]
+            _lib.check(fn(P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr(),
+                          buf[1].data_ptr(), buf[2].data_ptr(), sp.data_ptr(), sc.data_ptr(),
+                          int(sp.numel()) - 1, hparams.learning_rate, hparams.reg_user,
+                          hparams.reg_item, kernels.mix64(seed, b) & 0xFFFFFFFFFFFFFFFF, 0, 0,
+                          comp.cuda_stream), f"hmf_sgd_block_qband_{st}")
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            self.freed[b & 1] = ev
+            done += hi - lo
+        return done
+
+
 # -- calibration / benchmarking helpers ----------------------------------------
 
 
