@@ -213,6 +213,9 @@ class CudaRowBand:
         self.stream = torch.cuda.Stream(device=self.dev)
         self.copy_stream = torch.cuda.Stream(device=self.dev)
         self.done_events = {}
+        # P, Q and the grid were produced on the current stream; the band's
+        # own compute / copy streams must not start before they exist
+        torch.cuda.current_stream(self.dev).synchronize()
         # exchange IPC handles of the Q replicas
         import ctypes
         handle = (ctypes.c_uint8 * 64)()

@@ -143,6 +143,9 @@ class FactorStore:
                     g = DeviceGrid.from_host(grid, torch.device("cuda", dev), rd)
                     if kernel == "qband":
                         bucket_qbands(g, self.k)
+                    # built on the current stream, read by the engines' own
+                    # streams: finish it before anyone launches on it
+                    torch.cuda.current_stream(dev).synchronize()
                 self.grids[dev] = g
                 self.host_grid = grid
             return g
