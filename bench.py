@@ -555,7 +555,7 @@ def main():
                     help="qband: Q band in shared memory (engine fast path); hogwild: "
                          "global-Q kernel behind hmf_sgd_range")
     ap.add_argument("--multi-kernel", choices=["auto", "qband", "range"], default="auto")
-    ap.add_argument("--qband-impl", type=int, choices=[0, 1], default=0,
+    ap.add_argument("--qband-impl", type=int, choices=[0, 1, 2], default=0,
                     help="Q-band kernel: 0 = register prefetch (default), 1 = TMA pipeline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -107,9 +107,10 @@ int32_t hmf_qband_max_items(int64_t k);
 /* Warps per SM the Q-band kernel keeps resident (one sub-band each); needs a
  * current CUDA device.  f16 != 0 for fp16 storage. */
 int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16);
-/* Q-band implementation: 1 = TMA pipeline (bulk P-row loads into a shared
- * ring, bulk-reduce P deltas; default), 0 = register prefetch + per-lane
- * vector reductions. */
+/* Q-band implementation: 0 = register prefetch + per-lane vector reductions
+ * (default), 1 = TMA pipeline (bulk P-row loads into a shared ring, bulk
+ * reductions of P deltas), 2 = per-lane cp.async ring of P rows + vector
+ * reductions.  hmf_qband_max_items depends on the active implementation. */
 int hmf_qband_set_impl(int32_t impl);
 int64_t hmf_sgd_block_qband_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
                                 const int32_t* cols, const float* vals, const int64_t* sub_ptr,

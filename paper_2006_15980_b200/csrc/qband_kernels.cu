@@ -452,6 +452,228 @@ static int reg_warps_per_sm() {
 
 static int g_qband_impl = 0;  // 0 = register prefetch (default, faster), 1 = TMA pipeline
 
+// ---------------------------------------------------------------------------
+// Async-copy ring variant (impl 2).  Same ownership scheme; the P rows of the
+// next D-1 ratings are in flight as per-lane cp.async copies (LDGSTS) into a
+// per-warp shared-memory ring instead of registers.  Each lane copies and
+// later reads back only its own vector of a row, so a lane's own
+// cp.async.wait_group is the only synchronisation: no proxy fences, no
+// mbarriers, no cross-lane barriers on the P path.  Registers no longer bound
+// the prefetch depth, so D rows per warp stay in flight.
+// ---------------------------------------------------------------------------
+template <int K, typename S, int D> struct AsyncLayout {
+  static constexpr int ROWB = K * int(sizeof(S));
+  static constexpr int SLICE = 2048;  // fp32 Q slice per warp
+  static constexpr int O_TRIP = SLICE;
+  static constexpr int O_RING = O_TRIP + 2 * stage_bytes;
+  static constexpr int O_BARS = O_RING + D * ROWB;
+  static constexpr int BYTES = ((O_BARS + 16) + 127) / 128 * 128;
+};
+
+template <int BYTES> __device__ inline void cp_async(void* smem_dst, const void* gsrc) {
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem_dst)),
+                 "l"(gsrc)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_addr(smem_dst)),
+                 "l"(gsrc), "n"(BYTES)
+                 : "memory");
+}
+__device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ inline void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int K, typename S, int D, int WPB, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB)
+    qasync_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const int32_t* __restrict__ rows,
+                  const int32_t* __restrict__ cols, const float* __restrict__ vals,
+                  const int64_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_cuts,
+                  int n_sub, float lr, float ru, float ri, uint64_t seed) {
+  using L = Lay<K, S>;
+  using AL = AsyncLayout<K, S, D>;
+  constexpr int E = L::EPL;
+  constexpr int VB = L::W * int(sizeof(S));  // bytes per lane vector
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wbase = smem + warp * AL::BYTES;
+  float* qslice = reinterpret_cast<float*>(wbase);
+  S* ring = reinterpret_cast<S*>(wbase + AL::O_RING);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + AL::O_BARS);
+  auto rstage = [&](int b) -> Ring {
+    unsigned char* p = wbase + AL::O_TRIP + b * stage_bytes;
+    return Ring{reinterpret_cast<int32_t*>(p), reinterpret_cast<int32_t*>(p + kChunk * 4),
+                reinterpret_cast<float*>(p + kChunk * 8)};
+  };
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const int tw = gridDim.x * WPB;
+  const bool bulk_ok = ((reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(cols) |
+                         reinterpret_cast<uintptr_t>(vals)) & 15u) == 0;
+  uint32_t phase[2] = {0u, 0u};
+
+  // issue the P row of user u into ring slot `slot` (this lane's vectors)
+  auto fetch = [&](int32_t u, int slot) {
+    const S* src = Pb + int64_t(u) * K;
+    S* dst = ring + slot * K;
+#pragma unroll
+    for (int v = 0; v < L::NV; ++v) cp_async<VB>(dst + L::off(v, lane), src + L::off(v, lane));
+  };
+
+  for (int s = blockIdx.x * WPB + warp; s < n_sub; s += tw) {
+    const int c_lo = sub_cuts[s];
+    const int n_items = sub_cuts[s + 1] - c_lo;
+    if (n_items * K * 4 > AL::SLICE) __trap();  // host contract: slice fits
+    const int64_t beg = sub_ptr[s], end = sub_ptr[s + 1];
+    if (end <= beg) continue;
+    S* qrow0 = Qb + int64_t(c_lo) * K;
+    for (int it = 0; it < n_items; ++it) {
+      float t[E];
+      L::ldg(qrow0 + int64_t(it) * K, lane, t);
+      L::stsf(qslice + it * K, lane, t);
+    }
+    const int64_t a0 = beg & ~int64_t(3);
+    const int64_t n_chunks = (end - a0 + kChunk - 1) / kChunk;
+    const int64_t rot = int64_t(splitmix_finalize(seed + uint64_t(s) * kGolden) % uint64_t(n_chunks));
+    auto chunk_begin = [&](int64_t x) -> int64_t {
+      int64_t c = x + rot;
+      if (c >= n_chunks) c -= n_chunks;
+      return a0 + c * kChunk;
+    };
+    {
+      const int64_t cb = chunk_begin(0);
+      stage(rstage(0), &bars[0], rows, cols, vals, cb, min(cb + kChunk, end), bulk_ok, lane);
+    }
+    __syncwarp();
+    for (int64_t x = 0; x < n_chunks; ++x) {
+      const int b = int(x & 1);
+      if (x + 1 < n_chunks) {
+        const int64_t nb = chunk_begin(x + 1);
+        stage(rstage(b ^ 1), &bars[b ^ 1], rows, cols, vals, nb, min(nb + kChunk, end), bulk_ok,
+              lane);
+      }
+      const int64_t cb = chunk_begin(x);
+      const int lo = int(max(beg - cb, int64_t(0)));
+      const int hi = int(min(cb + kChunk, end) - cb);
+      mbar_wait(&bars[b], phase[b]);
+      phase[b] ^= 1u;
+      __syncwarp();
+      const Ring r = rstage(b);
+      // prologue: D-1 rows in flight, one commit group per rating
+#pragma unroll
+      for (int j = 0; j < D - 1; ++j) {
+        if (lo + j < hi) fetch(r.rows[lo + j], (lo + j) % D);
+        cp_async_commit();
+      }
+      for (int i = lo; i < hi; ++i) {
+        if (i + D - 1 < hi) fetch(r.rows[i + D - 1], (i + D - 1) % D);
+        cp_async_commit();
+        cp_async_wait<D - 1>();  // this lane's copy of row i has landed
+        float p[E], q[E];
+        L::lds(ring + (i % D) * K, lane, p);
+        float* qs_row = qslice + (r.cols[i] - c_lo) * K;
+        L::ldsf(qs_row, lane, q);
+        float d = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) d += p[e] * q[e];
+        d = group_sum<32>(d);
+        const float err = r.vals[i] - d;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const float pu = p[e], qv = q[e];
+          p[e] = lr * (err * qv - ru * pu);
+          q[e] = qv + lr * (err * pu - ri * qv);
+        }
+        L::stsf(qs_row, lane, q);
+        L::red(Pb + int64_t(r.rows[i]) * K, lane, p);
+      }
+      cp_async_wait<0>();
+      __syncwarp();
+    }
+    for (int it = 0; it < n_items; ++it) {
+      float t[E];
+      L::ldsf(qslice + it * K, lane, t);
+      L::stg(qrow0 + int64_t(it) * K, lane, t);
+    }
+    __syncwarp();
+  }
+}
+
+template <int K, typename S> struct AsyncCfg {
+  static constexpr int ROWB = K * int(sizeof(S));
+  static constexpr int D0 = 3072 / ROWB;
+  static constexpr int D = D0 < 4 ? 4 : (D0 > 16 ? 16 : D0);
+  static constexpr int WPB = 8, MINB = 3;
+};
+
+template <int K, typename S>
+static cudaError_t launch_async(S* P, S* Q, const int32_t* rows, const int32_t* cols,
+                                const float* vals, const int64_t* sub_ptr, const int32_t* sub_cuts,
+                                int n_sub, double lr, double ru, double ri, uint64_t seed,
+                                int64_t row_base, int64_t col_base, cudaStream_t stream) {
+  using C = AsyncCfg<K, S>;
+  using AL = AsyncLayout<K, S, C::D>;
+  auto kern = qasync_kernel<K, S, C::D, C::WPB, C::MINB>;
+  const int smem = C::WPB * AL::BYTES;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPB * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int want = (n_sub + C::WPB - 1) / C::WPB;
+  const int cap = device_sm_count() * per_sm;
+  const int grid = want < cap ? want : cap;
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
+                                            sub_ptr, sub_cuts, n_sub, float(lr), float(ru),
+                                            float(ri), seed);
+  return cudaGetLastError();
+}
+
+template <int K, typename S>
+static int async_warps_per_sm() {
+  using C = AsyncCfg<K, S>;
+  using AL = AsyncLayout<K, S, C::D>;
+  auto kern = qasync_kernel<K, S, C::D, C::WPB, C::MINB>;
+  const int smem = C::WPB * AL::BYTES;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPB * 32, smem);
+  return per_sm * C::WPB;
+}
+
+// impl 2 needs >= 4-byte lane vectors (cp.async sizes 4/8/16): not K=32 fp16
+template <int K, typename S> constexpr bool async_ok() {
+  return Lay<K, S>::W * int(sizeof(S)) >= 4;
+}
+
+template <int K, typename S>
+static cudaError_t launch_async_if(S* P, S* Q, const int32_t* rows, const int32_t* cols,
+                                   const float* vals, const int64_t* sub_ptr,
+                                   const int32_t* sub_cuts, int n_sub, double lr, double ru,
+                                   double ri, uint64_t seed, int64_t row_base, int64_t col_base,
+                                   cudaStream_t stream) {
+  if constexpr (async_ok<K, S>())
+    return launch_async<K, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, n_sub, lr, ru, ri, seed,
+                              row_base, col_base, stream);
+  else
+    return cudaErrorNotSupported;
+}
+
+template <int K, typename S>
+static int async_warps_per_sm_if() {
+  if constexpr (async_ok<K, S>()) return async_warps_per_sm<K, S>();
+  else return 0;
+}
+
 template <int K, typename S>
 constexpr int max_items() {
   return kSliceBytes / (K * 4);
@@ -495,14 +717,19 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
   if (((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) != 0)
     return set_error(HMF_ERR_ARG, "factor arrays must be 16-byte aligned");
   cudaError_t e;
-  const bool tma = g_qband_impl == 1;
+  const int impl = g_qband_impl;
   switch (k) {
 #define HMF_QB_CASE(KK)                                                                       \
   case KK:                                                                                    \
-    e = tma ? launch_tma<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, \
-                                ri, seed, row_base, col_base, stream)                         \
-            : launch<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, \
+    if (impl == 2 && async_ok<KK, S>())                                                       \
+      e = launch_async_if<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr,   \
+                                 ru, ri, seed, row_base, col_base, stream);                   \
+    else if (impl == 1)                                                                       \
+      e = launch_tma<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, \
                             seed, row_base, col_base, stream);                                \
+    else                                                                                      \
+      e = launch<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri,    \
+                        seed, row_base, col_base, stream);                                    \
     break;
     HMF_QB_CASE(32)
     HMF_QB_CASE(64)
@@ -517,13 +744,31 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
 
 template <typename S>
 static int warps_per_sm(int64_t k) {
-  const bool tma = g_qband_impl == 1;
+  const int impl = g_qband_impl;
   switch (k) {
-    case 32: return tma ? tma_warps_per_sm<32, S>() : reg_warps_per_sm<32, S>();
-    case 64: return tma ? tma_warps_per_sm<64, S>() : reg_warps_per_sm<64, S>();
-    case 128: return tma ? tma_warps_per_sm<128, S>() : reg_warps_per_sm<128, S>();
-    case 256: return tma ? tma_warps_per_sm<256, S>() : reg_warps_per_sm<256, S>();
+#define HMF_WPS(KK)                                                                   \
+  case KK:                                                                            \
+    if (impl == 2 && async_ok<KK, S>()) return async_warps_per_sm_if<KK, S>();        \
+    return impl == 1 ? tma_warps_per_sm<KK, S>() : reg_warps_per_sm<KK, S>();
+    HMF_WPS(32)
+    HMF_WPS(64)
+    HMF_WPS(128)
+    HMF_WPS(256)
+#undef HMF_WPS
     default: return 0;
+  }
+}
+
+// Q-slice budget of the active implementation (bytes of fp32 Q per warp)
+template <typename S>
+static int slice_bytes(int64_t k) {
+  if (g_qband_impl != 2) return kSliceBytes;
+  switch (k) {
+    case 32: return async_ok<32, S>() ? AsyncLayout<32, S, 4>::SLICE : kSliceBytes;
+    case 64: return async_ok<64, S>() ? AsyncLayout<64, S, 4>::SLICE : kSliceBytes;
+    case 128: return async_ok<128, S>() ? AsyncLayout<128, S, 4>::SLICE : kSliceBytes;
+    case 256: return async_ok<256, S>() ? AsyncLayout<256, S, 4>::SLICE : kSliceBytes;
+    default: return kSliceBytes;
   }
 }
 
@@ -537,14 +782,16 @@ int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16) {
 }
 
 int hmf_qband_set_impl(int32_t impl) {
-  if (impl != 0 && impl != 1) return int(hmf::set_error(HMF_ERR_ARG, "impl must be 0 or 1"));
+  if (impl < 0 || impl > 2) return int(hmf::set_error(HMF_ERR_ARG, "impl must be 0, 1 or 2"));
   hmf::qs::g_qband_impl = impl;
   return HMF_OK;
 }
 
 int32_t hmf_qband_max_items(int64_t k) {
   if (k != 32 && k != 64 && k != 128 && k != 256) return 0;
-  return int32_t(hmf::qs::kSliceBytes / (k * 4));
+  // the tighter of the fp32 / fp16 budgets of the active implementation
+  const int b = min(hmf::qs::slice_bytes<float>(k), hmf::qs::slice_bytes<__half>(k));
+  return int32_t(b / (k * 4));
 }
 
 int64_t hmf_sgd_block_qband_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,

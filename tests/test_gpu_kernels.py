@@ -394,7 +394,7 @@ def test_qband_bucketing_contract(dev, k):
             assert np.all((seg >= cuts[s]) & (seg < cuts[s + 1]))
 
 
-@pytest.fixture(params=[1, 0], ids=["tma", "regs"])
+@pytest.fixture(params=[2, 1, 0], ids=["cpasync", "tma", "regs"])
 def qband_impl(request):
     from paper_2006_15980_b200 import _lib
     _lib.check(_lib.load().hmf_qband_set_impl(request.param), "set_impl")
