@@ -268,7 +268,13 @@ def run_ours(args, world, rank, local):
     row_cuts = np.array([0, n_users], dtype=np.int64)
     col_cuts = np.array([0, (n_items + 1) // 2, n_items], dtype=np.int64)
     grid = build_device_grid(train, row_cuts, col_cuts)
-    del trip
+    # free the generator's arrays (train/test are views of them): keep a
+    # compact copy of the test set only — Hugewiki needs the headroom
+    from paper_2006_15980_b200.data import DeviceTriples
+    test = DeviceTriples(test.n_users, test.n_items, test.users.clone(), test.items.clone(),
+                         test.ratings.clone())
+    del trip, train
+    torch.cuda.empty_cache()
     stream_epoch = None
     if not args.no_e2e and args.kernel == "qband" and world == 1:
         from paper_2006_15980_b200.workers import StreamingEpoch

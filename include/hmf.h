@@ -187,6 +187,12 @@ int64_t hmf_synthetic_count(int64_t n_rows, int64_t n_cols, double p, uint64_t s
 int hmf_synthetic_cells(int64_t n_rows, int64_t n_cols, double p, uint64_t seed,
                         const int64_t* row_ptr, int32_t* out_rows, int32_t* out_cols,
                         void* stream);
+/* out[i] = in[pi(i)] for i < n_out, pi a keyed pseudo-random permutation of
+ * [0, n_in) (Feistel network with cycle walking): the reference's
+ * permutation(chosen)[:target] without a sort or an index array. */
+int hmf_permute_cells(const int32_t* in_rows, const int32_t* in_cols, int64_t n_in,
+                      int32_t* out_rows, int32_t* out_cols, int64_t n_out, uint64_t seed,
+                      void* stream);
 int hmf_synthetic_fill(const int32_t* rows, const int32_t* cols, int64_t n, int32_t rank,
                        double noise, double factor_scale, uint64_t seed, float* vals,
                        void* stream);

@@ -64,6 +64,7 @@ SIGNATURES = {
     "hmf_synthetic_count": (_i64, [_i64, _i64, _f64, _u64, _p, _p]),
     "hmf_synthetic_cells": (C.c_int, [_i64, _i64, _f64, _u64, _p, _p, _p, _p]),
     "hmf_synthetic_fill": (C.c_int, [_p, _p, _i64, _i32, _f64, _f64, _u64, _p, _p]),
+    "hmf_permute_cells": (C.c_int, [_p, _p, _i64, _p, _p, _i64, _u64, _p]),
     "hmf_device_count": (C.c_int, [C.POINTER(_i32)]),
     "hmf_set_device": (C.c_int, [_i32]),
     "hmf_enable_peer_access": (C.c_int, [_i32, _i32]),

@@ -91,6 +91,43 @@ __global__ void synth_fill_kernel(const int32_t* __restrict__ rows,
   }
 }
 
+// Keyed pseudo-random permutation of [0, n): a 4-round balanced Feistel
+// network over [0, 4^h) >= n with cycle walking (expected < 4 steps), so a
+// random reordering of billions of cells needs no sort and no index array.
+struct Feistel {
+  uint32_t half_bits;
+  uint64_t mask, keys[4];
+  __device__ uint64_t round(uint64_t r, int i) const {
+    return splitmix_finalize(r * kGolden ^ keys[i]) & mask;
+  }
+  __device__ uint64_t once(uint64_t x) const {
+    uint64_t l = x >> half_bits, r = x & mask;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint64_t t = l ^ round(r, i);
+      l = r;
+      r = t;
+    }
+    return (l << half_bits) | r;
+  }
+  __device__ uint64_t operator()(uint64_t x, uint64_t n) const {
+    do { x = once(x); } while (x >= n);
+    return x;
+  }
+};
+
+__global__ void permute_cells_kernel(const int32_t* __restrict__ in_rows,
+                                     const int32_t* __restrict__ in_cols, int64_t n_in,
+                                     int32_t* __restrict__ out_rows, int32_t* __restrict__ out_cols,
+                                     int64_t n_out, Feistel f) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_out;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = int64_t(f(uint64_t(i), uint64_t(n_in)));
+    out_rows[i] = in_rows[j];
+    out_cols[i] = in_cols[j];
+  }
+}
+
 static double log_keep(double p) {
   if (p >= 1.0) return 0.0;
   return log1p(-p);
@@ -129,6 +166,28 @@ int hmf_synthetic_cells(int64_t n_rows, int64_t n_cols, double p, uint64_t seed,
   const int64_t blocks = n_rows > 0 ? (n_rows + 255) / 256 : 1;
   hmf::synth_cells_kernel<<<unsigned(blocks < 65535 * 16 ? blocks : 65535 * 16), 256, 0, stream>>>(
       n_rows, n_cols, hmf::log_keep(p), seed, row_ptr, out_rows, out_cols);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HMF_OK : int(hmf::set_cuda_error(e));
+}
+
+int hmf_permute_cells(const int32_t* in_rows, const int32_t* in_cols, int64_t n_in,
+                      int32_t* out_rows, int32_t* out_cols, int64_t n_out, uint64_t seed,
+                      void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (n_in < 0 || n_out < 0 || n_out > n_in)
+    return int(hmf::set_error(HMF_ERR_ARG, "need 0 <= n_out <= n_in"));
+  if (n_out == 0) return HMF_OK;
+  hmf::Feistel f;
+  uint32_t bits = 1;
+  while ((uint64_t(1) << (2 * bits)) < uint64_t(n_in)) ++bits;
+  f.half_bits = bits;
+  f.mask = (uint64_t(1) << bits) - 1;
+  for (int i = 0; i < 4; ++i) f.keys[i] = hmf::splitmix_finalize(seed + uint64_t(i + 1) * hmf::kMixB);
+  int64_t blocks = (n_out + 255) / 256;
+  const int64_t cap = int64_t(hmf::device_sm_count()) * 32;
+  if (blocks > cap) blocks = cap;
+  hmf::permute_cells_kernel<<<unsigned(blocks), 256, 0, stream>>>(in_rows, in_cols, n_in, out_rows,
+                                                                  out_cols, n_out, f);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? HMF_OK : int(hmf::set_cuda_error(e));
 }

@@ -566,12 +566,13 @@ def synthetic_device(n_users: int, n_items: int, nnz: int, rank: int = 8, noise:
     _lib.check(lib.hmf_synthetic_cells(n_users, n_items, p, gseed, row_ptr.data_ptr(),
                                        users.data_ptr(), items.data_ptr(), s), "hmf_synthetic_cells")
     del row_ptr
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(int(seed) & 0x7FFFFFFFFFFFFFFF)
-    keep = torch.randperm(got, device=dev, generator=gen)[:nnz]
-    users = users[keep].contiguous()
-    items = items[keep].contiguous()
-    del keep
+    # random order, first nnz kept (a keyed permutation: no sort, no index array)
+    out_u = torch.empty(nnz, dtype=torch.int32, device=dev)
+    out_i = torch.empty(nnz, dtype=torch.int32, device=dev)
+    _lib.check(lib.hmf_permute_cells(users.data_ptr(), items.data_ptr(), got, out_u.data_ptr(),
+                                     out_i.data_ptr(), nnz, (seed * 0x2545F491 + 7) & 0xFFFFFFFFFFFFFFFF,
+                                     s), "hmf_permute_cells")
+    users, items = out_u, out_i
     vals = torch.empty(nnz, dtype=torch.float32, device=dev)
     _lib.check(lib.hmf_synthetic_fill(users.data_ptr(), items.data_ptr(), nnz, rank, noise,
                                       factor_scale, (seed + 0x5EED) & 0xFFFFFFFFFFFFFFFF,
