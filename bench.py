@@ -253,6 +253,7 @@ def run_ours(args, world, rank, local):
     if args.variant is not None:
         _lib.set_variant(args.variant)
     _lib.check(_lib.load().hmf_qband_set_impl(args.qband_impl), "hmf_qband_set_impl")
+    _lib.check(_lib.load().hmf_qband_set_chain_cfg(args.chain_cfg), "hmf_qband_set_chain_cfg")
     dev = torch.device("cuda", local)
     n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
     k = args.k or k0
@@ -268,6 +269,7 @@ def run_ours(args, world, rank, local):
     row_cuts = np.array([0, n_users], dtype=np.int64)
     col_cuts = np.array([0, (n_items + 1) // 2, n_items], dtype=np.int64)
     grid = build_device_grid(train, row_cuts, col_cuts)
+    tile_bytes = None if args.tile_mb is None else int(args.tile_mb * (1 << 20))
     # free the generator's arrays (train/test are views of them): keep a
     # compact copy of the test set only — Hugewiki needs the headroom
     from paper_2006_15980_b200.data import DeviceTriples
@@ -278,9 +280,9 @@ def run_ours(args, world, rank, local):
     stream_epoch = None
     if not args.no_e2e and args.kernel == "qband" and world == 1:
         from paper_2006_15980_b200.workers import StreamingEpoch
-        stream_epoch = StreamingEpoch(grid, k)   # stripes of the random-order grid
+        stream_epoch = StreamingEpoch(grid, k, tile_bytes=tile_bytes)
     if args.kernel == "qband":
-        bucket_qbands(grid, k)
+        bucket_qbands(grid, k, tile_bytes=tile_bytes, elem_bytes=2 if precision == "f16" else 4)
     model = init_device_model(n_users, n_items, k, SEED, device=dev,
                               dtype="float16" if precision == "f16" else "float32")
     torch.cuda.synchronize(dev)
@@ -386,7 +388,10 @@ def run_ours(args, world, rank, local):
                        "grid": "uniform 1x2 (1 batch worker per GPU)",
                        "parallelism": f"replica x{world}" if world > 1 else "single GPU",
                        "lr": LR, "reg": REG, "mode": args.mode, "kernel": args.kernel,
-                       "variant": args.variant,
+                       "variant": args.variant, "qband_impl": args.qband_impl,
+                       "chain_cfg": args.chain_cfg if args.qband_impl == 4 else None,
+                       "row_tiles": (list(grid.sub_tiles) if getattr(grid, "sub_tiles", None)
+                                     else None),
                        "l2": "inputs larger than L2 (P + triples >> 126 MB); no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -561,8 +566,12 @@ def main():
                     help="qband: Q band in shared memory (engine fast path); hogwild: "
                          "global-Q kernel behind hmf_sgd_range")
     ap.add_argument("--multi-kernel", choices=["auto", "qband", "range"], default="auto")
-    ap.add_argument("--qband-impl", type=int, choices=[0, 1, 2], default=0,
+    ap.add_argument("--qband-impl", type=int, choices=[0, 1, 2, 3, 4], default=0,
                     help="Q-band kernel: 0 = register prefetch (default), 1 = TMA pipeline")
+    ap.add_argument("--chain-cfg", type=int, choices=[0, 1, 2, 3], default=1,
+                    help="configuration of Q-band implementation 4 (qchain.cuh ChainCfg)")
+    ap.add_argument("--tile-mb", type=float, default=None,
+                    help="P rows per Q-band row tile in MiB (default data.QBAND_TILE_BYTES; 0 = no tiling)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

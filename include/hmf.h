@@ -102,6 +102,13 @@ int64_t hmf_sgd_range_f64(double* user_f, double* item_f, int64_t k, const int32
  * sub-band may span at most hmf_qband_max_items(k) items; k in
  * {32, 64, 128, 256}; ratings are f32.  Same update rule and indexing
  * (row_base / col_base) as hmf_sgd_range_*.  Returns 0 or < 0.
+ *
+ * Row tiles: with n_tiles > 1 the block's triples are bucketed tile-major
+ * (n_tiles row tiles x n_sub sub-bands, sub_ptr holding n_tiles*n_sub + 1
+ * offsets); tile t's sub-band s is [sub_ptr[t*n_sub+s], sub_ptr[t*n_sub+s+1]).
+ * The launch walks the tiles in a seeded rotation so that one tile's P rows
+ * stay resident in L2; sub-band s keeps the same owning warp in every tile.
+ * n_tiles = 1 is the plain sub-band layout.
  */
 int32_t hmf_qband_max_items(int64_t k);
 /* Warps per SM the Q-band kernel keeps resident (one sub-band each); needs a
@@ -110,18 +117,28 @@ int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16);
 /* Q-band implementation: 0 = register prefetch + per-lane vector reductions
  * (default), 1 = TMA pipeline (bulk P-row loads into a shared ring, bulk
  * reductions of P deltas), 2 = per-lane cp.async ring of P rows + vector
- * reductions.  hmf_qband_max_items depends on the active implementation. */
+ * reductions, 3 = implementation 0 with one CTA per SM and twice the
+ * prefetch depth, 4 = chained item runs (several lane groups per warp, each
+ * walking its own sub-band with the item's Q row in registers).
+ * hmf_qband_max_items and hmf_qband_warps_per_sm (sub-band slots per SM:
+ * chains for implementation 4) depend on the active implementation. */
 int hmf_qband_set_impl(int32_t impl);
+/* Implementation 4 (chained item runs, qchain.cuh): configuration 0..3
+ * (lanes per chain, prefetch distance, occupancy) and the lanes per chain it
+ * uses for k; the chain walks full batches of that many triples in a seeded
+ * rotation, then the partial batch. */
+int hmf_qband_set_chain_cfg(int32_t cfg);
+int32_t hmf_qband_chain_lanes(int64_t k);
 int64_t hmf_sgd_block_qband_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
                                 const int32_t* cols, const float* vals, const int64_t* sub_ptr,
-                                const int32_t* sub_cuts, int64_t n_sub, double lr, double reg_user,
-                                double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
-                                void* stream);
+                                const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles, double lr,
+                                double reg_user, double reg_item, uint64_t seed, int64_t row_base,
+                                int64_t col_base, void* stream);
 int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                 const int32_t* rows, const int32_t* cols, const float* vals,
                                 const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
-                                double lr, double reg_user, double reg_item, uint64_t seed,
-                                int64_t row_base, int64_t col_base, void* stream);
+                                int64_t n_tiles, double lr, double reg_user, double reg_item,
+                                uint64_t seed, int64_t row_base, int64_t col_base, void* stream);
 
 /*
  * The reference visit order of a range of n triples under `seed`

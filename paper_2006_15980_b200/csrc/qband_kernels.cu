@@ -17,6 +17,13 @@
 // Versus the global-Q HOGWILD kernel this removes the Q loads and Q
 // reductions from the SM->L2 path (half of its traffic, the binding unit in
 // the r01 ncu profile) and all races on Q.
+//
+// Row tiles (L2 residency of P).  The block's user span is cut into n_tiles
+// equal row tiles sized to sit in L2; triples are bucketed tile-major, so
+// sub-band s of tile t is [sub_ptr[t*n_sub+s], sub_ptr[t*n_sub+s+1]).  All
+// warps walk the tiles in one seeded rotation: the P rows live at any moment
+// are about one tile's, so P reads and reductions hit L2 instead of HBM.
+// Sub-band s belongs to the same warp in every tile, so Q stays race-free.
 #include "hmf_common.cuh"
 #include "hmf_internal.h"
 #include "lanevec.cuh"
@@ -36,6 +43,22 @@ template <int K, typename S> using Lay = RowLay<K, S>;
 
 constexpr int stage_bytes = kChunk * 12;
 constexpr int warp_bytes = kSliceBytes + 2 * stage_bytes + 16;
+
+// i-th row tile of an epoch: the same seeded rotation for every warp
+__device__ inline int tile_at(int i, int n_tiles, uint64_t seed) {
+  if (n_tiles <= 1) return 0;
+  const int rot = int(splitmix_finalize(seed ^ 0x5851F42D4C957F2DULL) % uint64_t(n_tiles));
+  const int t = i + rot;
+  return t >= n_tiles ? t - n_tiles : t;
+}
+
+}  // namespace qs
+}  // namespace hmf
+
+#include "qchain.cuh"
+
+namespace hmf {
+namespace qs {
 
 struct Ring {
   int32_t* rows;
@@ -70,12 +93,12 @@ __device__ inline void stage(const Ring& r, uint64_t* bar, const int32_t* rows,
   }
 }
 
-template <int K, typename S, int U>
-__global__ void __launch_bounds__(kWarps * 32, 2)
+template <int K, typename S, int U, int MINB = 2>
+__global__ void __launch_bounds__(kWarps * 32, MINB)
     qband_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const int32_t* __restrict__ rows,
                  const int32_t* __restrict__ cols, const float* __restrict__ vals,
                  const int64_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_cuts,
-                 int n_sub, float lr, float ru, float ri, uint64_t seed) {
+                 int n_sub, int n_tiles, float lr, float ru, float ri, uint64_t seed) {
   using L = Lay<K, S>;
   constexpr int E = L::EPL;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -94,10 +117,15 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
                          reinterpret_cast<uintptr_t>(vals)) & 15u) == 0;
   uint32_t phase[2] = {0u, 0u};
 
+  for (int ti = 0; ti < n_tiles; ++ti) {
+  const int tile = tile_at(ti, n_tiles, seed);
+  const int64_t* sp = sub_ptr + int64_t(tile) * n_sub;
+  const uint64_t bin0 = uint64_t(tile) * uint64_t(n_sub);
   for (int s = blockIdx.x * kWarps + warp; s < n_sub; s += tw) {
     const int c_lo = sub_cuts[s];
     const int n_items = sub_cuts[s + 1] - c_lo;
     if (n_items > kSliceBytes / (K * 4)) __trap();  // host contract: slice fits
+    if (sp[s + 1] <= sp[s]) continue;  // no triples in this tile: nothing to stage
     S* qrow0 = Qb + int64_t(c_lo) * K;
     // 1. Q slice -> shared memory (fp32)
     for (int it = 0; it < n_items; ++it) {
@@ -105,13 +133,14 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       Lay<K, S>::ldg(qrow0 + int64_t(it) * K, lane, t);
       Lay<K, S>::stsf(qslice + it * K, lane, t);
     }
-    const int64_t beg = sub_ptr[s], end = sub_ptr[s + 1];
+    const int64_t beg = sp[s], end = sp[s + 1];
     const int64_t a0 = beg & ~int64_t(3);
     const int64_t n_chunks = (end - a0 + kChunk - 1) / kChunk;
     // seeded rotation of the chunk visit order (fresh order every epoch)
-    const int64_t rot = n_chunks > 0 ? int64_t(splitmix_finalize(seed + uint64_t(s) * kGolden) %
-                                                uint64_t(n_chunks))
-                                     : 0;
+    const int64_t rot =
+        n_chunks > 0
+            ? int64_t(splitmix_finalize(seed + (bin0 + uint64_t(s)) * kGolden) % uint64_t(n_chunks))
+            : 0;
     auto chunk_begin = [&](int64_t x) -> int64_t {
       int64_t c = x + rot;
       if (c >= n_chunks) c -= n_chunks;
@@ -122,6 +151,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       stage(ring_at(wbase, 0), &bars[0], rows, cols, vals, cb, min(cb + kChunk, end), bulk_ok,
             lane);
     }
+    int qcur = -1;  // slice index of the Q row held in q[]
+    float q[E];
     __syncwarp();
     for (int64_t x = 0; x < n_chunks; ++x) {
       const int b = int(x & 1);
@@ -159,9 +190,14 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
         for (int j = 0; j < U; ++j) {
           if (uc[j] >= 0) {
             const int i = base + j;
-            float* qs_row = qslice + (r.cols[i] - c_lo) * K;
-            float q[E];
-            Lay<K, S>::ldsf(qs_row, lane, q);
+            // item runs: the current item's Q row stays in registers; the
+            // shared slice is touched only when the item changes (warp-uniform)
+            const int v = r.cols[i] - c_lo;
+            if (v != qcur) {
+              if (qcur >= 0) Lay<K, S>::stsf(qslice + qcur * K, lane, q);
+              Lay<K, S>::ldsf(qslice + v * K, lane, q);
+              qcur = v;
+            }
             float d = 0.f;
 #pragma unroll
             for (int e = 0; e < E; ++e) d += pc[j][e] * q[e];
@@ -173,8 +209,6 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
               pc[j][e] = lr * (err * qv - ru * pu);
               q[e] = qv + lr * (err * pu - ri * qv);
             }
-            Lay<K, S>::stsf(qs_row, lane, q);
-            __syncwarp();
             Lay<K, S>::red(Pb + int64_t(uc[j]) * K, lane, pc[j]);
           }
         }
@@ -187,6 +221,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       }
       __syncwarp();
     }
+    if (qcur >= 0) Lay<K, S>::stsf(qslice + qcur * K, lane, q);
+    __syncwarp();
     // 4. Q slice back to HBM (rounded to the storage type once per lease)
     for (int it = 0; it < n_items; ++it) {
       float t[E];
@@ -195,6 +231,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
     }
     __syncwarp();
   }
+  }  // tiles
 }
 
 // ---------------------------------------------------------------------------
@@ -247,7 +284,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     qtma_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const int32_t* __restrict__ rows,
                 const int32_t* __restrict__ cols, const float* __restrict__ vals,
                 const int64_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_cuts,
-                int n_sub, float lr, float ru, float ri, uint64_t seed) {
+                int n_sub, int n_tiles, float lr, float ru, float ri, uint64_t seed) {
   using T = TmaLayout<K, S, D, E>;
   constexpr int EL = Lay<K, S>::EPL;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -271,22 +308,26 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
   uint32_t tpar[2] = {0u, 0u};  // wait parity per triple stage
   uint32_t issued = 0, consumed = 0;
 
+  for (int ti = 0; ti < n_tiles; ++ti) {
+  const int tile = tile_at(ti, n_tiles, seed);
+  const int64_t* sp = sub_ptr + int64_t(tile) * n_sub;
+  const uint64_t bin0 = uint64_t(tile) * uint64_t(n_sub);
   for (int s = blockIdx.x * WPB + warp; s < n_sub; s += tw) {
     const int c_lo = sub_cuts[s];
     const int n_items = sub_cuts[s + 1] - c_lo;
     if (n_items > kSliceBytes / (K * 4)) __trap();
-    if (sub_ptr[s + 1] <= sub_ptr[s]) continue;  // no triples: nothing to stage
+    if (sp[s + 1] <= sp[s]) continue;  // no triples: nothing to stage
     S* qrow0 = Qb + int64_t(c_lo) * K;
     for (int it = 0; it < n_items; ++it) {
       float t[EL];
       Lay<K, S>::ldg(qrow0 + int64_t(it) * K, lane, t);
       Lay<K, S>::stsf(qslice + it * K, lane, t);
     }
-    const int64_t beg = sub_ptr[s], end = sub_ptr[s + 1];
+    const int64_t beg = sp[s], end = sp[s + 1];
     const int64_t a0 = beg & ~int64_t(3);
     const int n_chunks = int((end - a0 + kChunk - 1) / kChunk);
     if (n_chunks <= 0) continue;
-    const int rot = int(splitmix_finalize(seed + uint64_t(s) * kGolden) % uint64_t(n_chunks));
+    const int rot = int(splitmix_finalize(seed + (bin0 + uint64_t(s)) * kGolden) % uint64_t(n_chunks));
     auto cbeg = [&](int x) -> int64_t {
       int c = x + rot;
       if (c >= n_chunks) c -= n_chunks;
@@ -387,6 +428,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     }
     __syncwarp();
   }
+  }  // tiles
   if (lane == 0) bulk_wait_all();
   __syncwarp();
 }
@@ -403,7 +445,7 @@ template <int K, typename S> struct TmaCfg {
 template <int K, typename S>
 static cudaError_t launch_tma(S* P, S* Q, const int32_t* rows, const int32_t* cols,
                               const float* vals, const int64_t* sub_ptr, const int32_t* sub_cuts,
-                              int n_sub, double lr, double ru, double ri, uint64_t seed,
+                              int n_sub, int n_tiles, double lr, double ru, double ri, uint64_t seed,
                               int64_t row_base, int64_t col_base, cudaStream_t stream) {
   using C = TmaCfg<K, S>;
   using T = TmaLayout<K, S, C::D, C::E>;
@@ -422,7 +464,7 @@ static cudaError_t launch_tma(S* P, S* Q, const int32_t* rows, const int32_t* co
   const int grid = want < cap ? want : cap;
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
-                                            sub_ptr, sub_cuts, n_sub, float(lr), float(ru),
+                                            sub_ptr, sub_cuts, n_sub, n_tiles, float(lr), float(ru),
                                             float(ri), seed);
   return cudaGetLastError();
 }
@@ -439,10 +481,17 @@ static int tma_warps_per_sm() {
   return per_sm * C::WPB;
 }
 
-template <int K, typename S>
+// register-prefetch configurations: impl 0 = 2 CTAs/SM, U ratings per group;
+// impl 3 = 1 CTA/SM with twice the registers and a group twice as deep
+template <int K, bool Deep> struct RegCfg {
+  static constexpr int U = ((K / 32) >= 4 ? 2 : 4) * (Deep ? 2 : 1);
+  static constexpr int MINB = Deep ? 1 : 2;
+};
+
+template <int K, typename S, bool Deep = false>
 static int reg_warps_per_sm() {
-  constexpr int U = (K / 32) >= 4 ? 2 : 4;
-  auto kern = qband_kernel<K, S, U>;
+  using C = RegCfg<K, Deep>;
+  auto kern = qband_kernel<K, S, C::U, C::MINB>;
   const int smem = kWarps * warp_bytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int per_sm = 0;
@@ -490,7 +539,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     qasync_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const int32_t* __restrict__ rows,
                   const int32_t* __restrict__ cols, const float* __restrict__ vals,
                   const int64_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_cuts,
-                  int n_sub, float lr, float ru, float ri, uint64_t seed) {
+                  int n_sub, int n_tiles, float lr, float ru, float ri, uint64_t seed) {
   using L = Lay<K, S>;
   using AL = AsyncLayout<K, S, D>;
   constexpr int E = L::EPL;
@@ -525,11 +574,15 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     for (int v = 0; v < L::NV; ++v) cp_async<VB>(dst + L::off(v, lane), src + L::off(v, lane));
   };
 
+  for (int ti = 0; ti < n_tiles; ++ti) {
+  const int tile = tile_at(ti, n_tiles, seed);
+  const int64_t* sp = sub_ptr + int64_t(tile) * n_sub;
+  const uint64_t bin0 = uint64_t(tile) * uint64_t(n_sub);
   for (int s = blockIdx.x * WPB + warp; s < n_sub; s += tw) {
     const int c_lo = sub_cuts[s];
     const int n_items = sub_cuts[s + 1] - c_lo;
     if (n_items * K * 4 > AL::SLICE) __trap();  // host contract: slice fits
-    const int64_t beg = sub_ptr[s], end = sub_ptr[s + 1];
+    const int64_t beg = sp[s], end = sp[s + 1];
     if (end <= beg) continue;
     S* qrow0 = Qb + int64_t(c_lo) * K;
     for (int it = 0; it < n_items; ++it) {
@@ -539,7 +592,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     }
     const int64_t a0 = beg & ~int64_t(3);
     const int64_t n_chunks = (end - a0 + kChunk - 1) / kChunk;
-    const int64_t rot = int64_t(splitmix_finalize(seed + uint64_t(s) * kGolden) % uint64_t(n_chunks));
+    const int64_t rot = int64_t(splitmix_finalize(seed + (bin0 + uint64_t(s)) * kGolden) % uint64_t(n_chunks));
     auto chunk_begin = [&](int64_t x) -> int64_t {
       int64_t c = x + rot;
       if (c >= n_chunks) c -= n_chunks;
@@ -602,6 +655,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     }
     __syncwarp();
   }
+  }  // tiles
 }
 
 template <int K, typename S> struct AsyncCfg {
@@ -614,7 +668,7 @@ template <int K, typename S> struct AsyncCfg {
 template <int K, typename S>
 static cudaError_t launch_async(S* P, S* Q, const int32_t* rows, const int32_t* cols,
                                 const float* vals, const int64_t* sub_ptr, const int32_t* sub_cuts,
-                                int n_sub, double lr, double ru, double ri, uint64_t seed,
+                                int n_sub, int n_tiles, double lr, double ru, double ri, uint64_t seed,
                                 int64_t row_base, int64_t col_base, cudaStream_t stream) {
   using C = AsyncCfg<K, S>;
   using AL = AsyncLayout<K, S, C::D>;
@@ -633,7 +687,7 @@ static cudaError_t launch_async(S* P, S* Q, const int32_t* rows, const int32_t* 
   const int grid = want < cap ? want : cap;
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
-                                            sub_ptr, sub_cuts, n_sub, float(lr), float(ru),
+                                            sub_ptr, sub_cuts, n_sub, n_tiles, float(lr), float(ru),
                                             float(ri), seed);
   return cudaGetLastError();
 }
@@ -658,11 +712,11 @@ template <int K, typename S> constexpr bool async_ok() {
 template <int K, typename S>
 static cudaError_t launch_async_if(S* P, S* Q, const int32_t* rows, const int32_t* cols,
                                    const float* vals, const int64_t* sub_ptr,
-                                   const int32_t* sub_cuts, int n_sub, double lr, double ru,
+                                   const int32_t* sub_cuts, int n_sub, int n_tiles, double lr, double ru,
                                    double ri, uint64_t seed, int64_t row_base, int64_t col_base,
                                    cudaStream_t stream) {
   if constexpr (async_ok<K, S>())
-    return launch_async<K, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, n_sub, lr, ru, ri, seed,
+    return launch_async<K, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, n_sub, n_tiles, lr, ru, ri, seed,
                               row_base, col_base, stream);
   else
     return cudaErrorNotSupported;
@@ -679,14 +733,14 @@ constexpr int max_items() {
   return kSliceBytes / (K * 4);
 }
 
-template <int K, typename S>
+template <int K, typename S, bool Deep = false>
 static cudaError_t launch(S* P, S* Q, const int32_t* rows, const int32_t* cols, const float* vals,
-                          const int64_t* sub_ptr, const int32_t* sub_cuts, int n_sub, double lr,
-                          double ru, double ri, uint64_t seed, int64_t row_base, int64_t col_base,
-                          cudaStream_t stream) {
+                          const int64_t* sub_ptr, const int32_t* sub_cuts, int n_sub, int n_tiles,
+                          double lr, double ru, double ri, uint64_t seed, int64_t row_base,
+                          int64_t col_base, cudaStream_t stream) {
   // P rows prefetched one group ahead: 2 x U x (K/32) floats per lane in flight
-  constexpr int U = (K / 32) >= 4 ? 2 : 4;
-  auto kern = qband_kernel<K, S, U>;
+  using C = RegCfg<K, Deep>;
+  auto kern = qband_kernel<K, S, C::U, C::MINB>;
   const int smem = kWarps * warp_bytes;
   static int per_sm = 0;
   if (per_sm == 0) {
@@ -701,7 +755,7 @@ static cudaError_t launch(S* P, S* Q, const int32_t* rows, const int32_t* cols, 
   const int grid = want < cap ? want : cap;
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, kWarps * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
-                                            sub_ptr, sub_cuts, n_sub, float(lr), float(ru),
+                                            sub_ptr, sub_cuts, n_sub, n_tiles, float(lr), float(ru),
                                             float(ri), seed);
   return cudaGetLastError();
 }
@@ -709,9 +763,11 @@ static cudaError_t launch(S* P, S* Q, const int32_t* rows, const int32_t* cols, 
 template <typename S>
 static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* cols,
                    const float* vals, const int64_t* sub_ptr, const int32_t* sub_cuts,
-                   int64_t n_sub, double lr, double ru, double ri, uint64_t seed,
+                   int64_t n_sub, int64_t n_tiles, double lr, double ru, double ri, uint64_t seed,
                    int64_t row_base, int64_t col_base, cudaStream_t stream) {
-  if (n_sub <= 0) return 0;
+  if (n_sub <= 0 || n_tiles <= 0) return 0;
+  if (n_sub * n_tiles > (int64_t(1) << 31))
+    return set_error(HMF_ERR_ARG, "n_sub * n_tiles too large");
   if (!P || !Q || !rows || !cols || !vals || !sub_ptr || !sub_cuts)
     return set_error(HMF_ERR_ARG, "null pointer");
   if (((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) != 0)
@@ -719,17 +775,24 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
   cudaError_t e;
   const int impl = g_qband_impl;
   switch (k) {
-#define HMF_QB_CASE(KK)                                                                       \
-  case KK:                                                                                    \
-    if (impl == 2 && async_ok<KK, S>())                                                       \
-      e = launch_async_if<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr,   \
-                                 ru, ri, seed, row_base, col_base, stream);                   \
-    else if (impl == 1)                                                                       \
-      e = launch_tma<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri, \
-                            seed, row_base, col_base, stream);                                \
-    else                                                                                      \
-      e = launch<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), lr, ru, ri,    \
-                        seed, row_base, col_base, stream);                                    \
+#define HMF_QB_CASE(KK)                                                                    \
+  case KK:                                                                                 \
+    if (impl == 2 && async_ok<KK, S>())                                                    \
+      e = launch_async_if<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub),    \
+                                 int(n_tiles), lr, ru, ri, seed, row_base, col_base,       \
+                                 stream);                                                  \
+    else if (impl == 4)                                                                    \
+      e = launch_chain<KK, S>(P, Q, rows, cols, vals, sub_ptr, int(n_sub), int(n_tiles),   \
+                              lr, ru, ri, seed, row_base, col_base, stream);               \
+    else if (impl == 3)                                                                    \
+      e = launch<KK, S, true>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub),       \
+                              int(n_tiles), lr, ru, ri, seed, row_base, col_base, stream); \
+    else if (impl == 1)                                                                    \
+      e = launch_tma<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub),         \
+                            int(n_tiles), lr, ru, ri, seed, row_base, col_base, stream);   \
+    else                                                                                   \
+      e = launch<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub), int(n_tiles), \
+                        lr, ru, ri, seed, row_base, col_base, stream);                     \
     break;
     HMF_QB_CASE(32)
     HMF_QB_CASE(64)
@@ -749,6 +812,8 @@ static int warps_per_sm(int64_t k) {
 #define HMF_WPS(KK)                                                                   \
   case KK:                                                                            \
     if (impl == 2 && async_ok<KK, S>()) return async_warps_per_sm_if<KK, S>();        \
+    if (impl == 3) return reg_warps_per_sm<KK, S, true>();                            \
+    if (impl == 4) return chain_slots_per_sm<KK, S>();                                \
     return impl == 1 ? tma_warps_per_sm<KK, S>() : reg_warps_per_sm<KK, S>();
     HMF_WPS(32)
     HMF_WPS(64)
@@ -781,14 +846,30 @@ int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16) {
   return f16 ? hmf::qs::warps_per_sm<__half>(k) : hmf::qs::warps_per_sm<float>(k);
 }
 
+int hmf_qband_set_chain_cfg(int32_t cfg) {
+  if (cfg < 0 || cfg >= hmf::qs::kChainCfgs)
+    return int(hmf::set_error(HMF_ERR_ARG, "chain configuration out of range"));
+  hmf::qs::g_chain_cfg = cfg;
+  return HMF_OK;
+}
+
+int32_t hmf_qband_chain_lanes(int64_t k) {
+  const int cfg = hmf::qs::g_chain_cfg;
+  const int per = (cfg == 2 || cfg == 3) ? 8 : 16;
+  const int lpc = int(k) / per;
+  return lpc < 4 ? 4 : (lpc > 32 ? 32 : lpc);
+}
+
 int hmf_qband_set_impl(int32_t impl) {
-  if (impl < 0 || impl > 2) return int(hmf::set_error(HMF_ERR_ARG, "impl must be 0, 1 or 2"));
+  if (impl < 0 || impl > 4)
+    return int(hmf::set_error(HMF_ERR_ARG, "impl must be 0..4"));
   hmf::qs::g_qband_impl = impl;
   return HMF_OK;
 }
 
 int32_t hmf_qband_max_items(int64_t k) {
   if (k != 32 && k != 64 && k != 128 && k != 256) return 0;
+  if (hmf::qs::g_qband_impl == 4) return 1 << 30;  // Q rows in registers: no slice bound
   // the tighter of the fp32 / fp16 budgets of the active implementation
   const int b = min(hmf::qs::slice_bytes<float>(k), hmf::qs::slice_bytes<__half>(k));
   return int32_t(b / (k * 4));
@@ -796,22 +877,23 @@ int32_t hmf_qband_max_items(int64_t k) {
 
 int64_t hmf_sgd_block_qband_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
                                 const int32_t* cols, const float* vals, const int64_t* sub_ptr,
-                                const int32_t* sub_cuts, int64_t n_sub, double lr, double reg_user,
-                                double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
-                                void* stream) {
-  return hmf::qs::run<float>(user_f, item_f, k, rows, cols, vals, sub_ptr, sub_cuts, n_sub, lr,
-                             reg_user, reg_item, seed, row_base, col_base,
+                                const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles, double lr,
+                                double reg_user, double reg_item, uint64_t seed, int64_t row_base,
+                                int64_t col_base, void* stream) {
+  return hmf::qs::run<float>(user_f, item_f, k, rows, cols, vals, sub_ptr, sub_cuts, n_sub,
+                             n_tiles, lr, reg_user, reg_item, seed, row_base, col_base,
                              static_cast<cudaStream_t>(stream));
 }
 
 int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                 const int32_t* rows, const int32_t* cols, const float* vals,
                                 const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
-                                double lr, double reg_user, double reg_item, uint64_t seed,
-                                int64_t row_base, int64_t col_base, void* stream) {
+                                int64_t n_tiles, double lr, double reg_user, double reg_item,
+                                uint64_t seed, int64_t row_base, int64_t col_base, void* stream) {
   return hmf::qs::run<__half>(reinterpret_cast<__half*>(user_f), reinterpret_cast<__half*>(item_f),
-                              k, rows, cols, vals, sub_ptr, sub_cuts, n_sub, lr, reg_user, reg_item,
-                              seed, row_base, col_base, static_cast<cudaStream_t>(stream));
+                              k, rows, cols, vals, sub_ptr, sub_cuts, n_sub, n_tiles, lr,
+                              reg_user, reg_item, seed, row_base, col_base,
+                              static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

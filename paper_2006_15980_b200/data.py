@@ -372,6 +372,9 @@ class DeviceGrid:
     # see hmf_sgd_block_qband_* and bucket_qbands().
     sub_ptr: list | None = None
     sub_cuts: list | None = None
+    # row tiles per block (L2 residency of P): sub_ptr[b] then holds
+    # sub_tiles[b] * S + 1 offsets, tile-major
+    sub_tiles: list | None = None
 
     n_row_bands = BlockGrid.n_row_bands
     n_col_bands = BlockGrid.n_col_bands
@@ -460,9 +463,32 @@ def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int) -> np.ndarray:
     return np.concatenate([[c_lo], c_lo + np.cumsum(widths)]).astype(np.int64)
 
 
-def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None) -> DeviceGrid:
-    """Re-bucket every block of a device grid by item sub-band (stable), in
-    place, and attach sub_ptr / sub_cuts for the Q-band kernel."""
+# P rows per row tile of the Q-band kernel: one tile's P rows, the Q band and
+# the triple stream share the 126 MB L2 (sweep: profiles/r02_tile_sweep*).
+QBAND_TILE_BYTES = 32 << 20
+
+
+def qband_row_tiles(n_rows: int, k: int, elem_bytes: int = 4,
+                    tile_bytes: int | None = None) -> int:
+    """Row tiles for a block spanning n_rows users: the fewest equal tiles
+    whose P rows (n_rows/T x k x elem_bytes) fit tile_bytes.  tile_bytes <= 0
+    disables tiling."""
+    tb = QBAND_TILE_BYTES if tile_bytes is None else int(tile_bytes)
+    if tb <= 0 or n_rows <= 0:
+        return 1
+    return max(1, min(n_rows, -(-(n_rows * k * elem_bytes) // tb)))
+
+
+def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
+                  tile_bytes: int | None = None, elem_bytes: int = 4) -> DeviceGrid:
+    """Re-bucket every block of a device grid for the Q-band kernel, in place:
+    row tile major, then item (both stable), and attach sub_ptr / sub_cuts /
+    sub_tiles.  Row tiles are equal user ranges of the block's row band, sized
+    by qband_row_tiles (tile_bytes <= 0: one tile).  Sorting by item inside a
+    tile makes every (tile, sub-band) range contiguous and lays each item's
+    ratings out as one run, so the kernel keeps the current item's Q row in
+    registers.  The order of ratings within an item is the block order
+    (stable), i.e. the reference's shuffled order (data.py:242-244, 264)."""
     torch = _torch()
     dev = grid.device
     lib = _lib.load()
@@ -471,36 +497,66 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None) -> Device
     out_u = torch.empty_like(grid.users)
     out_i = torch.empty_like(grid.items)
     out_r = torch.empty_like(grid.ratings)
-    row_cuts = torch.tensor([0, grid.n_rows], dtype=torch.int64, device=dev)
-    sub_ptrs, sub_cuts = [], []
+    sub_ptrs, sub_cuts, sub_tiles = [], [], []
     for b in range(grid.n_blocks):
         lo, hi = grid.block_range(b)
         c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
+        r_lo, r_hi = grid.row_span(b // grid.n_col_bands)
+        n_tiles = qband_row_tiles(r_hi - r_lo, k, elem_bytes, tile_bytes)
+        tiles = np.linspace(r_lo, r_hi, n_tiles + 1).round().astype(np.int64)
         cuts = qband_sub_cuts(c_lo, c_hi, k, target)
         n_sub = len(cuts) - 1
-        d_cuts = torch.from_numpy(cuts).to(dev)
-        ptr = torch.zeros(n_sub + 1, dtype=torch.int64, device=dev)
-        if hi > lo and n_sub > 12288:
-            # beyond the tile-histogram bucketing's bin limit: a stable key sort
-            # (layout preparation, once per grid; the reference uses
-            # np.argsort(kind="stable") here, data.py:264)
-            key = torch.bucketize(grid.items[lo:hi], d_cuts[1:-1].to(torch.int32), right=True)
-            order = torch.sort(key, stable=True).indices
-            out_u[lo:hi] = grid.users[lo:hi][order]
-            out_i[lo:hi] = grid.items[lo:hi][order]
-            out_r[lo:hi] = grid.ratings[lo:hi][order]
-            ptr[1:] = torch.cumsum(torch.bincount(key, minlength=n_sub), 0)
-            del key, order
-        elif hi > lo:
-            _lib.check(lib.hmf_bucket_triples(
-                grid.users.data_ptr() + 4 * lo, grid.items.data_ptr() + 4 * lo,
-                grid.ratings.data_ptr() + 4 * lo, hi - lo, row_cuts.data_ptr(), 1,
-                d_cuts.data_ptr(), n_sub, out_u.data_ptr() + 4 * lo, out_i.data_ptr() + 4 * lo,
-                out_r.data_ptr() + 4 * lo, ptr.data_ptr(), s), "hmf_bucket_triples")
-        sub_ptrs.append(ptr + lo)
-        sub_cuts.append(d_cuts.to(torch.int32))
-    grid.users, grid.items, grid.ratings = out_u, out_i, out_r
-    grid.sub_ptr, grid.sub_cuts = sub_ptrs, sub_cuts
+        rel = torch.from_numpy(cuts[:-1] - c_lo).to(dev)
+        ptr = torch.full((n_tiles * n_sub + 1,), hi, dtype=torch.int64, device=dev)
+        if hi > lo:
+            # 1. row-tile major (stable), grid arrays -> out_*
+            if n_tiles == 1:
+                out_u[lo:hi], out_i[lo:hi], out_r[lo:hi] = (grid.users[lo:hi],
+                                                            grid.items[lo:hi],
+                                                            grid.ratings[lo:hi])
+                tp = np.array([lo, hi], dtype=np.int64)
+            else:
+                d_tiles = torch.from_numpy(tiles).to(dev)
+                tptr = torch.zeros(n_tiles + 1, dtype=torch.int64, device=dev)
+                if n_tiles <= 12288:
+                    d_cc = torch.tensor([c_lo, c_hi], dtype=torch.int64, device=dev)
+                    _lib.check(lib.hmf_bucket_triples(
+                        grid.users.data_ptr() + 4 * lo, grid.items.data_ptr() + 4 * lo,
+                        grid.ratings.data_ptr() + 4 * lo, hi - lo, d_tiles.data_ptr(), n_tiles,
+                        d_cc.data_ptr(), 1, out_u.data_ptr() + 4 * lo,
+                        out_i.data_ptr() + 4 * lo, out_r.data_ptr() + 4 * lo, tptr.data_ptr(),
+                        s), "hmf_bucket_triples")
+                else:
+                    key = torch.bucketize(grid.users[lo:hi], d_tiles[1:-1].to(torch.int32),
+                                          right=True)
+                    order = torch.sort(key, stable=True).indices
+                    out_u[lo:hi] = grid.users[lo:hi][order]
+                    out_i[lo:hi] = grid.items[lo:hi][order]
+                    out_r[lo:hi] = grid.ratings[lo:hi][order]
+                    tptr[1:] = torch.cumsum(torch.bincount(key, minlength=n_tiles), 0)
+                    del key, order
+                tp = tptr.cpu().numpy() + lo
+            # 2. by item inside each tile (stable), out_* -> grid arrays
+            n_items = c_hi - c_lo
+            for t in range(n_tiles):
+                a, z = int(tp[t]), int(tp[t + 1])
+                if z <= a:
+                    ptr[t * n_sub:(t + 1) * n_sub] = a
+                    continue
+                key = out_i[a:z] - c_lo
+                order = torch.sort(key, stable=True).indices
+                grid.users[a:z] = out_u[a:z][order]
+                grid.items[a:z] = out_i[a:z][order]
+                grid.ratings[a:z] = out_r[a:z][order]
+                iptr = torch.zeros(n_items + 1, dtype=torch.int64, device=dev)
+                iptr[1:] = torch.cumsum(torch.bincount(key, minlength=n_items), 0)
+                ptr[t * n_sub:(t + 1) * n_sub] = iptr[rel] + a
+                del key, order, iptr
+        sub_ptrs.append(ptr)
+        sub_cuts.append(torch.from_numpy(cuts).to(device=dev, dtype=torch.int32))
+        sub_tiles.append(n_tiles)
+    del out_u, out_i, out_r
+    grid.sub_ptr, grid.sub_cuts, grid.sub_tiles = sub_ptrs, sub_cuts, sub_tiles
     return grid
 
 

@@ -120,11 +120,15 @@ def launch_block_qband(user_f, item_f, grid, block, lr, reg_user, reg_item, seed
     if hi <= lo:
         return 0
     sp, sc = grid.sub_ptr[block], grid.sub_cuts[block]
+    n_tiles = grid.sub_tiles[block] if grid.sub_tiles is not None else 1
+    n_sub = int(sc.numel()) - 1
+    if int(sp.numel()) != n_tiles * n_sub + 1:
+        raise ValueError("sub_ptr does not match sub_cuts x sub_tiles")
     s = current_stream_handle(user_f.device) if stream is None else int(stream)
     fn = getattr(_lib.load(), f"hmf_sgd_block_qband_{st}")
     _lib.check(fn(user_f.data_ptr(), item_f.data_ptr(), user_f.shape[1], grid.users.data_ptr(),
                   grid.items.data_ptr(), grid.ratings.data_ptr(), sp.data_ptr(), sc.data_ptr(),
-                  int(sp.numel()) - 1, float(lr), float(reg_user), float(reg_item),
+                  n_sub, n_tiles, float(lr), float(reg_user), float(reg_item),
                   int(seed) & _MASK64, int(row_base), int(col_base), s),
                f"hmf_sgd_block_qband_{st}")
     return hi - lo

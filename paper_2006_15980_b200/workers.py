@@ -142,7 +142,8 @@ class FactorStore:
                 with torch.cuda.device(dev):
                     g = DeviceGrid.from_host(grid, torch.device("cuda", dev), rd)
                     if kernel == "qband":
-                        bucket_qbands(g, self.k)
+                        bucket_qbands(g, self.k,
+                                      elem_bytes=2 if self.precision == "f16" else 4)
                     # built on the current stream, read by the engines' own
                     # streams: finish it before anyone launches on it
                     torch.cuda.current_stream(dev).synchronize()
@@ -452,11 +453,11 @@ class StreamingEpoch:
     traffic is exactly the triples (12 bytes per rating).
     """
 
-    def __init__(self, grid: DeviceGrid, k: int, n_stripes: int = 8):
+    def __init__(self, grid: DeviceGrid, k: int, n_stripes: int = 8, tile_bytes=None):
         from .data import stripe_layout
         torch = _torch()
         self.dev = grid.device
-        sg = bucket_qbands(stripe_layout(grid, n_stripes), k)
+        sg = bucket_qbands(stripe_layout(grid, n_stripes), k, tile_bytes=tile_bytes)
         self.k = k
         self.n_blocks = sg.n_blocks
         self.nnz = sg.nnz
@@ -468,6 +469,7 @@ class StreamingEpoch:
         # per block: sub_ptr relative to the block start (device) and sub_cuts
         self.sub_rel = [(p - int(sg.block_ptr[b])).contiguous() for b, p in enumerate(sg.sub_ptr)]
         self.sub_cuts = sg.sub_cuts
+        self.sub_tiles = sg.sub_tiles
         cap = int(np.max(np.diff(sg.block_ptr))) + 4
         self.bufs = [tuple(torch.empty(cap, dtype=dt, device=self.dev)
                            for dt in (torch.int32, torch.int32, torch.float32)) for _ in range(2)]
@@ -502,7 +504,7 @@ class StreamingEpoch:
             sp, sc = self.sub_rel[b], self.sub_cuts[b]
             _lib.check(fn(P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr(),
                           buf[1].data_ptr(), buf[2].data_ptr(), sp.data_ptr(), sc.data_ptr(),
-                          int(sp.numel()) - 1, hparams.learning_rate, hparams.reg_user,
+                          int(sc.numel()) - 1, self.sub_tiles[b], hparams.learning_rate, hparams.reg_user,
                           hparams.reg_item, kernels.mix64(seed, b) & 0xFFFFFFFFFFFFFFFF, 0, 0,
                           comp.cuda_stream), f"hmf_sgd_block_qband_{st}")
             ev = torch.cuda.Event()

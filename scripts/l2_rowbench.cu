@@ -1,0 +1,105 @@
+// L2 random-row microbenchmark: the memory pattern of the Q-band kernels
+// without their arithmetic.  Every warp-instruction touches 4 random rows of
+// ROWB bytes (8 lanes x 16 B per row, like a chain of implementation 4) in a
+// buffer that fits in L2, and either loads them (ld.global.cg), adds to them
+// (red.global.add.v4.f32), or both.  Reports rows/s per mode, the ceiling
+// for "P row read + P delta reduction" at a given row size.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o l2_rowbench l2_rowbench.cu
+//   ./l2_rowbench [buffer_MB]
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+  return x;
+}
+
+// MODE 0 = load, 1 = red, 2 = load + red of the loaded values' negation.
+// LPR lanes per row; lane l of a row group moves NV = ROWB/(16*LPR) 16-byte
+// vectors at byte offsets (v*LPR + l)*16 (the chain layout of qchain.cuh).
+template <int MODE, int ROWB, int DEPTH, int LPR>
+__global__ void __launch_bounds__(512, 1) rowbench(float* buf, uint32_t n_rows, int iters,
+                                                  float* sink) {
+  constexpr int NV = ROWB / (16 * LPR);
+  const int lane = threadIdx.x & 31;
+  const int l = lane % LPR;
+  uint32_t seed = (blockIdx.x * blockDim.x + threadIdx.x) / LPR * 7919u + 17u;
+  float acc = 0.f;
+  for (int it = 0; it < iters; ++it) {
+    float4 v[DEPTH][NV];
+    uint32_t r[DEPTH];
+#pragma unroll
+    for (int d = 0; d < DEPTH; ++d) {
+      r[d] = hash32(seed + uint32_t(it * DEPTH + d) * 0x9E3779B9u) % n_rows;
+      const float4* p = reinterpret_cast<const float4*>(buf + size_t(r[d]) * (ROWB / 4));
+#pragma unroll
+      for (int w = 0; w < NV; ++w)
+        if (MODE != 1) v[d][w] = __ldcg(p + w * LPR + l);
+    }
+#pragma unroll
+    for (int d = 0; d < DEPTH; ++d) {
+#pragma unroll
+      for (int w = 0; w < NV; ++w) {
+        float* p = buf + size_t(r[d]) * (ROWB / 4) + 4 * (w * LPR + l);
+        if (MODE == 0) {
+          acc += v[d][w].x + v[d][w].y + v[d][w].z + v[d][w].w;
+        } else {
+          const float a = MODE == 2 ? -1e-30f * v[d][w].x : 1e-30f;
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(a),
+                       "f"(a), "f"(a)
+                       : "memory");
+        }
+      }
+    }
+  }
+  if (acc == 12345.f) sink[0] = acc;
+}
+
+template <int MODE, int ROWB, int DEPTH, int LPR>
+static void run(float* buf, uint32_t n_rows, float* sink, int sms) {
+  const int iters = 400;
+  const int blocks = sms, threads = 512;
+  rowbench<MODE, ROWB, DEPTH, LPR><<<blocks, threads>>>(buf, n_rows, 4, sink);  // warm
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  rowbench<MODE, ROWB, DEPTH, LPR><<<blocks, threads>>>(buf, n_rows, iters, sink);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  const double rows = double(blocks) * threads / LPR * iters * DEPTH;
+  printf("{\"mode\": \"%s\", \"row_bytes\": %d, \"depth\": %d, \"lanes_per_row\": %d, "
+         "\"rows_per_s\": %.4g, \"GBps_rowbytes\": %.1f}\n",
+         MODE == 0 ? "load" : (MODE == 1 ? "red" : "load+red"), ROWB, DEPTH, LPR, rows / (ms * 1e-3),
+         rows * ROWB / (ms * 1e-3) / 1e9);
+}
+
+int main(int argc, char** argv) {
+  const size_t mb = argc > 1 ? size_t(atoi(argv[1])) : 32;
+  float* buf;
+  float* sink;
+  cudaMalloc(&buf, mb << 20);
+  cudaMalloc(&sink, 16);
+  cudaMemset(buf, 0, mb << 20);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  printf("{\"buffer_MB\": %zu, \"sms\": %d}\n", mb, sms);
+#define RUN3(RB, D, LPR)                                              \
+  run<0, RB, D, LPR>(buf, uint32_t((mb << 20) / RB), sink, sms);      \
+  run<1, RB, D, LPR>(buf, uint32_t((mb << 20) / RB), sink, sms);      \
+  run<2, RB, D, LPR>(buf, uint32_t((mb << 20) / RB), sink, sms);
+  RUN3(512, 4, 8)
+  RUN3(512, 8, 8)
+  RUN3(512, 4, 32)
+  RUN3(256, 4, 8)
+  RUN3(256, 8, 8)
+  RUN3(256, 4, 16)
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
+  return 0;
+}

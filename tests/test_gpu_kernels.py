@@ -371,10 +371,88 @@ def test_ml1m_quality_within_0005_of_reference(dev):
 # ---------------------------------------------------------------------------
 # Q-band-stationary kernel
 # ---------------------------------------------------------------------------
-def _qband_grid(dev, m, k, col_cuts, target):
+def _qband_grid(dev, m, k, col_cuts, target, tile_bytes=None):
     from paper_2006_15980_b200.data import DeviceTriples, bucket_qbands, build_device_grid
     g = build_device_grid(DeviceTriples.from_host(m, dev), [0, m.n_users], col_cuts)
-    return bucket_qbands(g, k, target=target)
+    return bucket_qbands(g, k, target=target, tile_bytes=tile_bytes)
+
+
+def _fin(z):
+    from paper_2006_15980_b200.kernels import _MASK64
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9 & _MASK64
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EB & _MASK64
+    return z ^ (z >> 31)
+
+
+def _chain_lanes(k):
+    """Lanes per chain of Q-band implementation 4 (qchain.cuh ChainCfg)."""
+    from paper_2006_15980_b200 import _lib
+    return int(_lib.load().hmf_qband_chain_lanes(k))
+
+
+def _bin_visit(impl, k, beg, end, seed, bin_index):
+    """Triple indices of one (tile, sub-band) bin in the kernel's visit order:
+    impl 4 walks batches of LPC triples from the bin start, the others chunks
+    of 128 from the 4-aligned base; both rotated by the bin's seed."""
+    from paper_2006_15980_b200.kernels import _MASK64
+    if end <= beg:
+        return []
+    if impl == 4:   # full batches rotated, the partial batch last
+        step = _chain_lanes(k)
+        nf = (end - beg) // step
+        out = []
+        if nf:
+            rot = _fin((seed + bin_index * 0x9E3779B97F4A7C15) & _MASK64) % nf
+            for x in range(nf):
+                c = (x + rot) % nf
+                out.extend(range(beg + c * step, beg + (c + 1) * step))
+        out.extend(range(beg + nf * step, end))
+        return out
+    step, a0 = 128, beg & ~3
+    n = (end - a0 + step - 1) // step
+    rot = _fin((seed + bin_index * 0x9E3779B97F4A7C15) & _MASK64) % n
+    out = []
+    for x in range(n):
+        c = (x + rot) % n
+        out.extend(range(max(beg, a0 + c * step), min(a0 + (c + 1) * step, end)))
+    return out
+
+
+def _tile_order(seed, n_tiles):
+    """The kernel's row-tile rotation (qband_kernels.cu tile_at)."""
+    if n_tiles <= 1:
+        return [0]
+    rot = _fin(seed ^ 0x5851F42D4C957F2D) % n_tiles
+    return [(i + rot) % n_tiles for i in range(n_tiles)]
+
+
+@pytest.mark.parametrize("n_sub_target", [7, 20000])
+def test_qband_tiled_bucketing_contract(dev, n_sub_target):
+    """Row tiles x sub-bands, tile-major, item runs inside a tile, stable;
+    with few and with many (> 12288 bins) sub-bands."""
+    from paper_2006_15980_b200.data import qband_row_tiles
+    m = random_matrix(5000, 30000, 300_000, 78)
+    k = 128
+    tb = 5000 * k * 4 // 5 + 1           # 5 row tiles of 1000 users
+    g = _qband_grid(dev, m, k, [0, 30000], target=n_sub_target, tile_bytes=tb)
+    T = qband_row_tiles(5000, k, 4, tb)
+    assert T == 5 and g.sub_tiles == [T]
+    cuts = g.sub_cuts[0].cpu().numpy()
+    S = len(cuts) - 1
+    ptr = g.sub_ptr[0].cpu().numpy()
+    assert len(ptr) == T * S + 1 and ptr[0] == 0 and ptr[-1] == m.nnz
+    assert np.all(np.diff(ptr) >= 0)
+    users, items = g.users.cpu().numpy(), g.items.cpu().numpy()
+    tiles = np.linspace(0, 5000, T + 1).round().astype(np.int64)
+    for t in range(T):
+        for s_ in range(0, S, max(1, S // 50)):
+            a, b = ptr[t * S + s_], ptr[t * S + s_ + 1]
+            assert np.all((users[a:b] >= tiles[t]) & (users[a:b] < tiles[t + 1]))
+            assert np.all((items[a:b] >= cuts[s_]) & (items[a:b] < cuts[s_ + 1]))
+    # tile-major, then item runs (stable): sub-band ranges stay contiguous
+    key = (np.searchsorted(tiles, m.users, side="right") - 1) * 30000 + m.items
+    order = np.argsort(key, kind="stable")
+    assert np.array_equal(users, m.users[order]) and np.array_equal(items, m.items[order])
 
 
 @pytest.mark.parametrize("k", [32, 64, 128, 256])
@@ -394,12 +472,16 @@ def test_qband_bucketing_contract(dev, k):
             assert np.all((seg >= cuts[s]) & (seg < cuts[s + 1]))
 
 
-@pytest.fixture(params=[2, 1, 0], ids=["cpasync", "tma", "regs"])
+@pytest.fixture(params=[(4, 1), (4, 2), (3, 0), (2, 0), (1, 0), (0, 0)],
+                ids=["chains", "chains_cfg2", "regs_deep", "cpasync", "tma", "regs"])
 def qband_impl(request):
     from paper_2006_15980_b200 import _lib
-    _lib.check(_lib.load().hmf_qband_set_impl(request.param), "set_impl")
-    yield request.param
+    impl, cfg = request.param
+    _lib.check(_lib.load().hmf_qband_set_impl(impl), "set_impl")
+    _lib.check(_lib.load().hmf_qband_set_chain_cfg(cfg if impl == 4 else 1), "set_chain_cfg")
+    yield impl
     _lib.load().hmf_qband_set_impl(0)
+    _lib.load().hmf_qband_set_chain_cfg(1)
 
 
 @pytest.mark.parametrize("k", [32, 64, 128, 256])
@@ -421,10 +503,15 @@ def test_qband_equals_sequential_per_item(dev, k, qband_impl):
     P, Q = to_dev(P0, dev), to_dev(Q0, dev)
     got = kernels.launch_block_qband(P, Q, g, 0, 0.05, 0.02, 0.03, 11)
     assert got == n
-    # sequential replay in the bucketed storage order
+    # sequential replay of every sub-band in the kernel's visit order
+    ptr = g.sub_ptr[0].cpu().numpy()
+    order = [i for b_ in range(len(ptr) - 1)
+             for i in _bin_visit(qband_impl, k, int(ptr[b_]), int(ptr[b_ + 1]), 11, b_)]
+    assert sorted(order) == list(range(n))
     Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
-    for u, v, r in zip(g.users.cpu().numpy(), g.items.cpu().numpy(),
-                       g.ratings.cpu().numpy().astype(np.float64)):
+    gu, gi = g.users.cpu().numpy(), g.items.cpu().numpy()
+    gr = g.ratings.cpu().numpy().astype(np.float64)
+    for u, v, r in zip(gu[order], gi[order], gr[order]):
         pu, qv = Pe[u].copy(), Qe[v].copy()
         e = r - pu @ qv
         Pe[u] = pu + 0.05 * (e * qv - 0.02 * pu)
@@ -433,7 +520,8 @@ def test_qband_equals_sequential_per_item(dev, k, qband_impl):
     assert rel_err(Q.double().cpu().numpy(), Qe) < 1e-5
 
 
-def test_qband_ml1m_quality_within_0005_of_reference(dev, qband_impl):
+@pytest.mark.parametrize("tile_bytes", [None, 100_000], ids=["default_tiles", "8_tiles"])
+def test_qband_ml1m_quality_within_0005_of_reference(dev, qband_impl, tile_bytes):
     from paper_2006_15980_b200 import kernels
     from paper_2006_15980_b200.data import (DeviceGrid, RatingMatrix, bucket_qbands, build_grid,
                                             shuffle_triples, synthetic_ratings)
@@ -448,7 +536,8 @@ def test_qband_ml1m_quality_within_0005_of_reference(dev, qband_impl):
     hp = Hyperparams(n_factors=32, reg_user=0.01, reg_item=0.01, learning_rate=0.01)
     grid = DeviceGrid.from_host(build_grid(shuffle_triples(train, 0), [0, 6040], [0, 1853, 3706]),
                                 dev)
-    bucket_qbands(grid, 32)
+    bucket_qbands(grid, 32, tile_bytes=tile_bytes)
+    assert grid.sub_tiles == ([1, 1] if tile_bytes is None else [8, 8])
     model = DeviceModel.from_host(init_model(6040, 3706, hp, 0), dev)
     got = {}
     for epoch in range(1, 21):
@@ -463,11 +552,13 @@ def test_qband_ml1m_quality_within_0005_of_reference(dev, qband_impl):
     assert abs(got["e5"] - ref["e5"]["test_rmse"]) <= 0.005
 
 
+@pytest.mark.parametrize("n_tiles", [1, 3])
 @pytest.mark.parametrize("k", [64, 128])
-def test_qband_multi_chunk_subbands_match_sequential(dev, k, qband_impl):
+def test_qband_multi_chunk_subbands_match_sequential(dev, k, n_tiles, qband_impl):
     """Sub-bands of several hundred triples (several staging chunks, rotated
-    per seed): with distinct users the result still equals a sequential
-    replay in the kernel's visit order (chunks rotated by the seed)."""
+    per seed), optionally split into row tiles walked in a seeded rotation:
+    with distinct users the result still equals a sequential replay in the
+    kernel's visit order."""
     from paper_2006_15980_b200 import kernels
     from paper_2006_15980_b200.data import RatingMatrix
     rng = np.random.default_rng(k + 1)
@@ -476,7 +567,9 @@ def test_qband_multi_chunk_subbands_match_sequential(dev, k, qband_impl):
     items = rng.integers(0, n_items, n).astype(np.int32)
     vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
     m = RatingMatrix(n_users, n_items, users, items, vals)
-    g = _qband_grid(dev, m, k, [0, n_items], target=n_items)
+    tb = 0 if n_tiles == 1 else n_users * k * 4 // n_tiles + 1
+    g = _qband_grid(dev, m, k, [0, n_items], target=n_items, tile_bytes=tb)
+    assert g.sub_tiles == [n_tiles]
     P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
     Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
     P, Q = to_dev(P0, dev), to_dev(Q0, dev)
@@ -487,27 +580,16 @@ def test_qband_multi_chunk_subbands_match_sequential(dev, k, qband_impl):
     gu, gi = g.users.cpu().numpy(), g.items.cpu().numpy()
     gr = g.ratings.cpu().numpy().astype(np.float64)
     ptr = g.sub_ptr[0].cpu().numpy()
+    S = g.sub_cuts[0].numel() - 1
     Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
-
-    def fin(z):
-        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9 & _MASK64
-        z = (z ^ (z >> 27)) * 0x94D049BB133111EB & _MASK64
-        return z ^ (z >> 31)
-    for s_ in range(len(ptr) - 1):
-        beg, end = int(ptr[s_]), int(ptr[s_ + 1])
-        a0 = beg & ~3
-        nch = (end - a0 + 127) // 128
-        if nch == 0:
-            continue
-        rot = fin((seed + s_ * 0x9E3779B97F4A7C15) & _MASK64) % nch
-        for x in range(nch):
-            c = (x + rot) % nch
-            for i in range(max(beg, a0 + c * 128), min(a0 + (c + 1) * 128, end)):
-                u, v, r = gu[i], gi[i], gr[i]
-                pu, qv = Pe[u].copy(), Qe[v].copy()
-                e = r - pu @ qv
-                Pe[u] = pu + 0.05 * (e * qv - 0.02 * pu)
-                Qe[v] = qv + 0.05 * (e * pu - 0.03 * qv)
+    bins = [t * S + s_ for t in _tile_order(seed, n_tiles) for s_ in range(S)]
+    for bn in bins:
+        for i in _bin_visit(qband_impl, k, int(ptr[bn]), int(ptr[bn + 1]), seed, bn):
+            u, v, r = gu[i], gi[i], gr[i]
+            pu, qv = Pe[u].copy(), Qe[v].copy()
+            e = r - pu @ qv
+            Pe[u] = pu + 0.05 * (e * qv - 0.02 * pu)
+            Qe[v] = qv + 0.05 * (e * pu - 0.03 * qv)
     assert rel_err(Q.double().cpu().numpy(), Qe) < 1e-5
     assert rel_err(P.double().cpu().numpy(), Pe) < 1e-5
 
@@ -542,7 +624,6 @@ def test_qband_bucketing_many_subbands(dev):
     for s in range(0, 20000, 97):
         seg = items[ptr[s]:ptr[s + 1]]
         assert np.all((seg >= cuts[s]) & (seg < cuts[s + 1]))
-    # stable: inside a sub-band the original (block) order is preserved
-    key = np.searchsorted(cuts, m.items, side="right") - 1
-    order = np.argsort(key, kind="stable")
+    # stable item runs: inside an item the original (block) order is preserved
+    order = np.argsort(m.items, kind="stable")
     assert np.array_equal(users, m.users[order]) and np.array_equal(items, m.items[order])
