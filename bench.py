@@ -64,6 +64,30 @@ def measured_peak():
     return 6650.0, "fallback"
 
 
+def l2_ceiling(k: int, precision: str):
+    """The measured ceiling of the dominant kernel's memory pattern once the
+    P tile sits in L2: one random k-row load plus one vector reduction into it
+    per update, no arithmetic (scripts/l2_rowbench.cu on a B200, 32 MB
+    buffer; profiles/r02/l2_rowbench.jsonl).  Best rows/s over prefetch
+    depths and lane layouts; None when that row size was not measured."""
+    p = ROOT / "profiles" / "r02" / "l2_rowbench.jsonl"
+    if not p.exists():
+        return None
+    row = k * (2 if precision == "f16" else 4)
+    mode = "load+red_f16x2" if precision == "f16" else "load+red"
+    best, buf = None, None
+    for line in p.read_text().splitlines():
+        try:
+            d = json.loads(line)
+        except ValueError:
+            continue
+        if "buffer_MB" in d:
+            buf = d["buffer_MB"]
+        elif buf == 32 and d.get("mode") == mode and d.get("row_bytes") == row:
+            best = max(best or 0.0, float(d["rows_per_s"]))
+    return best
+
+
 def bytes_per_update(k: int, precision: str) -> int:
     s = 2 if precision == "f16" else 4
     return 12 + 4 * k * s  # triple + read+write of p_u and q_v
@@ -254,6 +278,9 @@ def run_ours(args, world, rank, local):
         _lib.set_variant(args.variant)
     _lib.check(_lib.load().hmf_qband_set_impl(args.qband_impl), "hmf_qband_set_impl")
     _lib.check(_lib.load().hmf_qband_set_chain_cfg(args.chain_cfg), "hmf_qband_set_chain_cfg")
+    if args.chain_lockstep is not None:
+        _lib.check(_lib.load().hmf_qband_set_chain_lockstep(args.chain_lockstep),
+                   "hmf_qband_set_chain_lockstep")
     dev = torch.device("cuda", local)
     n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
     k = args.k or k0
@@ -340,6 +367,8 @@ def run_ours(args, world, rank, local):
     bpu = bytes_per_update(k, precision)
     achieved = mean_updates * bpu / (mean_ms / 1e3) / 1e9
     peak, peak_kind = measured_peak()
+    l2_rows = l2_ceiling(k, precision)
+    kernel_ups = mean_updates / (mean_ms / 1e3)
     traffic = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
@@ -388,13 +417,21 @@ def run_ours(args, world, rank, local):
                        "grid": "uniform 1x2 (1 batch worker per GPU)",
                        "parallelism": f"replica x{world}" if world > 1 else "single GPU",
                        "lr": LR, "reg": REG, "mode": args.mode, "kernel": args.kernel,
-                       "variant": args.variant, "qband_impl": args.qband_impl,
-                       "chain_cfg": args.chain_cfg if args.qband_impl == 4 else None,
+                       "variant": args.variant,
+                       "qband_impl": getattr(grid, "sub_impl", None),
+                       "chain_cfg": (args.chain_cfg if getattr(grid, "sub_impl", None) == 4
+                                     else None),
                        "row_tiles": (list(grid.sub_tiles) if getattr(grid, "sub_tiles", None)
                                      else None),
                        "l2": "inputs larger than L2 (P + triples >> 126 MB); no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "l2_ceiling": (None if l2_rows is None else {
+                             "updates_per_s": l2_rows, "kernel_updates_per_s": kernel_ups,
+                             "frac": kernel_ups / l2_rows,
+                             "source": "scripts/l2_rowbench.cu: random P-row load + vector "
+                                       "reduction, L2-resident 32 MB, no arithmetic "
+                                       "(profiles/r02/l2_rowbench.jsonl)"}),
                          "peak_kind": peak_kind, "bytes_per_update": bpu,
                          "kernel": ("qband_kernel" if args.kernel == "qband"
                                     else "sgd_hogwild_kernel"),
@@ -566,10 +603,11 @@ def main():
                     help="qband: Q band in shared memory (engine fast path); hogwild: "
                          "global-Q kernel behind hmf_sgd_range")
     ap.add_argument("--multi-kernel", choices=["auto", "qband", "range"], default="auto")
-    ap.add_argument("--qband-impl", type=int, choices=[0, 1, 2, 3, 4], default=0,
+    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 1, 2, 3, 4], default=-1,
                     help="Q-band kernel: 0 = register prefetch (default), 1 = TMA pipeline")
-    ap.add_argument("--chain-cfg", type=int, choices=[0, 1, 2, 3], default=1,
+    ap.add_argument("--chain-cfg", type=int, choices=list(range(7)), default=5,
                     help="configuration of Q-band implementation 4 (qchain.cuh ChainCfg)")
+    ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)
     ap.add_argument("--tile-mb", type=float, default=None,
                     help="P rows per Q-band row tile in MiB (default data.QBAND_TILE_BYTES; 0 = no tiling)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -96,12 +96,14 @@ int64_t hmf_sgd_range_f64(double* user_f, double* item_f, int64_t k, const int32
  * Q-band-stationary update of one block (the engine's fast path): the block's
  * triples are bucketed into n_sub column sub-bands (stable), sub-band s being
  * triples [sub_ptr[s], sub_ptr[s+1]) whose items lie in [sub_cuts[s],
- * sub_cuts[s+1]) (absolute item ids; device arrays).  One warp owns a
- * sub-band: its Q rows live in shared memory for the whole launch (exact
- * sequential SGD on Q), P deltas go back by vector reductions.  Each
- * sub-band may span at most hmf_qband_max_items(k) items; k in
- * {32, 64, 128, 256}; ratings are f32.  Same update rule and indexing
- * (row_base / col_base) as hmf_sgd_range_*.  Returns 0 or < 0.
+ * sub_cuts[s+1]) (absolute item ids; device arrays).  One warp (or one
+ * lane group, implementation 4) owns a sub-band: its Q rows stay on chip for
+ * the whole launch (exact sequential SGD on Q), P deltas go back by vector
+ * reductions.  Each sub-band may span at most hmf_qband_max_items_for(k, f16,
+ * impl) items; k in {32, 64, 128, 256}; ratings are f32.  Triples of a
+ * sub-band sorted by item (data.bucket_qbands) keep the current item's Q row
+ * in registers.  Same update rule and indexing (row_base / col_base) as
+ * hmf_sgd_range_*.  Returns 0 or < 0.
  *
  * Row tiles: with n_tiles > 1 the block's triples are bucketed tile-major
  * (n_tiles row tiles x n_sub sub-bands, sub_ptr holding n_tiles*n_sub + 1
@@ -111,34 +113,46 @@ int64_t hmf_sgd_range_f64(double* user_f, double* item_f, int64_t k, const int32
  * n_tiles = 1 is the plain sub-band layout.
  */
 int32_t hmf_qband_max_items(int64_t k);
-/* Warps per SM the Q-band kernel keeps resident (one sub-band each); needs a
- * current CUDA device.  f16 != 0 for fp16 storage. */
+/* The same for one storage type and implementation (impl -1: default). */
+int32_t hmf_qband_max_items_for(int64_t k, int32_t f16, int32_t impl);
+/* Sub-band slots per SM of an implementation (warps, or chains for
+ * implementation 4); needs a current CUDA device.  f16 != 0 for fp16
+ * storage; impl -1 = the default.  hmf_qband_warps_per_sm(k, f16) is
+ * hmf_qband_slots_per_sm(k, f16, -1). */
+int32_t hmf_qband_slots_per_sm(int64_t k, int32_t f16, int32_t impl);
 int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16);
-/* Q-band implementation: 0 = register prefetch + per-lane vector reductions
- * (default), 1 = TMA pipeline (bulk P-row loads into a shared ring, bulk
- * reductions of P deltas), 2 = per-lane cp.async ring of P rows + vector
- * reductions, 3 = implementation 0 with one CTA per SM and twice the
- * prefetch depth, 4 = chained item runs (several lane groups per warp, each
- * walking its own sub-band with the item's Q row in registers).
- * hmf_qband_max_items and hmf_qband_warps_per_sm (sub-band slots per SM:
- * chains for implementation 4) depend on the active implementation. */
+/* Q-band implementations: 0 = register prefetch + per-lane vector reductions,
+ * 1 = TMA pipeline (bulk P-row loads into a shared ring, bulk reductions of
+ * P deltas), 2 = per-lane cp.async ring of P rows + vector reductions, 3 =
+ * implementation 0 with one CTA per SM and twice the prefetch depth, 4 =
+ * chained item runs (several lane groups per warp, each walking its own
+ * sub-band with the item's Q row in registers).  hmf_qband_set_impl sets the
+ * process default; -1 (initial) = automatic: 4 for fp16 rows and k >= 128,
+ * else 0.  hmf_qband_resolve_impl gives what the default resolves to. */
 int hmf_qband_set_impl(int32_t impl);
-/* Implementation 4 (chained item runs, qchain.cuh): configuration 0..3
- * (lanes per chain, prefetch distance, occupancy) and the lanes per chain it
- * uses for k; the chain walks full batches of that many triples in a seeded
- * rotation, then the partial batch. */
+int32_t hmf_qband_get_impl(void);
+int32_t hmf_qband_resolve_impl(int64_t k, int32_t f16);
+/* Implementation 4 configuration 0..6 (lanes per chain, prefetch distance,
+ * occupancy; default 5 = 8 lanes per chain, 16 for k = 256) and the lanes per
+ * chain it uses for k; a chain walks full batches of that many triples in a
+ * seeded rotation, then the partial batch. */
 int hmf_qband_set_chain_cfg(int32_t cfg);
 int32_t hmf_qband_chain_lanes(int64_t k);
+/* Implementation 4: chains of a warp change bins together (bit 0: static
+ * scheduler, bit 1: dynamic scheduler; default 3). */
+int hmf_qband_set_chain_lockstep(int32_t bits);
+/* impl: the implementation for this launch (-1 = the process default). */
 int64_t hmf_sgd_block_qband_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
                                 const int32_t* cols, const float* vals, const int64_t* sub_ptr,
-                                const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles, double lr,
-                                double reg_user, double reg_item, uint64_t seed, int64_t row_base,
-                                int64_t col_base, void* stream);
+                                const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles,
+                                int32_t impl, double lr, double reg_user, double reg_item,
+                                uint64_t seed, int64_t row_base, int64_t col_base, void* stream);
 int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                 const int32_t* rows, const int32_t* cols, const float* vals,
                                 const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
-                                int64_t n_tiles, double lr, double reg_user, double reg_item,
-                                uint64_t seed, int64_t row_base, int64_t col_base, void* stream);
+                                int64_t n_tiles, int32_t impl, double lr, double reg_user,
+                                double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
+                                void* stream);
 
 /*
  * The reference visit order of a range of n triples under `seed`

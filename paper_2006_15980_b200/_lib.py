@@ -49,14 +49,19 @@ SIGNATURES = {
     "hmf_sgd_range_f64": (_i64, [_p, _p, _i64, _p, _p, _p, _i64, _i64, _f64, _f64, _f64, _u64,
                                  _i64, _i64, _i32, _p]),
     "hmf_qband_max_items": (_i32, [_i64]),
+    "hmf_qband_max_items_for": (_i32, [_i64, _i32, _i32]),
     "hmf_qband_warps_per_sm": (_i32, [_i64, _i32]),
+    "hmf_qband_slots_per_sm": (_i32, [_i64, _i32, _i32]),
+    "hmf_qband_resolve_impl": (_i32, [_i64, _i32]),
+    "hmf_qband_get_impl": (_i32, []),
     "hmf_qband_set_impl": (C.c_int, [_i32]),
     "hmf_qband_set_chain_cfg": (C.c_int, [_i32]),
     "hmf_qband_chain_lanes": (_i32, [_i64]),
-    "hmf_sgd_block_qband_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _f64, _f64,
-                                       _f64, _u64, _i64, _i64, _p]),
-    "hmf_sgd_block_qband_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _f64, _f64,
-                                       _f64, _u64, _i64, _i64, _p]),
+    "hmf_qband_set_chain_lockstep": (C.c_int, [_i32]),
+    "hmf_sgd_block_qband_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i32, _f64,
+                                       _f64, _f64, _u64, _i64, _i64, _p]),
+    "hmf_sgd_block_qband_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i32, _f64,
+                                       _f64, _f64, _u64, _i64, _i64, _p]),
     "hmf_visit_order": (C.c_int, [_i64, _u64, _p, _p]),
     "hmf_mix64": (_u64, [C.POINTER(_u64), _i32]),
     "hmf_residual_sums_f32": (C.c_int, [_p, _p, _i64, _p, _p, _p, _i64, _i64, _i64, _i32, _p, _p]),

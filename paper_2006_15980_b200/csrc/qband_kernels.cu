@@ -499,7 +499,19 @@ static int reg_warps_per_sm() {
   return per_sm * kWarps;
 }
 
-static int g_qband_impl = 0;  // 0 = register prefetch (default, faster), 1 = TMA pipeline
+// process default implementation; -1 = automatic (resolve_impl)
+static int g_qband_impl = -1;
+
+// Implementation for a launch: an explicit impl >= 0, else the process
+// default, else automatic: chained item runs (4) for fp16 rows and for
+// k >= 128, where they reach the L2 load+reduction ceiling
+// (profiles/r02/l2_rowbench.jsonl); the warp-per-rating kernel (0) for fp32
+// rows of k <= 64, where it is faster (profiles/r02/ksweep.jsonl).
+static int resolve_impl(int impl, int64_t k, bool f16) {
+  if (impl < 0) impl = g_qband_impl;
+  if (impl < 0) impl = (f16 || k >= 128) ? 4 : 0;
+  return impl;
+}
 
 // ---------------------------------------------------------------------------
 // Async-copy ring variant (impl 2).  Same ownership scheme; the P rows of the
@@ -763,9 +775,10 @@ static cudaError_t launch(S* P, S* Q, const int32_t* rows, const int32_t* cols, 
 template <typename S>
 static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* cols,
                    const float* vals, const int64_t* sub_ptr, const int32_t* sub_cuts,
-                   int64_t n_sub, int64_t n_tiles, double lr, double ru, double ri, uint64_t seed,
-                   int64_t row_base, int64_t col_base, cudaStream_t stream) {
+                   int64_t n_sub, int64_t n_tiles, int impl_req, double lr, double ru, double ri,
+                   uint64_t seed, int64_t row_base, int64_t col_base, cudaStream_t stream) {
   if (n_sub <= 0 || n_tiles <= 0) return 0;
+  if (impl_req > 4) return set_error(HMF_ERR_ARG, "impl must be -1..4");
   if (n_sub * n_tiles > (int64_t(1) << 31))
     return set_error(HMF_ERR_ARG, "n_sub * n_tiles too large");
   if (!P || !Q || !rows || !cols || !vals || !sub_ptr || !sub_cuts)
@@ -773,7 +786,7 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
   if (((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) != 0)
     return set_error(HMF_ERR_ARG, "factor arrays must be 16-byte aligned");
   cudaError_t e;
-  const int impl = g_qband_impl;
+  const int impl = resolve_impl(impl_req, k, sizeof(S) == 2);
   switch (k) {
 #define HMF_QB_CASE(KK)                                                                    \
   case KK:                                                                                 \
@@ -806,8 +819,8 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
 }
 
 template <typename S>
-static int warps_per_sm(int64_t k) {
-  const int impl = g_qband_impl;
+static int warps_per_sm(int64_t k, int impl) {
+  impl = resolve_impl(impl, k, sizeof(S) == 2);
   switch (k) {
 #define HMF_WPS(KK)                                                                   \
   case KK:                                                                            \
@@ -826,8 +839,10 @@ static int warps_per_sm(int64_t k) {
 
 // Q-slice budget of the active implementation (bytes of fp32 Q per warp)
 template <typename S>
-static int slice_bytes(int64_t k) {
-  if (g_qband_impl != 2) return kSliceBytes;
+static int slice_bytes(int64_t k, int impl) {
+  impl = resolve_impl(impl, k, sizeof(S) == 2);
+  if (impl == 4) return 1 << 30;  // Q rows in registers: no slice bound
+  if (impl != 2) return kSliceBytes;
   switch (k) {
     case 32: return async_ok<32, S>() ? AsyncLayout<32, S, 4>::SLICE : kSliceBytes;
     case 64: return async_ok<64, S>() ? AsyncLayout<64, S, 4>::SLICE : kSliceBytes;
@@ -842,9 +857,19 @@ static int slice_bytes(int64_t k) {
 
 extern "C" {
 
-int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16) {
-  return f16 ? hmf::qs::warps_per_sm<__half>(k) : hmf::qs::warps_per_sm<float>(k);
+int32_t hmf_qband_slots_per_sm(int64_t k, int32_t f16, int32_t impl) {
+  return f16 ? hmf::qs::warps_per_sm<__half>(k, impl) : hmf::qs::warps_per_sm<float>(k, impl);
 }
+
+int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16) {
+  return hmf_qband_slots_per_sm(k, f16, -1);
+}
+
+int32_t hmf_qband_resolve_impl(int64_t k, int32_t f16) {
+  return hmf::qs::resolve_impl(-1, k, f16 != 0);
+}
+
+int32_t hmf_qband_get_impl() { return hmf::qs::g_qband_impl; }
 
 int hmf_qband_set_chain_cfg(int32_t cfg) {
   if (cfg < 0 || cfg >= hmf::qs::kChainCfgs)
@@ -853,45 +878,57 @@ int hmf_qband_set_chain_cfg(int32_t cfg) {
   return HMF_OK;
 }
 
+int hmf_qband_set_chain_lockstep(int32_t bits) {
+  if (bits < 0 || bits > 3) return int(hmf::set_error(HMF_ERR_ARG, "lockstep bits must be 0..3"));
+  hmf::qs::g_chain_lockstep = bits;
+  return HMF_OK;
+}
+
 int32_t hmf_qband_chain_lanes(int64_t k) {
   const int cfg = hmf::qs::g_chain_cfg;
-  const int per = (cfg == 2 || cfg == 3) ? 8 : 16;
+  if (cfg == 5 || cfg == 6) return k >= 256 ? 16 : 8;
+  const int per = (cfg == 2 || cfg == 3) ? 8 : 16;  // elements per lane
   const int lpc = int(k) / per;
   return lpc < 4 ? 4 : (lpc > 32 ? 32 : lpc);
 }
 
 int hmf_qband_set_impl(int32_t impl) {
-  if (impl < 0 || impl > 4)
-    return int(hmf::set_error(HMF_ERR_ARG, "impl must be 0..4"));
+  if (impl < -1 || impl > 4)
+    return int(hmf::set_error(HMF_ERR_ARG, "impl must be -1..4"));
   hmf::qs::g_qband_impl = impl;
   return HMF_OK;
 }
 
-int32_t hmf_qband_max_items(int64_t k) {
+int32_t hmf_qband_max_items_for(int64_t k, int32_t f16, int32_t impl) {
   if (k != 32 && k != 64 && k != 128 && k != 256) return 0;
-  if (hmf::qs::g_qband_impl == 4) return 1 << 30;  // Q rows in registers: no slice bound
-  // the tighter of the fp32 / fp16 budgets of the active implementation
-  const int b = min(hmf::qs::slice_bytes<float>(k), hmf::qs::slice_bytes<__half>(k));
-  return int32_t(b / (k * 4));
+  const int b = f16 ? hmf::qs::slice_bytes<__half>(k, impl) : hmf::qs::slice_bytes<float>(k, impl);
+  return b >= (1 << 30) ? int32_t(1 << 30) : int32_t(b / (k * 4));
+}
+
+int32_t hmf_qband_max_items(int64_t k) {
+  // the tighter of the fp32 / fp16 budgets of the default implementation
+  const int32_t a = hmf_qband_max_items_for(k, 0, -1), b = hmf_qband_max_items_for(k, 1, -1);
+  return a < b ? a : b;
 }
 
 int64_t hmf_sgd_block_qband_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
                                 const int32_t* cols, const float* vals, const int64_t* sub_ptr,
-                                const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles, double lr,
-                                double reg_user, double reg_item, uint64_t seed, int64_t row_base,
-                                int64_t col_base, void* stream) {
+                                const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles,
+                                int32_t impl, double lr, double reg_user, double reg_item,
+                                uint64_t seed, int64_t row_base, int64_t col_base, void* stream) {
   return hmf::qs::run<float>(user_f, item_f, k, rows, cols, vals, sub_ptr, sub_cuts, n_sub,
-                             n_tiles, lr, reg_user, reg_item, seed, row_base, col_base,
+                             n_tiles, impl, lr, reg_user, reg_item, seed, row_base, col_base,
                              static_cast<cudaStream_t>(stream));
 }
 
 int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                 const int32_t* rows, const int32_t* cols, const float* vals,
                                 const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
-                                int64_t n_tiles, double lr, double reg_user, double reg_item,
-                                uint64_t seed, int64_t row_base, int64_t col_base, void* stream) {
+                                int64_t n_tiles, int32_t impl, double lr, double reg_user,
+                                double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
+                                void* stream) {
   return hmf::qs::run<__half>(reinterpret_cast<__half*>(user_f), reinterpret_cast<__half*>(item_f),
-                              k, rows, cols, vals, sub_ptr, sub_cuts, n_sub, n_tiles, lr,
+                              k, rows, cols, vals, sub_ptr, sub_cuts, n_sub, n_tiles, impl, lr,
                               reg_user, reg_item, seed, row_base, col_base,
                               static_cast<cudaStream_t>(stream));
 }

@@ -28,6 +28,10 @@
 // a = lr*err:  dP = a*q - (lr*reg_u)*p,  q' = (1 - lr*reg_i)*q + a*p.
 #pragma once
 
+#include <mutex>
+#include <unordered_map>
+#include <utility>
+
 #include "hmf_common.cuh"
 #include "lanevec.cuh"
 
@@ -59,6 +63,34 @@ template <int K, typename S, int LPC> struct ChainLay {
 #pragma unroll
     for (int v = 0; v < NV; ++v) V::red(row + off(v, l), d + v * W);
   }
+  // storage-typed row kept raw in registers (RW 32-bit words per lane), so a
+  // prefetched fp16 row costs half the registers of its fp32 expansion
+  static constexpr int VW = W * int(sizeof(S)) / 4;
+  static constexpr int RW = NV * VW;
+  __device__ static void ldraw(const S* row, int l, uint32_t* o) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const void* p = row + off(v, l);
+      if constexpr (VW == 4) {
+        const uint4 t = __ldcg(reinterpret_cast<const uint4*>(p));
+        o[v * 4] = t.x; o[v * 4 + 1] = t.y; o[v * 4 + 2] = t.z; o[v * 4 + 3] = t.w;
+      } else if constexpr (VW == 2) {
+        const uint2 t = __ldcg(reinterpret_cast<const uint2*>(p));
+        o[v * 2] = t.x; o[v * 2 + 1] = t.y;
+      } else {
+        o[v] = __ldcg(reinterpret_cast<const unsigned int*>(p));
+      }
+    }
+  }
+  __device__ static void cvt(const uint32_t* raw, float* o) {
+    if constexpr (sizeof(S) == 4) {
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) o[e] = __uint_as_float(raw[e]);
+    } else {
+#pragma unroll
+      for (int w = 0; w < RW; ++w) unpack_h2(raw[w], o + 2 * w);
+    }
+  }
 };
 
 // Configurations (hmf_qband_set_chain_cfg): lanes per chain (about 16 or 8
@@ -81,138 +113,246 @@ template <int K> struct ChainCfg<K, 3> {  // 8 elements/lane, 2 steps ahead, 24 
   static constexpr int LPC = ChainCfg<K, 2>::LPC;
   static constexpr int PD = 2, WPB = 8, MINB = 3;
 };
-constexpr int kChainCfgs = 4;
+template <int K> struct ChainCfg<K, 4> {  // 16 elements/lane, 4 steps ahead (fp16 rows)
+  static constexpr int LPC = ChainCfg<K, 0>::LPC;
+  static constexpr int PD = LPC > 4 ? 4 : LPC - 1, WPB = 16, MINB = 1;
+};
+template <int K> struct ChainCfg<K, 5> {  // 8 lanes per chain (4 chains), 2 steps ahead
+  static constexpr int LPC = K >= 256 ? 16 : 8;
+  static constexpr int PD = 2, WPB = 16, MINB = 1;
+};
+template <int K> struct ChainCfg<K, 6> {  // 8 lanes per chain (4 chains), 4 steps ahead
+  static constexpr int LPC = K >= 256 ? 16 : 8;
+  static constexpr int PD = 4, WPB = 16, MINB = 1;
+};
+constexpr int kChainCfgs = 7;
 
-template <int K, typename S, int LPC, int PD, int WPB, int MINB>
+__device__ inline unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ inline void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Units of work are (tile step i, sub-band s) bins.  Static mode (DYN =
+// false): chain g owns sub-bands g, g + n_slots, ... and walks them tile step
+// by tile step.  Dynamic mode (DYN = true, `work` = zeroed {counter,
+// done[n_sub]}): chains take units in order from a global counter and start
+// unit (i, s) once done[s] == i, i.e. once the chain that had (i-1, s)
+// released it — Q row ownership moves between chains through
+// release/acquire, and load balance no longer depends on the number of
+// sub-bands being a multiple of the number of chains.
+template <int K, typename S, int LPC, int PD, int WPB, int MINB, bool DYN>
 __global__ void __launch_bounds__(WPB * 32, MINB)
     qchain_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const int32_t* __restrict__ rows,
                   const int32_t* __restrict__ cols, const float* __restrict__ vals,
                   const int64_t* __restrict__ sub_ptr, int n_sub, int n_tiles, float lr, float ru,
-                  float ri, uint64_t seed) {
+                  float ri, uint64_t seed, unsigned* __restrict__ work, int lockstep) {
   using L = ChainLay<K, S, LPC>;
   constexpr int NC = L::NC, E = L::EPL, NS = PD + 1;
   static_assert(PD >= 1 && PD < LPC, "prefetch distance must stay within one batch");
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int c = lane / LPC, l = lane % LPC;
-  const int gw = blockIdx.x * WPB + (threadIdx.x >> 5);
+  const unsigned cmask = LPC == 32 ? FULL : (((1u << LPC) - 1u) << (c * LPC));
+  const int cg = (blockIdx.x * WPB + (threadIdx.x >> 5)) * NC + c;  // global chain id
   const int n_slots = gridDim.x * WPB * NC;
   const float a_ru = lr * ru, keep_q = 1.f - lr * ri;
+  const unsigned n_units = unsigned(n_tiles) * unsigned(n_sub);
 
-  for (int ti = 0; ti < n_tiles; ++ti) {
-    const int tile = tile_at(ti, n_tiles, seed);
-    const int64_t* sp = sub_ptr + int64_t(tile) * n_sub;
-    const uint64_t bin0 = uint64_t(tile) * uint64_t(n_sub);
-    for (int s0 = gw * NC; s0 < n_sub; s0 += n_slots) {  // warp-uniform
-      const int s = s0 + c;
-      int64_t beg = 0;
-      int len = 0;
-      if (s < n_sub) {
-        beg = sp[s];
-        len = int(sp[s + 1] - beg);
+  // -- per-chain state ------------------------------------------------------
+  int ui = 0, us = cg;          // current unit (tile step, sub-band)
+  bool done = false;            // no units left for this chain
+  bool pend = false;            // unit taken, waiting for its sub-band (dynamic)
+  bool have = false;            // a bin is in progress (its Q row to write back)
+  bool first = true;            // static mode: no unit taken yet
+  int64_t beg = 0;
+  int len = 0, nf = 0, nb = 0, rot = 0, x = 0, j = 0, cnt = 0;
+  int32_t cu = -1, cv = 0, nu = -1, nv = 0;
+  float cr = 0.f, nr = 0.f;
+  uint32_t p[NS][L::RW];
+  float q[E];
+  int qcur = -1;  // item whose Q row is in q[]
+
+  auto bstart = [&](int xx) -> int {
+    if (xx >= nf) return nf * LPC;
+    int b = xx + rot;
+    if (b >= nf) b -= nf;
+    return b * LPC;
+  };
+  auto load_batch = [&](int xx, int32_t& u, int32_t& v, float& r) {
+    u = -1;
+    if (xx < nb) {
+      const int o = bstart(xx) + l;
+      if (o < len) {
+        u = __ldg(rows + beg + o);
+        v = __ldg(cols + beg + o);
+        r = __ldg(vals + beg + o);
       }
-      // nf full batches of LPC triples visited from a seeded rotation, then
-      // the partial batch (if any) last
-      const int nf = len / LPC;
-      const int nb = (len + LPC - 1) / LPC;
-      const int rot =
-          nf > 0 ? int(splitmix_finalize(seed + (bin0 + uint64_t(s)) * kGolden) % uint64_t(nf))
-                 : 0;
-      auto bstart = [&](int x) -> int {
-        if (x >= nf) return nf * LPC;
-        int b = x + rot;
-        if (b >= nf) b -= nf;
-        return b * LPC;
-      };
-      auto load_batch = [&](int x, int32_t& u, int32_t& v, float& r) {
-        u = -1;
-        if (x < nb) {
-          const int o = bstart(x) + l;
-          if (o < len) {
-            u = __ldg(rows + beg + o);
-            v = __ldg(cols + beg + o);
-            r = __ldg(vals + beg + o);
-          }
-        }
-      };
-      int32_t cu, cv = 0, nu, nv = 0;
-      float cr = 0.f, nr = 0.f;
-      load_batch(0, cu, cv, cr);
-      load_batch(1, nu, nv, nr);
-      int x = 0, j = 0;
-      int cnt = x < nf ? LPC : len - nf * LPC;  // ratings in the current batch
-      float p[NS][E], q[E];
-      int qcur = -1;  // item whose Q row is in q[]
-      // prologue: P rows of ratings 0 .. PD-1 (all in batch 0 when it is full)
-#pragma unroll
-      for (int t = 0; t < PD; ++t) {
-        const int32_t u0 = __shfl_sync(FULL, cu, t, LPC);
-        if (t < cnt && u0 >= 0) L::ldg(Pb + int64_t(u0) * K, l, p[t]);
-      }
-      // one rating per chain: pc holds its P row, pn receives the row of the
-      // rating PD steps ahead
-      auto step = [&](float* pc, float* pn) {
-        const bool act = x < nb;  // chain-uniform
-        const int32_t u = __shfl_sync(FULL, cu, j, LPC);
-        const int32_t v = __shfl_sync(FULL, cv, j, LPC);
-        const float r = __shfl_sync(FULL, cr, j, LPC);
-        const bool ahead_in = j + PD < cnt;
-        const int32_t un =
-            __shfl_sync(FULL, ahead_in ? cu : nu, ahead_in ? j + PD : j + PD - cnt, LPC);
-        if (act && un >= 0) L::ldg(Pb + int64_t(un) * K, l, pn);
-        if (act && v != qcur) {
-          if (qcur >= 0) L::stg(Qb + int64_t(qcur) * K, l, q);
-          L::ldg(Qb + int64_t(v) * K, l, q);
-          qcur = v;
-        }
-        float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
-#pragma unroll
-        for (int e = 0; e < E; e += 4) {
-          d0 = fmaf(pc[e], q[e], d0);
-          if (e + 1 < E) d1 = fmaf(pc[e + 1], q[e + 1], d1);
-          if (e + 2 < E) d2 = fmaf(pc[e + 2], q[e + 2], d2);
-          if (e + 3 < E) d3 = fmaf(pc[e + 3], q[e + 3], d3);
-        }
-        float d = (d0 + d1) + (d2 + d3);
-#pragma unroll
-        for (int o = LPC / 2; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
-        if (act) {
-          const float a = lr * (r - d);
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const float pu = pc[e], qv = q[e];
-            pc[e] = fmaf(a, qv, -a_ru * pu);
-            q[e] = fmaf(a, pu, keep_q * qv);
-          }
-          L::red(Pb + int64_t(u) * K, l, pc);
-          if (j + 1 < cnt) {
-            ++j;
-          } else {
-            ++x;
-            j = 0;
-            cu = nu;
-            cv = nv;
-            cr = nr;
-            load_batch(x + 1, nu, nv, nr);
-            cnt = x < nf ? LPC : len - nf * LPC;
-          }
-        }
-      };
-      while (__any_sync(FULL, x < nb)) {
-#pragma unroll
-        for (int t = 0; t < NS; ++t) step(p[t], p[(t + PD) % NS]);
-      }
-      if (qcur >= 0) L::stg(Qb + int64_t(qcur) * K, l, q);
     }
+  };
+  // set up the bin of unit (ui, us): nf full batches of LPC triples visited
+  // from a seeded rotation, then the partial batch (if any) last
+  auto begin_bin = [&]() {
+    const int tile = tile_at(ui, n_tiles, seed);
+    const int64_t* sp = sub_ptr + int64_t(tile) * n_sub;
+    beg = sp[us];
+    len = int(sp[us + 1] - beg);
+    nf = len / LPC;
+    nb = (len + LPC - 1) / LPC;
+    const uint64_t bin = uint64_t(tile) * uint64_t(n_sub) + uint64_t(us);
+    rot = nf > 0 ? int(splitmix_finalize(seed + bin * kGolden) % uint64_t(nf)) : 0;
+    x = 0;
+    j = 0;
+    cnt = nf > 0 ? LPC : len;
+    load_batch(0, cu, cv, cr);
+    load_batch(1, nu, nv, nr);
+    qcur = -1;
+    have = true;
+#pragma unroll
+    for (int t = 0; t < PD; ++t) {
+      const int32_t u0 = __shfl_sync(cmask, cu, t, LPC);
+      if (t < cnt && u0 >= 0) L::ldraw(Pb + int64_t(u0) * K, l, p[t]);
+    }
+  };
+  // the finished bin: Q row back, the unit released (dynamic)
+  auto end_bin = [&]() {
+    if (qcur >= 0) L::stg(Qb + int64_t(qcur) * K, l, q);
+    qcur = -1;
+    have = false;
+    if constexpr (DYN) {
+      __syncwarp(cmask);
+      if (l == 0) {
+        __threadfence();
+        st_release_u32(work + 1 + us, unsigned(ui + 1));
+      }
+    }
+  };
+  // take the next unit (chain-divergent); false when there is none
+  auto take = [&]() -> bool {
+    if constexpr (DYN) {
+      unsigned w = 0;
+      if (l == 0) w = atomicAdd(work, 1u);
+      w = __shfl_sync(cmask, w, c * LPC);
+      if (w >= n_units) return false;
+      ui = int(w / unsigned(n_sub));
+      us = int(w % unsigned(n_sub));
+      pend = true;
+      return true;
+    } else {
+      if (!first) us += n_slots;
+      first = false;
+      if (us >= n_sub) {
+        us = cg;
+        ++ui;
+      }
+      if (ui >= n_tiles || us >= n_sub) return false;
+      pend = true;
+      return true;
+    }
+  };
+  // start the taken unit if its sub-band is free (never blocks: a chain
+  // waiting here must not stall the other chains of its warp, one of which
+  // may hold the predecessor unit)
+  auto try_start = [&]() -> bool {
+    if constexpr (DYN) {
+      const unsigned f = ld_acquire_u32(work + 1 + us);  // every lane acquires
+      if (!__all_sync(cmask, f == unsigned(ui))) return false;
+    }
+    pend = false;
+    begin_bin();
+    return true;
+  };
+
+  // one rating per active chain: praw holds its P row, pn receives the row of
+  // the rating PD steps ahead
+  auto step = [&](const uint32_t* praw, uint32_t* pn) {
+    const bool act = !done && !pend && x < nb;  // chain-uniform
+    const int32_t u = __shfl_sync(FULL, cu, j, LPC);
+    const int32_t v = __shfl_sync(FULL, cv, j, LPC);
+    const float r = __shfl_sync(FULL, cr, j, LPC);
+    const bool ahead_in = j + PD < cnt;
+    const int32_t un =
+        __shfl_sync(FULL, ahead_in ? cu : nu, ahead_in ? j + PD : j + PD - cnt, LPC);
+    if (act && un >= 0) L::ldraw(Pb + int64_t(un) * K, l, pn);
+    if (act && v != qcur) {
+      if (qcur >= 0) L::stg(Qb + int64_t(qcur) * K, l, q);
+      L::ldg(Qb + int64_t(v) * K, l, q);
+      qcur = v;
+    }
+    float pc[E];
+    L::cvt(praw, pc);
+    float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; e += 4) {
+      d0 = fmaf(pc[e], q[e], d0);
+      if (e + 1 < E) d1 = fmaf(pc[e + 1], q[e + 1], d1);
+      if (e + 2 < E) d2 = fmaf(pc[e + 2], q[e + 2], d2);
+      if (e + 3 < E) d3 = fmaf(pc[e + 3], q[e + 3], d3);
+    }
+    float d = (d0 + d1) + (d2 + d3);
+#pragma unroll
+    for (int o = LPC / 2; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
+    if (act) {
+      const float a = lr * (r - d);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const float pu = pc[e], qv = q[e];
+        pc[e] = fmaf(a, qv, -a_ru * pu);
+        q[e] = fmaf(a, pu, keep_q * qv);
+      }
+      L::red(Pb + int64_t(u) * K, l, pc);
+      if (j + 1 < cnt) {
+        ++j;
+      } else {
+        ++x;
+        j = 0;
+        cu = nu;
+        cv = nv;
+        cr = nr;
+        load_batch(x + 1, nu, nv, nr);
+        cnt = x < nf ? LPC : len - nf * LPC;
+      }
+    }
+  };
+
+  auto advance = [&]() {
+    // lockstep: the chains of a warp change bins together (their start-up
+    // load latencies overlap) once every one of them has run out
+    if (lockstep && !__all_sync(FULL, done || pend || x >= nb)) return;
+    while (!done) {
+      if (pend) {
+        if (!try_start()) break;  // sub-band still busy: retry after the next group
+      } else if (x >= nb) {
+        if (have) end_bin();
+        if (!take()) done = true;
+      } else {
+        break;  // bin in progress
+      }
+    }
+  };
+  advance();
+  while (__any_sync(FULL, !done)) {
+    if (__all_sync(FULL, done || pend)) __nanosleep(256);
+#pragma unroll
+    for (int t = 0; t < NS; ++t) step(p[t], p[(t + PD) % NS]);
+    // chains whose bin ran out move on (bins start at slot 0 of the unrolled
+    // group, so the prologue's slots are static)
+    advance();
   }
 }
 
-static int g_chain_cfg = 1;
+static int g_chain_cfg = 5;
+// bin changes in warp lockstep: bit 0 for the static, bit 1 for the dynamic
+// scheduler
+static int g_chain_lockstep = 3;
 
 template <int K, typename S, int CFG>
 static int chain_slots_per_sm_cfg() {
   using C = ChainCfg<K, CFG>;
-  auto kern = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB>;
+  auto kern = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPB * 32, 0);
   return per_sm * C::WPB * (32 / C::LPC);
@@ -224,8 +364,34 @@ static int chain_slots_per_sm() {
     case 0: return chain_slots_per_sm_cfg<K, S, 0>();
     case 2: return chain_slots_per_sm_cfg<K, S, 2>();
     case 3: return chain_slots_per_sm_cfg<K, S, 3>();
+    case 4: return chain_slots_per_sm_cfg<K, S, 4>();
+    case 5: return chain_slots_per_sm_cfg<K, S, 5>();
+    case 6: return chain_slots_per_sm_cfg<K, S, 6>();
     default: return chain_slots_per_sm_cfg<K, S, 1>();
   }
+}
+
+// Per-stream scratch for the dynamic scheduler ({counter, done[n_sub]});
+// launches on one stream are ordered, so they can share it.
+static cudaError_t chain_work(cudaStream_t stream, size_t words, unsigned** out) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, std::pair<unsigned*, size_t>> bufs;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& b = bufs[stream];
+  if (b.second < words) {
+    if (b.first) {
+      cudaError_t e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) return e;
+      cudaFree(b.first);
+      b.first = nullptr;
+      b.second = 0;
+    }
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&b.first), words * sizeof(unsigned));
+    if (e != cudaSuccess) return e;
+    b.second = words;
+  }
+  *out = b.first;
+  return cudaMemsetAsync(b.first, 0, words * sizeof(unsigned), stream);
 }
 
 template <int K, typename S, int CFG>
@@ -235,11 +401,12 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const int32_t* rows, const int32
                                     int64_t row_base, int64_t col_base, cudaStream_t stream) {
   using C = ChainCfg<K, CFG>;
   constexpr int NC = 32 / C::LPC;
-  auto kern = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB>;
+  auto kstat = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false>;
+  auto kdyn = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, true>;
   static int per_sm = 0;
   if (per_sm == 0) {
     const cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPB * 32, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kstat, C::WPB * 32, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
   }
@@ -247,9 +414,20 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const int32_t* rows, const int32
   const int cap = device_sm_count() * per_sm;
   const int grid = want < cap ? want : cap;
   if (grid <= 0) return cudaSuccess;
+  // more sub-bands than chains: units are handed out dynamically (a static
+  // split would leave some chains with one sub-band more than others in
+  // every tile)
+  const bool dyn = int64_t(n_sub) > int64_t(grid) * C::WPB * NC;
+  unsigned* work = nullptr;
+  if (dyn) {
+    const cudaError_t e = chain_work(stream, size_t(n_sub) + 1, &work);
+    if (e != cudaSuccess) return e;
+  }
+  auto kern = dyn ? kdyn : kstat;
+  const int lockstep = dyn ? (g_chain_lockstep & 2) != 0 : (g_chain_lockstep & 1) != 0;
   kern<<<grid, C::WPB * 32, 0, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
                                          sub_ptr, n_sub, n_tiles, float(lr), float(ru), float(ri),
-                                         seed);
+                                         seed, work, lockstep);
   return cudaGetLastError();
 }
 
@@ -265,6 +443,9 @@ static cudaError_t launch_chain(S* P, S* Q, const int32_t* rows, const int32_t* 
     case 0: HMF_CHAIN_CFG(0);
     case 2: HMF_CHAIN_CFG(2);
     case 3: HMF_CHAIN_CFG(3);
+    case 4: HMF_CHAIN_CFG(4);
+    case 5: HMF_CHAIN_CFG(5);
+    case 6: HMF_CHAIN_CFG(6);
     default: HMF_CHAIN_CFG(1);
   }
 #undef HMF_CHAIN_CFG

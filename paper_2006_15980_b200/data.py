@@ -375,6 +375,7 @@ class DeviceGrid:
     # row tiles per block (L2 residency of P): sub_ptr[b] then holds
     # sub_tiles[b] * S + 1 offsets, tile-major
     sub_tiles: list | None = None
+    sub_impl: int = -1          # Q-band implementation the layout is for
 
     n_row_bands = BlockGrid.n_row_bands
     n_col_bands = BlockGrid.n_col_bands
@@ -439,21 +440,38 @@ def build_device_grid(triples: DeviceTriples, row_cuts, col_cuts, region_of_row=
                       sub_row_parent, out_u, out_i, out_r, ptr)
 
 
-def resident_warps(device, k: int = 128, f16: bool = False) -> int:
-    """Warps the active Q-band kernel keeps resident on `device` (one item
-    sub-band each): SMs x the kernel's occupancy in warps."""
+def resident_warps(device, k: int = 128, f16: bool = False, impl: int = -1) -> int:
+    """Sub-band slots the Q-band kernel keeps resident on `device` (warps, or
+    lane-group chains for implementation 4): SMs x slots per SM."""
     torch = _torch()
     with torch.cuda.device(device):
-        per_sm = int(_lib.load().hmf_qband_warps_per_sm(int(k), 1 if f16 else 0))
+        per_sm = int(_lib.load().hmf_qband_slots_per_sm(int(k), 1 if f16 else 0, int(impl)))
     return int(torch.cuda.get_device_properties(device).multi_processor_count) * max(per_sm, 1)
 
 
-def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int) -> np.ndarray:
+def qband_impl_for(device, k: int, f16: bool, n_items: int) -> int:
+    """The Q-band implementation a grid is laid out and launched for: the
+    process default (hmf_qband_set_impl) when one is set, else the library's
+    automatic choice (hmf_qband_resolve_impl), except that the chained kernel
+    (4) gives way to the warp-per-rating kernel (0) when a block has fewer
+    than half as many items as there are chains to feed (ML-1M-sized
+    blocks: measured 2.7 vs 6.9 G upd/s, profiles/r02/)."""
+    lib = _lib.load()
+    impl = int(lib.hmf_qband_get_impl())
+    if impl >= 0:
+        return impl
+    impl = int(lib.hmf_qband_resolve_impl(int(k), 1 if f16 else 0))
+    if impl == 4 and 2 * n_items < resident_warps(device, k, f16, 4):
+        impl = 0
+    return impl
+
+
+def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int, cap: int | None = None) -> np.ndarray:
     """Equal-width item sub-bands of [c_lo, c_hi): about `target` of them
-    (one per resident warp), never more than the items, and narrow enough
-    that each sub-band's Q slice fits the kernel's shared-memory slice."""
+    (one per resident warp or chain), never more than the items, and at most
+    `cap` items wide (the kernel's Q-slice bound; default hmf_qband_max_items)."""
     items = c_hi - c_lo
-    cap = int(_lib.load().hmf_qband_max_items(k))
+    cap = int(_lib.load().hmf_qband_max_items(k)) if cap is None else int(cap)
     if cap <= 0:
         raise ValueError(f"Q-band kernel does not support k={k}")
     n_sub = min(items, max(target, -(-items // cap)))
@@ -480,7 +498,8 @@ def qband_row_tiles(n_rows: int, k: int, elem_bytes: int = 4,
 
 
 def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
-                  tile_bytes: int | None = None, elem_bytes: int = 4) -> DeviceGrid:
+                  tile_bytes: int | None = None, elem_bytes: int = 4,
+                  impl: int | None = None) -> DeviceGrid:
     """Re-bucket every block of a device grid for the Q-band kernel, in place:
     row tile major, then item (both stable), and attach sub_ptr / sub_cuts /
     sub_tiles.  Row tiles are equal user ranges of the block's row band, sized
@@ -488,12 +507,29 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     tile makes every (tile, sub-band) range contiguous and lays each item's
     ratings out as one run, so the kernel keeps the current item's Q row in
     registers.  The order of ratings within an item is the block order
-    (stable), i.e. the reference's shuffled order (data.py:242-244, 264)."""
+    (stable), i.e. the reference's shuffled order (data.py:242-244, 264).
+    The grid records the implementation it is laid out for (sub_impl;
+    qband_impl_for unless `impl` is given) and launches use it."""
     torch = _torch()
     dev = grid.device
     lib = _lib.load()
     s = _stream(dev)
-    target = resident_warps(dev, k) if target is None else int(target)
+    f16 = elem_bytes == 2
+    if impl is None:
+        impl = qband_impl_for(dev, k, f16, max((grid.col_span(c)[1] - grid.col_span(c)[0]
+                                                for c in range(grid.n_col_bands)), default=0))
+    impl = int(impl)
+    if target is None:
+        # one sub-band per resident slot; for the chained kernel with at least
+        # twice as many items as chains, narrower sub-bands (up to 4 per
+        # chain) that its dynamic scheduler balances (qchain.cuh)
+        target = resident_warps(dev, k, f16, impl)
+        widest = max((grid.col_span(c)[1] - grid.col_span(c)[0]
+                      for c in range(grid.n_col_bands)), default=0)
+        if impl == 4 and widest >= 2 * target:
+            target = min(widest, 4 * target)
+    target = int(target)
+    cap = int(lib.hmf_qband_max_items_for(int(k), 1 if f16 else 0, impl))
     out_u = torch.empty_like(grid.users)
     out_i = torch.empty_like(grid.items)
     out_r = torch.empty_like(grid.ratings)
@@ -504,7 +540,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         r_lo, r_hi = grid.row_span(b // grid.n_col_bands)
         n_tiles = qband_row_tiles(r_hi - r_lo, k, elem_bytes, tile_bytes)
         tiles = np.linspace(r_lo, r_hi, n_tiles + 1).round().astype(np.int64)
-        cuts = qband_sub_cuts(c_lo, c_hi, k, target)
+        cuts = qband_sub_cuts(c_lo, c_hi, k, target, cap)
         n_sub = len(cuts) - 1
         rel = torch.from_numpy(cuts[:-1] - c_lo).to(dev)
         ptr = torch.full((n_tiles * n_sub + 1,), hi, dtype=torch.int64, device=dev)
@@ -557,6 +593,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         sub_tiles.append(n_tiles)
     del out_u, out_i, out_r
     grid.sub_ptr, grid.sub_cuts, grid.sub_tiles = sub_ptrs, sub_cuts, sub_tiles
+    grid.sub_impl = impl
     return grid
 
 

@@ -128,7 +128,8 @@ def launch_block_qband(user_f, item_f, grid, block, lr, reg_user, reg_item, seed
     fn = getattr(_lib.load(), f"hmf_sgd_block_qband_{st}")
     _lib.check(fn(user_f.data_ptr(), item_f.data_ptr(), user_f.shape[1], grid.users.data_ptr(),
                   grid.items.data_ptr(), grid.ratings.data_ptr(), sp.data_ptr(), sc.data_ptr(),
-                  n_sub, n_tiles, float(lr), float(reg_user), float(reg_item),
+                  n_sub, n_tiles, int(grid.sub_impl), float(lr), float(reg_user),
+                  float(reg_item),
                   int(seed) & _MASK64, int(row_base), int(col_base), s),
                f"hmf_sgd_block_qband_{st}")
     return hi - lo

@@ -470,6 +470,7 @@ class StreamingEpoch:
         self.sub_rel = [(p - int(sg.block_ptr[b])).contiguous() for b, p in enumerate(sg.sub_ptr)]
         self.sub_cuts = sg.sub_cuts
         self.sub_tiles = sg.sub_tiles
+        self.sub_impl = sg.sub_impl
         cap = int(np.max(np.diff(sg.block_ptr))) + 4
         self.bufs = [tuple(torch.empty(cap, dtype=dt, device=self.dev)
                            for dt in (torch.int32, torch.int32, torch.float32)) for _ in range(2)]
@@ -504,7 +505,8 @@ class StreamingEpoch:
             sp, sc = self.sub_rel[b], self.sub_cuts[b]
             _lib.check(fn(P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr(),
                           buf[1].data_ptr(), buf[2].data_ptr(), sp.data_ptr(), sc.data_ptr(),
-                          int(sc.numel()) - 1, self.sub_tiles[b], hparams.learning_rate, hparams.reg_user,
+                          int(sc.numel()) - 1, self.sub_tiles[b], self.sub_impl,
+                          hparams.learning_rate, hparams.reg_user,
                           hparams.reg_item, kernels.mix64(seed, b) & 0xFFFFFFFFFFFFFFFF, 0, 0,
                           comp.cuda_stream), f"hmf_sgd_block_qband_{st}")
             ev = torch.cuda.Event()

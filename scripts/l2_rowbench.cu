@@ -17,7 +17,8 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
   return x;
 }
 
-// MODE 0 = load, 1 = red, 2 = load + red of the loaded values' negation.
+// MODE 0 = load, 1 = red, 2 = load + red of the loaded values' negation,
+// 3 = f16x2 red, 4 = load + f16x2 red.
 // LPR lanes per row; lane l of a row group moves NV = ROWB/(16*LPR) 16-byte
 // vectors at byte offsets (v*LPR + l)*16 (the chain layout of qchain.cuh).
 template <int MODE, int ROWB, int DEPTH, int LPR>
@@ -37,7 +38,7 @@ __global__ void __launch_bounds__(512, 1) rowbench(float* buf, uint32_t n_rows, 
       const float4* p = reinterpret_cast<const float4*>(buf + size_t(r[d]) * (ROWB / 4));
 #pragma unroll
       for (int w = 0; w < NV; ++w)
-        if (MODE != 1) v[d][w] = __ldcg(p + w * LPR + l);
+        if (MODE != 1 && MODE != 3) v[d][w] = __ldcg(p + w * LPR + l);
     }
 #pragma unroll
     for (int d = 0; d < DEPTH; ++d) {
@@ -46,6 +47,11 @@ __global__ void __launch_bounds__(512, 1) rowbench(float* buf, uint32_t n_rows, 
         float* p = buf + size_t(r[d]) * (ROWB / 4) + 4 * (w * LPR + l);
         if (MODE == 0) {
           acc += v[d][w].x + v[d][w].y + v[d][w].z + v[d][w].w;
+        } else if (MODE >= 3) {  // fp16 rows: 8 halves per 16-byte vector
+          const unsigned a = MODE == 4 ? (__float_as_uint(v[d][w].x) & 0x00010001u) : 0x00010001u;
+          asm volatile("red.global.add.noftz.v4.f16x2 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a),
+                       "r"(a), "r"(a), "r"(a)
+                       : "memory");
         } else {
           const float a = MODE == 2 ? -1e-30f * v[d][w].x : 1e-30f;
           asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(a),
@@ -75,7 +81,9 @@ static void run(float* buf, uint32_t n_rows, float* sink, int sms) {
   const double rows = double(blocks) * threads / LPR * iters * DEPTH;
   printf("{\"mode\": \"%s\", \"row_bytes\": %d, \"depth\": %d, \"lanes_per_row\": %d, "
          "\"rows_per_s\": %.4g, \"GBps_rowbytes\": %.1f}\n",
-         MODE == 0 ? "load" : (MODE == 1 ? "red" : "load+red"), ROWB, DEPTH, LPR, rows / (ms * 1e-3),
+         MODE == 0 ? "load" : MODE == 1 ? "red" : MODE == 2 ? "load+red" : MODE == 3 ? "red_f16x2"
+                                                                                : "load+red_f16x2",
+         ROWB, DEPTH, LPR, rows / (ms * 1e-3),
          rows * ROWB / (ms * 1e-3) / 1e9);
 }
 
@@ -89,16 +97,22 @@ int main(int argc, char** argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   printf("{\"buffer_MB\": %zu, \"sms\": %d}\n", mb, sms);
-#define RUN3(RB, D, LPR)                                              \
-  run<0, RB, D, LPR>(buf, uint32_t((mb << 20) / RB), sink, sms);      \
-  run<1, RB, D, LPR>(buf, uint32_t((mb << 20) / RB), sink, sms);      \
-  run<2, RB, D, LPR>(buf, uint32_t((mb << 20) / RB), sink, sms);
-  RUN3(512, 4, 8)
-  RUN3(512, 8, 8)
-  RUN3(512, 4, 32)
-  RUN3(256, 4, 8)
-  RUN3(256, 8, 8)
-  RUN3(256, 4, 16)
+#define RUN5(RB, D, LPR)                                         \
+  run<0, RB, D, LPR>(buf, uint32_t((mb << 20) / RB), sink, sms); \
+  run<1, RB, D, LPR>(buf, uint32_t((mb << 20) / RB), sink, sms); \
+  run<2, RB, D, LPR>(buf, uint32_t((mb << 20) / RB), sink, sms); \
+  run<3, RB, D, LPR>(buf, uint32_t((mb << 20) / RB), sink, sms); \
+  run<4, RB, D, LPR>(buf, uint32_t((mb << 20) / RB), sink, sms);
+  // 8 lanes per row (the chain layout), rows of 128 B .. 1 KB
+  RUN5(128, 4, 8)
+  RUN5(128, 8, 8)
+  RUN5(256, 4, 8)
+  RUN5(256, 8, 8)
+  RUN5(512, 4, 8)
+  RUN5(512, 8, 8)
+  RUN5(1024, 4, 8)
+  // whole-warp rows (the warp-per-rating layout)
+  RUN5(512, 4, 32)
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
   return 0;

@@ -472,16 +472,17 @@ def test_qband_bucketing_contract(dev, k):
             assert np.all((seg >= cuts[s]) & (seg < cuts[s + 1]))
 
 
-@pytest.fixture(params=[(4, 1), (4, 2), (3, 0), (2, 0), (1, 0), (0, 0)],
-                ids=["chains", "chains_cfg2", "regs_deep", "cpasync", "tma", "regs"])
+@pytest.fixture(params=[(4, 5), (4, 1), (4, 2), (3, 5), (2, 5), (1, 5), (0, 5)],
+                ids=["chains", "chains_cfg1", "chains_cfg2", "regs_deep", "cpasync", "tma",
+                     "regs"])
 def qband_impl(request):
     from paper_2006_15980_b200 import _lib
     impl, cfg = request.param
     _lib.check(_lib.load().hmf_qband_set_impl(impl), "set_impl")
-    _lib.check(_lib.load().hmf_qband_set_chain_cfg(cfg if impl == 4 else 1), "set_chain_cfg")
+    _lib.check(_lib.load().hmf_qband_set_chain_cfg(cfg), "set_chain_cfg")
     yield impl
-    _lib.load().hmf_qband_set_impl(0)
-    _lib.load().hmf_qband_set_chain_cfg(1)
+    _lib.load().hmf_qband_set_impl(-1)
+    _lib.load().hmf_qband_set_chain_cfg(5)
 
 
 @pytest.mark.parametrize("k", [32, 64, 128, 256])
@@ -592,6 +593,54 @@ def test_qband_multi_chunk_subbands_match_sequential(dev, k, n_tiles, qband_impl
             Qe[v] = qv + 0.05 * (e * pu - 0.03 * qv)
     assert rel_err(Q.double().cpu().numpy(), Qe) < 1e-5
     assert rel_err(P.double().cpu().numpy(), Pe) < 1e-5
+
+
+@pytest.mark.parametrize("n_tiles", [1, 3])
+def test_qband_chains_dynamic_matches_sequential(dev, n_tiles):
+    """More sub-bands than chains: implementation 4 hands (tile, sub-band)
+    units out dynamically and passes each Q row between chains by
+    release/acquire.  With distinct users the result equals a sequential
+    replay of every sub-band's units in tile order."""
+    from paper_2006_15980_b200 import _lib, kernels
+    from paper_2006_15980_b200.data import RatingMatrix, resident_warps
+    from paper_2006_15980_b200.kernels import _MASK64
+    k = 128
+    _lib.check(_lib.load().hmf_qband_set_impl(4), "set_impl")
+    try:
+        slots = resident_warps(dev, k, False, 4)
+        rng = np.random.default_rng(99)
+        n_items = 2 * slots + 777
+        n_users, n = 400_000, 150_000
+        users = rng.permutation(n_users)[:n].astype(np.int32)
+        items = rng.integers(0, n_items, n).astype(np.int32)
+        vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
+        m = RatingMatrix(n_users, n_items, users, items, vals)
+        tb = 0 if n_tiles == 1 else n_users * k * 4 // n_tiles + 1
+        g = _qband_grid(dev, m, k, [0, n_items], target=n_items, tile_bytes=tb)
+        S = g.sub_cuts[0].numel() - 1
+        assert S == n_items > slots and g.sub_impl == 4
+        P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
+        Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
+        P, Q = to_dev(P0, dev), to_dev(Q0, dev)
+        seed = 4242
+        assert kernels.launch_block_qband(P, Q, g, 0, 0.05, 0.02, 0.03, seed) == n
+        gu, gi = g.users.cpu().numpy(), g.items.cpu().numpy()
+        gr = g.ratings.cpu().numpy().astype(np.float64)
+        ptr = g.sub_ptr[0].cpu().numpy()
+        order = [i for t in _tile_order(seed, n_tiles) for s_ in range(S)
+                 for i in _bin_visit(4, k, int(ptr[t * S + s_]), int(ptr[t * S + s_ + 1]), seed,
+                                     t * S + s_)]
+        assert sorted(order) == list(range(n))
+        Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
+        for u, v, r in zip(gu[order], gi[order], gr[order]):
+            pu, qv = Pe[u].copy(), Qe[v].copy()
+            e = r - pu @ qv
+            Pe[u] = pu + 0.05 * (e * qv - 0.02 * pu)
+            Qe[v] = qv + 0.05 * (e * pu - 0.03 * qv)
+        assert rel_err(Q.double().cpu().numpy(), Qe) < 1e-5
+        assert rel_err(P.double().cpu().numpy(), Pe) < 1e-5
+    finally:
+        _lib.load().hmf_qband_set_impl(-1)
 
 
 def test_qband_fp16_storage_tracks_fp32(dev, qband_impl):
