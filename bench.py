@@ -307,7 +307,7 @@ def run_ours(args, world, rank, local):
     stream_epoch = None
     if not args.no_e2e and args.kernel == "qband" and world == 1:
         from paper_2006_15980_b200.workers import StreamingEpoch
-        stream_epoch = StreamingEpoch(grid, k, tile_bytes=tile_bytes)
+        stream_epoch = StreamingEpoch(grid, k, tile_bytes=0 if tile_bytes is None else tile_bytes)
     if args.kernel == "qband":
         bucket_qbands(grid, k, tile_bytes=tile_bytes, elem_bytes=2 if precision == "f16" else 4)
     model = init_device_model(n_users, n_items, k, SEED, device=dev,
@@ -546,7 +546,9 @@ def run_e2e_stream(args, se, model, test, dev):
             "h2d_bytes_per_step": int(se.h2d_bytes), "d2h_bytes_per_step": 8, "steps": steps,
             "test_rmse_after": float(np.sqrt(sq / test.nnz)),
             "path": "workers.StreamingEpoch (pinned host triples streamed per epoch, "
-                    "double-buffered H2D overlapped with the Q-band kernel) + device RMSE read"}
+                    + ("users + ratings, 8 B/rating, item implicit in its sub-band; "
+                       if se.implicit_items else "12 B/rating; ")
+                    + "double-buffered H2D overlapped with the Q-band kernel) + device RMSE read"}
 
 
 def run_e2e(args, grid, model, k, precision, dev, world):
@@ -605,7 +607,7 @@ def main():
     ap.add_argument("--multi-kernel", choices=["auto", "qband", "range"], default="auto")
     ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 1, 2, 3, 4], default=-1,
                     help="Q-band kernel: 0 = register prefetch (default), 1 = TMA pipeline")
-    ap.add_argument("--chain-cfg", type=int, choices=list(range(7)), default=5,
+    ap.add_argument("--chain-cfg", type=int, choices=list(range(-1, 7)), default=-1,
                     help="configuration of Q-band implementation 4 (qchain.cuh ChainCfg)")
     ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)
     ap.add_argument("--tile-mb", type=float, default=None,

@@ -133,7 +133,8 @@ int hmf_qband_set_impl(int32_t impl);
 int32_t hmf_qband_get_impl(void);
 int32_t hmf_qband_resolve_impl(int64_t k, int32_t f16);
 /* Implementation 4 configuration 0..6 (lanes per chain, prefetch distance,
- * occupancy; default 5 = 8 lanes per chain, 16 for k = 256) and the lanes per
+ * occupancy; -1 = default: 5 for fp32 rows, 6 for fp16 rows, both 8 lanes per
+ * chain, 16 for k = 256, prefetching 2 and 4 ratings ahead) and the lanes per
  * chain it uses for k; a chain walks full batches of that many triples in a
  * seeded rotation, then the partial batch. */
 int hmf_qband_set_chain_cfg(int32_t cfg);
@@ -141,7 +142,10 @@ int32_t hmf_qband_chain_lanes(int64_t k);
 /* Implementation 4: chains of a warp change bins together (bit 0: static
  * scheduler, bit 1: dynamic scheduler; default 3). */
 int hmf_qband_set_chain_lockstep(int32_t bits);
-/* impl: the implementation for this launch (-1 = the process default). */
+/* impl: the implementation for this launch (-1 = the process default).
+ * cols may be NULL with implementation 4 when every sub-band is a single
+ * item (sub_cuts[s+1] = sub_cuts[s] + 1): the item of sub-band s is then
+ * sub_cuts[s] (a host->device stream of 8 instead of 12 bytes per rating). */
 int64_t hmf_sgd_block_qband_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
                                 const int32_t* cols, const float* vals, const int64_t* sub_ptr,
                                 const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles,

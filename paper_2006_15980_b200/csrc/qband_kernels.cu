@@ -781,12 +781,15 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
   if (impl_req > 4) return set_error(HMF_ERR_ARG, "impl must be -1..4");
   if (n_sub * n_tiles > (int64_t(1) << 31))
     return set_error(HMF_ERR_ARG, "n_sub * n_tiles too large");
-  if (!P || !Q || !rows || !cols || !vals || !sub_ptr || !sub_cuts)
+  if (!P || !Q || !rows || !vals || !sub_ptr || !sub_cuts)
     return set_error(HMF_ERR_ARG, "null pointer");
   if (((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) != 0)
     return set_error(HMF_ERR_ARG, "factor arrays must be 16-byte aligned");
   cudaError_t e;
   const int impl = resolve_impl(impl_req, k, sizeof(S) == 2);
+  // cols == nullptr: every sub-band is one item, sub_cuts[s] (chained kernel only)
+  if (!cols && impl != 4)
+    return set_error(HMF_ERR_ARG, "cols may be null only for implementation 4");
   switch (k) {
 #define HMF_QB_CASE(KK)                                                                    \
   case KK:                                                                                 \
@@ -795,8 +798,8 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
                                  int(n_tiles), lr, ru, ri, seed, row_base, col_base,       \
                                  stream);                                                  \
     else if (impl == 4)                                                                    \
-      e = launch_chain<KK, S>(P, Q, rows, cols, vals, sub_ptr, int(n_sub), int(n_tiles),   \
-                              lr, ru, ri, seed, row_base, col_base, stream);               \
+      e = launch_chain<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub),       \
+                              int(n_tiles), lr, ru, ri, seed, row_base, col_base, stream); \
     else if (impl == 3)                                                                    \
       e = launch<KK, S, true>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub),       \
                               int(n_tiles), lr, ru, ri, seed, row_base, col_base, stream); \
@@ -872,7 +875,7 @@ int32_t hmf_qband_resolve_impl(int64_t k, int32_t f16) {
 int32_t hmf_qband_get_impl() { return hmf::qs::g_qband_impl; }
 
 int hmf_qband_set_chain_cfg(int32_t cfg) {
-  if (cfg < 0 || cfg >= hmf::qs::kChainCfgs)
+  if (cfg < -1 || cfg >= hmf::qs::kChainCfgs)
     return int(hmf::set_error(HMF_ERR_ARG, "chain configuration out of range"));
   hmf::qs::g_chain_cfg = cfg;
   return HMF_OK;
@@ -885,7 +888,7 @@ int hmf_qband_set_chain_lockstep(int32_t bits) {
 }
 
 int32_t hmf_qband_chain_lanes(int64_t k) {
-  const int cfg = hmf::qs::g_chain_cfg;
+  const int cfg = hmf::qs::g_chain_cfg < 0 ? 5 : hmf::qs::g_chain_cfg;  // 5 and 6: same lanes
   if (cfg == 5 || cfg == 6) return k >= 256 ? 16 : 8;
   const int per = (cfg == 2 || cfg == 3) ? 8 : 16;  // elements per lane
   const int lpc = int(k) / per;

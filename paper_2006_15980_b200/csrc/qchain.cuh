@@ -148,8 +148,9 @@ template <int K, typename S, int LPC, int PD, int WPB, int MINB, bool DYN>
 __global__ void __launch_bounds__(WPB * 32, MINB)
     qchain_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const int32_t* __restrict__ rows,
                   const int32_t* __restrict__ cols, const float* __restrict__ vals,
-                  const int64_t* __restrict__ sub_ptr, int n_sub, int n_tiles, float lr, float ru,
-                  float ri, uint64_t seed, unsigned* __restrict__ work, int lockstep) {
+                  const int64_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_cuts,
+                  int n_sub, int n_tiles, float lr, float ru, float ri, uint64_t seed,
+                  unsigned* __restrict__ work, int lockstep) {
   using L = ChainLay<K, S, LPC>;
   constexpr int NC = L::NC, E = L::EPL, NS = PD + 1;
   static_assert(PD >= 1 && PD < LPC, "prefetch distance must stay within one batch");
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
   int64_t beg = 0;
   int len = 0, nf = 0, nb = 0, rot = 0, x = 0, j = 0, cnt = 0;
   int32_t cu = -1, cv = 0, nu = -1, nv = 0;
+  int32_t vbin = 0;  // the bin's item when cols == nullptr (one item per sub-band)
   float cr = 0.f, nr = 0.f;
   uint32_t p[NS][L::RW];
   float q[E];
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
       const int o = bstart(xx) + l;
       if (o < len) {
         u = __ldg(rows + beg + o);
-        v = __ldg(cols + beg + o);
+        v = cols ? __ldg(cols + beg + o) : vbin;
         r = __ldg(vals + beg + o);
       }
     }
@@ -200,6 +202,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     const int64_t* sp = sub_ptr + int64_t(tile) * n_sub;
     beg = sp[us];
     len = int(sp[us + 1] - beg);
+    if (!cols) vbin = __ldg(sub_cuts + us);
     nf = len / LPC;
     nb = (len + LPC - 1) / LPC;
     const uint64_t bin = uint64_t(tile) * uint64_t(n_sub) + uint64_t(us);
@@ -344,7 +347,12 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
   }
 }
 
-static int g_chain_cfg = 5;
+// -1 = automatic: 5 for fp32 rows, 6 (deeper prefetch; raw fp16 slots are
+// half the registers) for fp16 rows (profiles/r02/chain_cfg_*.jsonl)
+static int g_chain_cfg = -1;
+template <typename S> static int chain_cfg() {
+  return g_chain_cfg >= 0 ? g_chain_cfg : (sizeof(S) == 2 ? 6 : 5);
+}
 // bin changes in warp lockstep: bit 0 for the static, bit 1 for the dynamic
 // scheduler
 static int g_chain_lockstep = 3;
@@ -360,7 +368,7 @@ static int chain_slots_per_sm_cfg() {
 
 template <int K, typename S>
 static int chain_slots_per_sm() {
-  switch (g_chain_cfg) {
+  switch (chain_cfg<S>()) {
     case 0: return chain_slots_per_sm_cfg<K, S, 0>();
     case 2: return chain_slots_per_sm_cfg<K, S, 2>();
     case 3: return chain_slots_per_sm_cfg<K, S, 3>();
@@ -396,7 +404,8 @@ static cudaError_t chain_work(cudaStream_t stream, size_t words, unsigned** out)
 
 template <int K, typename S, int CFG>
 static cudaError_t launch_chain_cfg(S* P, S* Q, const int32_t* rows, const int32_t* cols,
-                                    const float* vals, const int64_t* sub_ptr, int n_sub,
+                                    const float* vals, const int64_t* sub_ptr,
+                                    const int32_t* sub_cuts, int n_sub,
                                     int n_tiles, double lr, double ru, double ri, uint64_t seed,
                                     int64_t row_base, int64_t col_base, cudaStream_t stream) {
   using C = ChainCfg<K, CFG>;
@@ -426,20 +435,21 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const int32_t* rows, const int32
   auto kern = dyn ? kdyn : kstat;
   const int lockstep = dyn ? (g_chain_lockstep & 2) != 0 : (g_chain_lockstep & 1) != 0;
   kern<<<grid, C::WPB * 32, 0, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
-                                         sub_ptr, n_sub, n_tiles, float(lr), float(ru), float(ri),
-                                         seed, work, lockstep);
+                                         sub_ptr, sub_cuts, n_sub, n_tiles, float(lr), float(ru),
+                                         float(ri), seed, work, lockstep);
   return cudaGetLastError();
 }
 
 template <int K, typename S>
 static cudaError_t launch_chain(S* P, S* Q, const int32_t* rows, const int32_t* cols,
-                                const float* vals, const int64_t* sub_ptr, int n_sub, int n_tiles,
+                                const float* vals, const int64_t* sub_ptr,
+                                const int32_t* sub_cuts, int n_sub, int n_tiles,
                                 double lr, double ru, double ri, uint64_t seed, int64_t row_base,
                                 int64_t col_base, cudaStream_t stream) {
 #define HMF_CHAIN_CFG(CFG)                                                                   \
-  return launch_chain_cfg<K, S, CFG>(P, Q, rows, cols, vals, sub_ptr, n_sub, n_tiles, lr, ru, \
-                                     ri, seed, row_base, col_base, stream)
-  switch (g_chain_cfg) {
+  return launch_chain_cfg<K, S, CFG>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, n_sub,      \
+                                     n_tiles, lr, ru, ri, seed, row_base, col_base, stream)
+  switch (chain_cfg<S>()) {
     case 0: HMF_CHAIN_CFG(0);
     case 2: HMF_CHAIN_CFG(2);
     case 3: HMF_CHAIN_CFG(3);

@@ -454,14 +454,16 @@ def qband_impl_for(device, k: int, f16: bool, n_items: int) -> int:
     process default (hmf_qband_set_impl) when one is set, else the library's
     automatic choice (hmf_qband_resolve_impl), except that the chained kernel
     (4) gives way to the warp-per-rating kernel (0) when a block has fewer
-    than half as many items as there are chains to feed (ML-1M-sized
-    blocks: measured 2.7 vs 6.9 G upd/s, profiles/r02/)."""
+    than a quarter as many items as there are chains to feed (ML-1M-sized
+    blocks: measured 2.7 vs 6.9 G upd/s, profiles/r02/chain_cfg_sweep_small_k.jsonl;
+    Netflix-sized blocks at k = 32 fp16, half as many items as chains: 20.1
+    vs 13.3 G upd/s for the chains)."""
     lib = _lib.load()
     impl = int(lib.hmf_qband_get_impl())
     if impl >= 0:
         return impl
     impl = int(lib.hmf_qband_resolve_impl(int(k), 1 if f16 else 0))
-    if impl == 4 and 2 * n_items < resident_warps(device, k, f16, 4):
+    if impl == 4 and 4 * n_items < resident_warps(device, k, f16, 4):
         impl = 0
     return impl
 

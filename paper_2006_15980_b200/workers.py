@@ -449,11 +449,16 @@ class StreamingEpoch:
     (data.stripe_layout) and Q-band bucketed once, copied to pinned host
     memory, and every epoch uploads stripe s+1 on a copy stream while the
     Q-band kernel updates stripe s (double-buffered device staging, ordered by
-    CUDA events).  P and Q stay on the device.  Per epoch the host->device
-    traffic is exactly the triples (12 bytes per rating).
+    CUDA events).  P and Q stay on the device.
+
+    Per epoch the host->device traffic is the triples: 12 bytes per rating,
+    or 8 when every sub-band is a single item and the chained kernel runs —
+    the item id is then implicit in the sub-band (hmf_sgd_block_qband_* with
+    cols = NULL), so only users and ratings cross PCIe.  Stripes are already
+    short, so no row tiles by default (tile_bytes=0).
     """
 
-    def __init__(self, grid: DeviceGrid, k: int, n_stripes: int = 8, tile_bytes=None):
+    def __init__(self, grid: DeviceGrid, k: int, n_stripes: int = 8, tile_bytes=0):
         from .data import stripe_layout
         torch = _torch()
         self.dev = grid.device
@@ -461,26 +466,27 @@ class StreamingEpoch:
         self.k = k
         self.n_blocks = sg.n_blocks
         self.nnz = sg.nnz
-        # host copies (pinned) of the stripe-major, sub-band bucketed triples
-        self.h_users = sg.users.cpu().pin_memory()
-        self.h_items = sg.items.cpu().pin_memory()
-        self.h_vals = sg.ratings.cpu().pin_memory()
         self.block_ptr = sg.block_ptr
         # per block: sub_ptr relative to the block start (device) and sub_cuts
         self.sub_rel = [(p - int(sg.block_ptr[b])).contiguous() for b, p in enumerate(sg.sub_ptr)]
         self.sub_cuts = sg.sub_cuts
         self.sub_tiles = sg.sub_tiles
         self.sub_impl = sg.sub_impl
+        self.implicit_items = sg.sub_impl == 4 and all(
+            bool(torch.all(c[1:] - c[:-1] == 1)) for c in sg.sub_cuts)
+        # host copies (pinned) of the stripe-major, sub-band bucketed triples
+        arrays = [sg.users] + ([] if self.implicit_items else [sg.items]) + [sg.ratings]
+        self.host = [a.cpu().pin_memory() for a in arrays]
         cap = int(np.max(np.diff(sg.block_ptr))) + 4
-        self.bufs = [tuple(torch.empty(cap, dtype=dt, device=self.dev)
-                           for dt in (torch.int32, torch.int32, torch.float32)) for _ in range(2)]
+        self.bufs = [tuple(torch.empty(cap, dtype=a.dtype, device=self.dev) for a in arrays)
+                     for _ in range(2)]
         self.copy_stream = torch.cuda.Stream(device=self.dev)
         self.freed = [None, None]
         del sg
 
     @property
     def h2d_bytes(self) -> int:
-        return 12 * self.nnz
+        return (8 if self.implicit_items else 12) * self.nnz
 
     def run(self, P, Q, hparams: Hyperparams, seed: int, stream=None) -> int:
         """One epoch over every block; returns triples processed (async)."""
@@ -497,14 +503,16 @@ class StreamingEpoch:
             with torch.cuda.stream(self.copy_stream):
                 if self.freed[b & 1] is not None:
                     self.copy_stream.wait_event(self.freed[b & 1])
-                for dst, src in zip(buf, (self.h_users, self.h_items, self.h_vals)):
+                for dst, src in zip(buf, self.host):
                     dst[:hi - lo].copy_(src[lo:hi], non_blocking=True)
                 up = torch.cuda.Event()
                 up.record(self.copy_stream)
             comp.wait_event(up)
             sp, sc = self.sub_rel[b], self.sub_cuts[b]
-            _lib.check(fn(P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr(),
-                          buf[1].data_ptr(), buf[2].data_ptr(), sp.data_ptr(), sc.data_ptr(),
+            users, vals = buf[0], buf[-1]
+            items = 0 if self.implicit_items else buf[1].data_ptr()
+            _lib.check(fn(P.data_ptr(), Q.data_ptr(), self.k, users.data_ptr(), items,
+                          vals.data_ptr(), sp.data_ptr(), sc.data_ptr(),
                           int(sc.numel()) - 1, self.sub_tiles[b], self.sub_impl,
                           hparams.learning_rate, hparams.reg_user,
                           hparams.reg_item, kernels.mix64(seed, b) & 0xFFFFFFFFFFFFFFFF, 0, 0,

@@ -144,7 +144,8 @@ def test_throughput_sweep_reports_stages(dev):
         throughput_sweep("batch", [2, 1], batch_config=BatchWorkerConfig(device=dev))
 
 
-def test_streaming_epoch_applies_every_triple_once(dev):
+@pytest.mark.parametrize("k", [64, 128])
+def test_streaming_epoch_applies_every_triple_once(dev, k):
     """StreamingEpoch (triples streamed from pinned host memory, double
     buffered) on conflict-free triples equals the reference update of each
     triple exactly once."""
@@ -154,7 +155,7 @@ def test_streaming_epoch_applies_every_triple_once(dev):
     from paper_2006_15980_b200.workers import StreamingEpoch
     from paper_2006_15980_b200.data import RatingMatrix
     rng = np.random.default_rng(3)
-    n, k = 6000, 64
+    n = 6000
     users = rng.permutation(9000)[:n].astype(np.int32)
     items = rng.permutation(7000)[:n].astype(np.int32)
     vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
@@ -173,4 +174,6 @@ def test_streaming_epoch_applies_every_triple_once(dev):
     rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)  # noqa: E731
     assert rel(P.double().cpu().numpy(), Pe) < 1e-6
     assert rel(Q.double().cpu().numpy(), Qe) < 1e-6
-    assert se.h2d_bytes == 12 * n
+    # k = 128: the chained kernel with one item per sub-band, items implicit
+    assert se.implicit_items == (k == 128)
+    assert se.h2d_bytes == (8 if k == 128 else 12) * n

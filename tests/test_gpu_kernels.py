@@ -472,7 +472,7 @@ def test_qband_bucketing_contract(dev, k):
             assert np.all((seg >= cuts[s]) & (seg < cuts[s + 1]))
 
 
-@pytest.fixture(params=[(4, 5), (4, 1), (4, 2), (3, 5), (2, 5), (1, 5), (0, 5)],
+@pytest.fixture(params=[(4, -1), (4, 1), (4, 2), (3, -1), (2, -1), (1, -1), (0, -1)],
                 ids=["chains", "chains_cfg1", "chains_cfg2", "regs_deep", "cpasync", "tma",
                      "regs"])
 def qband_impl(request):
@@ -482,7 +482,7 @@ def qband_impl(request):
     _lib.check(_lib.load().hmf_qband_set_chain_cfg(cfg), "set_chain_cfg")
     yield impl
     _lib.load().hmf_qband_set_impl(-1)
-    _lib.load().hmf_qband_set_chain_cfg(5)
+    _lib.load().hmf_qband_set_chain_cfg(-1)
 
 
 @pytest.mark.parametrize("k", [32, 64, 128, 256])
