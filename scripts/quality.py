@@ -83,27 +83,36 @@ def netflix(args):
     h_test = test.to_host()
     out = {"config": dict(n_users=n_users, n_items=n_items, train=train.nnz, test=test.nnz, k=k,
                           lr=lr, reg=reg, epochs=args.epochs)}
-    qgrid = None
-    if "qband" in args.modes.split(","):
-        from paper_2006_15980_b200.data import bucket_qbands
-        qgrid = build_device_grid(train, [0, n_users], [0, (n_items + 1) // 2, n_items])
-        bucket_qbands(qgrid, k)
+    # Q-band modes: qband (default implementation, fp32), qband_f16 (fp16
+    # storage), qband_implN (implementation N, fp32)
+    qgrids = {}
     for mode in args.modes.split(","):
-        model = DeviceModel(torch.from_numpy(P0).to(dev), torch.from_numpy(Q0).to(dev))
+        if mode.startswith("qband"):
+            from paper_2006_15980_b200.data import bucket_qbands
+            impl = int(mode[len("qband_impl"):]) if mode.startswith("qband_impl") else None
+            g = build_device_grid(train, [0, n_users], [0, (n_items + 1) // 2, n_items])
+            qgrids[mode] = bucket_qbands(g, k, impl=impl,
+                                         elem_bytes=2 if mode == "qband_f16" else 4)
+    for mode in args.modes.split(","):
+        dt = torch.float16 if mode == "qband_f16" else torch.float32
+        model = DeviceModel(torch.from_numpy(P0).to(dev, dt), torch.from_numpy(Q0).to(dev, dt))
         traj = []
         counts = np.zeros(2, dtype=np.int64)
         for epoch in range(args.epochs):
             for b in (0, 1):
                 lo, hi = grid.block_range(b)
                 seed = kernels.mix64(kernels.mix64(0, b, int(counts[b])), 0)
-                if mode == "qband":
-                    kernels.launch_block_qband(model.P, model.Q, qgrid, b, lr, reg, reg, seed)
+                if mode in qgrids:
+                    kernels.launch_block_qband(model.P, model.Q, qgrids[mode], b, lr, reg, reg,
+                                               seed)
                 else:
                     kernels.launch_sgd_range(model.P, model.Q, grid.users, grid.items,
                                              grid.ratings, lo, hi, lr, reg, reg, seed, 0, 0, mode)
                 counts[b] += 1
             traj.append(rmse(test, model).value)
         out[f"gpu_{mode}"] = traj
+        if mode in qgrids:
+            out[f"gpu_{mode}_impl"] = qgrids[mode].sub_impl
     if args.threads:
         # CPU reference path on the same triples (host copy) and same init
         h_train = train.to_host()
