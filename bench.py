@@ -304,12 +304,13 @@ def run_ours(args, world, rank, local):
                          test.ratings.clone())
     del trip, train
     torch.cuda.empty_cache()
-    stream_epoch = None
-    if not args.no_e2e and args.kernel == "qband" and world == 1:
-        from paper_2006_15980_b200.workers import StreamingEpoch
-        stream_epoch = StreamingEpoch(grid, k, tile_bytes=0 if tile_bytes is None else tile_bytes)
     if args.kernel == "qband":
         bucket_qbands(grid, k, tile_bytes=tile_bytes, elem_bytes=2 if precision == "f16" else 4)
+    stream_epoch = None
+    if not args.no_e2e and args.kernel == "qband" and world == 1:
+        # e2e streams the same layout from pinned host memory, tile by tile
+        from paper_2006_15980_b200.workers import StreamingEpoch
+        stream_epoch = StreamingEpoch(grid, k, n_buffers=args.stream_buffers)
     model = init_device_model(n_users, n_items, k, SEED, device=dev,
                               dtype="float16" if precision == "f16" else "float32")
     torch.cuda.synchronize(dev)
@@ -546,8 +547,9 @@ def run_e2e_stream(args, se, model, test, dev):
             "h2d_bytes_per_step": int(se.h2d_bytes), "d2h_bytes_per_step": 8, "steps": steps,
             "test_rmse_after": float(np.sqrt(sq / test.nnz)),
             "path": "workers.StreamingEpoch (pinned host triples streamed per epoch, "
-                    + ("users + ratings, 8 B/rating, item implicit in its sub-band; "
-                       if se.implicit_items else "12 B/rating; ")
+                    + (f"{se.bytes_per_rating} B/rating: "
+                       + ("2-byte user ids relative to the row tile, " if se.u16 else "")
+                       + ("item implicit in its sub-band; " if se.implicit_items else "triples; "))
                     + "double-buffered H2D overlapped with the Q-band kernel) + device RMSE read"}
 
 
@@ -610,6 +612,8 @@ def main():
     ap.add_argument("--chain-cfg", type=int, choices=list(range(-1, 7)), default=-1,
                     help="configuration of Q-band implementation 4 (qchain.cuh ChainCfg)")
     ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)
+    ap.add_argument("--stream-buffers", type=int, default=2,
+                    help="e2e: device staging buffers (ring)")
     ap.add_argument("--tile-mb", type=float, default=None,
                     help="P rows per Q-band row tile in MiB (default data.QBAND_TILE_BYTES; 0 = no tiling)")
     ap.add_argument("--no-e2e", action="store_true")

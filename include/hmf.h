@@ -138,6 +138,7 @@ int32_t hmf_qband_resolve_impl(int64_t k, int32_t f16);
  * chain it uses for k; a chain walks full batches of that many triples in a
  * seeded rotation, then the partial batch. */
 int hmf_qband_set_chain_cfg(int32_t cfg);
+int32_t hmf_qband_get_chain_cfg(void);
 int32_t hmf_qband_chain_lanes(int64_t k);
 /* Implementation 4: chains of a warp change bins together (bit 0: static
  * scheduler, bit 1: dynamic scheduler; default 3). */
@@ -157,6 +158,23 @@ int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                 int64_t n_tiles, int32_t impl, double lr, double reg_user,
                                 double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
                                 void* stream);
+
+/* The chained kernel (implementation 4, chain configuration 5 or 6) with
+ * uint16 row ids: row = rows[i] - row_base, so a row tile of at most 65536
+ * rows streams 2-byte ids with row_base = -(the tile's first row).  Same
+ * arguments and contract as hmf_sgd_block_qband_*. */
+int64_t hmf_sgd_block_qband_u16_f32(float* user_f, float* item_f, int64_t k,
+                                    const uint16_t* rows, const int32_t* cols, const float* vals,
+                                    const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
+                                    int64_t n_tiles, double lr, double reg_user, double reg_item,
+                                    uint64_t seed, int64_t row_base, int64_t col_base,
+                                    void* stream);
+int64_t hmf_sgd_block_qband_u16_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                                    const uint16_t* rows, const int32_t* cols, const float* vals,
+                                    const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
+                                    int64_t n_tiles, double lr, double reg_user, double reg_item,
+                                    uint64_t seed, int64_t row_base, int64_t col_base,
+                                    void* stream);
 
 /*
  * The reference visit order of a range of n triples under `seed`

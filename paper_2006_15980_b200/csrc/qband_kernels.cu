@@ -821,6 +821,42 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
   return 0;
 }
 
+// the chained kernel with uint16 row ids (row tile relative, see launch_chain)
+template <typename S>
+static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_t* cols,
+                       const float* vals, const int64_t* sub_ptr, const int32_t* sub_cuts,
+                       int64_t n_sub, int64_t n_tiles, double lr, double ru, double ri,
+                       uint64_t seed, int64_t row_base, int64_t col_base, cudaStream_t stream) {
+  if (n_sub <= 0 || n_tiles <= 0) return 0;
+  if (n_sub * n_tiles > (int64_t(1) << 31))
+    return set_error(HMF_ERR_ARG, "n_sub * n_tiles too large");
+  if (!P || !Q || !rows || !vals || !sub_ptr || !sub_cuts)
+    return set_error(HMF_ERR_ARG, "null pointer");
+  if (((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) != 0)
+    return set_error(HMF_ERR_ARG, "factor arrays must be 16-byte aligned");
+  const int cfg = chain_cfg<S>();
+  if (cfg != 5 && cfg != 6)
+    return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need chain configuration 5 or 6");
+  cudaError_t e;
+  switch (k) {
+    case 32: e = launch_chain<32, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
+                                                int(n_sub), int(n_tiles), lr, ru, ri, seed,
+                                                row_base, col_base, stream); break;
+    case 64: e = launch_chain<64, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
+                                                int(n_sub), int(n_tiles), lr, ru, ri, seed,
+                                                row_base, col_base, stream); break;
+    case 128: e = launch_chain<128, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
+                                                  int(n_sub), int(n_tiles), lr, ru, ri, seed,
+                                                  row_base, col_base, stream); break;
+    case 256: e = launch_chain<256, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
+                                                  int(n_sub), int(n_tiles), lr, ru, ri, seed,
+                                                  row_base, col_base, stream); break;
+    default: return set_error(HMF_ERR_UNSUPPORTED, "Q-band kernel needs k in {32,64,128,256}");
+  }
+  if (e != cudaSuccess) return set_cuda_error(e);
+  return 0;
+}
+
 template <typename S>
 static int warps_per_sm(int64_t k, int impl) {
   impl = resolve_impl(impl, k, sizeof(S) == 2);
@@ -887,6 +923,8 @@ int hmf_qband_set_chain_lockstep(int32_t bits) {
   return HMF_OK;
 }
 
+int32_t hmf_qband_get_chain_cfg(void) { return hmf::qs::g_chain_cfg; }
+
 int32_t hmf_qband_chain_lanes(int64_t k) {
   const int cfg = hmf::qs::g_chain_cfg < 0 ? 5 : hmf::qs::g_chain_cfg;  // 5 and 6: same lanes
   if (cfg == 5 || cfg == 6) return k >= 256 ? 16 : 8;
@@ -934,6 +972,29 @@ int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                               k, rows, cols, vals, sub_ptr, sub_cuts, n_sub, n_tiles, impl, lr,
                               reg_user, reg_item, seed, row_base, col_base,
                               static_cast<cudaStream_t>(stream));
+}
+
+int64_t hmf_sgd_block_qband_u16_f32(float* user_f, float* item_f, int64_t k,
+                                    const uint16_t* rows, const int32_t* cols, const float* vals,
+                                    const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
+                                    int64_t n_tiles, double lr, double reg_user, double reg_item,
+                                    uint64_t seed, int64_t row_base, int64_t col_base,
+                                    void* stream) {
+  return hmf::qs::run_u16<float>(user_f, item_f, k, rows, cols, vals, sub_ptr, sub_cuts, n_sub,
+                                 n_tiles, lr, reg_user, reg_item, seed, row_base, col_base,
+                                 static_cast<cudaStream_t>(stream));
+}
+
+int64_t hmf_sgd_block_qband_u16_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                                    const uint16_t* rows, const int32_t* cols, const float* vals,
+                                    const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
+                                    int64_t n_tiles, double lr, double reg_user, double reg_item,
+                                    uint64_t seed, int64_t row_base, int64_t col_base,
+                                    void* stream) {
+  return hmf::qs::run_u16<__half>(reinterpret_cast<__half*>(user_f),
+                                  reinterpret_cast<__half*>(item_f), k, rows, cols, vals, sub_ptr,
+                                  sub_cuts, n_sub, n_tiles, lr, reg_user, reg_item, seed, row_base,
+                                  col_base, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

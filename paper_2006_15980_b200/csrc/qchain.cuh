@@ -144,9 +144,10 @@ __device__ inline void st_release_u32(unsigned* p, unsigned v) {
 // released it — Q row ownership moves between chains through
 // release/acquire, and load balance no longer depends on the number of
 // sub-bands being a multiple of the number of chains.
-template <int K, typename S, int LPC, int PD, int WPB, int MINB, bool DYN>
+template <int K, typename S, int LPC, int PD, int WPB, int MINB, bool DYN,
+          typename RowT = int32_t>
 __global__ void __launch_bounds__(WPB * 32, MINB)
-    qchain_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const int32_t* __restrict__ rows,
+    qchain_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const RowT* __restrict__ rows,
                   const int32_t* __restrict__ cols, const float* __restrict__ vals,
                   const int64_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_cuts,
                   int n_sub, int n_tiles, float lr, float ru, float ri, uint64_t seed,
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     if (xx < nb) {
       const int o = bstart(xx) + l;
       if (o < len) {
-        u = __ldg(rows + beg + o);
+        u = int32_t(__ldg(rows + beg + o));
         v = cols ? __ldg(cols + beg + o) : vbin;
         r = __ldg(vals + beg + o);
       }
@@ -402,16 +403,16 @@ static cudaError_t chain_work(cudaStream_t stream, size_t words, unsigned** out)
   return cudaMemsetAsync(b.first, 0, words * sizeof(unsigned), stream);
 }
 
-template <int K, typename S, int CFG>
-static cudaError_t launch_chain_cfg(S* P, S* Q, const int32_t* rows, const int32_t* cols,
+template <int K, typename S, int CFG, typename RowT>
+static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t* cols,
                                     const float* vals, const int64_t* sub_ptr,
                                     const int32_t* sub_cuts, int n_sub,
                                     int n_tiles, double lr, double ru, double ri, uint64_t seed,
                                     int64_t row_base, int64_t col_base, cudaStream_t stream) {
   using C = ChainCfg<K, CFG>;
   constexpr int NC = 32 / C::LPC;
-  auto kstat = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false>;
-  auto kdyn = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, true>;
+  auto kstat = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false, RowT>;
+  auto kdyn = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, true, RowT>;
   static int per_sm = 0;
   if (per_sm == 0) {
     const cudaError_t e =
@@ -440,23 +441,35 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const int32_t* rows, const int32
   return cudaGetLastError();
 }
 
-template <int K, typename S>
-static cudaError_t launch_chain(S* P, S* Q, const int32_t* rows, const int32_t* cols,
+// rows: int32 row ids, or uint16 (a row tile's ids relative to its first row,
+// passed as row_base = -first row: 2 bytes per rating on the host stream;
+// default configurations 5 and 6 only)
+template <int K, typename S, typename RowT = int32_t>
+static cudaError_t launch_chain(S* P, S* Q, const RowT* rows, const int32_t* cols,
                                 const float* vals, const int64_t* sub_ptr,
                                 const int32_t* sub_cuts, int n_sub, int n_tiles,
                                 double lr, double ru, double ri, uint64_t seed, int64_t row_base,
                                 int64_t col_base, cudaStream_t stream) {
-#define HMF_CHAIN_CFG(CFG)                                                                   \
-  return launch_chain_cfg<K, S, CFG>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, n_sub,      \
-                                     n_tiles, lr, ru, ri, seed, row_base, col_base, stream)
-  switch (chain_cfg<S>()) {
-    case 0: HMF_CHAIN_CFG(0);
-    case 2: HMF_CHAIN_CFG(2);
-    case 3: HMF_CHAIN_CFG(3);
-    case 4: HMF_CHAIN_CFG(4);
-    case 5: HMF_CHAIN_CFG(5);
-    case 6: HMF_CHAIN_CFG(6);
-    default: HMF_CHAIN_CFG(1);
+#define HMF_CHAIN_CFG(CFG)                                                                     \
+  return launch_chain_cfg<K, S, CFG, RowT>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, n_sub,  \
+                                           n_tiles, lr, ru, ri, seed, row_base, col_base,      \
+                                           stream)
+  if constexpr (sizeof(RowT) == 2) {
+    switch (chain_cfg<S>()) {
+      case 5: HMF_CHAIN_CFG(5);
+      case 6: HMF_CHAIN_CFG(6);
+      default: return cudaErrorNotSupported;
+    }
+  } else {
+    switch (chain_cfg<S>()) {
+      case 0: HMF_CHAIN_CFG(0);
+      case 2: HMF_CHAIN_CFG(2);
+      case 3: HMF_CHAIN_CFG(3);
+      case 4: HMF_CHAIN_CFG(4);
+      case 5: HMF_CHAIN_CFG(5);
+      case 6: HMF_CHAIN_CFG(6);
+      default: HMF_CHAIN_CFG(1);
+    }
   }
 #undef HMF_CHAIN_CFG
 }

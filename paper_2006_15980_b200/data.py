@@ -376,6 +376,7 @@ class DeviceGrid:
     # sub_tiles[b] * S + 1 offsets, tile-major
     sub_tiles: list | None = None
     sub_impl: int = -1          # Q-band implementation the layout is for
+    sub_tile_rows: list | None = None   # per block: row cuts of its tiles (host int64)
 
     n_row_bands = BlockGrid.n_row_bands
     n_col_bands = BlockGrid.n_col_bands
@@ -535,7 +536,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     out_u = torch.empty_like(grid.users)
     out_i = torch.empty_like(grid.items)
     out_r = torch.empty_like(grid.ratings)
-    sub_ptrs, sub_cuts, sub_tiles = [], [], []
+    sub_ptrs, sub_cuts, sub_tiles, tile_rows = [], [], [], []
     for b in range(grid.n_blocks):
         lo, hi = grid.block_range(b)
         c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
@@ -593,38 +594,12 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         sub_ptrs.append(ptr)
         sub_cuts.append(torch.from_numpy(cuts).to(device=dev, dtype=torch.int32))
         sub_tiles.append(n_tiles)
+        tile_rows.append(tiles)
     del out_u, out_i, out_r
     grid.sub_ptr, grid.sub_cuts, grid.sub_tiles = sub_ptrs, sub_cuts, sub_tiles
     grid.sub_impl = impl
+    grid.sub_tile_rows = tile_rows
     return grid
-
-
-def stripe_layout(grid: DeviceGrid, n_stripes: int) -> DeviceGrid:
-    """Split every block into `n_stripes` index stripes and lay the grid out
-    stripe-major: stripe 0 of every block, then stripe 1, ...  The result is a
-    DeviceGrid with n_stripes row bands (all spanning every row) whose block
-    (r, c) is stripe r of the original column band c — each stripe a
-    contiguous slice holding part of every item, so a host->device stream can
-    upload stripe s+1 while the GPU updates stripe s with all warps busy.
-    Blocks keep their original relative order inside a stripe."""
-    torch = _torch()
-    if grid.n_row_bands != 1:
-        raise GridError("stripe_layout expects a single-row-band grid (one GPU's band)")
-    ncb = grid.n_col_bands
-    pieces, ptr = [], [0]
-    for r in range(n_stripes):
-        for c in range(ncb):
-            lo, hi = grid.block_range(c)
-            n = hi - lo
-            a, b = lo + (n * r) // n_stripes, lo + (n * (r + 1)) // n_stripes
-            pieces.append((a, b))
-            ptr.append(ptr[-1] + (b - a))
-    idx = torch.cat([torch.arange(a, b, device=grid.device) for a, b in pieces])
-    row_cuts = np.linspace(0, grid.n_rows, n_stripes + 1).astype(np.int64)
-    return DeviceGrid(grid.n_rows, grid.n_cols, row_cuts, grid.col_cuts,
-                      np.full(n_stripes, REGION_BATCH, dtype=np.int8), None,
-                      grid.users[idx].contiguous(), grid.items[idx].contiguous(),
-                      grid.ratings[idx].contiguous(), np.asarray(ptr, dtype=np.int64))
 
 
 def synthetic_device(n_users: int, n_items: int, nnz: int, rank: int = 8, noise: float = 0.1,

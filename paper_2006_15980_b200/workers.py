@@ -445,82 +445,116 @@ class StreamingEpoch:
 
     The reference stages a unit's triples into the accelerator for every
     lease (BatchEngine.stage_in, workers.py:186-202).  This is that pipeline
-    for data that is not kept resident: the grid is laid out stripe-major
-    (data.stripe_layout) and Q-band bucketed once, copied to pinned host
-    memory, and every epoch uploads stripe s+1 on a copy stream while the
-    Q-band kernel updates stripe s (double-buffered device staging, ordered by
-    CUDA events).  P and Q stay on the device.
+    for data that is not kept resident.  P and Q stay on the device; every
+    epoch uploads chunk c+1 on a copy stream while the Q-band kernel updates
+    chunk c (a ring of device staging buffers, ordered by CUDA events).
 
-    Per epoch the host->device traffic is the triples: 12 bytes per rating,
-    or 8 when every sub-band is a single item and the chained kernel runs —
-    the item id is then implicit in the sub-band (hmf_sgd_block_qband_* with
-    cols = NULL), so only users and ratings cross PCIe.  Stripes are already
-    short, so no row tiles by default (tile_bytes=0).
+    Chunks are the row tiles of each block (data.bucket_qbands): chunk (b, t)
+    holds block b's triples of row tile t, item runs inside.  While a chunk
+    trains, its tile's P rows sit in L2, as in the resident layout, and the
+    epoch walks each block's tiles in a seeded rotation.
+
+    Bytes per rating on the host stream (the chained kernel, one item per
+    sub-band, every tile at most 65536 rows): a 2-byte user id relative to
+    the tile plus the 4-byte rating — the item is implicit in the sub-band
+    (hmf_sgd_block_qband_u16_*, cols = NULL).  Otherwise 8 (4-byte user ids,
+    implicit items) or 12.
     """
 
-    def __init__(self, grid: DeviceGrid, k: int, n_stripes: int = 8, tile_bytes=0):
-        from .data import stripe_layout
+    def __init__(self, grid: DeviceGrid, k: int, tile_bytes=None, n_buffers: int = 2,
+                 elem_bytes: int = 4, compact: bool = True):
         torch = _torch()
         self.dev = grid.device
-        sg = bucket_qbands(stripe_layout(grid, n_stripes), k, tile_bytes=tile_bytes)
+        # a grid the caller already laid out for the Q-band kernel is used as is
+        sg = grid if grid.sub_ptr is not None else bucket_qbands(
+            grid, k, tile_bytes=tile_bytes, elem_bytes=elem_bytes)
         self.k = k
-        self.n_blocks = sg.n_blocks
         self.nnz = sg.nnz
-        self.block_ptr = sg.block_ptr
-        # per block: sub_ptr relative to the block start (device) and sub_cuts
-        self.sub_rel = [(p - int(sg.block_ptr[b])).contiguous() for b, p in enumerate(sg.sub_ptr)]
-        self.sub_cuts = sg.sub_cuts
-        self.sub_tiles = sg.sub_tiles
         self.sub_impl = sg.sub_impl
-        self.implicit_items = sg.sub_impl == 4 and all(
+        self.implicit_items = compact and sg.sub_impl == 4 and all(
             bool(torch.all(c[1:] - c[:-1] == 1)) for c in sg.sub_cuts)
-        # host copies (pinned) of the stripe-major, sub-band bucketed triples
-        arrays = [sg.users] + ([] if self.implicit_items else [sg.items]) + [sg.ratings]
+        cfg_ok = int(_lib.load().hmf_qband_get_chain_cfg()) in (-1, 5, 6)
+        self.u16 = self.implicit_items and cfg_ok and all(
+            int(np.max(np.diff(r))) <= 65536 for r in sg.sub_tile_rows)
+        # chunks: (block, tile) -> [lo, hi) of the bucketed arrays, the tile's
+        # first row, its sub-band offsets relative to lo, the block's sub_cuts
+        self.blocks = []
+        users = sg.users
+        if self.u16:
+            users = torch.empty(sg.nnz, dtype=torch.int16, device=self.dev)
+        for b in range(sg.n_blocks):
+            sp = sg.sub_ptr[b].cpu().numpy()
+            T = sg.sub_tiles[b]
+            S = (len(sp) - 1) // T
+            tiles = []
+            for t in range(T):
+                lo, hi = int(sp[t * S]), int(sp[(t + 1) * S])
+                row0 = int(sg.sub_tile_rows[b][t])
+                rel = (sg.sub_ptr[b][t * S:(t + 1) * S + 1] - lo).contiguous()
+                tiles.append((lo, hi, row0, rel))
+                if self.u16 and hi > lo:
+                    # uint16 bit pattern of (user - row0), 0..65535
+                    users[lo:hi] = (sg.users[lo:hi] - row0).to(torch.int32).to(torch.int16)
+            self.blocks.append((tiles, sg.sub_cuts[b]))
+        arrays = [users] + ([] if self.implicit_items else [sg.items]) + [sg.ratings]
         self.host = [a.cpu().pin_memory() for a in arrays]
-        cap = int(np.max(np.diff(sg.block_ptr))) + 4
+        cap = max([hi - lo for tiles, _ in self.blocks for lo, hi, _, _ in tiles] + [0]) + 8
+        self.n_buffers = max(2, int(n_buffers))
         self.bufs = [tuple(torch.empty(cap, dtype=a.dtype, device=self.dev) for a in arrays)
-                     for _ in range(2)]
+                     for _ in range(self.n_buffers)]
         self.copy_stream = torch.cuda.Stream(device=self.dev)
-        self.freed = [None, None]
-        del sg
+        self.freed = [None] * self.n_buffers
+        self.n_chunks = sum(len(t) for t, _ in self.blocks)
+        del users
+
+    @property
+    def bytes_per_rating(self) -> int:
+        return 6 if self.u16 else (8 if self.implicit_items else 12)
 
     @property
     def h2d_bytes(self) -> int:
-        return (8 if self.implicit_items else 12) * self.nnz
+        return self.bytes_per_rating * self.nnz
 
     def run(self, P, Q, hparams: Hyperparams, seed: int, stream=None) -> int:
         """One epoch over every block; returns triples processed (async)."""
         torch = _torch()
         comp = torch.cuda.current_stream(self.dev) if stream is None else stream
         st = "f16" if P.dtype == torch.float16 else "f32"
-        fn = getattr(_lib.load(), f"hmf_sgd_block_qband_{st}")
-        done = 0
-        for b in range(self.n_blocks):
-            lo, hi = int(self.block_ptr[b]), int(self.block_ptr[b + 1])
-            if hi <= lo:
-                continue
-            buf = self.bufs[b & 1]
-            with torch.cuda.stream(self.copy_stream):
-                if self.freed[b & 1] is not None:
-                    self.copy_stream.wait_event(self.freed[b & 1])
-                for dst, src in zip(buf, self.host):
-                    dst[:hi - lo].copy_(src[lo:hi], non_blocking=True)
-                up = torch.cuda.Event()
-                up.record(self.copy_stream)
-            comp.wait_event(up)
-            sp, sc = self.sub_rel[b], self.sub_cuts[b]
-            users, vals = buf[0], buf[-1]
-            items = 0 if self.implicit_items else buf[1].data_ptr()
-            _lib.check(fn(P.data_ptr(), Q.data_ptr(), self.k, users.data_ptr(), items,
-                          vals.data_ptr(), sp.data_ptr(), sc.data_ptr(),
-                          int(sc.numel()) - 1, self.sub_tiles[b], self.sub_impl,
-                          hparams.learning_rate, hparams.reg_user,
-                          hparams.reg_item, kernels.mix64(seed, b) & 0xFFFFFFFFFFFFFFFF, 0, 0,
-                          comp.cuda_stream), f"hmf_sgd_block_qband_{st}")
-            ev = torch.cuda.Event()
-            ev.record(comp)
-            self.freed[b & 1] = ev
-            done += hi - lo
+        lib = _lib.load()
+        fn = getattr(lib, f"hmf_sgd_block_qband_u16_{st}" if self.u16
+                     else f"hmf_sgd_block_qband_{st}")
+        done, c = 0, 0
+        for b, (tiles, sc) in enumerate(self.blocks):
+            bseed = kernels.mix64(seed, b) & 0xFFFFFFFFFFFFFFFF
+            rot = bseed % len(tiles) if tiles else 0
+            for i in range(len(tiles)):
+                t = (i + rot) % len(tiles)
+                lo, hi, row0, rel = tiles[t]
+                if hi <= lo:
+                    continue
+                slot = c % self.n_buffers
+                c += 1
+                buf = self.bufs[slot]
+                with torch.cuda.stream(self.copy_stream):
+                    if self.freed[slot] is not None:
+                        self.copy_stream.wait_event(self.freed[slot])
+                    for dst, src in zip(buf, self.host):
+                        dst[:hi - lo].copy_(src[lo:hi], non_blocking=True)
+                    up = torch.cuda.Event()
+                    up.record(self.copy_stream)
+                comp.wait_event(up)
+                items = 0 if self.implicit_items else buf[1].data_ptr()
+                tseed = kernels.mix64(bseed, t) & 0xFFFFFFFFFFFFFFFF
+                head = (P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr(), items,
+                        buf[-1].data_ptr(), rel.data_ptr(), sc.data_ptr(), int(sc.numel()) - 1, 1)
+                tail = (hparams.learning_rate, hparams.reg_user, hparams.reg_item, tseed,
+                        -row0 if self.u16 else 0, 0, comp.cuda_stream)
+                mid = () if self.u16 else (self.sub_impl,)
+                _lib.check(fn(*head, *mid, *tail), "hmf_sgd_block_qband")
+                ev = torch.cuda.Event()
+                ev.record(comp)
+                self.freed[slot] = ev
+                done += hi - lo
         return done
 
 

@@ -146,9 +146,9 @@ def test_throughput_sweep_reports_stages(dev):
 
 @pytest.mark.parametrize("k", [64, 128])
 def test_streaming_epoch_applies_every_triple_once(dev, k):
-    """StreamingEpoch (triples streamed from pinned host memory, double
-    buffered) on conflict-free triples equals the reference update of each
-    triple exactly once."""
+    """StreamingEpoch (triples streamed from pinned host memory tile by tile,
+    double buffered) on conflict-free triples equals the reference update of
+    each triple exactly once."""
     import oracle
     from paper_2006_15980_b200.data import DeviceTriples, build_device_grid
     from paper_2006_15980_b200.sgd import Hyperparams
@@ -162,7 +162,8 @@ def test_streaming_epoch_applies_every_triple_once(dev, k):
     m = RatingMatrix(9000, 7000, users, items, vals)
     d = torch.device("cuda", dev)
     g = build_device_grid(DeviceTriples.from_host(m, d), [0, 9000], [0, 3500, 7000])
-    se = StreamingEpoch(g, k, n_stripes=3)
+    se = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1)   # 3 row tiles per block
+    assert se.n_chunks == 6
     P0 = rng.uniform(0, 0.1, size=(9000, k)).astype(np.float32)
     Q0 = rng.uniform(0, 0.1, size=(7000, k)).astype(np.float32)
     P, Q = torch.from_numpy(P0).to(d), torch.from_numpy(Q0).to(d)
@@ -174,6 +175,7 @@ def test_streaming_epoch_applies_every_triple_once(dev, k):
     rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)  # noqa: E731
     assert rel(P.double().cpu().numpy(), Pe) < 1e-6
     assert rel(Q.double().cpu().numpy(), Qe) < 1e-6
-    # k = 128: the chained kernel with one item per sub-band, items implicit
-    assert se.implicit_items == (k == 128)
-    assert se.h2d_bytes == (8 if k == 128 else 12) * n
+    # k = 128: the chained kernel with one item per sub-band: items implicit,
+    # 2-byte user ids relative to the row tile
+    assert se.implicit_items == (k == 128) and se.u16 == (k == 128)
+    assert se.h2d_bytes == (6 if k == 128 else 12) * n
