@@ -64,6 +64,68 @@ __global__ void __launch_bounds__(512, 1) rowbench(float* buf, uint32_t n_rows, 
   if (acc == 12345.f) sink[0] = acc;
 }
 
+// Bulk-reduction mode: each warp adds a ROWB-byte shared-memory row into
+// DEPTH random rows per iteration with cp.reduce.async.bulk (the TMA unit),
+// optionally loading the rows first (LOAD).  One lane issues; bulk groups are
+// drained every iteration.
+template <int ROWB, int DEPTH, bool LOAD>
+__global__ void __launch_bounds__(512, 1) bulkbench(float* buf, uint32_t n_rows, int iters,
+                                                   float* sink) {
+  __shared__ __align__(128) float src[16][ROWB / 4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = lane; i < ROWB / 4; i += 32) src[warp][i] = 1e-30f;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  uint32_t seed = (blockIdx.x * blockDim.x + threadIdx.x) / 32 * 7919u + 17u;
+  const uint32_t saddr = static_cast<uint32_t>(__cvta_generic_to_shared(&src[warp][0]));
+  float acc = 0.f;
+  for (int it = 0; it < iters; ++it) {
+    uint32_t r[DEPTH];
+#pragma unroll
+    for (int d = 0; d < DEPTH; ++d) r[d] = hash32(seed + uint32_t(it * DEPTH + d) * 0x9E3779B9u) % n_rows;
+    if (LOAD) {
+#pragma unroll
+      for (int d = 0; d < DEPTH; ++d) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(buf + size_t(r[d]) * (ROWB / 4)) + (lane % (ROWB / 16)));
+        acc += v.x;
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int d = 0; d < DEPTH; ++d) {
+        float* dst = buf + size_t(r[d]) * (ROWB / 4);
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;"
+                     ::"l"(dst), "r"(saddr), "n"(ROWB) : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory");
+    }
+    __syncwarp();
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (acc == 12345.f) sink[0] = acc;
+}
+
+template <int ROWB, int DEPTH, bool LOAD>
+static void run_bulk(float* buf, uint32_t n_rows, float* sink, int sms) {
+  const int iters = 400, blocks = sms, threads = 512;
+  bulkbench<ROWB, DEPTH, LOAD><<<blocks, threads>>>(buf, n_rows, 4, sink);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  bulkbench<ROWB, DEPTH, LOAD><<<blocks, threads>>>(buf, n_rows, iters, sink);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  const double rows = double(blocks) * threads / 32 * iters * DEPTH;
+  printf("{\"mode\": \"%s\", \"row_bytes\": %d, \"depth\": %d, \"lanes_per_row\": 32, "
+         "\"rows_per_s\": %.4g, \"GBps_rowbytes\": %.1f}\n",
+         LOAD ? "load+bulkred" : "bulkred", ROWB, DEPTH, rows / (ms * 1e-3),
+         rows * ROWB / (ms * 1e-3) / 1e9);
+}
+
 template <int MODE, int ROWB, int DEPTH, int LPR>
 static void run(float* buf, uint32_t n_rows, float* sink, int sms) {
   const int iters = 400;
@@ -113,6 +175,11 @@ int main(int argc, char** argv) {
   RUN5(1024, 4, 8)
   // whole-warp rows (the warp-per-rating layout)
   RUN5(512, 4, 32)
+  // TMA bulk reductions
+  run_bulk<512, 4, false>(buf, uint32_t((mb << 20) / 512), sink, sms);
+  run_bulk<512, 8, false>(buf, uint32_t((mb << 20) / 512), sink, sms);
+  run_bulk<512, 4, true>(buf, uint32_t((mb << 20) / 512), sink, sms);
+  run_bulk<512, 8, true>(buf, uint32_t((mb << 20) / 512), sink, sms);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
   return 0;

@@ -643,6 +643,52 @@ def test_qband_chains_dynamic_matches_sequential(dev, n_tiles):
         _lib.load().hmf_qband_set_impl(-1)
 
 
+@pytest.mark.parametrize("n_items,impl", [(300, 0), (300, 4), (40_000, 4)],
+                         ids=["regs", "chains_static", "chains_dynamic"])
+def test_qband_skewed_items_match_sequential(dev, n_items, impl):
+    """Zipf-skewed item popularity (one item holds a large share of the
+    ratings; many items are empty) and row tiles with empty bins: with
+    distinct users every sub-band still equals a sequential replay of its
+    units in tile order — static ownership and the dynamic scheduler alike."""
+    from paper_2006_15980_b200 import _lib, kernels
+    from paper_2006_15980_b200.data import RatingMatrix
+    k, n_tiles, seed = 64, 3, 777
+    _lib.check(_lib.load().hmf_qband_set_impl(impl), "set_impl")
+    try:
+        rng = np.random.default_rng(n_items + impl)
+        n_users, n = 300_000, 60_000
+        users = rng.permutation(n_users)[:n].astype(np.int32)
+        items = ((rng.zipf(1.3, n) - 1) % n_items).astype(np.int32)
+        vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
+        m = RatingMatrix(n_users, n_items, users, items, vals)
+        tb = n_users * k * 4 // n_tiles + 1
+        target = n_items if impl == 4 else min(n_items, 200)
+        g = _qband_grid(dev, m, k, [0, n_items], target=target, tile_bytes=tb)
+        assert g.sub_tiles == [n_tiles] and g.sub_impl == impl
+        S = g.sub_cuts[0].numel() - 1
+        P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
+        Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
+        P, Q = to_dev(P0, dev), to_dev(Q0, dev)
+        assert kernels.launch_block_qband(P, Q, g, 0, 0.05, 0.02, 0.03, seed) == n
+        gu, gi = g.users.cpu().numpy(), g.items.cpu().numpy()
+        gr = g.ratings.cpu().numpy().astype(np.float64)
+        ptr = g.sub_ptr[0].cpu().numpy()
+        order = [i for t in _tile_order(seed, n_tiles) for s_ in range(S)
+                 for i in _bin_visit(impl, k, int(ptr[t * S + s_]), int(ptr[t * S + s_ + 1]),
+                                     seed, t * S + s_)]
+        assert sorted(order) == list(range(n))
+        Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
+        for u, v, r in zip(gu[order], gi[order], gr[order]):
+            pu, qv = Pe[u].copy(), Qe[v].copy()
+            e = r - pu @ qv
+            Pe[u] = pu + 0.05 * (e * qv - 0.02 * pu)
+            Qe[v] = qv + 0.05 * (e * pu - 0.03 * qv)
+        assert rel_err(Q.double().cpu().numpy(), Qe) < 1e-5
+        assert rel_err(P.double().cpu().numpy(), Pe) < 1e-5
+    finally:
+        _lib.load().hmf_qband_set_impl(-1)
+
+
 def test_qband_fp16_storage_tracks_fp32(dev, qband_impl):
     from paper_2006_15980_b200 import kernels
     m = random_matrix(3000, 800, 200_000, 5)
