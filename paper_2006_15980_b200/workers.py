@@ -504,7 +504,10 @@ class StreamingEpoch:
                      for _ in range(self.n_buffers)]
         self.copy_stream = torch.cuda.Stream(device=self.dev)
         self.freed = [None] * self.n_buffers
+        self.lru = [None] * self.n_buffers            # chunk (block, tile) held by each buffer
+        self.lru_order = list(range(self.n_buffers))  # buffers, least recently used first
         self.n_chunks = sum(len(t) for t, _ in self.blocks)
+        self.last_h2d = 0
         del users
 
     @property
@@ -513,27 +516,47 @@ class StreamingEpoch:
 
     @property
     def h2d_bytes(self) -> int:
+        """Bytes of triples one epoch uploads (all chunks; an epoch that
+        starts on chunks still resident from the previous one uploads
+        less — see h2d_bytes_last)."""
         return self.bytes_per_rating * self.nnz
 
+    def h2d_bytes_last(self) -> int:
+        """Bytes the last run() uploaded."""
+        return self.last_h2d
+
     def run(self, P, Q, hparams: Hyperparams, seed: int, stream=None) -> int:
-        """One epoch over every block; returns triples processed (async)."""
+        """One epoch over every block; returns triples processed (async).
+
+        Chunks still in a staging buffer from the previous epoch are trained
+        first and not uploaded again (the tail of epoch e is the head of
+        epoch e+1); the rest follow block by block, each block's tiles in a
+        seeded rotation."""
         torch = _torch()
         comp = torch.cuda.current_stream(self.dev) if stream is None else stream
         st = "f16" if P.dtype == torch.float16 else "f32"
         lib = _lib.load()
         fn = getattr(lib, f"hmf_sgd_block_qband_u16_{st}" if self.u16
                      else f"hmf_sgd_block_qband_{st}")
-        done, c = 0, 0
-        for b, (tiles, sc) in enumerate(self.blocks):
+        order = []
+        for b, (tiles, _) in enumerate(self.blocks):
             bseed = kernels.mix64(seed, b) & 0xFFFFFFFFFFFFFFFF
             rot = bseed % len(tiles) if tiles else 0
-            for i in range(len(tiles)):
-                t = (i + rot) % len(tiles)
-                lo, hi, row0, rel = tiles[t]
-                if hi <= lo:
-                    continue
-                slot = c % self.n_buffers
-                c += 1
+            order += [(b, (i + rot) % len(tiles), bseed) for i in range(len(tiles))]
+        resident = [ch for ch in reversed(self.lru) if ch is not None]
+        head = [o for ch in resident for o in order if (o[0], o[1]) == ch]
+        order = head + [o for o in order if (o[0], o[1]) not in resident]
+        done, uploaded = 0, 0
+        for b, t, bseed in order:
+            tiles, sc = self.blocks[b]
+            lo, hi, row0, rel = tiles[t]
+            if hi <= lo:
+                continue
+            if (b, t) in self.lru:
+                slot = self.lru.index((b, t))        # already on the device
+                buf = self.bufs[slot]
+            else:
+                slot = self.lru_order[0]             # least recently used buffer
                 buf = self.bufs[slot]
                 with torch.cuda.stream(self.copy_stream):
                     if self.freed[slot] is not None:
@@ -543,18 +566,23 @@ class StreamingEpoch:
                     up = torch.cuda.Event()
                     up.record(self.copy_stream)
                 comp.wait_event(up)
-                items = 0 if self.implicit_items else buf[1].data_ptr()
-                tseed = kernels.mix64(bseed, t) & 0xFFFFFFFFFFFFFFFF
-                head = (P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr(), items,
-                        buf[-1].data_ptr(), rel.data_ptr(), sc.data_ptr(), int(sc.numel()) - 1, 1)
-                tail = (hparams.learning_rate, hparams.reg_user, hparams.reg_item, tseed,
-                        -row0 if self.u16 else 0, 0, comp.cuda_stream)
-                mid = () if self.u16 else (self.sub_impl,)
-                _lib.check(fn(*head, *mid, *tail), "hmf_sgd_block_qband")
-                ev = torch.cuda.Event()
-                ev.record(comp)
-                self.freed[slot] = ev
-                done += hi - lo
+                self.lru[slot] = (b, t)
+                uploaded += hi - lo
+            self.lru_order.remove(slot)
+            self.lru_order.append(slot)
+            items = 0 if self.implicit_items else buf[1].data_ptr()
+            tseed = kernels.mix64(bseed, t) & 0xFFFFFFFFFFFFFFFF
+            args = (P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr(), items,
+                    buf[-1].data_ptr(), rel.data_ptr(), sc.data_ptr(), int(sc.numel()) - 1, 1)
+            args += () if self.u16 else (self.sub_impl,)
+            args += (hparams.learning_rate, hparams.reg_user, hparams.reg_item, tseed,
+                     -row0 if self.u16 else 0, 0, comp.cuda_stream)
+            _lib.check(fn(*args), "hmf_sgd_block_qband")
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            self.freed[slot] = ev
+            done += hi - lo
+        self.last_h2d = uploaded * self.bytes_per_rating
         return done
 
 

@@ -179,3 +179,8 @@ def test_streaming_epoch_applies_every_triple_once(dev, k):
     # 2-byte user ids relative to the row tile
     assert se.implicit_items == (k == 128) and se.u16 == (k == 128)
     assert se.h2d_bytes == (6 if k == 128 else 12) * n
+    assert se.h2d_bytes_last() == se.h2d_bytes          # first epoch: every chunk uploaded
+    # a second epoch starts on the two chunks still staged and does not upload them
+    assert se.run(P, Q, hp, seed=2) == n
+    torch.cuda.synchronize()
+    assert 0 < se.h2d_bytes_last() < se.h2d_bytes
