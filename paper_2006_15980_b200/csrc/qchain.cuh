@@ -159,7 +159,9 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
   const int lane = threadIdx.x & 31;
   const int c = lane / LPC, l = lane % LPC;
   const unsigned cmask = LPC == 32 ? FULL : (((1u << LPC) - 1u) << (c * LPC));
-  const int cg = (blockIdx.x * WPB + (threadIdx.x >> 5)) * NC + c;  // global chain id
+  // global chain id, CTA-minor: consecutive sub-bands land on different SMs,
+  // so a block with fewer sub-bands than chains still spreads over the GPU
+  const int cg = ((threadIdx.x >> 5) * NC + c) * int(gridDim.x) + int(blockIdx.x);
   const int n_slots = gridDim.x * WPB * NC;
   const float a_ru = lr * ru, keep_q = 1.f - lr * ri;
   const unsigned n_units = unsigned(n_tiles) * unsigned(n_sub);
@@ -420,9 +422,10 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
   }
-  const int want = (n_sub + C::WPB * NC - 1) / (C::WPB * NC);
+  // a full grid (chains are spread CTA-minor, so even a block with few
+  // sub-bands uses every SM); blocks with fewer sub-bands than CTAs need fewer
   const int cap = device_sm_count() * per_sm;
-  const int grid = want < cap ? want : cap;
+  const int grid = n_sub < cap ? n_sub : cap;
   if (grid <= 0) return cudaSuccess;
   // more sub-bands than chains: units are handed out dynamically (a static
   // split would leave some chains with one sub-band more than others in

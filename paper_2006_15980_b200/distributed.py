@@ -203,8 +203,12 @@ class CudaRowBand:
             self.Q = (torch.rand((n_items, k), generator=gq, device=self.dev) * top).contiguous()
         # local triples (users already global ids within [row_lo, row_hi))
         local = DeviceTriples(row_hi, n_items, triples.users, triples.items, triples.ratings)
-        self.grid = build_device_grid(local, [0, row_hi], self.col_cuts)
-        self.block_of = list(range(self.n_cols))   # one row band: block c = column c
+        # row bands [0, row_lo) (empty) and [row_lo, row_hi): row tiles of the
+        # Q-band layout then cover this rank's band only
+        rows = [0, row_hi] if row_lo == 0 else [0, row_lo, row_hi]
+        self.grid = build_device_grid(local, rows, self.col_cuts)
+        first = 0 if row_lo == 0 else self.n_cols
+        self.block_of = [first + c for c in range(self.n_cols)]   # block of column c
         widest = int(np.max(np.diff(self.col_cuts)))
         want = resident_warps(self.dev, k) // 2
         self.kernel = kernel if kernel != "auto" else ("qband" if widest >= want else "range")
