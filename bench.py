@@ -471,7 +471,8 @@ def run_ours_multi(args, world, rank, local):
     row_lo, row_hi = rank * n_users, (rank + 1) * n_users
     trip.users += row_lo                       # global user ids of this rank's band
     train, test = split_device(trip, TEST_FRACTION)
-    n_cols = 2 * world + 1
+    geo = args.sim_world or world      # --sim-world: rank 0's share of a larger job
+    n_cols = 2 * geo + 1
     col_cuts = np.linspace(0, n_items, n_cols + 1).astype(np.int64)
     band = CudaRowBand(dist, rank, world, dev, train, row_lo, row_hi, col_cuts, k, LR, REG, REG,
                        init_seed=SEED, kernel=args.multi_kernel)
@@ -510,7 +511,11 @@ def run_ours_multi(args, world, rank, local):
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synthetic_ratings law, device generator)",
             "config": {"workload": f"{desc} row band per GPU (weak scaling), k={k}",
-                       "grid": f"{world} row bands x {n_cols} column bands",
+                       "grid": f"{geo} row bands x {n_cols} column bands",
+                       "simulated": (None if not args.sim_world else
+                                     f"one process with rank 0's band and column geometry of "
+                                     f"a {geo}-GPU job (per-GPU throughput; peer pulls of Q "
+                                     f"bands not exercised)"),
                        "parallelism": f"dp{world} row bands, Q bands leased and pulled peer-to-peer",
                        "kernel": band.kernel, "lr": LR, "reg": REG},
             "rmse": {"epochs": args.warmup + args.steps,
@@ -542,14 +547,17 @@ def run_e2e_stream(args, se, model, test, dev):
     torch.cuda.synchronize(dev)
     steps = max(3, args.steps)
     h2d = 0
-    t0 = time.perf_counter()
+    marks = [time.perf_counter()]
     for i in range(steps):
         sq = step(2 + i)
         h2d += se.h2d_bytes_last()
-    dt = time.perf_counter() - t0
+        marks.append(time.perf_counter())
+    dt = marks[-1] - marks[0]
+    per = sorted(1e3 * (b - a) for a, b in zip(marks, marks[1:]))
     return {"value": se.nnz * steps / dt, "unit": "updates/s",
             "h2d_bytes_per_step": int(round(h2d / steps)), "d2h_bytes_per_step": 8,
             "steps": steps,
+            "ms_per_step": {"min": per[0], "median": per[len(per) // 2], "max": per[-1]},
             "test_rmse_after": float(np.sqrt(sq / test.nnz)),
             "path": "workers.StreamingEpoch (pinned host triples streamed per epoch, "
                     + (f"{se.bytes_per_rating} B/rating: "
@@ -622,6 +630,8 @@ def main():
                     help="e2e: device staging buffers (ring)")
     ap.add_argument("--tile-mb", type=float, default=None,
                     help="P rows per Q-band row tile in MiB (default data.QBAND_TILE_BYTES; 0 = no tiling)")
+    ap.add_argument("--sim-world", type=int, default=0,
+                    help="N=1 only: run rank 0 of an N-GPU job's geometry (projected per-GPU rate)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -633,6 +643,14 @@ def main():
         run_reference_arm(args, world, rank)
         return
     world, rank, local = dist_setup()
+    if world == 1 and args.sim_world:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29000 + os.getpid() % 1000))
+        dist.init_process_group("gloo", rank=0, world_size=1)
+        run_ours_multi(args, world, rank, local)
+        dist.destroy_process_group()
+        return
     if world > 1:
         run_ours_multi(args, world, rank, local)
     else:

@@ -139,6 +139,10 @@ int32_t hmf_qband_resolve_impl(int64_t k, int32_t f16);
  * seeded rotation, then the partial batch. */
 int hmf_qband_set_chain_cfg(int32_t cfg);
 int32_t hmf_qband_get_chain_cfg(void);
+/* Cap every Q-band launch's grid at 1/div of the resident CTA slots (default
+ * 1), so div launches on separate streams — several column blocks of one row
+ * band — run side by side. */
+int hmf_qband_set_grid_share(int32_t div);
 int32_t hmf_qband_chain_lanes(int64_t k);
 /* Implementation 4: chains of a warp change bins together (bit 0: static
  * scheduler, bit 1: dynamic scheduler; default 3). */

@@ -460,7 +460,7 @@ static cudaError_t launch_tma(S* P, S* Q, const int32_t* rows, const int32_t* co
     if (per_sm < 1) per_sm = 1;
   }
   const int want = (n_sub + C::WPB - 1) / C::WPB;
-  const int cap = device_sm_count() * per_sm;
+  const int cap = grid_share(device_sm_count() * per_sm);
   const int grid = want < cap ? want : cap;
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
@@ -695,7 +695,7 @@ static cudaError_t launch_async(S* P, S* Q, const int32_t* rows, const int32_t* 
     if (per_sm < 1) per_sm = 1;
   }
   const int want = (n_sub + C::WPB - 1) / C::WPB;
-  const int cap = device_sm_count() * per_sm;
+  const int cap = grid_share(device_sm_count() * per_sm);
   const int grid = want < cap ? want : cap;
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
@@ -763,7 +763,7 @@ static cudaError_t launch(S* P, S* Q, const int32_t* rows, const int32_t* cols, 
     if (per_sm < 1) per_sm = 1;
   }
   const int want = (n_sub + kWarps - 1) / kWarps;
-  const int cap = device_sm_count() * per_sm;
+  const int cap = grid_share(device_sm_count() * per_sm);
   const int grid = want < cap ? want : cap;
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, kWarps * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
@@ -924,6 +924,12 @@ int hmf_qband_set_chain_lockstep(int32_t bits) {
 }
 
 int32_t hmf_qband_get_chain_cfg(void) { return hmf::qs::g_chain_cfg; }
+
+int hmf_qband_set_grid_share(int32_t div) {
+  if (div < 1 || div > 64) return int(hmf::set_error(HMF_ERR_ARG, "grid share must be 1..64"));
+  hmf::qs::g_grid_div = div;
+  return HMF_OK;
+}
 
 int32_t hmf_qband_chain_lanes(int64_t k) {
   const int cfg = hmf::qs::g_chain_cfg < 0 ? 5 : hmf::qs::g_chain_cfg;  // 5 and 6: same lanes

@@ -127,6 +127,15 @@ template <int K> struct ChainCfg<K, 6> {  // 8 lanes per chain (4 chains), 4 ste
 };
 constexpr int kChainCfgs = 7;
 
+// Share of the GPU one Q-band launch may fill: its grid is capped at
+// 1/g_grid_div of the resident CTA slots, so g_grid_div launches on separate
+// streams (several column blocks of one row band) run side by side.
+static int g_grid_div = 1;
+static inline int grid_share(int cap) {
+  const int c = (cap + g_grid_div - 1) / g_grid_div;
+  return c < 1 ? 1 : c;
+}
+
 __device__ inline unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -424,7 +433,7 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
   }
   // a full grid (chains are spread CTA-minor, so even a block with few
   // sub-bands uses every SM); blocks with fewer sub-bands than CTAs need fewer
-  const int cap = device_sm_count() * per_sm;
+  const int cap = grid_share(device_sm_count() * per_sm);
   const int grid = n_sub < cap ? n_sub : cap;
   if (grid <= 0) return cudaSuccess;
   // more sub-bands than chains: units are handed out dynamically (a static

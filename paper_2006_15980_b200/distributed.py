@@ -166,17 +166,17 @@ class CudaRowBand:
 
     Q replicas of all ranks are mapped into every process with CUDA IPC, so a
     pull is a one-sided peer copy from the band's last owner — the owner does
-    not participate.  Blocks use the Q-band kernel when the column bands are
-    wide enough to fill the GPU with one warp per item sub-band, else the
-    global-Q HOGWILD kernel.
+    not participate.  Blocks use the Q-band layout and kernel (row tiles of
+    this band, item runs; two column blocks in flight on two streams, each
+    with half the GPU), or the global-Q HOGWILD / EXACT range kernels.
     """
 
     def __init__(self, dist, rank: int, world: int, device, triples, row_lo: int, row_hi: int,
                  col_cuts, k: int, lr: float, reg_user: float, reg_item: float,
-                 init_seed: int = 0, kernel: str = "auto", init=None):
+                 init_seed: int = 0, kernel: str = "auto", init=None, concurrency: int = 2):
         import torch
         from . import _lib
-        from .data import DeviceTriples, bucket_qbands, build_device_grid, resident_warps
+        from .data import DeviceTriples, bucket_qbands, build_device_grid
         self.torch = torch
         self.lib = _lib
         self.dev = torch.device(device)
@@ -209,12 +209,22 @@ class CudaRowBand:
         self.grid = build_device_grid(local, rows, self.col_cuts)
         first = 0 if row_lo == 0 else self.n_cols
         self.block_of = [first + c for c in range(self.n_cols)]   # block of column c
-        widest = int(np.max(np.diff(self.col_cuts)))
-        want = resident_warps(self.dev, k) // 2
-        self.kernel = kernel if kernel != "auto" else ("qband" if widest >= want else "range")
+        # the Q-band layout (row tiles: this band's P rows in L2) also wins for
+        # narrow column bands once two of them run side by side: projected
+        # 6.5 vs 4.0 G upd/s per GPU for the global-Q kernel at the 8-GPU
+        # geometry (bench.py --sim-world 8, profiles/r02/sim_world8_*.json)
+        self.kernel = kernel if kernel != "auto" else (
+            "qband" if k in (32, 64, 128, 256) else "range")
         if self.kernel == "qband":
             bucket_qbands(self.grid, k)
-        self.stream = torch.cuda.Stream(device=self.dev)
+        # column blocks in flight at once (the current and the staged-ahead
+        # one): each on its own stream with a 1/concurrency share of the GPU,
+        # so narrow column bands still fill every SM with chains
+        self.concurrency = max(1, int(concurrency)) if self.kernel == "qband" else 1
+        self.streams = [torch.cuda.Stream(device=self.dev) for _ in range(self.concurrency)]
+        self.stream = self.streams[0]
+        self._next_stream = 0
+        self.stream_of = {}
         self.copy_stream = torch.cuda.Stream(device=self.dev)
         self.done_events = {}
         # P, Q and the grid were produced on the current stream; the band's
@@ -240,7 +250,15 @@ class CudaRowBand:
             self.peer_q[r] = (ptr.value + offset, pdev)
 
     # -- backend protocol ------------------------------------------------------
+    def _stream_for(self, c: int):
+        """The compute stream column c's block runs on (assigned at its pull)."""
+        if c not in self.stream_of:
+            self.stream_of[c] = self.streams[self._next_stream]
+            self._next_stream = (self._next_stream + 1) % len(self.streams)
+        return self.stream_of[c]
+
     def pull(self, c: int, owner: int) -> None:
+        stream = self._stream_for(c)
         if owner < 0 or owner == self.rank:
             return
         lo, hi = int(self.col_cuts[c]), int(self.col_cuts[c + 1])
@@ -253,29 +271,36 @@ class CudaRowBand:
             nbytes, self.copy_stream.cuda_stream), "hmf_memcpy_peer_async")
         ev = self.torch.cuda.Event()
         ev.record(self.copy_stream)
-        self.stream.wait_event(ev)
+        stream.wait_event(ev)
 
     def compute(self, c: int, seed: int) -> int:
         from . import kernels
         b = self.block_of[c]
         lo, hi = self.grid.block_range(b)
+        stream = self._stream_for(c)
         if self.kernel == "qband":
-            n = kernels.launch_block_qband(self.P, self.Q, self.grid, b, self.lr, self.ru, self.ri,
-                                           seed, row_base=self.row_lo,
-                                           stream=self.stream.cuda_stream)
+            lib = self.lib.load()
+            lib.hmf_qband_set_grid_share(self.concurrency)
+            try:
+                n = kernels.launch_block_qband(self.P, self.Q, self.grid, b, self.lr, self.ru,
+                                               self.ri, seed, row_base=self.row_lo,
+                                               stream=stream.cuda_stream)
+            finally:
+                lib.hmf_qband_set_grid_share(1)
         else:   # "range" (HOGWILD) or "exact" (reference order and arithmetic)
             n = kernels.launch_sgd_range(self.P, self.Q, self.grid.users, self.grid.items,
                                          self.grid.ratings, lo, hi, self.lr, self.ru, self.ri,
                                          seed, self.row_lo, 0,
                                          "exact" if self.kernel == "exact" else "hogwild",
-                                         self.stream.cuda_stream)
+                                         stream.cuda_stream)
         ev = self.torch.cuda.Event()
-        ev.record(self.stream)
+        ev.record(stream)
         self.done_events[c] = ev
         return n
 
     def finish(self, c: int) -> None:
         ev = self.done_events.pop(c, None)
+        self.stream_of.pop(c, None)
         if ev is not None:
             ev.synchronize()
 
@@ -283,4 +308,6 @@ class CudaRowBand:
         """Pull every band from its owner (metrics / end of run)."""
         for c in range(self.n_cols):
             self.pull(c, table.owner(c))
-        self.stream.synchronize()
+            self.stream_of.pop(c, None)
+        for s in self.streams:
+            s.synchronize()
