@@ -420,8 +420,9 @@ def run_ours(args, world, rank, local):
                        "lr": LR, "reg": REG, "mode": args.mode, "kernel": args.kernel,
                        "variant": args.variant,
                        "qband_impl": getattr(grid, "sub_impl", None),
-                       "chain_cfg": (args.chain_cfg if getattr(grid, "sub_impl", None) == 4
+                       "chain_cfg": (args.chain_cfg if getattr(grid, "sub_impl", None) in (4, 5)
                                      else None),
+                       "item_run_split": getattr(grid, "sub_split", None),
                        "row_tiles": (list(grid.sub_tiles) if getattr(grid, "sub_tiles", None)
                                      else None),
                        "l2": "inputs larger than L2 (P + triples >> 126 MB); no flush"},
@@ -621,7 +622,7 @@ def main():
                     help="qband: Q band in shared memory (engine fast path); hogwild: "
                          "global-Q kernel behind hmf_sgd_range")
     ap.add_argument("--multi-kernel", choices=["auto", "qband", "range"], default="auto")
-    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 1, 2, 3, 4], default=-1,
+    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 1, 2, 3, 4, 5], default=-1,
                     help="Q-band kernel: 0 = register prefetch (default), 1 = TMA pipeline")
     ap.add_argument("--chain-cfg", type=int, choices=list(range(-1, 7)), default=-1,
                     help="configuration of Q-band implementation 4 (qchain.cuh ChainCfg)")

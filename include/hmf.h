@@ -126,9 +126,13 @@ int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16);
  * P deltas), 2 = per-lane cp.async ring of P rows + vector reductions, 3 =
  * implementation 0 with one CTA per SM and twice the prefetch depth, 4 =
  * chained item runs (several lane groups per warp, each walking its own
- * sub-band with the item's Q row in registers).  hmf_qband_set_impl sets the
- * process default; -1 (initial) = automatic: 4 for fp16 rows and k >= 128,
- * else 0.  hmf_qband_resolve_impl gives what the default resolves to. */
+ * sub-band with the item's Q row in registers), 5 = implementation 4 with
+ * Q deltas: several sub-bands may hold runs of the same item (a narrow block's
+ * item runs split over chains); each chain updates its own copy of the Q row
+ * and adds the change back with vector reductions.  hmf_qband_set_impl sets the
+ * process default; -1 (initial) = automatic: 5 (4 when every sub-band holds
+ * whole item runs).  hmf_qband_resolve_impl gives what the default resolves
+ * to. */
 int hmf_qband_set_impl(int32_t impl);
 int32_t hmf_qband_get_impl(void);
 int32_t hmf_qband_resolve_impl(int64_t k, int32_t f16);
@@ -163,22 +167,22 @@ int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                 double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
                                 void* stream);
 
-/* The chained kernel (implementation 4, chain configuration 5 or 6) with
+/* The chained kernel (implementation 4 or 5, chain configuration 5 or 6) with
  * uint16 row ids: row = rows[i] - row_base, so a row tile of at most 65536
  * rows streams 2-byte ids with row_base = -(the tile's first row).  Same
  * arguments and contract as hmf_sgd_block_qband_*. */
 int64_t hmf_sgd_block_qband_u16_f32(float* user_f, float* item_f, int64_t k,
                                     const uint16_t* rows, const int32_t* cols, const float* vals,
                                     const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
-                                    int64_t n_tiles, double lr, double reg_user, double reg_item,
-                                    uint64_t seed, int64_t row_base, int64_t col_base,
-                                    void* stream);
+                                    int64_t n_tiles, int32_t impl, double lr, double reg_user,
+                                    double reg_item, uint64_t seed, int64_t row_base,
+                                    int64_t col_base, void* stream);
 int64_t hmf_sgd_block_qband_u16_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                     const uint16_t* rows, const int32_t* cols, const float* vals,
                                     const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
-                                    int64_t n_tiles, double lr, double reg_user, double reg_item,
-                                    uint64_t seed, int64_t row_base, int64_t col_base,
-                                    void* stream);
+                                    int64_t n_tiles, int32_t impl, double lr, double reg_user,
+                                    double reg_item, uint64_t seed, int64_t row_base,
+                                    int64_t col_base, void* stream);
 
 /*
  * The reference visit order of a range of n triples under `seed`

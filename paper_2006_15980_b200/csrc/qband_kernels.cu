@@ -503,13 +503,17 @@ static int reg_warps_per_sm() {
 static int g_qband_impl = -1;
 
 // Implementation for a launch: an explicit impl >= 0, else the process
-// default, else automatic: chained item runs (4) for fp16 rows and for
-// k >= 128, where they reach the L2 load+reduction ceiling
-// (profiles/r02/l2_rowbench.jsonl); the warp-per-rating kernel (0) for fp32
-// rows of k <= 64, where it is faster (profiles/r02/ksweep.jsonl).
+// default, else automatic: the chained kernel with Q deltas (5).  With whole
+// item runs per sub-band it is the chained kernel (4), on the L2
+// load+reduction ceiling at k >= 128 (profiles/r02/l2_rowbench.jsonl); with
+// item runs split over chains it also beats the warp-per-rating kernel (0)
+// on narrow blocks and small k (ML-1M 12.1 vs 6.5, NF k=32 fp32 21.1 vs 16.5
+// G upd/s; profiles/r02/impl5_*.jsonl).
 static int resolve_impl(int impl, int64_t k, bool f16) {
+  (void)k;
+  (void)f16;
   if (impl < 0) impl = g_qband_impl;
-  if (impl < 0) impl = (f16 || k >= 128) ? 4 : 0;
+  if (impl < 0) impl = 5;
   return impl;
 }
 
@@ -778,7 +782,7 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
                    int64_t n_sub, int64_t n_tiles, int impl_req, double lr, double ru, double ri,
                    uint64_t seed, int64_t row_base, int64_t col_base, cudaStream_t stream) {
   if (n_sub <= 0 || n_tiles <= 0) return 0;
-  if (impl_req > 4) return set_error(HMF_ERR_ARG, "impl must be -1..4");
+  if (impl_req > 5) return set_error(HMF_ERR_ARG, "impl must be -1..5");
   if (n_sub * n_tiles > (int64_t(1) << 31))
     return set_error(HMF_ERR_ARG, "n_sub * n_tiles too large");
   if (!P || !Q || !rows || !vals || !sub_ptr || !sub_cuts)
@@ -788,8 +792,8 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
   cudaError_t e;
   const int impl = resolve_impl(impl_req, k, sizeof(S) == 2);
   // cols == nullptr: every sub-band is one item, sub_cuts[s] (chained kernel only)
-  if (!cols && impl != 4)
-    return set_error(HMF_ERR_ARG, "cols may be null only for implementation 4");
+  if (!cols && impl != 4 && impl != 5)
+    return set_error(HMF_ERR_ARG, "cols may be null only for implementations 4 and 5");
   switch (k) {
 #define HMF_QB_CASE(KK)                                                                    \
   case KK:                                                                                 \
@@ -797,9 +801,10 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
       e = launch_async_if<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub),    \
                                  int(n_tiles), lr, ru, ri, seed, row_base, col_base,       \
                                  stream);                                                  \
-    else if (impl == 4)                                                                    \
+    else if (impl == 4 || impl == 5)                                                       \
       e = launch_chain<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub),       \
-                              int(n_tiles), lr, ru, ri, seed, row_base, col_base, stream); \
+                              int(n_tiles), lr, ru, ri, seed, row_base, col_base, stream,  \
+                              impl == 5);                                                  \
     else if (impl == 3)                                                                    \
       e = launch<KK, S, true>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub),       \
                               int(n_tiles), lr, ru, ri, seed, row_base, col_base, stream); \
@@ -825,8 +830,9 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
 template <typename S>
 static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_t* cols,
                        const float* vals, const int64_t* sub_ptr, const int32_t* sub_cuts,
-                       int64_t n_sub, int64_t n_tiles, double lr, double ru, double ri,
-                       uint64_t seed, int64_t row_base, int64_t col_base, cudaStream_t stream) {
+                       int64_t n_sub, int64_t n_tiles, int impl_req, double lr, double ru,
+                       double ri, uint64_t seed, int64_t row_base, int64_t col_base,
+                       cudaStream_t stream) {
   if (n_sub <= 0 || n_tiles <= 0) return 0;
   if (n_sub * n_tiles > (int64_t(1) << 31))
     return set_error(HMF_ERR_ARG, "n_sub * n_tiles too large");
@@ -837,20 +843,24 @@ static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_
   const int cfg = chain_cfg<S>();
   if (cfg != 5 && cfg != 6)
     return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need chain configuration 5 or 6");
+  const int impl = resolve_impl(impl_req, k, sizeof(S) == 2);
+  if (impl != 4 && impl != 5)
+    return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need implementation 4 or 5");
+  const int qdelta = impl == 5;
   cudaError_t e;
   switch (k) {
     case 32: e = launch_chain<32, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
                                                 int(n_sub), int(n_tiles), lr, ru, ri, seed,
-                                                row_base, col_base, stream); break;
+                                                row_base, col_base, stream, qdelta); break;
     case 64: e = launch_chain<64, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
                                                 int(n_sub), int(n_tiles), lr, ru, ri, seed,
-                                                row_base, col_base, stream); break;
+                                                row_base, col_base, stream, qdelta); break;
     case 128: e = launch_chain<128, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
                                                   int(n_sub), int(n_tiles), lr, ru, ri, seed,
-                                                  row_base, col_base, stream); break;
+                                                  row_base, col_base, stream, qdelta); break;
     case 256: e = launch_chain<256, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
                                                   int(n_sub), int(n_tiles), lr, ru, ri, seed,
-                                                  row_base, col_base, stream); break;
+                                                  row_base, col_base, stream, qdelta); break;
     default: return set_error(HMF_ERR_UNSUPPORTED, "Q-band kernel needs k in {32,64,128,256}");
   }
   if (e != cudaSuccess) return set_cuda_error(e);
@@ -865,7 +875,7 @@ static int warps_per_sm(int64_t k, int impl) {
   case KK:                                                                            \
     if (impl == 2 && async_ok<KK, S>()) return async_warps_per_sm_if<KK, S>();        \
     if (impl == 3) return reg_warps_per_sm<KK, S, true>();                            \
-    if (impl == 4) return chain_slots_per_sm<KK, S>();                                \
+    if (impl == 4 || impl == 5) return chain_slots_per_sm<KK, S>();                   \
     return impl == 1 ? tma_warps_per_sm<KK, S>() : reg_warps_per_sm<KK, S>();
     HMF_WPS(32)
     HMF_WPS(64)
@@ -880,7 +890,7 @@ static int warps_per_sm(int64_t k, int impl) {
 template <typename S>
 static int slice_bytes(int64_t k, int impl) {
   impl = resolve_impl(impl, k, sizeof(S) == 2);
-  if (impl == 4) return 1 << 30;  // Q rows in registers: no slice bound
+  if (impl == 4 || impl == 5) return 1 << 30;  // Q rows in registers: no slice bound
   if (impl != 2) return kSliceBytes;
   switch (k) {
     case 32: return async_ok<32, S>() ? AsyncLayout<32, S, 4>::SLICE : kSliceBytes;
@@ -940,8 +950,8 @@ int32_t hmf_qband_chain_lanes(int64_t k) {
 }
 
 int hmf_qband_set_impl(int32_t impl) {
-  if (impl < -1 || impl > 4)
-    return int(hmf::set_error(HMF_ERR_ARG, "impl must be -1..4"));
+  if (impl < -1 || impl > 5)
+    return int(hmf::set_error(HMF_ERR_ARG, "impl must be -1..5"));
   hmf::qs::g_qband_impl = impl;
   return HMF_OK;
 }
@@ -983,24 +993,24 @@ int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
 int64_t hmf_sgd_block_qband_u16_f32(float* user_f, float* item_f, int64_t k,
                                     const uint16_t* rows, const int32_t* cols, const float* vals,
                                     const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
-                                    int64_t n_tiles, double lr, double reg_user, double reg_item,
-                                    uint64_t seed, int64_t row_base, int64_t col_base,
-                                    void* stream) {
+                                    int64_t n_tiles, int32_t impl, double lr, double reg_user,
+                                    double reg_item, uint64_t seed, int64_t row_base,
+                                    int64_t col_base, void* stream) {
   return hmf::qs::run_u16<float>(user_f, item_f, k, rows, cols, vals, sub_ptr, sub_cuts, n_sub,
-                                 n_tiles, lr, reg_user, reg_item, seed, row_base, col_base,
+                                 n_tiles, impl, lr, reg_user, reg_item, seed, row_base, col_base,
                                  static_cast<cudaStream_t>(stream));
 }
 
 int64_t hmf_sgd_block_qband_u16_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                     const uint16_t* rows, const int32_t* cols, const float* vals,
                                     const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
-                                    int64_t n_tiles, double lr, double reg_user, double reg_item,
-                                    uint64_t seed, int64_t row_base, int64_t col_base,
-                                    void* stream) {
+                                    int64_t n_tiles, int32_t impl, double lr, double reg_user,
+                                    double reg_item, uint64_t seed, int64_t row_base,
+                                    int64_t col_base, void* stream) {
   return hmf::qs::run_u16<__half>(reinterpret_cast<__half*>(user_f),
                                   reinterpret_cast<__half*>(item_f), k, rows, cols, vals, sub_ptr,
-                                  sub_cuts, n_sub, n_tiles, lr, reg_user, reg_item, seed, row_base,
-                                  col_base, static_cast<cudaStream_t>(stream));
+                                  sub_cuts, n_sub, n_tiles, impl, lr, reg_user, reg_item, seed,
+                                  row_base, col_base, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

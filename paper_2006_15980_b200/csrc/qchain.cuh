@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
                   const int32_t* __restrict__ cols, const float* __restrict__ vals,
                   const int64_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_cuts,
                   int n_sub, int n_tiles, float lr, float ru, float ri, uint64_t seed,
-                  unsigned* __restrict__ work, int lockstep) {
+                  unsigned* __restrict__ work, int lockstep, int qdelta) {
   using L = ChainLay<K, S, LPC>;
   constexpr int NC = L::NC, E = L::EPL, NS = PD + 1;
   static_assert(PD >= 1 && PD < LPC, "prefetch distance must stay within one batch");
@@ -189,6 +189,34 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
   uint32_t p[NS][L::RW];
   float q[E];
   int qcur = -1;  // item whose Q row is in q[]
+  // qdelta: an item's run may be split over several chains (bins of one item
+  // in different sub-bands): each chain works on its own copy of the Q row
+  // and adds its change back with vector reductions, the value it loaded
+  // kept in shared memory (the reference's lanes race on the staged Q band,
+  // workers.py:222-266; reductions lose no update)
+  extern __shared__ float q0_smem[];
+  float* q0 = q0_smem + ((threadIdx.x >> 5) * NC + c) * K;
+  auto q_load = [&](int item) {
+    L::ldg(Qb + int64_t(item) * K, l, q);
+    if (qdelta) {
+#pragma unroll
+      for (int v = 0; v < L::NV; ++v)
+#pragma unroll
+        for (int w = 0; w < L::W; ++w) q0[L::off(v, l) + w] = q[v * L::W + w];
+    }
+  };
+  auto q_store = [&](int item) {
+    if (qdelta) {
+      float dq[E];
+#pragma unroll
+      for (int v = 0; v < L::NV; ++v)
+#pragma unroll
+        for (int w = 0; w < L::W; ++w) dq[v * L::W + w] = q[v * L::W + w] - q0[L::off(v, l) + w];
+      L::red(Qb + int64_t(item) * K, l, dq);
+    } else {
+      L::stg(Qb + int64_t(item) * K, l, q);
+    }
+  };
 
   auto bstart = [&](int xx) -> int {
     if (xx >= nf) return nf * LPC;
@@ -234,7 +262,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
   };
   // the finished bin: Q row back, the unit released (dynamic)
   auto end_bin = [&]() {
-    if (qcur >= 0) L::stg(Qb + int64_t(qcur) * K, l, q);
+    if (qcur >= 0) q_store(qcur);
     qcur = -1;
     have = false;
     if constexpr (DYN) {
@@ -272,7 +300,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
   // waiting here must not stall the other chains of its warp, one of which
   // may hold the predecessor unit)
   auto try_start = [&]() -> bool {
-    if constexpr (DYN) {
+    if (DYN && !qdelta) {
       const unsigned f = ld_acquire_u32(work + 1 + us);  // every lane acquires
       if (!__all_sync(cmask, f == unsigned(ui))) return false;
     }
@@ -293,8 +321,8 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
         __shfl_sync(FULL, ahead_in ? cu : nu, ahead_in ? j + PD : j + PD - cnt, LPC);
     if (act && un >= 0) L::ldraw(Pb + int64_t(un) * K, l, pn);
     if (act && v != qcur) {
-      if (qcur >= 0) L::stg(Qb + int64_t(qcur) * K, l, q);
-      L::ldg(Qb + int64_t(v) * K, l, q);
+      if (qcur >= 0) q_store(qcur);
+      q_load(v);
       qcur = v;
     }
     float pc[E];
@@ -419,7 +447,8 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
                                     const float* vals, const int64_t* sub_ptr,
                                     const int32_t* sub_cuts, int n_sub,
                                     int n_tiles, double lr, double ru, double ri, uint64_t seed,
-                                    int64_t row_base, int64_t col_base, cudaStream_t stream) {
+                                    int64_t row_base, int64_t col_base, cudaStream_t stream,
+                                    int qdelta) {
   using C = ChainCfg<K, CFG>;
   constexpr int NC = 32 / C::LPC;
   auto kstat = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false, RowT>;
@@ -447,9 +476,10 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
   }
   auto kern = dyn ? kdyn : kstat;
   const int lockstep = dyn ? (g_chain_lockstep & 2) != 0 : (g_chain_lockstep & 1) != 0;
-  kern<<<grid, C::WPB * 32, 0, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
+  const int smem = qdelta ? C::WPB * NC * K * int(sizeof(float)) : 0;
+  kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
                                          sub_ptr, sub_cuts, n_sub, n_tiles, float(lr), float(ru),
-                                         float(ri), seed, work, lockstep);
+                                         float(ri), seed, work, lockstep, qdelta);
   return cudaGetLastError();
 }
 
@@ -461,11 +491,11 @@ static cudaError_t launch_chain(S* P, S* Q, const RowT* rows, const int32_t* col
                                 const float* vals, const int64_t* sub_ptr,
                                 const int32_t* sub_cuts, int n_sub, int n_tiles,
                                 double lr, double ru, double ri, uint64_t seed, int64_t row_base,
-                                int64_t col_base, cudaStream_t stream) {
+                                int64_t col_base, cudaStream_t stream, int qdelta = 0) {
 #define HMF_CHAIN_CFG(CFG)                                                                     \
   return launch_chain_cfg<K, S, CFG, RowT>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, n_sub,  \
                                            n_tiles, lr, ru, ri, seed, row_base, col_base,      \
-                                           stream)
+                                           stream, qdelta)
   if constexpr (sizeof(RowT) == 2) {
     switch (chain_cfg<S>()) {
       case 5: HMF_CHAIN_CFG(5);

@@ -377,6 +377,7 @@ class DeviceGrid:
     sub_tiles: list | None = None
     sub_impl: int = -1          # Q-band implementation the layout is for
     sub_tile_rows: list | None = None   # per block: row cuts of its tiles (host int64)
+    sub_split: int = 1                  # parts per item run (implementation 5)
 
     n_row_bands = BlockGrid.n_row_bands
     n_col_bands = BlockGrid.n_col_bands
@@ -453,20 +454,14 @@ def resident_warps(device, k: int = 128, f16: bool = False, impl: int = -1) -> i
 def qband_impl_for(device, k: int, f16: bool, n_items: int) -> int:
     """The Q-band implementation a grid is laid out and launched for: the
     process default (hmf_qband_set_impl) when one is set, else the library's
-    automatic choice (hmf_qband_resolve_impl), except that the chained kernel
-    (4) gives way to the warp-per-rating kernel (0) when a block has fewer
-    than a quarter as many items as there are chains to feed (ML-1M-sized
-    blocks: measured 2.7 vs 6.9 G upd/s, profiles/r02/chain_cfg_sweep_small_k.jsonl;
-    Netflix-sized blocks at k = 32 fp16, half as many items as chains: 20.1
-    vs 13.3 G upd/s for the chains)."""
+    automatic choice (hmf_qband_resolve_impl): the chained kernel with Q
+    deltas (5), whose layout splits item runs only when a block has fewer
+    items than chains (bucket_qbands)."""
     lib = _lib.load()
     impl = int(lib.hmf_qband_get_impl())
     if impl >= 0:
         return impl
-    impl = int(lib.hmf_qband_resolve_impl(int(k), 1 if f16 else 0))
-    if impl == 4 and 4 * n_items < resident_warps(device, k, f16, 4):
-        impl = 0
-    return impl
+    return int(lib.hmf_qband_resolve_impl(int(k), 1 if f16 else 0))
 
 
 def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int, cap: int | None = None) -> np.ndarray:
@@ -502,7 +497,7 @@ def qband_row_tiles(n_rows: int, k: int, elem_bytes: int = 4,
 
 def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
                   tile_bytes: int | None = None, elem_bytes: int = 4,
-                  impl: int | None = None) -> DeviceGrid:
+                  impl: int | None = None, split: int | None = None) -> DeviceGrid:
     """Re-bucket every block of a device grid for the Q-band kernel, in place:
     row tile major, then item (both stable), and attach sub_ptr / sub_cuts /
     sub_tiles.  Row tiles are equal user ranges of the block's row band, sized
@@ -512,7 +507,12 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     registers.  The order of ratings within an item is the block order
     (stable), i.e. the reference's shuffled order (data.py:242-244, 264).
     The grid records the implementation it is laid out for (sub_impl;
-    qband_impl_for unless `impl` is given) and launches use it."""
+    qband_impl_for unless `impl` is given) and launches use it.
+
+    Implementation 5 (Q deltas) splits every (tile, item) run into `split`
+    consecutive parts, each its own sub-band (default: enough parts for
+    every chain to have one), so a block with few items still feeds every
+    chain; sub-band s then holds part s % split of item sub_cuts[s]."""
     torch = _torch()
     dev = grid.device
     lib = _lib.load()
@@ -522,14 +522,22 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         impl = qband_impl_for(dev, k, f16, max((grid.col_span(c)[1] - grid.col_span(c)[0]
                                                 for c in range(grid.n_col_bands)), default=0))
     impl = int(impl)
-    if target is None:
+    widest = max((grid.col_span(c)[1] - grid.col_span(c)[0]
+                  for c in range(grid.n_col_bands)), default=0)
+    if impl == 5 and split is None:
+        # fewer items than chains: split every item run so each chain has a
+        # part (an explicit sub-band count keeps whole runs)
+        slots = resident_warps(dev, k, f16, 5)
+        split = max(1, min(16, slots // max(widest, 1))) if target is None else 1
+    split = 1 if impl != 5 or not split else int(split)
+    if split > 1:
+        target = widest          # one item per sub-band, then its parts
+    elif target is None:
         # one sub-band per resident slot; for the chained kernel with at least
         # twice as many items as chains, narrower sub-bands (up to 4 per
         # chain) that its dynamic scheduler balances (qchain.cuh)
         target = resident_warps(dev, k, f16, impl)
-        widest = max((grid.col_span(c)[1] - grid.col_span(c)[0]
-                      for c in range(grid.n_col_bands)), default=0)
-        if impl == 4 and widest >= 2 * target:
+        if impl in (4, 5) and widest >= 2 * target:
             target = min(widest, 4 * target)
     target = int(target)
     cap = int(lib.hmf_qband_max_items_for(int(k), 1 if f16 else 0, impl))
@@ -544,7 +552,10 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         n_tiles = qband_row_tiles(r_hi - r_lo, k, elem_bytes, tile_bytes)
         tiles = np.linspace(r_lo, r_hi, n_tiles + 1).round().astype(np.int64)
         cuts = qband_sub_cuts(c_lo, c_hi, k, target, cap)
-        n_sub = len(cuts) - 1
+        if split > 1:
+            cuts = np.arange(c_lo, c_hi + 1, dtype=np.int64)   # single items, then parts
+        n_item_sub = len(cuts) - 1
+        n_sub = n_item_sub * split
         rel = torch.from_numpy(cuts[:-1] - c_lo).to(dev)
         ptr = torch.full((n_tiles * n_sub + 1,), hi, dtype=torch.int64, device=dev)
         if hi > lo:
@@ -589,15 +600,24 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
                 grid.ratings[a:z] = out_r[a:z][order]
                 iptr = torch.zeros(n_items + 1, dtype=torch.int64, device=dev)
                 iptr[1:] = torch.cumsum(torch.bincount(key, minlength=n_items), 0)
-                ptr[t * n_sub:(t + 1) * n_sub] = iptr[rel] + a
+                if split > 1:
+                    # part r of item i starts at iptr[i] + len_i * r // split
+                    ln = (iptr[1:] - iptr[:-1]).unsqueeze(1)
+                    parts = iptr[:-1].unsqueeze(1) + ln * torch.arange(split, device=dev) // split
+                    ptr[t * n_sub:(t + 1) * n_sub] = parts.reshape(-1) + a
+                else:
+                    ptr[t * n_sub:(t + 1) * n_sub] = iptr[rel] + a
                 del key, order, iptr
         sub_ptrs.append(ptr)
+        if split > 1:
+            cuts = np.concatenate([np.repeat(cuts[:-1], split), cuts[-1:]])
         sub_cuts.append(torch.from_numpy(cuts).to(device=dev, dtype=torch.int32))
         sub_tiles.append(n_tiles)
         tile_rows.append(tiles)
     del out_u, out_i, out_r
     grid.sub_ptr, grid.sub_cuts, grid.sub_tiles = sub_ptrs, sub_cuts, sub_tiles
     grid.sub_impl = impl
+    grid.sub_split = split
     grid.sub_tile_rows = tile_rows
     return grid
 

@@ -176,7 +176,7 @@ class CudaRowBand:
                  init_seed: int = 0, kernel: str = "auto", init=None, concurrency: int = 2):
         import torch
         from . import _lib
-        from .data import DeviceTriples, bucket_qbands, build_device_grid
+        from .data import DeviceTriples, bucket_qbands, build_device_grid, resident_warps
         self.torch = torch
         self.lib = _lib
         self.dev = torch.device(device)
@@ -216,7 +216,14 @@ class CudaRowBand:
         self.kernel = kernel if kernel != "auto" else (
             "qband" if k in (32, 64, 128, 256) else "range")
         if self.kernel == "qband":
-            bucket_qbands(self.grid, k)
+            # blocks with fewer items than the chains of their GPU share feed
+            # every chain by splitting item runs (implementation 5, Q deltas)
+            slots = resident_warps(self.dev, k, False, 4) // max(1, int(concurrency))
+            widest = int(np.max(np.diff(self.col_cuts)))
+            if widest < slots:
+                bucket_qbands(self.grid, k, impl=5, split=max(1, min(16, slots // widest)))
+            else:
+                bucket_qbands(self.grid, k)
         # column blocks in flight at once (the current and the staged-ahead
         # one): each on its own stream with a 1/concurrency share of the GPU,
         # so narrow column bands still fill every SM with chains

@@ -471,8 +471,9 @@ class StreamingEpoch:
         self.k = k
         self.nnz = sg.nnz
         self.sub_impl = sg.sub_impl
-        self.implicit_items = compact and sg.sub_impl == 4 and all(
-            bool(torch.all(c[1:] - c[:-1] == 1)) for c in sg.sub_cuts)
+        # every sub-band a single item (or a part of one): the item is implicit
+        self.implicit_items = compact and sg.sub_impl in (4, 5) and all(
+            bool(torch.all(c[1:] - c[:-1] <= 1)) for c in sg.sub_cuts)
         cfg_ok = int(_lib.load().hmf_qband_get_chain_cfg()) in (-1, 5, 6)
         self.u16 = self.implicit_items and cfg_ok and all(
             int(np.max(np.diff(r))) <= 65536 for r in sg.sub_tile_rows)
@@ -574,7 +575,7 @@ class StreamingEpoch:
             tseed = kernels.mix64(bseed, t) & 0xFFFFFFFFFFFFFFFF
             args = (P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr(), items,
                     buf[-1].data_ptr(), rel.data_ptr(), sc.data_ptr(), int(sc.numel()) - 1, 1)
-            args += () if self.u16 else (self.sub_impl,)
+            args += (self.sub_impl,)
             args += (hparams.learning_rate, hparams.reg_user, hparams.reg_item, tseed,
                      -row0 if self.u16 else 0, 0, comp.cuda_stream)
             _lib.check(fn(*args), "hmf_sgd_block_qband")

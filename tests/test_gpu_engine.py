@@ -144,8 +144,8 @@ def test_throughput_sweep_reports_stages(dev):
         throughput_sweep("batch", [2, 1], batch_config=BatchWorkerConfig(device=dev))
 
 
-@pytest.mark.parametrize("k", [64, 128])
-def test_streaming_epoch_applies_every_triple_once(dev, k):
+@pytest.mark.parametrize("k,impl", [(64, -1), (128, -1), (64, 0)])
+def test_streaming_epoch_applies_every_triple_once(dev, k, impl):
     """StreamingEpoch (triples streamed from pinned host memory tile by tile,
     double buffered) on conflict-free triples equals the reference update of
     each triple exactly once."""
@@ -162,7 +162,12 @@ def test_streaming_epoch_applies_every_triple_once(dev, k):
     m = RatingMatrix(9000, 7000, users, items, vals)
     d = torch.device("cuda", dev)
     g = build_device_grid(DeviceTriples.from_host(m, d), [0, 9000], [0, 3500, 7000])
-    se = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1)   # 3 row tiles per block
+    from paper_2006_15980_b200 import _lib
+    _lib.check(_lib.load().hmf_qband_set_impl(impl), "set_impl")
+    try:
+        se = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1)   # 3 row tiles per block
+    finally:
+        _lib.load().hmf_qband_set_impl(-1)
     assert se.n_chunks == 6
     P0 = rng.uniform(0, 0.1, size=(9000, k)).astype(np.float32)
     Q0 = rng.uniform(0, 0.1, size=(7000, k)).astype(np.float32)
@@ -175,10 +180,11 @@ def test_streaming_epoch_applies_every_triple_once(dev, k):
     rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)  # noqa: E731
     assert rel(P.double().cpu().numpy(), Pe) < 1e-6
     assert rel(Q.double().cpu().numpy(), Qe) < 1e-6
-    # k = 128: the chained kernel with one item per sub-band: items implicit,
-    # 2-byte user ids relative to the row tile
-    assert se.implicit_items == (k == 128) and se.u16 == (k == 128)
-    assert se.h2d_bytes == (6 if k == 128 else 12) * n
+    # the chained kernel (default) with single-item sub-bands: items implicit,
+    # 2-byte user ids relative to the row tile; warp-per-rating: triples
+    chained = impl != 0
+    assert se.implicit_items == chained and se.u16 == chained
+    assert se.h2d_bytes == (6 if chained else 12) * n
     assert se.h2d_bytes_last() == se.h2d_bytes          # first epoch: every chunk uploaded
     # a second epoch starts on the two chunks still staged and does not upload them
     assert se.run(P, Q, hp, seed=2) == n

@@ -397,7 +397,7 @@ def _bin_visit(impl, k, beg, end, seed, bin_index):
     from paper_2006_15980_b200.kernels import _MASK64
     if end <= beg:
         return []
-    if impl == 4:   # full batches rotated, the partial batch last
+    if impl in (4, 5):   # full batches rotated, the partial batch last
         step = _chain_lanes(k)
         nf = (end - beg) // step
         out = []
@@ -687,6 +687,78 @@ def test_qband_skewed_items_match_sequential(dev, n_items, impl):
         assert rel_err(P.double().cpu().numpy(), Pe) < 1e-5
     finally:
         _lib.load().hmf_qband_set_impl(-1)
+
+
+@pytest.mark.parametrize("n_tiles", [1, 3])
+def test_qband_split_runs_apply_every_rating(dev, n_tiles):
+    """Implementation 5: a narrow block's item runs split over chains, each
+    chain on its own Q copy, changes added back by reductions.  At a small
+    step SGD is linear in the ratings, so the factor changes must equal the
+    sequential reference's to first order: every rating applied once, every
+    Q delta added once (nothing lost, nothing doubled)."""
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import RatingMatrix
+    k, lr = 128, 1e-4
+    rng = np.random.default_rng(5 + n_tiles)
+    n_users, n_items, n = 30_000, 64, 40_000
+    users = rng.integers(0, n_users, n).astype(np.int32)
+    items = rng.integers(0, n_items, n).astype(np.int32)
+    vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
+    m = RatingMatrix(n_users, n_items, users, items, vals)
+    from paper_2006_15980_b200.data import DeviceTriples, bucket_qbands, build_device_grid
+    g = build_device_grid(DeviceTriples.from_host(m, dev), [0, n_users], [0, n_items])
+    tb = 0 if n_tiles == 1 else n_users * k * 4 // n_tiles + 1
+    bucket_qbands(g, k, tile_bytes=tb, impl=5, split=8)
+    assert g.sub_impl == 5 and g.sub_split == 8 and g.sub_tiles == [n_tiles]
+    assert g.sub_cuts[0].numel() - 1 == n_items * 8
+    P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
+    Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
+    P, Q = to_dev(P0, dev), to_dev(Q0, dev)
+    assert kernels.launch_block_qband(P, Q, g, 0, lr, 0.02, 0.03, 3) == n
+    Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
+    for u, v, r in zip(users, items, vals):
+        pu, qv = Pe[u].copy(), Qe[v].copy()
+        e = r - pu @ qv
+        Pe[u] = pu + lr * (e * qv - 0.02 * pu)
+        Qe[v] = qv + lr * (e * pu - 0.03 * qv)
+    dP, dQ = P.double().cpu().numpy() - P0, Q.double().cpu().numpy() - Q0
+    # second-order terms (each part starts from a stale Q row): ~ lr x the
+    # ratings per item x the change, a few percent here
+    assert rel_err(dQ, Qe - Q0) < 0.03
+    assert rel_err(dP, Pe - P0) < 0.03
+
+
+def test_qband_split_runs_ml1m_quality(dev):
+    """Implementation 5 on the ML-1M shape (few items per block): test RMSE
+    within 0.005 of the reference's stream-only run at epochs 5 and 20."""
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import (DeviceGrid, RatingMatrix, bucket_qbands, build_grid,
+                                            shuffle_triples, synthetic_ratings)
+    from paper_2006_15980_b200.sgd import DeviceModel, Hyperparams, init_model, rmse
+    ref = json.loads((GOLDEN / "training.json").read_text())
+    full = synthetic_ratings(6040, 3706, rank=8, density=1.05e6 / (6040 * 3706), noise=0.1, seed=0)
+    perm = np.random.default_rng(1).permutation(full.nnz)
+    n_test = full.nnz // 21
+    te, tr = perm[:n_test], perm[n_test:]
+    train = RatingMatrix(6040, 3706, full.users[tr], full.items[tr], full.ratings[tr])
+    test = RatingMatrix(6040, 3706, full.users[te], full.items[te], full.ratings[te])
+    hp = Hyperparams(n_factors=32, reg_user=0.01, reg_item=0.01, learning_rate=0.01)
+    grid = DeviceGrid.from_host(build_grid(shuffle_triples(train, 0), [0, 6040], [0, 1853, 3706]),
+                                dev)
+    bucket_qbands(grid, 32, impl=5)
+    assert grid.sub_split > 1
+    model = DeviceModel.from_host(init_model(6040, 3706, hp, 0), dev)
+    got = {}
+    for epoch in range(1, 21):
+        for b in (0, 1):
+            kernels.launch_block_qband(model.P, model.Q, grid, b, 0.01, 0.01, 0.01,
+                                       kernels.mix64(0, b, epoch))
+        if epoch in (1, 5, 20):
+            got[f"e{epoch}"] = rmse(test, model).value
+    for key in ("e1", "e5", "e20"):
+        print(f"{key}: gpu split runs {got[key]:.5f} reference {ref[key]['test_rmse']:.5f}")
+    assert abs(got["e20"] - ref["e20"]["test_rmse"]) <= 0.005
+    assert abs(got["e5"] - ref["e5"]["test_rmse"]) <= 0.005
 
 
 def test_qband_fp16_storage_tracks_fp32(dev, qband_impl):
