@@ -476,7 +476,8 @@ def run_ours_multi(args, world, rank, local):
     n_cols = 2 * geo + 1
     col_cuts = np.linspace(0, n_items, n_cols + 1).astype(np.int64)
     band = CudaRowBand(dist, rank, world, dev, train, row_lo, row_hi, col_cuts, k, LR, REG, REG,
-                       init_seed=SEED, kernel=args.multi_kernel)
+                       init_seed=SEED, kernel=args.multi_kernel,
+                       concurrency=args.multi_concurrency)
     table = LeaseTable(dist.distributed_c10d._get_default_store(), n_cols, rank,
                        f"bench{os.getpid() if world == 1 else 0}")
     if rank == 0:
@@ -518,7 +519,9 @@ def run_ours_multi(args, world, rank, local):
                                      f"a {geo}-GPU job (per-GPU throughput; peer pulls of Q "
                                      f"bands not exercised)"),
                        "parallelism": f"dp{world} row bands, Q bands leased and pulled peer-to-peer",
-                       "kernel": band.kernel, "lr": LR, "reg": REG},
+                       "kernel": band.kernel, "qband_impl": getattr(band.grid, "sub_impl", None),
+                       "item_run_split": getattr(band.grid, "sub_split", None),
+                       "blocks_in_flight": band.concurrency, "lr": LR, "reg": REG},
             "rmse": {"epochs": args.warmup + args.steps,
                      "test": float(np.sqrt(sums[0].item() / n_test))},
             "lease_wait_seconds_rank0": trainer.wait_seconds,
@@ -622,6 +625,8 @@ def main():
                     help="qband: Q band in shared memory (engine fast path); hogwild: "
                          "global-Q kernel behind hmf_sgd_range")
     ap.add_argument("--multi-kernel", choices=["auto", "qband", "range"], default="auto")
+    ap.add_argument("--multi-concurrency", type=int, default=1,
+                    help="N>1: column blocks in flight per GPU (each on its own stream)")
     ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 1, 2, 3, 4, 5], default=-1,
                     help="Q-band kernel: 0 = register prefetch (default), 1 = TMA pipeline")
     ap.add_argument("--chain-cfg", type=int, choices=list(range(-1, 7)), default=-1,

@@ -167,13 +167,13 @@ class CudaRowBand:
     Q replicas of all ranks are mapped into every process with CUDA IPC, so a
     pull is a one-sided peer copy from the band's last owner — the owner does
     not participate.  Blocks use the Q-band layout and kernel (row tiles of
-    this band, item runs; two column blocks in flight on two streams, each
-    with half the GPU), or the global-Q HOGWILD / EXACT range kernels.
+    this band, item runs split over the chains when the band is narrow), or
+    the global-Q HOGWILD / EXACT range kernels.
     """
 
     def __init__(self, dist, rank: int, world: int, device, triples, row_lo: int, row_hi: int,
                  col_cuts, k: int, lr: float, reg_user: float, reg_item: float,
-                 init_seed: int = 0, kernel: str = "auto", init=None, concurrency: int = 2):
+                 init_seed: int = 0, kernel: str = "auto", init=None, concurrency: int = 1):
         import torch
         from . import _lib
         from .data import DeviceTriples, bucket_qbands, build_device_grid, resident_warps
@@ -224,9 +224,11 @@ class CudaRowBand:
                 bucket_qbands(self.grid, k, impl=5, split=max(1, min(16, slots // widest)))
             else:
                 bucket_qbands(self.grid, k)
-        # column blocks in flight at once (the current and the staged-ahead
-        # one): each on its own stream with a 1/concurrency share of the GPU,
-        # so narrow column bands still fill every SM with chains
+        # column blocks in flight at once, each on its own stream with a
+        # 1/concurrency share of the GPU.  Default 1: with item runs split
+        # over chains (implementation 5) one narrow block fills the GPU, and
+        # a single full-GPU launch has no tail (bench.py --sim-world 8:
+        # 8.85 vs 8.05 G upd/s per GPU with two half-GPU launches)
         self.concurrency = max(1, int(concurrency)) if self.kernel == "qband" else 1
         self.streams = [torch.cuda.Stream(device=self.dev) for _ in range(self.concurrency)]
         self.stream = self.streams[0]
