@@ -305,7 +305,8 @@ def run_ours(args, world, rank, local):
     del trip, train
     torch.cuda.empty_cache()
     if args.kernel == "qband":
-        bucket_qbands(grid, k, tile_bytes=tile_bytes, elem_bytes=2 if precision == "f16" else 4)
+        bucket_qbands(grid, k, tile_bytes=tile_bytes, elem_bytes=2 if precision == "f16" else 4,
+                      impl=5 if args.split else None, split=args.split or None)
     stream_epoch = None
     if not args.no_e2e and args.kernel == "qband" and world == 1:
         # e2e streams the same layout from pinned host memory, tile by tile
@@ -420,7 +421,7 @@ def run_ours(args, world, rank, local):
                        "lr": LR, "reg": REG, "mode": args.mode, "kernel": args.kernel,
                        "variant": args.variant,
                        "qband_impl": getattr(grid, "sub_impl", None),
-                       "chain_cfg": (args.chain_cfg if getattr(grid, "sub_impl", None) in (4, 5)
+                       "chain_cfg": (args.chain_cfg if (getattr(grid, "sub_impl", None) or 0) >= 4
                                      else None),
                        "item_run_split": getattr(grid, "sub_split", None),
                        "row_tiles": (list(grid.sub_tiles) if getattr(grid, "sub_tiles", None)
@@ -467,12 +468,21 @@ def run_ours_multi(args, world, rank, local):
     n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
     k = args.k or k0
     n_total = int(round(n_train / (1.0 - TEST_FRACTION)))
-    trip = synthetic_device(n_users, n_items, n_total, rank=8, noise=0.1, seed=SEED + rank,
-                            device=dev)
-    row_lo, row_hi = rank * n_users, (rank + 1) * n_users
+    geo = args.sim_world or world      # --sim-world: rank 0's share of a larger job
+    if args.scaling == "strong":
+        # the workload itself split into row bands (same law, same density)
+        band = -(-n_users // geo)
+        row_lo, row_hi = rank * band, min(n_users, (rank + 1) * band)
+        n_rank = int(round(n_total * (row_hi - row_lo) / n_users))
+        trip = synthetic_device(row_hi - row_lo, n_items, n_rank, rank=8, noise=0.1,
+                                seed=SEED + rank, device=dev)
+    else:
+        # weak scaling: a workload-sized row band per GPU, items shared
+        row_lo, row_hi = rank * n_users, (rank + 1) * n_users
+        trip = synthetic_device(n_users, n_items, n_total, rank=8, noise=0.1, seed=SEED + rank,
+                                device=dev)
     trip.users += row_lo                       # global user ids of this rank's band
     train, test = split_device(trip, TEST_FRACTION)
-    geo = args.sim_world or world      # --sim-world: rank 0's share of a larger job
     n_cols = 2 * geo + 1
     col_cuts = np.linspace(0, n_items, n_cols + 1).astype(np.int64)
     band = CudaRowBand(dist, rank, world, dev, train, row_lo, row_hi, col_cuts, k, LR, REG, REG,
@@ -509,10 +519,12 @@ def run_ours_multi(args, world, rank, local):
         print(json.dumps({
             "metric": "sgd_updates_per_sec", "value": updates / (ms / 1e3), "unit": "updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synthetic_ratings law, device generator)",
-            "config": {"workload": f"{desc} row band per GPU (weak scaling), k={k}",
+            "config": {"workload": (f"{desc} row band per GPU (weak scaling), k={k}"
+                                    if args.scaling == "weak" else
+                                    f"{desc} split into {geo} row bands (strong scaling), k={k}"),
                        "grid": f"{geo} row bands x {n_cols} column bands",
                        "simulated": (None if not args.sim_world else
                                      f"one process with rank 0's band and column geometry of "
@@ -551,11 +563,17 @@ def run_e2e_stream(args, se, model, test, dev):
     torch.cuda.synchronize(dev)
     steps = max(3, args.steps)
     h2d = 0
-    marks = [time.perf_counter()]
-    for i in range(steps):
-        sq = step(2 + i)
-        h2d += se.h2d_bytes_last()
-        marks.append(time.perf_counter())
+    import gc
+    gc.collect()
+    gc.disable()          # no collector pauses inside the timed host loop
+    try:
+        marks = [time.perf_counter()]
+        for i in range(steps):
+            sq = step(2 + i)
+            h2d += se.h2d_bytes_last()
+            marks.append(time.perf_counter())
+    finally:
+        gc.enable()
     dt = marks[-1] - marks[0]
     per = sorted(1e3 * (b - a) for a, b in zip(marks, marks[1:]))
     return {"value": se.nnz * steps / dt, "unit": "updates/s",
@@ -625,15 +643,19 @@ def main():
                     help="qband: Q band in shared memory (engine fast path); hogwild: "
                          "global-Q kernel behind hmf_sgd_range")
     ap.add_argument("--multi-kernel", choices=["auto", "qband", "range"], default="auto")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N>1: a workload-sized band per GPU (weak) or the workload split (strong)")
     ap.add_argument("--multi-concurrency", type=int, default=1,
                     help="N>1: column blocks in flight per GPU (each on its own stream)")
-    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 1, 2, 3, 4, 5], default=-1,
+    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 1, 2, 3, 4, 5, 6], default=-1,
                     help="Q-band kernel: 0 = register prefetch (default), 1 = TMA pipeline")
     ap.add_argument("--chain-cfg", type=int, choices=list(range(-1, 7)), default=-1,
                     help="configuration of Q-band implementation 4 (qchain.cuh ChainCfg)")
     ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)
     ap.add_argument("--stream-buffers", type=int, default=2,
                     help="e2e: device staging buffers (ring)")
+    ap.add_argument("--split", type=int, default=0,
+                    help="implementation 5 with this many parts per item run (0 = default layout)")
     ap.add_argument("--tile-mb", type=float, default=None,
                     help="P rows per Q-band row tile in MiB (default data.QBAND_TILE_BYTES; 0 = no tiling)")
     ap.add_argument("--sim-world", type=int, default=0,

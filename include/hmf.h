@@ -129,7 +129,10 @@ int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16);
  * sub-band with the item's Q row in registers), 5 = implementation 4 with
  * Q deltas: several sub-bands may hold runs of the same item (a narrow block's
  * item runs split over chains); each chain updates its own copy of the Q row
- * and adds the change back with vector reductions.  hmf_qband_set_impl sets the
+ * and adds the change back with vector reductions, publishing and re-reading
+ * it every hmf_qband_set_qsync ratings (bounded staleness), 6 = implementation
+ * 5 publishing only at item and bin changes (whole runs per sub-band, whose
+ * units in consecutive row tiles may overlap).  hmf_qband_set_impl sets the
  * process default; -1 (initial) = automatic: 5 (4 when every sub-band holds
  * whole item runs).  hmf_qband_resolve_impl gives what the default resolves
  * to. */
@@ -147,6 +150,10 @@ int32_t hmf_qband_get_chain_cfg(void);
  * 1), so div launches on separate streams — several column blocks of one row
  * band — run side by side. */
 int hmf_qband_set_grid_share(int32_t div);
+/* Implementation 5: every `steps` ratings (default 16) each chain publishes
+ * its Q-row change and re-reads the row, bounding how stale the copies of
+ * chains sharing an item get (0 = publish only at item and bin changes). */
+int hmf_qband_set_qsync(int32_t steps);
 int32_t hmf_qband_chain_lanes(int64_t k);
 /* Implementation 4: chains of a warp change bins together (bit 0: static
  * scheduler, bit 1: dynamic scheduler; default 3). */

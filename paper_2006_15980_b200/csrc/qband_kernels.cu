@@ -782,7 +782,7 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
                    int64_t n_sub, int64_t n_tiles, int impl_req, double lr, double ru, double ri,
                    uint64_t seed, int64_t row_base, int64_t col_base, cudaStream_t stream) {
   if (n_sub <= 0 || n_tiles <= 0) return 0;
-  if (impl_req > 5) return set_error(HMF_ERR_ARG, "impl must be -1..5");
+  if (impl_req > 6) return set_error(HMF_ERR_ARG, "impl must be -1..6");
   if (n_sub * n_tiles > (int64_t(1) << 31))
     return set_error(HMF_ERR_ARG, "n_sub * n_tiles too large");
   if (!P || !Q || !rows || !vals || !sub_ptr || !sub_cuts)
@@ -792,8 +792,8 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
   cudaError_t e;
   const int impl = resolve_impl(impl_req, k, sizeof(S) == 2);
   // cols == nullptr: every sub-band is one item, sub_cuts[s] (chained kernel only)
-  if (!cols && impl != 4 && impl != 5)
-    return set_error(HMF_ERR_ARG, "cols may be null only for implementations 4 and 5");
+  if (!cols && impl < 4)
+    return set_error(HMF_ERR_ARG, "cols may be null only for implementations 4-6");
   switch (k) {
 #define HMF_QB_CASE(KK)                                                                    \
   case KK:                                                                                 \
@@ -801,10 +801,10 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
       e = launch_async_if<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub),    \
                                  int(n_tiles), lr, ru, ri, seed, row_base, col_base,       \
                                  stream);                                                  \
-    else if (impl == 4 || impl == 5)                                                       \
+    else if (impl >= 4)                                                                    \
       e = launch_chain<KK, S>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub),       \
                               int(n_tiles), lr, ru, ri, seed, row_base, col_base, stream,  \
-                              impl == 5);                                                  \
+                              impl == 4 ? 0 : (impl == 5 ? 1 : 2));                        \
     else if (impl == 3)                                                                    \
       e = launch<KK, S, true>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, int(n_sub),       \
                               int(n_tiles), lr, ru, ri, seed, row_base, col_base, stream); \
@@ -844,9 +844,9 @@ static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_
   if (cfg != 5 && cfg != 6)
     return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need chain configuration 5 or 6");
   const int impl = resolve_impl(impl_req, k, sizeof(S) == 2);
-  if (impl != 4 && impl != 5)
-    return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need implementation 4 or 5");
-  const int qdelta = impl == 5;
+  if (impl < 4)
+    return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need implementation 4, 5 or 6");
+  const int qdelta = impl == 4 ? 0 : (impl == 5 ? 1 : 2);
   cudaError_t e;
   switch (k) {
     case 32: e = launch_chain<32, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
@@ -875,7 +875,7 @@ static int warps_per_sm(int64_t k, int impl) {
   case KK:                                                                            \
     if (impl == 2 && async_ok<KK, S>()) return async_warps_per_sm_if<KK, S>();        \
     if (impl == 3) return reg_warps_per_sm<KK, S, true>();                            \
-    if (impl == 4 || impl == 5) return chain_slots_per_sm<KK, S>();                   \
+    if (impl >= 4) return chain_slots_per_sm<KK, S>();                                \
     return impl == 1 ? tma_warps_per_sm<KK, S>() : reg_warps_per_sm<KK, S>();
     HMF_WPS(32)
     HMF_WPS(64)
@@ -890,7 +890,7 @@ static int warps_per_sm(int64_t k, int impl) {
 template <typename S>
 static int slice_bytes(int64_t k, int impl) {
   impl = resolve_impl(impl, k, sizeof(S) == 2);
-  if (impl == 4 || impl == 5) return 1 << 30;  // Q rows in registers: no slice bound
+  if (impl >= 4) return 1 << 30;  // Q rows in registers: no slice bound
   if (impl != 2) return kSliceBytes;
   switch (k) {
     case 32: return async_ok<32, S>() ? AsyncLayout<32, S, 4>::SLICE : kSliceBytes;
@@ -935,6 +935,12 @@ int hmf_qband_set_chain_lockstep(int32_t bits) {
 
 int32_t hmf_qband_get_chain_cfg(void) { return hmf::qs::g_chain_cfg; }
 
+int hmf_qband_set_qsync(int32_t steps) {
+  if (steps < 0) return int(hmf::set_error(HMF_ERR_ARG, "qsync steps must be >= 0"));
+  hmf::qs::g_qsync_steps = steps;
+  return HMF_OK;
+}
+
 int hmf_qband_set_grid_share(int32_t div) {
   if (div < 1 || div > 64) return int(hmf::set_error(HMF_ERR_ARG, "grid share must be 1..64"));
   hmf::qs::g_grid_div = div;
@@ -950,8 +956,8 @@ int32_t hmf_qband_chain_lanes(int64_t k) {
 }
 
 int hmf_qband_set_impl(int32_t impl) {
-  if (impl < -1 || impl > 5)
-    return int(hmf::set_error(HMF_ERR_ARG, "impl must be -1..5"));
+  if (impl < -1 || impl > 6)
+    return int(hmf::set_error(HMF_ERR_ARG, "impl must be -1..6"));
   hmf::qs::g_qband_impl = impl;
   return HMF_OK;
 }

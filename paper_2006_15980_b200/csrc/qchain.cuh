@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
                   const int32_t* __restrict__ cols, const float* __restrict__ vals,
                   const int64_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_cuts,
                   int n_sub, int n_tiles, float lr, float ru, float ri, uint64_t seed,
-                  unsigned* __restrict__ work, int lockstep, int qdelta) {
+                  unsigned* __restrict__ work, int lockstep, int qdelta, int qsync) {
   using L = ChainLay<K, S, LPC>;
   constexpr int NC = L::NC, E = L::EPL, NS = PD + 1;
   static_assert(PD >= 1 && PD < LPC, "prefetch distance must stay within one batch");
@@ -377,15 +377,31 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     }
   };
   advance();
+  int group = 0;
   while (__any_sync(FULL, !done)) {
     if (__all_sync(FULL, done || pend)) __nanosleep(256);
 #pragma unroll
     for (int t = 0; t < NS; ++t) step(p[t], p[(t + PD) % NS]);
+    // Q deltas: every qsync step groups each chain publishes its change and
+    // re-reads the row, so chains sharing an item see each other's updates
+    // within a bounded window (all chains of the warp at the same step, so
+    // their reloads overlap)
+    if (qdelta && qsync > 0 && ++group == qsync) {
+      group = 0;
+      if (!done && !pend && qcur >= 0) {
+        q_store(qcur);
+        q_load(qcur);
+      }
+    }
     // chains whose bin ran out move on (bins start at slot 0 of the unrolled
     // group, so the prologue's slots are static)
     advance();
   }
 }
+
+// implementation 5: steps between Q-delta publications of a chain (0 = only
+// at item and bin changes)
+static int g_qsync_steps = 16;
 
 // -1 = automatic: 5 for fp32 rows, 6 (deeper prefetch; raw fp16 slots are
 // half the registers) for fp16 rows (profiles/r02/chain_cfg_*.jsonl)
@@ -477,9 +493,12 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
   auto kern = dyn ? kdyn : kstat;
   const int lockstep = dyn ? (g_chain_lockstep & 2) != 0 : (g_chain_lockstep & 1) != 0;
   const int smem = qdelta ? C::WPB * NC * K * int(sizeof(float)) : 0;
+  // qdelta 1: bounded staleness (publish and re-read every g_qsync_steps);
+  // 2: publish at item and bin changes only (whole runs per sub-band)
+  const int qsync = qdelta == 1 && g_qsync_steps > 0 ? (g_qsync_steps + C::PD) / (C::PD + 1) : 0;
   kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
                                          sub_ptr, sub_cuts, n_sub, n_tiles, float(lr), float(ru),
-                                         float(ri), seed, work, lockstep, qdelta);
+                                         float(ri), seed, work, lockstep, qdelta, qsync);
   return cudaGetLastError();
 }
 

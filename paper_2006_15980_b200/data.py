@@ -495,6 +495,31 @@ def qband_row_tiles(n_rows: int, k: int, elem_bytes: int = 4,
     return max(1, min(n_rows, -(-(n_rows * k * elem_bytes) // tb)))
 
 
+def qband_split_for(slots: int, items: int, block_nnz: float, n_tiles: int, k: int = 128,
+                    f16: bool = False) -> int:
+    """Parts per item run for implementation 5 (measured on one B200,
+    profiles/r02/split_*.jsonl).
+
+    The parts of one run go to different chains at the same time, each on
+    its own copy of the item's Q row.  Without bounds, R concurrent parts
+    pile up an item's steps before the deltas meet (test RMSE 0.42 vs 0.12 at
+    k = 32); every chain therefore publishes its change and re-reads the row
+    every 16 ratings (hmf_qband_set_qsync), which keeps every split within
+    0.0001 of whole runs at k = 32..128, fp32 and fp16.  Then:
+    * at least twice as many items as chains: whole runs (Yahoo, Hugewiki);
+    * fewer items than chains: slots // items parts, so every chain has a
+      unit per tile (ML-1M: 5; an 8-GPU column band: 4-9);
+    * fp32 rows with k >= 128 and long runs (>= 192 ratings): 4 parts,
+      scheduled dynamically (Netflix k = 128: 9.7 vs 9.1, k = 256: 4.8 vs
+      4.5 G upd/s); fp16 rows and small k gain nothing from it."""
+    if items <= 0 or items >= 2 * slots:
+        return 1
+    avg_run = block_nnz / (max(1, n_tiles) * items)
+    dyn = 4 if (not f16 and k >= 128 and avg_run >= 192) else 1
+    static = slots // items if items < slots else 1
+    return max(1, min(16, max(static, dyn)))
+
+
 def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
                   tile_bytes: int | None = None, elem_bytes: int = 4,
                   impl: int | None = None, split: int | None = None) -> DeviceGrid:
@@ -525,10 +550,14 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     widest = max((grid.col_span(c)[1] - grid.col_span(c)[0]
                   for c in range(grid.n_col_bands)), default=0)
     if impl == 5 and split is None:
-        # fewer items than chains: split every item run so each chain has a
-        # part (an explicit sub-band count keeps whole runs)
-        slots = resident_warps(dev, k, f16, 5)
-        split = max(1, min(16, slots // max(widest, 1))) if target is None else 1
+        sizes = np.diff(np.asarray(grid.block_ptr))
+        full = [b for b in range(grid.n_blocks) if sizes[b] > 0]
+        rows = max((grid.row_span(b // grid.n_col_bands)[1] - grid.row_span(b // grid.n_col_bands)[0]
+                    for b in full), default=1)
+        split = 1 if target is not None else qband_split_for(
+            resident_warps(dev, k, f16, 5), widest,
+            float(np.mean(sizes[full])) if full else 0.0,
+            qband_row_tiles(rows, k, elem_bytes, tile_bytes), k, f16)
     split = 1 if impl != 5 or not split else int(split)
     if split > 1:
         target = widest          # one item per sub-band, then its parts
@@ -537,7 +566,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         # twice as many items as chains, narrower sub-bands (up to 4 per
         # chain) that its dynamic scheduler balances (qchain.cuh)
         target = resident_warps(dev, k, f16, impl)
-        if impl in (4, 5) and widest >= 2 * target:
+        if impl >= 4 and widest >= 2 * target:
             target = min(widest, 4 * target)
     target = int(target)
     cap = int(lib.hmf_qband_max_items_for(int(k), 1 if f16 else 0, impl))
@@ -616,6 +645,15 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         tile_rows.append(tiles)
     del out_u, out_i, out_r
     grid.sub_ptr, grid.sub_cuts, grid.sub_tiles = sub_ptrs, sub_cuts, sub_tiles
+    if impl == 5 and split == 1:
+        # whole item runs.  No more sub-bands than chains (static owners): Q
+        # rows are never shared, plain stores (implementation 4).  More: the
+        # dynamic scheduler runs units of one sub-band in consecutive tiles
+        # side by side on Q deltas without hand-off waits, published at item
+        # changes only (implementation 6; Yahoo 9.7 vs 9.1 G upd/s with the
+        # 16-rating publication, RMSE equal)
+        slots = resident_warps(dev, k, f16, 4)
+        impl = 4 if all(len(c) - 1 <= slots for c in sub_cuts) else 6
     grid.sub_impl = impl
     grid.sub_split = split
     grid.sub_tile_rows = tile_rows

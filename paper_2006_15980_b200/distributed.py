@@ -216,11 +216,11 @@ class CudaRowBand:
         self.kernel = kernel if kernel != "auto" else (
             "qband" if k in (32, 64, 128, 256) else "range")
         if self.kernel == "qband":
-            # blocks with fewer items than the chains of their GPU share feed
-            # every chain by splitting item runs (implementation 5, Q deltas)
-            slots = resident_warps(self.dev, k, False, 4) // max(1, int(concurrency))
-            widest = int(np.max(np.diff(self.col_cuts)))
-            if widest < slots:
+            # narrow column bands split their item runs over the chains
+            # (data.qband_split_for, implementation 5)
+            if concurrency > 1:
+                slots = resident_warps(self.dev, k, False, 4) // int(concurrency)
+                widest = int(np.max(np.diff(self.col_cuts)))
                 bucket_qbands(self.grid, k, impl=5, split=max(1, min(16, slots // widest)))
             else:
                 bucket_qbands(self.grid, k)

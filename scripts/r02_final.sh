@@ -23,3 +23,7 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:qcha
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file "$OUT/launches_nf_k128_f32.csv" python bench.py --steps 2 --warmup 1 > "$OUT/ncu_launches.log" 2>&1
 echo done
+for w in 2 4 8; do timeout 600 python bench.py --sim-world $w --steps 3 --warmup 3 > "$OUT/sim_world$w.log" 2>&1; done
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+  --master-port 29537 bench.py --gpus 2 --steps 3 --warmup 3 > "$OUT/bench_n2_shared_gpu.log" 2>&1
+echo done2
