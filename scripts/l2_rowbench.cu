@@ -175,6 +175,12 @@ int main(int argc, char** argv) {
   RUN5(1024, 4, 8)
   // whole-warp rows (the warp-per-rating layout)
   RUN5(512, 4, 32)
+  // deeper in-flight windows (the 8-lane chain layout)
+  run<2, 512, 16, 8>(buf, uint32_t((mb << 20) / 512), sink, sms);
+  run<2, 512, 32, 8>(buf, uint32_t((mb << 20) / 512), sink, sms);
+  run<2, 256, 16, 8>(buf, uint32_t((mb << 20) / 256), sink, sms);
+  run<4, 256, 16, 8>(buf, uint32_t((mb << 20) / 256), sink, sms);
+  run<2, 1024, 8, 8>(buf, uint32_t((mb << 20) / 1024), sink, sms);
   // TMA bulk reductions
   run_bulk<512, 4, false>(buf, uint32_t((mb << 20) / 512), sink, sms);
   run_bulk<512, 8, false>(buf, uint32_t((mb << 20) / 512), sink, sms);
