@@ -487,7 +487,7 @@ def run_ours_multi(args, world, rank, local):
     col_cuts = np.linspace(0, n_items, n_cols + 1).astype(np.int64)
     band = CudaRowBand(dist, rank, world, dev, train, row_lo, row_hi, col_cuts, k, LR, REG, REG,
                        init_seed=SEED, kernel=args.multi_kernel,
-                       concurrency=args.multi_concurrency)
+                       concurrency=args.multi_concurrency, split=args.split or None)
     table = LeaseTable(dist.distributed_c10d._get_default_store(), n_cols, rank,
                        f"bench{os.getpid() if world == 1 else 0}")
     if rank == 0:

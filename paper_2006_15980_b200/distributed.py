@@ -173,7 +173,8 @@ class CudaRowBand:
 
     def __init__(self, dist, rank: int, world: int, device, triples, row_lo: int, row_hi: int,
                  col_cuts, k: int, lr: float, reg_user: float, reg_item: float,
-                 init_seed: int = 0, kernel: str = "auto", init=None, concurrency: int = 1):
+                 init_seed: int = 0, kernel: str = "auto", init=None, concurrency: int = 1,
+                 split: int | None = None):
         import torch
         from . import _lib
         from .data import DeviceTriples, bucket_qbands, build_device_grid, resident_warps
@@ -218,7 +219,9 @@ class CudaRowBand:
         if self.kernel == "qband":
             # narrow column bands split their item runs over the chains
             # (data.qband_split_for, implementation 5)
-            if concurrency > 1:
+            if split:
+                bucket_qbands(self.grid, k, impl=5, split=int(split))
+            elif concurrency > 1:
                 slots = resident_warps(self.dev, k, False, 4) // int(concurrency)
                 widest = int(np.max(np.diff(self.col_cuts)))
                 bucket_qbands(self.grid, k, impl=5, split=max(1, min(16, slots // widest)))
