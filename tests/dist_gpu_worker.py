@@ -19,18 +19,22 @@ N_USERS, N_ITEMS, K, NNZ = 300, 260, 32, 12_000
 EPOCHS, SEED, LR, REG = 3, 9, 0.02, 0.01
 
 
-def problem():
+def problem(conflict_free=False):
     rng = np.random.default_rng(21)
     cells = rng.permutation(N_USERS * N_ITEMS)[:NNZ]
     users = (cells // N_ITEMS).astype(np.int32)
     items = (cells % N_ITEMS).astype(np.int32)
-    vals = rng.uniform(0, 1, NNZ).astype(np.float32).astype(np.float64)
+    if conflict_free:   # every user and every item in at most one rating
+        n = min(N_USERS, N_ITEMS)
+        users = rng.permutation(N_USERS)[:n].astype(np.int32)
+        items = rng.permutation(N_ITEMS)[:n].astype(np.int32)
+    vals = rng.uniform(0, 1, len(users)).astype(np.float32).astype(np.float64)
     P0 = rng.uniform(0, 0.3, size=(N_USERS, K)).astype(np.float32)
     Q0 = rng.uniform(0, 0.3, size=(N_ITEMS, K)).astype(np.float32)
     return users, items, vals, P0, Q0
 
 
-def main(out_dir):
+def main(out_dir, kernel="exact"):
     import torch
     import torch.distributed as dist
     from paper_2006_15980_b200.data import DeviceTriples
@@ -40,7 +44,7 @@ def main(out_dir):
     local = int(os.environ["LOCAL_RANK"]) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
-    users, items, vals, P0, Q0 = problem()
+    users, items, vals, P0, Q0 = problem(conflict_free=kernel != "exact")
     row_cuts = np.linspace(0, N_USERS, world + 1).astype(np.int64)
     col_cuts = np.linspace(0, N_ITEMS, 2 * world + 2).astype(np.int64)
     lo, hi = int(row_cuts[rank]), int(row_cuts[rank + 1])
@@ -50,7 +54,7 @@ def main(out_dir):
                          torch.from_numpy(items[keep]).to(dev),
                          torch.from_numpy(vals[keep].astype(np.float32)).to(dev))
     band = CudaRowBand(dist, rank, world, dev, trip, lo, hi, col_cuts, K, LR, REG, REG,
-                       kernel="exact", init=(P0[lo:hi], Q0))
+                       kernel=kernel, init=(P0[lo:hi], Q0))
     table = LeaseTable(dist.distributed_c10d._get_default_store(), band.n_cols, rank, "gputest")
     if rank == 0:
         table.initialize()
@@ -71,4 +75,4 @@ def main(out_dir):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "exact")

@@ -52,3 +52,31 @@ def test_two_ranks_ipc_lease_protocol_equals_serial_replay(tmp_path):
                          oracle.mix64(unit_seed, 0), 0, 0)
     assert np.array_equal(np.concatenate([x[1] for x in res]), P)
     assert np.array_equal(Q_final, Q)
+
+
+def test_two_ranks_qband_path_applies_every_triple(tmp_path):
+    """The default multi-GPU kernel path (Q-band layout of each rank's band,
+    narrow column bands split over the chains) on conflict-free triples:
+    order-free, so after the epochs P and Q equal the reference update of
+    every triple once per epoch (oracle, f64) within fp32 rounding."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import oracle
+    sys.path.insert(0, str(ROOT / "tests"))
+    import dist_gpu_worker as W
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           str(ROOT / "tests" / "dist_gpu_worker.py"), str(tmp_path), "qband"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res, Q_final, row_cuts, col_cuts = pickle.loads((tmp_path / "result.pkl").read_bytes())
+    for log, Pb, counts in res:
+        assert counts == [W.EPOCHS] * (len(col_cuts) - 1)
+    users, items, vals, P0, Q0 = W.problem(conflict_free=True)
+    P, Q = P0.astype(np.float64), Q0.astype(np.float64)
+    for e in range(W.EPOCHS):
+        oracle.sgd_range(P, Q, users, items, vals, 0, len(users), W.LR, W.REG, W.REG, e, 0, 0)
+    got_P = np.concatenate([x[1] for x in res]).astype(np.float64)
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)  # noqa: E731
+    assert rel(got_P, P) < 1e-5
+    assert rel(Q_final.astype(np.float64), Q) < 1e-5
