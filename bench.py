@@ -278,6 +278,8 @@ def run_ours(args, world, rank, local):
         _lib.set_variant(args.variant)
     _lib.check(_lib.load().hmf_qband_set_impl(args.qband_impl), "hmf_qband_set_impl")
     _lib.check(_lib.load().hmf_qband_set_chain_cfg(args.chain_cfg), "hmf_qband_set_chain_cfg")
+    if args.qsync is not None:
+        _lib.check(_lib.load().hmf_qband_set_qsync(args.qsync), "hmf_qband_set_qsync")
     if args.chain_lockstep is not None:
         _lib.check(_lib.load().hmf_qband_set_chain_lockstep(args.chain_lockstep),
                    "hmf_qband_set_chain_lockstep")
@@ -654,6 +656,8 @@ def main():
     ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)
     ap.add_argument("--stream-buffers", type=int, default=2,
                     help="e2e: device staging buffers (ring)")
+    ap.add_argument("--qsync", type=int, default=None,
+                    help="implementation 5: ratings between Q-delta publications (default 16)")
     ap.add_argument("--split", type=int, default=0,
                     help="implementation 5 with this many parts per item run (0 = default layout)")
     ap.add_argument("--tile-mb", type=float, default=None,
