@@ -657,7 +657,7 @@ def main():
     ap.add_argument("--stream-buffers", type=int, default=2,
                     help="e2e: device staging buffers (ring)")
     ap.add_argument("--qsync", type=int, default=None,
-                    help="implementation 5: ratings between Q-delta publications (default 16)")
+                    help="implementation 5: ratings between Q-delta publications (default 32)")
     ap.add_argument("--split", type=int, default=0,
                     help="implementation 5 with this many parts per item run (0 = default layout)")
     ap.add_argument("--tile-mb", type=float, default=None,

@@ -150,7 +150,7 @@ int32_t hmf_qband_get_chain_cfg(void);
  * 1), so div launches on separate streams — several column blocks of one row
  * band — run side by side. */
 int hmf_qband_set_grid_share(int32_t div);
-/* Implementation 5: every `steps` ratings (default 16) each chain publishes
+/* Implementation 5: every `steps` ratings (default 32) each chain publishes
  * its Q-row change and re-reads the row, bounding how stale the copies of
  * chains sharing an item get (0 = publish only at item and bin changes). */
 int hmf_qband_set_qsync(int32_t steps);

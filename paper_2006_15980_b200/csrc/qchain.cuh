@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
 
 // implementation 5: steps between Q-delta publications of a chain (0 = only
 // at item and bin changes)
-static int g_qsync_steps = 16;
+static int g_qsync_steps = 32;
 
 // -1 = automatic: 5 for fp32 rows, 6 (deeper prefetch; raw fp16 slots are
 // half the registers) for fp16 rows (profiles/r02/chain_cfg_*.jsonl)

@@ -504,7 +504,7 @@ def qband_split_for(slots: int, items: int, block_nnz: float, n_tiles: int, k: i
     its own copy of the item's Q row.  Without bounds, R concurrent parts
     pile up an item's steps before the deltas meet (test RMSE 0.42 vs 0.12 at
     k = 32); every chain therefore publishes its change and re-reads the row
-    every 16 ratings (hmf_qband_set_qsync), which keeps every split within
+    every 32 ratings (hmf_qband_set_qsync), which keeps every split within
     0.0001 of whole runs at k = 32..128, fp32 and fp16.  Then:
     * at least twice as many items as chains: whole runs (Yahoo, Hugewiki);
     * fewer items than chains: slots // items parts, so every chain has a
