@@ -512,13 +512,14 @@ def qband_split_for(slots: int, items: int, block_nnz: float, n_tiles: int, k: i
       and runs are short (< 192 ratings), 2 parts, scheduled dynamically
       (Hugewiki split over 2 GPUs, 8 000 items against 9 472 chains and
       40-rating runs: 9.05 vs 7.29 G upd/s);
-    * fp32 rows with k >= 128 and long runs (>= 192 ratings): 4 parts,
-      scheduled dynamically (Netflix k = 128: 9.7 vs 9.1, k = 256: 4.8 vs
-      4.5 G upd/s); fp16 rows and small k gain nothing from it."""
+    * k >= 64 and long runs (>= 192 ratings): 4 parts, scheduled
+      dynamically (Netflix k = 128: 9.9 vs 9.1 fp32, 16.6 vs 15.9 fp16;
+      k = 64: 17.3 vs 16.8; k = 256: 4.8 vs 4.5 G upd/s); at k = 32 whole runs
+      were faster."""
     if items <= 0 or items >= 2 * slots:
         return 1
     avg_run = block_nnz / (max(1, n_tiles) * items)
-    dyn = 4 if (not f16 and k >= 128 and avg_run >= 192) else 1
+    dyn = 4 if (k >= 64 and avg_run >= 192) else 1
     static = slots // items if items < slots else 1
     if items < slots and static == 1 and avg_run < 192:
         static = 2
