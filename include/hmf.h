@@ -11,7 +11,10 @@
  *
  *   hmf_sgd_range_{f32,f16,f64}   kernels.sgd_range            kernels.py:61-133
  *   hmf_sgd_block_qband_{f32,f16} BatchEngine.compute on a staged item band
+ *   hmf_sgd_block_qband_u16_*     (the same, uint16 tile-relative row ids)
  *                                                              workers.py:186-255
+ *   hmf_qband_set_*, _get_*       (kernel selection / configuration; no
+ *                                 reference counterpart)
  *   hmf_visit_order               sgd_range's visit order      kernels.py:77-119
  *   hmf_mix64                     kernels.mix64                kernels.py:32-48
  *   hmf_residual_sums_{f32,f16,f64}
@@ -39,7 +42,7 @@
 extern "C" {
 #endif
 
-#define HMF_ABI_VERSION 1
+#define HMF_ABI_VERSION 2
 
 #define HMF_OK 0
 #define HMF_ERR_ARG (-1)

@@ -121,7 +121,7 @@ def load() -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.hmf_abi_version() != 1:
+        if lib.hmf_abi_version() != 2:
             raise HmfError("libhmf ABI version mismatch")
         _lib = lib
         return lib
