@@ -407,10 +407,18 @@ def run_ours(args, world, rank, local):
     if rank == 0 and not args.no_cpu:
         threads = host_threads()
         sample = int(min(nnz, 1_000_000 * threads))
+        # about 10 s of CPU work: one epoch over the sample, then as many
+        # more as that takes to reach ~10 s
         rate, got, dt = cpu_sample_run(n_users, n_items, k, sample, threads, 1)
+        epochs = 1
+        if dt < 10.0:
+            more = max(1, int(round((10.0 - dt) / max(dt, 1e-3))))
+            _, got2, dt2 = cpu_sample_run(n_users, n_items, k, sample, threads, more, seed=SEED + 1)
+            got, dt, epochs = got + got2, dt + dt2, 1 + more
+            rate = got / dt
         cpu = {"value": rate, "unit": "updates/s", "cores": threads, "kind": "port",
-               "sample": f"{sample} ratings x 1 epoch, full {n_users}x{n_items} P/Q (f64) at "
-                         f"k={k}, stream-only uniform {threads}x{threads + 1} grid, "
+               "sample": f"{sample} ratings x {epochs} epochs, full {n_users}x{n_items} P/Q "
+                         f"(f64) at k={k}, stream-only uniform {threads}x{threads + 1} grid, "
                          f"{dt:.1f} s"}
 
     if rank == 0:
