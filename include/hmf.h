@@ -143,8 +143,9 @@ int hmf_qband_set_impl(int32_t impl);
 int32_t hmf_qband_get_impl(void);
 int32_t hmf_qband_resolve_impl(int64_t k, int32_t f16);
 /* Implementation 4 configuration 0..6 (lanes per chain, prefetch distance,
- * occupancy; -1 = default: 5 for fp32 rows, 6 for fp16 rows, both 8 lanes per
- * chain, 16 for k = 256, prefetching 2 and 4 ratings ahead) and the lanes per
+ * occupancy; -1 = default by k and storage: k = 32 cfg 4 (4 lanes, 4 ahead),
+ * k = 64 cfg 6 fp32 / 4 fp16, k >= 128 cfg 5 fp32 (8 lanes, 16 at k = 256, 2
+ * ahead) / 6 fp16 (4 ahead)) and the lanes per
  * chain it uses for k; a chain walks full batches of that many triples in a
  * seeded rotation, then the partial batch. */
 int hmf_qband_set_chain_cfg(int32_t cfg);
@@ -157,7 +158,8 @@ int hmf_qband_set_grid_share(int32_t div);
  * its Q-row change and re-reads the row, bounding how stale the copies of
  * chains sharing an item get (0 = publish only at item and bin changes). */
 int hmf_qband_set_qsync(int32_t steps);
-int32_t hmf_qband_chain_lanes(int64_t k);
+int32_t hmf_qband_chain_lanes(int64_t k);               /* fp32 rows */
+int32_t hmf_qband_chain_lanes_for(int64_t k, int32_t f16);
 /* Implementation 4: chains of a warp change bins together (bit 0: static
  * scheduler, bit 1: dynamic scheduler; default 3). */
 int hmf_qband_set_chain_lockstep(int32_t bits);

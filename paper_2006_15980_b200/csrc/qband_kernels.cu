@@ -840,9 +840,9 @@ static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_
     return set_error(HMF_ERR_ARG, "null pointer");
   if (((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) != 0)
     return set_error(HMF_ERR_ARG, "factor arrays must be 16-byte aligned");
-  const int cfg = chain_cfg<S>();
-  if (cfg != 5 && cfg != 6)
-    return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need chain configuration 5 or 6");
+  const int cfg = g_chain_cfg >= 0 ? g_chain_cfg : auto_chain_cfg(int(k), sizeof(S) == 2);
+  if (cfg < 4 || cfg > 6)
+    return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need chain configuration 4, 5 or 6");
   const int impl = resolve_impl(impl_req, k, sizeof(S) == 2);
   if (impl < 4)
     return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need implementation 4, 5 or 6");
@@ -947,13 +947,16 @@ int hmf_qband_set_grid_share(int32_t div) {
   return HMF_OK;
 }
 
-int32_t hmf_qband_chain_lanes(int64_t k) {
-  const int cfg = hmf::qs::g_chain_cfg < 0 ? 5 : hmf::qs::g_chain_cfg;  // 5 and 6: same lanes
+int32_t hmf_qband_chain_lanes_for(int64_t k, int32_t f16) {
+  const int cfg = hmf::qs::g_chain_cfg >= 0 ? hmf::qs::g_chain_cfg
+                                             : hmf::qs::auto_chain_cfg(int(k), f16 != 0);
   if (cfg == 5 || cfg == 6) return k >= 256 ? 16 : 8;
   const int per = (cfg == 2 || cfg == 3) ? 8 : 16;  // elements per lane
   const int lpc = int(k) / per;
   return lpc < 4 ? 4 : (lpc > 32 ? 32 : lpc);
 }
+
+int32_t hmf_qband_chain_lanes(int64_t k) { return hmf_qband_chain_lanes_for(k, 0); }
 
 int hmf_qband_set_impl(int32_t impl) {
   if (impl < -1 || impl > 6)

@@ -403,11 +403,19 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
 // at item and bin changes)
 static int g_qsync_steps = 32;
 
-// -1 = automatic: 5 for fp32 rows, 6 (deeper prefetch; raw fp16 slots are
-// half the registers) for fp16 rows (profiles/r02/chain_cfg_*.jsonl)
+// -1 = automatic (measured, profiles/r02/chain_cfg_by_k.jsonl): k = 32
+// 4 lanes per chain, 4 steps ahead (cfg 4; 28.8 / 33.6 G upd/s fp32 / fp16
+// vs 20.6 / 23.4 with 8 lanes); k = 64 fp32 8 lanes 4 ahead (cfg 6), fp16 4
+// lanes 4 ahead (cfg 4); k >= 128: 8 lanes (16 at k = 256), 2 ahead in fp32
+// (cfg 5, the register budget), 4 ahead in fp16 (cfg 6, raw fp16 slots).
 static int g_chain_cfg = -1;
-template <typename S> static int chain_cfg() {
-  return g_chain_cfg >= 0 ? g_chain_cfg : (sizeof(S) == 2 ? 6 : 5);
+static inline int auto_chain_cfg(int k, bool f16) {
+  if (k <= 32) return 4;
+  if (k <= 64) return f16 ? 4 : 6;
+  return f16 ? 6 : 5;
+}
+template <int K, typename S> static int chain_cfg() {
+  return g_chain_cfg >= 0 ? g_chain_cfg : auto_chain_cfg(K, sizeof(S) == 2);
 }
 // bin changes in warp lockstep: bit 0 for the static, bit 1 for the dynamic
 // scheduler
@@ -424,7 +432,7 @@ static int chain_slots_per_sm_cfg() {
 
 template <int K, typename S>
 static int chain_slots_per_sm() {
-  switch (chain_cfg<S>()) {
+  switch (chain_cfg<K, S>()) {
     case 0: return chain_slots_per_sm_cfg<K, S, 0>();
     case 2: return chain_slots_per_sm_cfg<K, S, 2>();
     case 3: return chain_slots_per_sm_cfg<K, S, 3>();
@@ -504,7 +512,7 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
 
 // rows: int32 row ids, or uint16 (a row tile's ids relative to its first row,
 // passed as row_base = -first row: 2 bytes per rating on the host stream;
-// default configurations 5 and 6 only)
+// configurations 4, 5 and 6 only)
 template <int K, typename S, typename RowT = int32_t>
 static cudaError_t launch_chain(S* P, S* Q, const RowT* rows, const int32_t* cols,
                                 const float* vals, const int64_t* sub_ptr,
@@ -516,13 +524,14 @@ static cudaError_t launch_chain(S* P, S* Q, const RowT* rows, const int32_t* col
                                            n_tiles, lr, ru, ri, seed, row_base, col_base,      \
                                            stream, qdelta)
   if constexpr (sizeof(RowT) == 2) {
-    switch (chain_cfg<S>()) {
+    switch (chain_cfg<K, S>()) {
+      case 4: HMF_CHAIN_CFG(4);
       case 5: HMF_CHAIN_CFG(5);
       case 6: HMF_CHAIN_CFG(6);
       default: return cudaErrorNotSupported;
     }
   } else {
-    switch (chain_cfg<S>()) {
+    switch (chain_cfg<K, S>()) {
       case 0: HMF_CHAIN_CFG(0);
       case 2: HMF_CHAIN_CFG(2);
       case 3: HMF_CHAIN_CFG(3);
