@@ -5,6 +5,10 @@
 // within rounding of the reference's f64 numpy evaluation on the same values.
 // Per-block partials are written to a scratch array and summed in a fixed order
 // by a second kernel, so the result is deterministic for a given n and device.
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "hmf_common.cuh"
 #include "hmf_internal.h"
 
@@ -142,6 +146,33 @@ __global__ void __launch_bounds__(kMetricThreads)
   }
 }
 
+// Per-(device, stream) partial-sum scratch, allocated once: launches on one
+// stream are ordered, so they can share it.  (A cudaMallocAsync per call
+// occasionally blocked the host for hundreds of ms on the GPU boxes, stalling
+// the per-epoch RMSE read of the streamed e2e loop.)
+static cudaError_t partials_for(cudaStream_t stream, size_t bytes, double** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<double*, size_t>> bufs;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& b = bufs[{dev, stream}];
+  if (b.second < bytes) {
+    if (b.first) {
+      e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) return e;
+      cudaFree(b.first);
+      b = {nullptr, 0};
+    }
+    e = cudaMalloc(reinterpret_cast<void**>(&b.first), bytes);
+    if (e != cudaSuccess) return e;
+    b.second = bytes;
+  }
+  *out = b.first;
+  return cudaSuccess;
+}
+
 template <typename S>
 static int residual_sums(const S* P, const S* Q, int64_t k, const int32_t* rows,
                          const int32_t* cols, const typename RatingOf<S>::T* vals, int64_t n,
@@ -154,8 +185,8 @@ static int residual_sums(const S* P, const S* Q, int64_t k, const int32_t* rows,
   if (want < blocks) blocks = want;
   if (blocks < 1) blocks = 1;
   double* partials = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&partials),
-                                  size_t(blocks) * 3 * sizeof(double), stream);
+  cudaError_t e = partials_for(stream, size_t(device_sm_count()) * 8 * 3 * sizeof(double),
+                               &partials);
   if (e != cudaSuccess) return int(set_cuda_error(e));
   const bool aligned =
       ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) == 0;
@@ -182,8 +213,6 @@ static int residual_sums(const S* P, const S* Q, int64_t k, const int32_t* rows,
         P, Q, rows, cols, vals, n, int(k), row_base, col_base, with_reg, partials);
   finalize_sums_kernel<<<1, kMetricThreads, 0, stream>>>(partials, int(blocks), out);
   e = cudaGetLastError();
-  cudaError_t e2 = cudaFreeAsync(partials, stream);
-  if (e == cudaSuccess) e = e2;
   return e == cudaSuccess ? HMF_OK : int(set_cuda_error(e));
 }
 

@@ -509,6 +509,7 @@ class StreamingEpoch:
         self.lru_order = list(range(self.n_buffers))  # buffers, least recently used first
         self.n_chunks = sum(len(t) for t, _ in self.blocks)
         self.last_h2d = 0
+        self.trace = None     # set to a list to record per-chunk CUDA events
         del users
 
     @property
@@ -553,6 +554,7 @@ class StreamingEpoch:
             lo, hi, row0, rel = tiles[t]
             if hi <= lo:
                 continue
+            tr = None if self.trace is None else {"chunk": (b, t), "copied": False}
             if (b, t) in self.lru:
                 slot = self.lru.index((b, t))        # already on the device
                 buf = self.bufs[slot]
@@ -562,10 +564,16 @@ class StreamingEpoch:
                 with torch.cuda.stream(self.copy_stream):
                     if self.freed[slot] is not None:
                         self.copy_stream.wait_event(self.freed[slot])
+                    if tr is not None:
+                        tr["copied"] = True
+                        tr["c0"] = torch.cuda.Event(enable_timing=True)
+                        tr["c0"].record(self.copy_stream)
                     for dst, src in zip(buf, self.host):
                         dst[:hi - lo].copy_(src[lo:hi], non_blocking=True)
-                    up = torch.cuda.Event()
+                    up = torch.cuda.Event(enable_timing=tr is not None)
                     up.record(self.copy_stream)
+                    if tr is not None:
+                        tr["c1"] = up
                 comp.wait_event(up)
                 self.lru[slot] = (b, t)
                 uploaded += hi - lo
@@ -578,10 +586,16 @@ class StreamingEpoch:
             args += (self.sub_impl,)
             args += (hparams.learning_rate, hparams.reg_user, hparams.reg_item, tseed,
                      -row0 if self.u16 else 0, 0, comp.cuda_stream)
+            if tr is not None:
+                tr["k0"] = torch.cuda.Event(enable_timing=True)
+                tr["k0"].record(comp)
             _lib.check(fn(*args), "hmf_sgd_block_qband")
-            ev = torch.cuda.Event()
+            ev = torch.cuda.Event(enable_timing=tr is not None)
             ev.record(comp)
             self.freed[slot] = ev
+            if tr is not None:
+                tr["k1"] = ev
+                self.trace.append(tr)
             done += hi - lo
         self.last_h2d = uploaded * self.bytes_per_rating
         return done

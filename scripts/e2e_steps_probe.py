@@ -30,6 +30,9 @@ def main():
     dm = DeviceModel(model.P, model.Q)
     hp = Hyperparams(n_factors=128, reg_user=0.05, reg_item=0.05, learning_rate=0.005)
     rows = []
+    se.trace = []
+    anchor = torch.cuda.Event(enable_timing=True)
+    anchor.record()
     for i in range(60):
         t0 = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -44,12 +47,20 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record()
         torch.cuda.synchronize()
+        chunks = [{"chunk": c["chunk"],
+                   "copy": (round(anchor.elapsed_time(c["c0"]), 2), round(anchor.elapsed_time(c["c1"]), 2)) if c["copied"] else None,
+                   "kernel": (round(anchor.elapsed_time(c["k0"]), 2), round(anchor.elapsed_time(c["k1"]), 2))}
+                  for c in se.trace]
+        se.trace = []
         rows.append({"step": i, "host_ms": 1e3 * (t2 - t0), "enqueue_ms": 1e3 * (t1 - t0),
-                     "wait_ms": 1e3 * (t2 - t1), "device_ms": e0.elapsed_time(e1)})
+                     "wait_ms": 1e3 * (t2 - t1), "device_ms": e0.elapsed_time(e1),
+                     "t0": round(anchor.elapsed_time(e0), 2), "chunks": chunks})
     host = np.array([r["host_ms"] for r in rows[3:]])
     out = {"variant": variant, "impl": grid.sub_impl, "median_ms": float(np.median(host)), "p90_ms": float(np.percentile(host, 90)),
            "max_ms": float(host.max()),
-           "slowest": [round(r["device_ms"], 1) for r in sorted(rows[3:], key=lambda r: -r["host_ms"])[:5]]}
+           "slowest": [round(r["device_ms"], 1) for r in sorted(rows[3:], key=lambda r: -r["host_ms"])[:5]],
+           "slowest_detail": sorted(rows[3:], key=lambda r: -r["host_ms"])[:2],
+           "typical_detail": rows[10]}
     print(json.dumps(out))
 
 
