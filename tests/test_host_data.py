@@ -77,3 +77,39 @@ def test_align_ratings_skips_unseen(tmp_path):
     u, i, r, skipped = align_ratings(load_ratings(tmp_path / "test.txt"),
                                      load_ratings(tmp_path / "train.txt"))
     assert len(r) == 1 and skipped == 2 and u[0] == 0 and i[0] == 0
+
+
+def test_qband_row_tiles():
+    from paper_2006_15980_b200.data import qband_row_tiles
+    # Netflix k=128 fp32: 480 000 rows x 512 B = 246 MB -> 8 tiles of <= 32 MB
+    assert qband_row_tiles(480_000, 128, 4) == 8
+    assert qband_row_tiles(480_000, 128, 2) == 4           # fp16 rows
+    assert qband_row_tiles(480_000, 128, 4, tile_bytes=0) == 1
+    assert qband_row_tiles(50_000_000, 128, 4) == 763       # Hugewiki on one GPU
+    assert qband_row_tiles(100, 128, 4, tile_bytes=1) == 100  # never more tiles than rows
+
+
+def test_qband_split_policy():
+    """data.qband_split_for on the measured configurations."""
+    from paper_2006_15980_b200.data import qband_split_for
+    slots = 9472
+    assert qband_split_for(slots, 8850, 50e6, 8, 128) == 4           # Netflix k=128
+    assert qband_split_for(slots, 8850, 50e6, 4, 128, True) == 4     # fp16
+    assert qband_split_for(18944, 8850, 50e6, 2, 32) == 2            # k=32: chains > items
+    assert qband_split_for(slots, 1853, 5e5, 1, 32) == 5             # ML-1M
+    assert qband_split_for(slots, 20_000, 1.55e9, 763) == 1          # Hugewiki: whole runs
+    assert qband_split_for(slots, 312_500, 1.25e8, 16) == 1          # Yahoo
+    assert qband_split_for(slots, 2353, 22.8e6, 100) == 4            # 8-GPU Hugewiki band
+    assert qband_split_for(slots, 8000, 124e6, 381) == 2             # 2-GPU Hugewiki band
+    assert qband_split_for(slots, 40, 1e6, 1) == 16                  # capped
+    assert qband_split_for(slots, 0, 0.0, 1) == 1
+
+
+def test_bench_l2_ceiling_lookup():
+    """bench.l2_ceiling reads the committed microbenchmark (a B200 measurement)."""
+    import bench
+    f32, f16 = bench.l2_ceiling(128, "f32"), bench.l2_ceiling(128, "f16")
+    assert f32 is not None and 8e9 < f32 < 12e9          # 512-byte rows, load + reduction
+    assert f16 is not None and f16 > 1.5 * f32           # 256-byte rows
+    assert bench.bytes_per_update(128, "f32") == 2060
+    assert bench.bytes_per_update(128, "f16") == 12 + 8 * 128
