@@ -292,6 +292,18 @@ def run_ours(args, world, rank, local):
     t0 = time.perf_counter()
     trip = synthetic_device(n_users, n_items, n_total, rank=8, noise=0.1, seed=SEED + rank,
                             device=dev)
+    if args.item_skew > 0:
+        # Zipf-like item popularity (p(item of rank r) ~ r^-alpha), for the
+        # layout's handling of hot items; ratings keep the law's values
+        g = torch.Generator(device=dev)
+        g.manual_seed(SEED + 17)
+        w = torch.arange(1, n_items + 1, device=dev, dtype=torch.float64).pow(-args.item_skew)
+        perm = torch.randperm(n_items, device=dev, generator=g)
+        for a in range(0, trip.nnz, 1 << 24):
+            z = min(trip.nnz, a + (1 << 24))
+            trip.items[a:z] = perm[torch.multinomial(w, z - a, replacement=True,
+                                                     generator=g)].to(torch.int32)
+        del w, perm
     train, test = split_device(trip, TEST_FRACTION)
     nnz = train.nnz
     # 1-GPU batch-only uniform plan: 1 row band x 2 column bands
@@ -438,6 +450,7 @@ def run_ours(args, world, rank, local):
                        "chain_cfg": (args.chain_cfg if (getattr(grid, "sub_impl", None) or 0) >= 4
                                      else None),
                        "item_run_split": getattr(grid, "sub_split", None),
+                       "item_skew": args.item_skew or None,
                        "row_tiles": (list(grid.sub_tiles) if getattr(grid, "sub_tiles", None)
                                      else None),
                        "l2": "inputs larger than L2 (P + triples >> 126 MB); no flush"},
@@ -689,6 +702,8 @@ def main():
                     help="e2e: device staging buffers (ring)")
     ap.add_argument("--qsync", type=int, default=None,
                     help="implementation 5: ratings between Q-delta publications (default 32)")
+    ap.add_argument("--item-skew", type=float, default=0.0,
+                    help="Zipf exponent of item popularity (0 = the synthetic law's uniform cells)")
     ap.add_argument("--split", type=int, default=0,
                     help="implementation 5 with this many parts per item run (0 = default layout)")
     ap.add_argument("--tile-mb", type=float, default=None,

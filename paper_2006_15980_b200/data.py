@@ -378,6 +378,7 @@ class DeviceGrid:
     sub_impl: int = -1          # Q-band implementation the layout is for
     sub_tile_rows: list | None = None   # per block: row cuts of its tiles (host int64)
     sub_split: int = 1                  # parts per item run (implementation 5)
+    sub_qsync: int = 0                  # Q publication period for implementation 5
 
     n_row_bands = BlockGrid.n_row_bands
     n_col_bands = BlockGrid.n_col_bands
@@ -549,6 +550,10 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     lib = _lib.load()
     s = _stream(dev)
     f16 = elem_bytes == 2
+    # an implementation asked for (argument or process default) keeps its
+    # layout rules; the automatic choice also splits hot items' runs
+    auto = impl is None and int(lib.hmf_qband_get_impl()) < 0
+    split_given = split is not None
     if impl is None:
         impl = qband_impl_for(dev, k, f16, max((grid.col_span(c)[1] - grid.col_span(c)[0]
                                                 for c in range(grid.n_col_bands)), default=0))
@@ -580,6 +585,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     out_i = torch.empty_like(grid.items)
     out_r = torch.empty_like(grid.ratings)
     sub_ptrs, sub_cuts, sub_tiles, tile_rows = [], [], [], []
+    max_parts = 1
     for b in range(grid.n_blocks):
         lo, hi = grid.block_range(b)
         c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
@@ -587,10 +593,30 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         n_tiles = qband_row_tiles(r_hi - r_lo, k, elem_bytes, tile_bytes)
         tiles = np.linspace(r_lo, r_hi, n_tiles + 1).round().astype(np.int64)
         cuts = qband_sub_cuts(c_lo, c_hi, k, target, cap)
-        if split > 1:
+        parts = None             # parts per item (single-item sub-bands), device int64
+        if hi > lo and not split_given and (impl == 5 or (auto and impl >= 4)) and c_hi > c_lo:
+            cnt = torch.bincount(grid.items[lo:hi] - c_lo, minlength=c_hi - c_lo)
+            mean = (hi - lo) / (c_hi - c_lo)
+            skewed = float(cnt.max()) > 4 * mean
+            if split > 1 or skewed:
+                # parts in proportion to the item's ratings: a hot item gets
+                # several chains (Q deltas), cold ones keep one
+                # (at most 16 parts: with Q publication every 32 ratings that
+                # bounds an item's concurrent stale steps to ~512, where
+                # training still matched whole runs)
+                parts = torch.clamp(torch.round(cnt.double() * (max(split, 1) / mean)),
+                                    1, 16).to(torch.int64)
+        elif split > 1:
+            parts = torch.full((c_hi - c_lo,), split, dtype=torch.int64, device=dev)
+        if parts is not None:
             cuts = np.arange(c_lo, c_hi + 1, dtype=np.int64)   # single items, then parts
-        n_item_sub = len(cuts) - 1
-        n_sub = n_item_sub * split
+            part_base = torch.cumsum(parts, 0) - parts              # first sub-band of item i
+            n_sub = int(parts.sum())
+            item_of = torch.repeat_interleave(torch.arange(c_hi - c_lo, device=dev), parts)
+            part_no = torch.arange(n_sub, device=dev) - part_base[item_of]
+            split_used = int(parts.max())
+        else:
+            n_sub = len(cuts) - 1
         rel = torch.from_numpy(cuts[:-1] - c_lo).to(dev)
         ptr = torch.full((n_tiles * n_sub + 1,), hi, dtype=torch.int64, device=dev)
         if hi > lo:
@@ -635,22 +661,26 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
                 grid.ratings[a:z] = out_r[a:z][order]
                 iptr = torch.zeros(n_items + 1, dtype=torch.int64, device=dev)
                 iptr[1:] = torch.cumsum(torch.bincount(key, minlength=n_items), 0)
-                if split > 1:
-                    # part r of item i starts at iptr[i] + len_i * r // split
-                    ln = (iptr[1:] - iptr[:-1]).unsqueeze(1)
-                    parts = iptr[:-1].unsqueeze(1) + ln * torch.arange(split, device=dev) // split
-                    ptr[t * n_sub:(t + 1) * n_sub] = parts.reshape(-1) + a
+                if parts is not None:
+                    # part r of item i starts at iptr[i] + len_i * r // parts_i
+                    ln = (iptr[1:] - iptr[:-1])[item_of]
+                    ptr[t * n_sub:(t + 1) * n_sub] = (iptr[:-1][item_of]
+                                                      + ln * part_no // parts[item_of] + a)
                 else:
                     ptr[t * n_sub:(t + 1) * n_sub] = iptr[rel] + a
                 del key, order, iptr
         sub_ptrs.append(ptr)
-        if split > 1:
-            cuts = np.concatenate([np.repeat(cuts[:-1], split), cuts[-1:]])
+        if parts is not None:
+            cuts = np.concatenate([np.repeat(cuts[:-1], parts.cpu().numpy()), cuts[-1:]])
+            max_parts = max(max_parts, split_used)
         sub_cuts.append(torch.from_numpy(cuts).to(device=dev, dtype=torch.int32))
         sub_tiles.append(n_tiles)
         tile_rows.append(tiles)
     del out_u, out_i, out_r
     grid.sub_ptr, grid.sub_cuts, grid.sub_tiles = sub_ptrs, sub_cuts, sub_tiles
+    if max_parts > 1 and auto and impl in (4, 6):
+        impl = 5                 # a hot item's runs are split: Q deltas
+    split = max(split, max_parts)
     if impl == 5 and split == 1:
         # whole item runs.  No more sub-bands than chains (static owners): Q
         # rows are never shared, plain stores (implementation 4).  More: the
@@ -662,6 +692,11 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         impl = 4 if all(len(c) - 1 <= slots for c in sub_cuts) else 6
     grid.sub_impl = impl
     grid.sub_split = split
+    # Q publication period for split runs: at most ~128 of an item's steps in
+    # flight across its parts (parts x period).  16 parts publishing every
+    # 16 ratings diverged on skewed items, every 8 trained like whole runs
+    # (profiles/r02/skew_*.jsonl)
+    grid.sub_qsync = max(4, min(32, 128 // max(split, 1))) if impl == 5 else 0
     grid.sub_tile_rows = tile_rows
     return grid
 

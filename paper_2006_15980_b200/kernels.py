@@ -105,6 +105,15 @@ def launch_sgd_range(user_f, item_f, rows, cols, vals, start, stop, lr, reg_user
     return _lib.check(got, f"hmf_sgd_range_{st}")
 
 
+def set_qsync(grid) -> None:
+    """The layout's Q publication period (data.bucket_qbands; a grid or the
+    period itself) for the launches that follow (process-wide setting,
+    hmf_qband_set_qsync)."""
+    q = int(grid if isinstance(grid, int) else (getattr(grid, "sub_qsync", 0) or 0))
+    if q > 0:
+        _lib.check(_lib.load().hmf_qband_set_qsync(q), "hmf_qband_set_qsync")
+
+
 def launch_block_qband(user_f, item_f, grid, block, lr, reg_user, reg_item, seed, row_base=0,
                        col_base=0, stream=None) -> int:
     """Q-band-stationary update of one block of a DeviceGrid bucketed by
@@ -125,6 +134,7 @@ def launch_block_qband(user_f, item_f, grid, block, lr, reg_user, reg_item, seed
     if int(sp.numel()) != n_tiles * n_sub + 1:
         raise ValueError("sub_ptr does not match sub_cuts x sub_tiles")
     s = current_stream_handle(user_f.device) if stream is None else int(stream)
+    set_qsync(grid)
     fn = getattr(_lib.load(), f"hmf_sgd_block_qband_{st}")
     _lib.check(fn(user_f.data_ptr(), item_f.data_ptr(), user_f.shape[1], grid.users.data_ptr(),
                   grid.items.data_ptr(), grid.ratings.data_ptr(), sp.data_ptr(), sc.data_ptr(),

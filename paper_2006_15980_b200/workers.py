@@ -471,6 +471,7 @@ class StreamingEpoch:
         self.k = k
         self.nnz = sg.nnz
         self.sub_impl = sg.sub_impl
+        self.qsync = sg.sub_qsync
         # every sub-band a single item (or a part of one): the item is implicit
         self.implicit_items = compact and sg.sub_impl >= 4 and all(
             bool(torch.all(c[1:] - c[:-1] <= 1)) for c in sg.sub_cuts)
@@ -548,6 +549,7 @@ class StreamingEpoch:
         resident = [ch for ch in reversed(self.lru) if ch is not None]
         head = [o for ch in resident for o in order if (o[0], o[1]) == ch]
         order = head + [o for o in order if (o[0], o[1]) not in resident]
+        kernels.set_qsync(self.qsync)
         done, uploaded = 0, 0
         for b, t, bseed in order:
             tiles, sc = self.blocks[b]
