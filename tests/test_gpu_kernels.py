@@ -796,6 +796,40 @@ def test_default_layout_quality_matches_whole_runs(dev, k, dtype):
     assert abs(out["default"][1] - out["whole"][1]) <= 0.005
 
 
+@pytest.mark.parametrize("k", [32, 128])
+def test_default_layout_quality_skewed_items(dev, k):
+    """Zipf-skewed item popularity: the default layout splits hot items' runs
+    over chains in proportion to their ratings (Q deltas, publication period
+    shrinking with the parts).  It must train like whole runs on one chain
+    per item: test RMSE after 6 epochs within 0.005, no divergence."""
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import (bucket_qbands, build_device_grid, split_device,
+                                            synthetic_device)
+    from paper_2006_15980_b200.sgd import init_device_model, rmse
+    d = dev
+    trip = synthetic_device(200_000, 2_000, 3_000_000, seed=5, device=d)
+    g = torch.Generator(device=d)
+    g.manual_seed(11)
+    w = torch.arange(1, 2_001, device=d, dtype=torch.float64).pow(-0.8)
+    trip.items[:] = torch.randperm(2_000, device=d, generator=g)[
+        torch.multinomial(w, trip.nnz, replacement=True, generator=g)].to(torch.int32)
+    train, test = split_device(trip, 0.05)
+    out = {}
+    for layout in ("default", "whole"):
+        grid = build_device_grid(train, [0, 200_000], [0, 1_000, 2_000])
+        bucket_qbands(grid, k, impl=None if layout == "default" else 4)
+        model = init_device_model(200_000, 2_000, k, 0, device=d)
+        for e in range(6):
+            for b in (0, 1):
+                kernels.launch_block_qband(model.P, model.Q, grid, b, 0.005, 0.05, 0.05,
+                                           kernels.mix64(b, e))
+        out[layout] = (rmse(test, model).value, grid.sub_impl, grid.sub_split, grid.sub_qsync)
+    print(out)
+    assert out["default"][2] > 1                 # hot items were split
+    assert np.isfinite(out["default"][0])
+    assert abs(out["default"][0] - out["whole"][0]) <= 0.005
+
+
 def test_qband_fp16_storage_tracks_fp32(dev, qband_impl):
     from paper_2006_15980_b200 import kernels
     m = random_matrix(3000, 800, 200_000, 5)
