@@ -24,6 +24,7 @@
 // warps walk the tiles in one seeded rotation: the P rows live at any moment
 // are about one tile's, so P reads and reductions hit L2 instead of HBM.
 // Sub-band s belongs to the same warp in every tile, so Q stays race-free.
+#include <atomic>
 #include "hmf_common.cuh"
 #include "hmf_internal.h"
 #include "lanevec.cuh"
@@ -500,7 +501,7 @@ static int reg_warps_per_sm() {
 }
 
 // process default implementation; -1 = automatic (resolve_impl)
-static int g_qband_impl = -1;
+static std::atomic<int> g_qband_impl{-1};
 
 // Implementation for a launch: an explicit impl >= 0, else the process
 // default, else automatic: the chained kernel with Q deltas (5).  With whole
@@ -840,7 +841,8 @@ static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_
     return set_error(HMF_ERR_ARG, "null pointer");
   if (((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) != 0)
     return set_error(HMF_ERR_ARG, "factor arrays must be 16-byte aligned");
-  const int cfg = g_chain_cfg >= 0 ? g_chain_cfg : auto_chain_cfg(int(k), sizeof(S) == 2);
+  const int set = g_chain_cfg.load();
+  const int cfg = set >= 0 ? set : auto_chain_cfg(int(k), sizeof(S) == 2);
   if (cfg < 4 || cfg > 6)
     return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need chain configuration 4, 5 or 6");
   const int impl = resolve_impl(impl_req, k, sizeof(S) == 2);
@@ -948,8 +950,8 @@ int hmf_qband_set_grid_share(int32_t div) {
 }
 
 int32_t hmf_qband_chain_lanes_for(int64_t k, int32_t f16) {
-  const int cfg = hmf::qs::g_chain_cfg >= 0 ? hmf::qs::g_chain_cfg
-                                             : hmf::qs::auto_chain_cfg(int(k), f16 != 0);
+  const int set = hmf::qs::g_chain_cfg.load();
+  const int cfg = set >= 0 ? set : hmf::qs::auto_chain_cfg(int(k), f16 != 0);
   if (cfg == 5 || cfg == 6) return k >= 256 ? 16 : 8;
   const int per = (cfg == 2 || cfg == 3) ? 8 : 16;  // elements per lane
   const int lpc = int(k) / per;

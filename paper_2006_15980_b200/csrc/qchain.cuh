@@ -28,6 +28,7 @@
 // a = lr*err:  dP = a*q - (lr*reg_u)*p,  q' = (1 - lr*reg_i)*q + a*p.
 #pragma once
 
+#include <atomic>
 #include <mutex>
 #include <unordered_map>
 #include <utility>
@@ -130,7 +131,7 @@ constexpr int kChainCfgs = 7;
 // Share of the GPU one Q-band launch may fill: its grid is capped at
 // 1/g_grid_div of the resident CTA slots, so g_grid_div launches on separate
 // streams (several column blocks of one row band) run side by side.
-static int g_grid_div = 1;
+static std::atomic<int> g_grid_div{1};
 static inline int grid_share(int cap) {
   const int c = (cap + g_grid_div - 1) / g_grid_div;
   return c < 1 ? 1 : c;
@@ -401,25 +402,26 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
 
 // implementation 5: steps between Q-delta publications of a chain (0 = only
 // at item and bin changes)
-static int g_qsync_steps = 32;
+static std::atomic<int> g_qsync_steps{32};
 
 // -1 = automatic (measured, profiles/r02/chain_cfg_by_k.jsonl): k = 32
 // 4 lanes per chain, 4 steps ahead (cfg 4; 28.8 / 33.6 G upd/s fp32 / fp16
 // vs 20.6 / 23.4 with 8 lanes); k = 64 fp32 8 lanes 4 ahead (cfg 6), fp16 4
 // lanes 4 ahead (cfg 4); k >= 128: 8 lanes (16 at k = 256), 2 ahead in fp32
 // (cfg 5, the register budget), 4 ahead in fp16 (cfg 6, raw fp16 slots).
-static int g_chain_cfg = -1;
+static std::atomic<int> g_chain_cfg{-1};
 static inline int auto_chain_cfg(int k, bool f16) {
   if (k <= 32) return 4;
   if (k <= 64) return f16 ? 4 : 6;
   return f16 ? 6 : 5;
 }
 template <int K, typename S> static int chain_cfg() {
-  return g_chain_cfg >= 0 ? g_chain_cfg : auto_chain_cfg(K, sizeof(S) == 2);
+  const int set = g_chain_cfg.load();
+  return set >= 0 ? set : auto_chain_cfg(K, sizeof(S) == 2);
 }
 // bin changes in warp lockstep: bit 0 for the static, bit 1 for the dynamic
 // scheduler
-static int g_chain_lockstep = 3;
+static std::atomic<int> g_chain_lockstep{3};
 
 template <int K, typename S, int CFG>
 static int chain_slots_per_sm_cfg() {

@@ -25,6 +25,7 @@
 //   EXACT    the same order with the reference's arithmetic: products and a
 //            serial f64 sum, f64 update, no FMA contraction, rounded to the
 //            storage type on store.  Bit-identical to the reference.
+#include <atomic>
 #include "hmf_common.cuh"
 #include "hmf_internal.h"
 
@@ -439,7 +440,7 @@ static uint64_t gcd_u64(uint64_t a, uint64_t b) {
   return a;
 }
 
-static int g_variant_override = -1;
+static std::atomic<int> g_variant_override{-1};
 
 template <int K, typename S, int U, int WPB, int MINB, bool ATOMIC>
 static cudaError_t launch_hogwild_v(S* P, S* Q, const int32_t* rows, const int32_t* cols,
@@ -501,7 +502,7 @@ static cudaError_t launch_hogwild_k(S* P, S* Q, const int32_t* rows, const int32
     return launch_variant<K, S, DV, ATOMIC>(P, Q, rows, cols, vals, start, stop, lr, ru, ri, seed,
                                             row_base, col_base, stream);
   } else {
-    switch (g_variant_override < 0 ? DV : g_variant_override) {
+    switch (g_variant_override.load() < 0 ? DV : g_variant_override.load()) {
 #define HMF_VARIANT_CASE(VV)                                                                    \
   case VV:                                                                                      \
     return launch_variant<K, S, VV, ATOMIC>(P, Q, rows, cols, vals, start, stop, lr, ru, ri,    \
