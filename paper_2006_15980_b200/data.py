@@ -586,6 +586,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     out_r = torch.empty_like(grid.ratings)
     sub_ptrs, sub_cuts, sub_tiles, tile_rows = [], [], [], []
     max_parts = 1
+    any_skewed = False
     for b in range(grid.n_blocks):
         lo, hi = grid.block_range(b)
         c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
@@ -598,6 +599,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
             cnt = torch.bincount(grid.items[lo:hi] - c_lo, minlength=c_hi - c_lo)
             mean = (hi - lo) / (c_hi - c_lo)
             skewed = float(cnt.max()) > 4 * mean
+            any_skewed = any_skewed or skewed
             if split > 1 or skewed:
                 # parts in proportion to the item's ratings: a hot item gets
                 # several chains (Q deltas), cold ones keep one
@@ -692,11 +694,14 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         impl = 4 if all(len(c) - 1 <= slots for c in sub_cuts) else 6
     grid.sub_impl = impl
     grid.sub_split = split
-    # Q publication period for split runs: at most ~128 of an item's steps in
-    # flight across its parts (parts x period).  16 parts publishing every
-    # 16 ratings diverged on skewed items, every 8 trained like whole runs
-    # (profiles/r02/skew_*.jsonl)
-    grid.sub_qsync = max(4, min(32, 128 // max(split, 1))) if impl == 5 else 0
+    # Q publication period for split runs, bounding an item's steps in
+    # flight across its parts (parts x period): ~128 when hot items are split
+    # (16 parts publishing every 16 ratings diverged on skewed items, every 8
+    # trained like whole runs, profiles/r02/skew_item_popularity.jsonl), ~512
+    # for uniform popularity (15 parts x 32 matched whole runs,
+    # profiles/r02/split_quality_bounded_staleness.jsonl)
+    bound = 128 if any_skewed else 512
+    grid.sub_qsync = max(4, min(32, bound // max(split, 1))) if impl == 5 else 0
     grid.sub_tile_rows = tile_rows
     return grid
 
