@@ -505,8 +505,9 @@ def qband_split_for(slots: int, items: int, block_nnz: float, n_tiles: int, k: i
     its own copy of the item's Q row.  Without bounds, R concurrent parts
     pile up an item's steps before the deltas meet (test RMSE 0.42 vs 0.12 at
     k = 32); every chain therefore publishes its change and re-reads the row
-    every 32 ratings (hmf_qband_set_qsync), which keeps every split within
-    0.0001 of whole runs at k = 32..128, fp32 and fp16.  Then:
+    every few ratings (grid.sub_qsync: 512 // parts, or 128 // parts when hot
+    items are split, clamped to 4..32; hmf_qband_set_qsync), which keeps every
+    split within 0.0001 of whole runs at k = 32..128, fp32 and fp16.  Then:
     * at least twice as many items as chains: whole runs (Yahoo, Hugewiki);
     * fewer items than chains: slots // items parts, so every chain has a
       unit per tile (ML-1M: 5; an 8-GPU column band: 4-9); when that is 1
@@ -603,9 +604,8 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
             if split > 1 or skewed:
                 # parts in proportion to the item's ratings: a hot item gets
                 # several chains (Q deltas), cold ones keep one
-                # (at most 16 parts: with Q publication every 32 ratings that
-                # bounds an item's concurrent stale steps to ~512, where
-                # training still matched whole runs)
+                # (at most 16 parts; with sub_qsync below, parts x period
+                # stays at ~128 stale item steps for skewed layouts)
                 parts = torch.clamp(torch.round(cnt.double() * (max(split, 1) / mean)),
                                     1, 16).to(torch.int64)
         elif split > 1:
