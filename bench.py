@@ -329,7 +329,10 @@ def run_ours(args, world, rank, local):
     if not args.no_e2e and args.kernel == "qband" and world == 1:
         # e2e streams the same layout from pinned host memory, tile by tile
         from paper_2006_15980_b200.workers import StreamingEpoch
-        stream_epoch = StreamingEpoch(grid, k, n_buffers=args.stream_buffers)
+        stream_epoch = StreamingEpoch(grid, k, n_buffers=args.stream_buffers,
+                                      tiles_per_chunk=args.stream_tiles,
+                                      first_chunk_tiles=args.stream_first,
+                                      reuse=args.stream_reuse)
     model = init_device_model(n_users, n_items, k, SEED, device=dev,
                               dtype="float16" if precision == "f16" else "float32")
     torch.cuda.synchronize(dev)
@@ -571,8 +574,8 @@ def run_ours_multi(args, world, rank, local):
 def run_e2e_stream(args, se, model, test, dev):
     """e2e through the public engine API: every step streams that epoch's
     triples from pinned host memory (workers.StreamingEpoch: chunk c+1
-    uploads while chunk c trains; the chunks still staged from the previous
-    epoch train first without a second upload) and reads the step's result —
+    uploads while chunk c trains; every chunk is uploaded every epoch unless
+    --stream-reuse) and reads the step's result —
     the test RMSE sum — back to the host.  P and Q stay resident, as in
     training.  Steps are software-pipelined: step i+1's uploads and kernels
     are queued before the host waits for step i's result, so the GPU does not
@@ -629,10 +632,14 @@ def run_e2e_stream(args, se, model, test, dev):
                     + (f"{se.bytes_per_rating} B/rating: "
                        + ("2-byte user ids relative to the row tile, " if se.u16 else "")
                        + ("item implicit in its sub-band; " if se.implicit_items else "triples; "))
-                    + "double-buffered H2D overlapped with the Q-band kernel; chunks still "
-                    "staged from the previous epoch are not uploaded again) + device RMSE sums "
-                    "read back every step (steps pipelined: step i+1 queued before step i's "
-                    "result is read)"}
+                    + f"{se.n_chunks} chunks of {se.tiles_per_chunk} row tile(s)"
+                    + (f" (each block's first {se.first_chunk_tiles})" if se.first_chunk_tiles
+                       else "") + ", "
+                    f"{se.n_buffers} staging buffers, H2D overlapped with the Q-band kernel; "
+                    + ("chunks still staged from the previous epoch are not uploaded again"
+                       if se.reuse else "every chunk uploaded every epoch")
+                    + ") + device RMSE sums read back every step (steps pipelined: step i+1 "
+                    "queued before step i's result is read)"}
 
 
 def run_e2e(args, grid, model, k, precision, dev, world):
@@ -700,8 +707,16 @@ def main():
     ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)
     ap.add_argument("--stream-buffers", type=int, default=2,
                     help="e2e: device staging buffers (ring)")
+    ap.add_argument("--stream-tiles", type=int, default=1,
+                    help="e2e: row tiles per streamed chunk (one launch each)")
+    ap.add_argument("--stream-first", type=int, default=0,
+                    help="e2e: row tiles in each block's first chunk (0 = --stream-tiles)")
+    ap.add_argument("--stream-reuse", action="store_true",
+                    help="e2e: do not re-upload chunks still staged from the previous epoch "
+                         "(default: every epoch uploads all of its triples)")
     ap.add_argument("--qsync", type=int, default=None,
-                    help="implementation 5: ratings between Q-delta publications (default 32)")
+                    help="implementation 5: ratings between Q-delta publications "
+                         "(default: the layout's grid.sub_qsync)")
     ap.add_argument("--item-skew", type=float, default=0.0,
                     help="Zipf exponent of item popularity (0 = the synthetic law's uniform cells)")
     ap.add_argument("--split", type=int, default=0,

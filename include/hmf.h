@@ -12,6 +12,7 @@
  *   hmf_sgd_range_{f32,f16,f64}   kernels.sgd_range            kernels.py:61-133
  *   hmf_sgd_block_qband_{f32,f16} BatchEngine.compute on a staged item band
  *   hmf_sgd_block_qband_u16_*     (the same, uint16 tile-relative row ids)
+ *   hmf_sgd_block_qband_u16_tiles_*  (the same over several row tiles)
  *                                                              workers.py:186-255
  *   hmf_qband_set_*, _get_*       (kernel selection / configuration; no
  *                                 reference counterpart)
@@ -42,7 +43,7 @@
 extern "C" {
 #endif
 
-#define HMF_ABI_VERSION 2
+#define HMF_ABI_VERSION 3
 
 #define HMF_OK 0
 #define HMF_ERR_ARG (-1)
@@ -195,6 +196,27 @@ int64_t hmf_sgd_block_qband_u16_f16(uint16_t* user_f, uint16_t* item_f, int64_t 
                                     int64_t n_tiles, int32_t impl, double lr, double reg_user,
                                     double reg_item, uint64_t seed, int64_t row_base,
                                     int64_t col_base, void* stream);
+
+/* uint16 row ids over n_tiles row tiles in one launch: a rating of tile t
+ * updates row tile_row0[t] + rows[i] (tile_row0: device int32[n_tiles], the
+ * tiles' first rows in user_f).  Lets a host stream stage several tiles of a
+ * block as one chunk at 2 bytes per user id.  Same contract as
+ * hmf_sgd_block_qband_u16_* otherwise (there is no row_base).  Added in ABI
+ * version 3. */
+int64_t hmf_sgd_block_qband_u16_tiles_f32(float* user_f, float* item_f, int64_t k,
+                                          const uint16_t* rows, const int32_t* cols,
+                                          const float* vals, const int64_t* sub_ptr,
+                                          const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles,
+                                          const int32_t* tile_row0, int32_t impl, double lr,
+                                          double reg_user, double reg_item, uint64_t seed,
+                                          int64_t col_base, void* stream);
+int64_t hmf_sgd_block_qband_u16_tiles_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                                          const uint16_t* rows, const int32_t* cols,
+                                          const float* vals, const int64_t* sub_ptr,
+                                          const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles,
+                                          const int32_t* tile_row0, int32_t impl, double lr,
+                                          double reg_user, double reg_item, uint64_t seed,
+                                          int64_t col_base, void* stream);
 
 /*
  * The reference visit order of a range of n triples under `seed`

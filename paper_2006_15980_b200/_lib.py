@@ -70,6 +70,10 @@ SIGNATURES = {
                                            _f64, _f64, _f64, _u64, _i64, _i64, _p]),
     "hmf_sgd_block_qband_u16_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i32,
                                            _f64, _f64, _f64, _u64, _i64, _i64, _p]),
+    "hmf_sgd_block_qband_u16_tiles_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64,
+                                                 _p, _i32, _f64, _f64, _f64, _u64, _i64, _p]),
+    "hmf_sgd_block_qband_u16_tiles_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64,
+                                                 _p, _i32, _f64, _f64, _f64, _u64, _i64, _p]),
     "hmf_visit_order": (C.c_int, [_i64, _u64, _p, _p]),
     "hmf_mix64": (_u64, [C.POINTER(_u64), _i32]),
     "hmf_residual_sums_f32": (C.c_int, [_p, _p, _i64, _p, _p, _p, _i64, _i64, _i64, _i32, _p, _p]),
@@ -122,7 +126,7 @@ def load() -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.hmf_abi_version() != 2:
+        if lib.hmf_abi_version() != 3:
             raise HmfError("libhmf ABI version mismatch")
         _lib = lib
         return lib

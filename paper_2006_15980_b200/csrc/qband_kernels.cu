@@ -833,7 +833,7 @@ static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_
                        const float* vals, const int64_t* sub_ptr, const int32_t* sub_cuts,
                        int64_t n_sub, int64_t n_tiles, int impl_req, double lr, double ru,
                        double ri, uint64_t seed, int64_t row_base, int64_t col_base,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, const int32_t* tile_row0 = nullptr) {
   if (n_sub <= 0 || n_tiles <= 0) return 0;
   if (n_sub * n_tiles > (int64_t(1) << 31))
     return set_error(HMF_ERR_ARG, "n_sub * n_tiles too large");
@@ -853,16 +853,16 @@ static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_
   switch (k) {
     case 32: e = launch_chain<32, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
                                                 int(n_sub), int(n_tiles), lr, ru, ri, seed,
-                                                row_base, col_base, stream, qdelta); break;
+                                                row_base, col_base, stream, qdelta, tile_row0); break;
     case 64: e = launch_chain<64, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
                                                 int(n_sub), int(n_tiles), lr, ru, ri, seed,
-                                                row_base, col_base, stream, qdelta); break;
+                                                row_base, col_base, stream, qdelta, tile_row0); break;
     case 128: e = launch_chain<128, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
                                                   int(n_sub), int(n_tiles), lr, ru, ri, seed,
-                                                  row_base, col_base, stream, qdelta); break;
+                                                  row_base, col_base, stream, qdelta, tile_row0); break;
     case 256: e = launch_chain<256, S, uint16_t>(P, Q, rows, cols, vals, sub_ptr, sub_cuts,
                                                   int(n_sub), int(n_tiles), lr, ru, ri, seed,
-                                                  row_base, col_base, stream, qdelta); break;
+                                                  row_base, col_base, stream, qdelta, tile_row0); break;
     default: return set_error(HMF_ERR_UNSUPPORTED, "Q-band kernel needs k in {32,64,128,256}");
   }
   if (e != cudaSuccess) return set_cuda_error(e);
@@ -1022,6 +1022,33 @@ int64_t hmf_sgd_block_qband_u16_f16(uint16_t* user_f, uint16_t* item_f, int64_t 
                                   reinterpret_cast<__half*>(item_f), k, rows, cols, vals, sub_ptr,
                                   sub_cuts, n_sub, n_tiles, impl, lr, reg_user, reg_item, seed,
                                   row_base, col_base, static_cast<cudaStream_t>(stream));
+}
+
+int64_t hmf_sgd_block_qband_u16_tiles_f32(float* user_f, float* item_f, int64_t k,
+                                          const uint16_t* rows, const int32_t* cols,
+                                          const float* vals, const int64_t* sub_ptr,
+                                          const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles,
+                                          const int32_t* tile_row0, int32_t impl, double lr,
+                                          double reg_user, double reg_item, uint64_t seed,
+                                          int64_t col_base, void* stream) {
+  if (!tile_row0 && n_sub > 0 && n_tiles > 0) return hmf::set_error(HMF_ERR_ARG, "null pointer");
+  return hmf::qs::run_u16<float>(user_f, item_f, k, rows, cols, vals, sub_ptr, sub_cuts, n_sub,
+                                 n_tiles, impl, lr, reg_user, reg_item, seed, 0, col_base,
+                                 static_cast<cudaStream_t>(stream), tile_row0);
+}
+
+int64_t hmf_sgd_block_qband_u16_tiles_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                                          const uint16_t* rows, const int32_t* cols,
+                                          const float* vals, const int64_t* sub_ptr,
+                                          const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles,
+                                          const int32_t* tile_row0, int32_t impl, double lr,
+                                          double reg_user, double reg_item, uint64_t seed,
+                                          int64_t col_base, void* stream) {
+  if (!tile_row0 && n_sub > 0 && n_tiles > 0) return hmf::set_error(HMF_ERR_ARG, "null pointer");
+  return hmf::qs::run_u16<__half>(reinterpret_cast<__half*>(user_f),
+                                  reinterpret_cast<__half*>(item_f), k, rows, cols, vals, sub_ptr,
+                                  sub_cuts, n_sub, n_tiles, impl, lr, reg_user, reg_item, seed, 0,
+                                  col_base, static_cast<cudaStream_t>(stream), tile_row0);
 }
 
 }  // extern "C"

@@ -160,8 +160,9 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     qchain_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const RowT* __restrict__ rows,
                   const int32_t* __restrict__ cols, const float* __restrict__ vals,
                   const int64_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_cuts,
-                  int n_sub, int n_tiles, float lr, float ru, float ri, uint64_t seed,
-                  unsigned* __restrict__ work, int lockstep, int qdelta, int qsync) {
+                  int n_sub, int n_tiles, const int32_t* __restrict__ tile_row0, float lr,
+                  float ru, float ri, uint64_t seed, unsigned* __restrict__ work, int lockstep,
+                  int qdelta, int qsync) {
   using L = ChainLay<K, S, LPC>;
   constexpr int NC = L::NC, E = L::EPL, NS = PD + 1;
   static_assert(PD >= 1 && PD < LPC, "prefetch distance must stay within one batch");
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
   int len = 0, nf = 0, nb = 0, rot = 0, x = 0, j = 0, cnt = 0;
   int32_t cu = -1, cv = 0, nu = -1, nv = 0;
   int32_t vbin = 0;  // the bin's item when cols == nullptr (one item per sub-band)
+  int32_t tb = 0;    // the bin's tile's first row when rows are tile-relative (tile_row0)
   float cr = 0.f, nr = 0.f;
   uint32_t p[NS][L::RW];
   float q[E];
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     if (xx < nb) {
       const int o = bstart(xx) + l;
       if (o < len) {
-        u = int32_t(__ldg(rows + beg + o));
+        u = int32_t(__ldg(rows + beg + o)) + tb;
         v = cols ? __ldg(cols + beg + o) : vbin;
         r = __ldg(vals + beg + o);
       }
@@ -244,6 +246,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     beg = sp[us];
     len = int(sp[us + 1] - beg);
     if (!cols) vbin = __ldg(sub_cuts + us);
+    if (tile_row0) tb = __ldg(tile_row0 + tile);
     nf = len / LPC;
     nb = (len + LPC - 1) / LPC;
     const uint64_t bin = uint64_t(tile) * uint64_t(n_sub) + uint64_t(us);
@@ -472,9 +475,9 @@ template <int K, typename S, int CFG, typename RowT>
 static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t* cols,
                                     const float* vals, const int64_t* sub_ptr,
                                     const int32_t* sub_cuts, int n_sub,
-                                    int n_tiles, double lr, double ru, double ri, uint64_t seed,
-                                    int64_t row_base, int64_t col_base, cudaStream_t stream,
-                                    int qdelta) {
+                                    int n_tiles, const int32_t* tile_row0, double lr, double ru,
+                                    double ri, uint64_t seed, int64_t row_base, int64_t col_base,
+                                    cudaStream_t stream, int qdelta) {
   using C = ChainCfg<K, CFG>;
   constexpr int NC = 32 / C::LPC;
   auto kstat = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false, RowT>;
@@ -507,24 +510,27 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
   // 2: publish at item and bin changes only (whole runs per sub-band)
   const int qsync = qdelta == 1 && g_qsync_steps > 0 ? (g_qsync_steps + C::PD) / (C::PD + 1) : 0;
   kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
-                                         sub_ptr, sub_cuts, n_sub, n_tiles, float(lr), float(ru),
-                                         float(ri), seed, work, lockstep, qdelta, qsync);
+                                         sub_ptr, sub_cuts, n_sub, n_tiles, tile_row0, float(lr),
+                                         float(ru), float(ri), seed, work, lockstep, qdelta,
+                                         qsync);
   return cudaGetLastError();
 }
 
-// rows: int32 row ids, or uint16 (a row tile's ids relative to its first row,
-// passed as row_base = -first row: 2 bytes per rating on the host stream;
-// configurations 4, 5 and 6 only)
+// rows: int32 row ids, or uint16 (a row tile's ids relative to its first row:
+// 2 bytes per rating on the host stream; configurations 4, 5 and 6 only).
+// The tile's first row is tile_row0[tile] (device, n_tiles entries) or, with
+// tile_row0 == nullptr, -row_base for every tile.
 template <int K, typename S, typename RowT = int32_t>
 static cudaError_t launch_chain(S* P, S* Q, const RowT* rows, const int32_t* cols,
                                 const float* vals, const int64_t* sub_ptr,
                                 const int32_t* sub_cuts, int n_sub, int n_tiles,
                                 double lr, double ru, double ri, uint64_t seed, int64_t row_base,
-                                int64_t col_base, cudaStream_t stream, int qdelta = 0) {
+                                int64_t col_base, cudaStream_t stream, int qdelta = 0,
+                                const int32_t* tile_row0 = nullptr) {
 #define HMF_CHAIN_CFG(CFG)                                                                     \
   return launch_chain_cfg<K, S, CFG, RowT>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, n_sub,  \
-                                           n_tiles, lr, ru, ri, seed, row_base, col_base,      \
-                                           stream, qdelta)
+                                           n_tiles, tile_row0, lr, ru, ri, seed, row_base,     \
+                                           col_base, stream, qdelta)
   if constexpr (sizeof(RowT) == 2) {
     switch (chain_cfg<K, S>()) {
       case 4: HMF_CHAIN_CFG(4);

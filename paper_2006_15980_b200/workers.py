@@ -449,10 +449,12 @@ class StreamingEpoch:
     epoch uploads chunk c+1 on a copy stream while the Q-band kernel updates
     chunk c (a ring of device staging buffers, ordered by CUDA events).
 
-    Chunks are the row tiles of each block (data.bucket_qbands): chunk (b, t)
-    holds block b's triples of row tile t, item runs inside.  While a chunk
-    trains, its tile's P rows sit in L2, as in the resident layout, and the
-    epoch walks each block's tiles in a seeded rotation.
+    Chunks are runs of `tiles_per_chunk` row tiles of each block
+    (data.bucket_qbands), the first one `first_chunk_tiles` long if set (a
+    short first upload before the first launch): chunk (b, c) holds block b's
+    triples of those tiles, item runs inside each.  One launch trains a chunk, walking its tiles as
+    the resident kernel walks a block's (each tile's P rows sit in L2 while
+    its bins run); the epoch walks each block's chunks in a seeded rotation.
 
     Bytes per rating on the host stream (the chained kernel, one item per
     sub-band, every tile at most 65536 rows): a 2-byte user id relative to
@@ -462,7 +464,8 @@ class StreamingEpoch:
     """
 
     def __init__(self, grid: DeviceGrid, k: int, tile_bytes=None, n_buffers: int = 2,
-                 elem_bytes: int = 4, compact: bool = True):
+                 elem_bytes: int = 4, compact: bool = True, tiles_per_chunk: int = 1,
+                 first_chunk_tiles: int = 0, reuse: bool = True):
         torch = _torch()
         self.dev = grid.device
         # a grid the caller already laid out for the Q-band kernel is used as is
@@ -472,14 +475,18 @@ class StreamingEpoch:
         self.nnz = sg.nnz
         self.sub_impl = sg.sub_impl
         self.qsync = sg.sub_qsync
+        self.reuse = bool(reuse)
         # every sub-band a single item (or a part of one): the item is implicit
         self.implicit_items = compact and sg.sub_impl >= 4 and all(
             bool(torch.all(c[1:] - c[:-1] <= 1)) for c in sg.sub_cuts)
         cfg_ok = int(_lib.load().hmf_qband_get_chain_cfg()) in (-1, 4, 5, 6)
         self.u16 = self.implicit_items and cfg_ok and all(
             int(np.max(np.diff(r))) <= 65536 for r in sg.sub_tile_rows)
-        # chunks: (block, tile) -> [lo, hi) of the bucketed arrays, the tile's
-        # first row, its sub-band offsets relative to lo, the block's sub_cuts
+        # chunks: G consecutive row tiles of a block -> [lo, hi) of the
+        # bucketed arrays, the number of tiles, their sub-band offsets relative
+        # to lo, their first rows (device int32, uint16 ids only)
+        self.tiles_per_chunk = max(1, int(tiles_per_chunk))
+        self.first_chunk_tiles = max(0, int(first_chunk_tiles))
         self.blocks = []
         users = sg.users
         if self.u16:
@@ -488,27 +495,35 @@ class StreamingEpoch:
             sp = sg.sub_ptr[b].cpu().numpy()
             T = sg.sub_tiles[b]
             S = (len(sp) - 1) // T
-            tiles = []
-            for t in range(T):
-                lo, hi = int(sp[t * S]), int(sp[(t + 1) * S])
-                row0 = int(sg.sub_tile_rows[b][t])
-                rel = (sg.sub_ptr[b][t * S:(t + 1) * S + 1] - lo).contiguous()
-                tiles.append((lo, hi, row0, rel))
-                if self.u16 and hi > lo:
-                    # uint16 bit pattern of (user - row0), 0..65535
-                    users[lo:hi] = (sg.users[lo:hi] - row0).to(torch.int32).to(torch.int16)
-            self.blocks.append((tiles, sg.sub_cuts[b]))
+            cuts = [0] + ([min(T, self.first_chunk_tiles)] if self.first_chunk_tiles else [])
+            while cuts[-1] < T:
+                cuts.append(min(T, cuts[-1] + self.tiles_per_chunk))
+            chunks = []
+            for t0, t1 in zip(cuts, cuts[1:]):
+                lo, hi = int(sp[t0 * S]), int(sp[t1 * S])
+                rows0 = [int(r) for r in sg.sub_tile_rows[b][t0:t1]]
+                rel = (sg.sub_ptr[b][t0 * S:t1 * S + 1] - lo).contiguous()
+                trow = torch.tensor(rows0, dtype=torch.int32, device=self.dev)
+                chunks.append((lo, hi, t1 - t0, rel, trow))
+                if self.u16:
+                    for t in range(t0, t1):
+                        a, z = int(sp[t * S]), int(sp[(t + 1) * S])
+                        if z > a:
+                            # uint16 bit pattern of (user - tile's first row)
+                            users[a:z] = (sg.users[a:z] - rows0[t - t0]).to(torch.int32).to(
+                                torch.int16)
+            self.blocks.append((chunks, sg.sub_cuts[b]))
         arrays = [users] + ([] if self.implicit_items else [sg.items]) + [sg.ratings]
         self.host = [a.cpu().pin_memory() for a in arrays]
-        cap = max([hi - lo for tiles, _ in self.blocks for lo, hi, _, _ in tiles] + [0]) + 8
+        cap = max([c[1] - c[0] for chunks, _ in self.blocks for c in chunks] + [0]) + 8
         self.n_buffers = max(2, int(n_buffers))
         self.bufs = [tuple(torch.empty(cap, dtype=a.dtype, device=self.dev) for a in arrays)
                      for _ in range(self.n_buffers)]
         self.copy_stream = torch.cuda.Stream(device=self.dev)
         self.freed = [None] * self.n_buffers
-        self.lru = [None] * self.n_buffers            # chunk (block, tile) held by each buffer
+        self.lru = [None] * self.n_buffers            # chunk (block, index) held by each buffer
         self.lru_order = list(range(self.n_buffers))  # buffers, least recently used first
-        self.n_chunks = sum(len(t) for t, _ in self.blocks)
+        self.n_chunks = sum(len(c) for c, _ in self.blocks)
         self.last_h2d = 0
         self.trace = None     # set to a list to record per-chunk CUDA events
         del users
@@ -531,33 +546,40 @@ class StreamingEpoch:
     def run(self, P, Q, hparams: Hyperparams, seed: int, stream=None) -> int:
         """One epoch over every block; returns triples processed (async).
 
-        Chunks still in a staging buffer from the previous epoch are trained
-        first and not uploaded again (the tail of epoch e is the head of
-        epoch e+1); the rest follow block by block, each block's tiles in a
-        seeded rotation."""
+        With `reuse`, chunks still in a staging buffer from the previous epoch
+        are trained first and not uploaded again (the tail of epoch e is the
+        head of epoch e+1); the rest follow block by block, each block's
+        chunks in a seeded rotation.  Without it every chunk is uploaded every
+        epoch."""
         torch = _torch()
         comp = torch.cuda.current_stream(self.dev) if stream is None else stream
         st = "f16" if P.dtype == torch.float16 else "f32"
         lib = _lib.load()
-        fn = getattr(lib, f"hmf_sgd_block_qband_u16_{st}" if self.u16
+        fn = getattr(lib, f"hmf_sgd_block_qband_u16_tiles_{st}" if self.u16
                      else f"hmf_sgd_block_qband_{st}")
         order = []
-        for b, (tiles, _) in enumerate(self.blocks):
+        for b, (chunks, _) in enumerate(self.blocks):
             bseed = kernels.mix64(seed, b) & 0xFFFFFFFFFFFFFFFF
-            rot = bseed % len(tiles) if tiles else 0
-            order += [(b, (i + rot) % len(tiles), bseed) for i in range(len(tiles))]
-        resident = [ch for ch in reversed(self.lru) if ch is not None]
-        head = [o for ch in resident for o in order if (o[0], o[1]) == ch]
-        order = head + [o for o in order if (o[0], o[1]) not in resident]
+            # a short first chunk (first_chunk_tiles) stays first: the
+            # pipeline starts after a short upload
+            h = 1 if self.first_chunk_tiles and len(chunks) > 1 else 0
+            n = len(chunks) - h
+            rot = bseed % n if n else 0
+            order += [(b, c, bseed) for c in range(h)]
+            order += [(b, h + (i + rot) % n, bseed) for i in range(n)]
+        if self.reuse:
+            resident = [ch for ch in reversed(self.lru) if ch is not None]
+            head = [o for ch in resident for o in order if (o[0], o[1]) == ch]
+            order = head + [o for o in order if (o[0], o[1]) not in resident]
         kernels.set_qsync(self.qsync)
         done, uploaded = 0, 0
         for b, t, bseed in order:
-            tiles, sc = self.blocks[b]
-            lo, hi, row0, rel = tiles[t]
+            chunks, sc = self.blocks[b]
+            lo, hi, n_tiles, rel, trow = chunks[t]
             if hi <= lo:
                 continue
             tr = None if self.trace is None else {"chunk": (b, t), "copied": False}
-            if (b, t) in self.lru:
+            if self.reuse and (b, t) in self.lru:
                 slot = self.lru.index((b, t))        # already on the device
                 buf = self.bufs[slot]
             else:
@@ -584,10 +606,14 @@ class StreamingEpoch:
             items = 0 if self.implicit_items else buf[1].data_ptr()
             tseed = kernels.mix64(bseed, t) & 0xFFFFFFFFFFFFFFFF
             args = (P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr(), items,
-                    buf[-1].data_ptr(), rel.data_ptr(), sc.data_ptr(), int(sc.numel()) - 1, 1)
-            args += (self.sub_impl,)
-            args += (hparams.learning_rate, hparams.reg_user, hparams.reg_item, tseed,
-                     -row0 if self.u16 else 0, 0, comp.cuda_stream)
+                    buf[-1].data_ptr(), rel.data_ptr(), sc.data_ptr(), int(sc.numel()) - 1,
+                    n_tiles)
+            if self.u16:        # tile-relative uint16 ids, first rows per tile
+                args += (trow.data_ptr(), self.sub_impl, hparams.learning_rate,
+                         hparams.reg_user, hparams.reg_item, tseed, 0, comp.cuda_stream)
+            else:
+                args += (self.sub_impl, hparams.learning_rate, hparams.reg_user,
+                         hparams.reg_item, tseed, 0, 0, comp.cuda_stream)
             if tr is not None:
                 tr["k0"] = torch.cuda.Event(enable_timing=True)
                 tr["k0"].record(comp)

@@ -41,7 +41,7 @@ def test_binding_matches_header():
 def test_host_only_entry_points():
     from paper_2006_15980_b200 import _lib, kernels
     lib = _lib.load()
-    assert lib.hmf_abi_version() == 2
+    assert lib.hmf_abi_version() == 3
     for parts in [(0,), (7, 3, 1), (2 ** 63 - 1, 5), (123456789, 42, 17, 3)]:
         assert _lib.mix64_native(*parts) == kernels.mix64(*parts)
     # argument validation happens before any device work

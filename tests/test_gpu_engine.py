@@ -144,11 +144,13 @@ def test_throughput_sweep_reports_stages(dev):
         throughput_sweep("batch", [2, 1], batch_config=BatchWorkerConfig(device=dev))
 
 
-@pytest.mark.parametrize("k,impl", [(64, -1), (128, -1), (64, 0)])
-def test_streaming_epoch_applies_every_triple_once(dev, k, impl):
-    """StreamingEpoch (triples streamed from pinned host memory tile by tile,
-    double buffered) on conflict-free triples equals the reference update of
-    each triple exactly once."""
+@pytest.mark.parametrize("k,impl,tiles,first", [(64, -1, 1, 0), (128, -1, 1, 0), (64, 0, 1, 0),
+                                                (128, -1, 2, 0), (64, -1, 3, 0), (64, 0, 3, 0),
+                                                (128, -1, 2, 1), (64, 0, 3, 1)])
+def test_streaming_epoch_applies_every_triple_once(dev, k, impl, tiles, first):
+    """StreamingEpoch (triples streamed from pinned host memory in chunks of
+    `tiles` row tiles, double buffered) on conflict-free triples equals the
+    reference update of each triple exactly once."""
     import oracle
     from paper_2006_15980_b200.data import DeviceTriples, build_device_grid
     from paper_2006_15980_b200.sgd import Hyperparams
@@ -165,10 +167,13 @@ def test_streaming_epoch_applies_every_triple_once(dev, k, impl):
     from paper_2006_15980_b200 import _lib
     _lib.check(_lib.load().hmf_qband_set_impl(impl), "set_impl")
     try:
-        se = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1)   # 3 row tiles per block
+        se = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1,   # 3 row tiles per block
+                            tiles_per_chunk=tiles, first_chunk_tiles=first)
+        se_all = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1, tiles_per_chunk=tiles,
+                                first_chunk_tiles=first, reuse=False)
     finally:
         _lib.load().hmf_qband_set_impl(-1)
-    assert se.n_chunks == 6
+    assert se.n_chunks == 2 * ((1 + -(-2 // tiles)) if first else -(-3 // tiles))
     P0 = rng.uniform(0, 0.1, size=(9000, k)).astype(np.float32)
     Q0 = rng.uniform(0, 0.1, size=(7000, k)).astype(np.float32)
     P, Q = torch.from_numpy(P0).to(d), torch.from_numpy(Q0).to(d)
@@ -189,4 +194,9 @@ def test_streaming_epoch_applies_every_triple_once(dev, k, impl):
     # a second epoch starts on the two chunks still staged and does not upload them
     assert se.run(P, Q, hp, seed=2) == n
     torch.cuda.synchronize()
-    assert 0 < se.h2d_bytes_last() < se.h2d_bytes
+    assert se.h2d_bytes_last() < se.h2d_bytes
+    assert se.h2d_bytes_last() > 0 or se.n_chunks <= se.n_buffers
+    # without reuse every epoch uploads all of its triples
+    for e in range(2):
+        assert se_all.run(P, Q, hp, seed=3 + e) == n
+        assert se_all.h2d_bytes_last() == se_all.h2d_bytes
