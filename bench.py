@@ -331,7 +331,7 @@ def run_ours(args, world, rank, local):
         from paper_2006_15980_b200.workers import StreamingEpoch
         stream_epoch = StreamingEpoch(grid, k, n_buffers=args.stream_buffers,
                                       tiles_per_chunk=args.stream_tiles,
-                                      first_chunk_tiles=args.stream_first,
+                                      last_chunk_tiles=args.stream_last,
                                       reuse=args.stream_reuse)
     model = init_device_model(n_users, n_items, k, SEED, device=dev,
                               dtype="float16" if precision == "f16" else "float32")
@@ -633,7 +633,7 @@ def run_e2e_stream(args, se, model, test, dev):
                        + ("2-byte user ids relative to the row tile, " if se.u16 else "")
                        + ("item implicit in its sub-band; " if se.implicit_items else "triples; "))
                     + f"{se.n_chunks} chunks of {se.tiles_per_chunk} row tile(s)"
-                    + (f" (each block's first {se.first_chunk_tiles})" if se.first_chunk_tiles
+                    + (f" (each block's last {se.last_chunk_tiles})" if se.last_chunk_tiles
                        else "") + ", "
                     f"{se.n_buffers} staging buffers, H2D overlapped with the Q-band kernel; "
                     + ("chunks still staged from the previous epoch are not uploaded again"
@@ -705,12 +705,12 @@ def main():
     ap.add_argument("--chain-cfg", type=int, choices=list(range(-1, 7)), default=-1,
                     help="configuration of Q-band implementation 4 (qchain.cuh ChainCfg)")
     ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)
-    ap.add_argument("--stream-buffers", type=int, default=2,
+    ap.add_argument("--stream-buffers", type=int, default=3,
                     help="e2e: device staging buffers (ring)")
-    ap.add_argument("--stream-tiles", type=int, default=1,
+    ap.add_argument("--stream-tiles", type=int, default=4,
                     help="e2e: row tiles per streamed chunk (one launch each)")
-    ap.add_argument("--stream-first", type=int, default=0,
-                    help="e2e: row tiles in each block's first chunk (0 = --stream-tiles)")
+    ap.add_argument("--stream-last", type=int, default=0,
+                    help="e2e: row tiles in each block's last chunk (0 = --stream-tiles)")
     ap.add_argument("--stream-reuse", action="store_true",
                     help="e2e: do not re-upload chunks still staged from the previous epoch "
                          "(default: every epoch uploads all of its triples)")

@@ -450,9 +450,11 @@ class StreamingEpoch:
     chunk c (a ring of device staging buffers, ordered by CUDA events).
 
     Chunks are runs of `tiles_per_chunk` row tiles of each block
-    (data.bucket_qbands), the first one `first_chunk_tiles` long if set (a
-    short first upload before the first launch): chunk (b, c) holds block b's
-    triples of those tiles, item runs inside each.  One launch trains a chunk, walking its tiles as
+    (data.bucket_qbands), the last one `last_chunk_tiles` long if set: once
+    the copy engine has uploaded an epoch, only that short launch remains
+    (uploads are the bound: an epoch takes its upload time plus the training
+    of its last chunk).  Chunk (b, c) holds block b's triples of those tiles,
+    item runs inside each.  One launch trains a chunk, walking its tiles as
     the resident kernel walks a block's (each tile's P rows sit in L2 while
     its bins run); the epoch walks each block's chunks in a seeded rotation.
 
@@ -463,9 +465,9 @@ class StreamingEpoch:
     implicit items) or 12.
     """
 
-    def __init__(self, grid: DeviceGrid, k: int, tile_bytes=None, n_buffers: int = 2,
-                 elem_bytes: int = 4, compact: bool = True, tiles_per_chunk: int = 1,
-                 first_chunk_tiles: int = 0, reuse: bool = True):
+    def __init__(self, grid: DeviceGrid, k: int, tile_bytes=None, n_buffers: int = 3,
+                 elem_bytes: int = 4, compact: bool = True, tiles_per_chunk: int = 4,
+                 last_chunk_tiles: int = 0, reuse: bool = False):
         torch = _torch()
         self.dev = grid.device
         # a grid the caller already laid out for the Q-band kernel is used as is
@@ -486,7 +488,7 @@ class StreamingEpoch:
         # bucketed arrays, the number of tiles, their sub-band offsets relative
         # to lo, their first rows (device int32, uint16 ids only)
         self.tiles_per_chunk = max(1, int(tiles_per_chunk))
-        self.first_chunk_tiles = max(0, int(first_chunk_tiles))
+        self.last_chunk_tiles = max(0, int(last_chunk_tiles))
         self.blocks = []
         users = sg.users
         if self.u16:
@@ -495,9 +497,12 @@ class StreamingEpoch:
             sp = sg.sub_ptr[b].cpu().numpy()
             T = sg.sub_tiles[b]
             S = (len(sp) - 1) // T
-            cuts = [0] + ([min(T, self.first_chunk_tiles)] if self.first_chunk_tiles else [])
-            while cuts[-1] < T:
-                cuts.append(min(T, cuts[-1] + self.tiles_per_chunk))
+            head = T - self.last_chunk_tiles if 0 < self.last_chunk_tiles < T else T
+            cuts = [0]
+            while cuts[-1] < head:
+                cuts.append(min(head, cuts[-1] + self.tiles_per_chunk))
+            if head < T:
+                cuts.append(T)
             chunks = []
             for t0, t1 in zip(cuts, cuts[1:]):
                 lo, hi = int(sp[t0 * S]), int(sp[t1 * S])
@@ -560,13 +565,13 @@ class StreamingEpoch:
         order = []
         for b, (chunks, _) in enumerate(self.blocks):
             bseed = kernels.mix64(seed, b) & 0xFFFFFFFFFFFFFFFF
-            # a short first chunk (first_chunk_tiles) stays first: the
-            # pipeline starts after a short upload
-            h = 1 if self.first_chunk_tiles and len(chunks) > 1 else 0
-            n = len(chunks) - h
+            # a short last chunk (last_chunk_tiles) stays last: after the
+            # epoch's final upload only a short launch remains
+            t = 1 if self.last_chunk_tiles and len(chunks) > 1 else 0
+            n = len(chunks) - t
             rot = bseed % n if n else 0
-            order += [(b, c, bseed) for c in range(h)]
-            order += [(b, h + (i + rot) % n, bseed) for i in range(n)]
+            order += [(b, (i + rot) % n, bseed) for i in range(n)]
+            order += [(b, n + c, bseed) for c in range(t)]
         if self.reuse:
             resident = [ch for ch in reversed(self.lru) if ch is not None]
             head = [o for ch in resident for o in order if (o[0], o[1]) == ch]

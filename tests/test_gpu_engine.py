@@ -144,10 +144,10 @@ def test_throughput_sweep_reports_stages(dev):
         throughput_sweep("batch", [2, 1], batch_config=BatchWorkerConfig(device=dev))
 
 
-@pytest.mark.parametrize("k,impl,tiles,first", [(64, -1, 1, 0), (128, -1, 1, 0), (64, 0, 1, 0),
+@pytest.mark.parametrize("k,impl,tiles,last", [(64, -1, 1, 0), (128, -1, 1, 0), (64, 0, 1, 0),
                                                 (128, -1, 2, 0), (64, -1, 3, 0), (64, 0, 3, 0),
                                                 (128, -1, 2, 1), (64, 0, 3, 1)])
-def test_streaming_epoch_applies_every_triple_once(dev, k, impl, tiles, first):
+def test_streaming_epoch_applies_every_triple_once(dev, k, impl, tiles, last):
     """StreamingEpoch (triples streamed from pinned host memory in chunks of
     `tiles` row tiles, double buffered) on conflict-free triples equals the
     reference update of each triple exactly once."""
@@ -168,12 +168,13 @@ def test_streaming_epoch_applies_every_triple_once(dev, k, impl, tiles, first):
     _lib.check(_lib.load().hmf_qband_set_impl(impl), "set_impl")
     try:
         se = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1,   # 3 row tiles per block
-                            tiles_per_chunk=tiles, first_chunk_tiles=first)
+                            tiles_per_chunk=tiles, last_chunk_tiles=last, n_buffers=2,
+                            reuse=True)
         se_all = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1, tiles_per_chunk=tiles,
-                                first_chunk_tiles=first, reuse=False)
+                                last_chunk_tiles=last, reuse=False)
     finally:
         _lib.load().hmf_qband_set_impl(-1)
-    assert se.n_chunks == 2 * ((1 + -(-2 // tiles)) if first else -(-3 // tiles))
+    assert se.n_chunks == 2 * ((1 + -(-2 // tiles)) if last else -(-3 // tiles))
     P0 = rng.uniform(0, 0.1, size=(9000, k)).astype(np.float32)
     Q0 = rng.uniform(0, 0.1, size=(7000, k)).astype(np.float32)
     P, Q = torch.from_numpy(P0).to(d), torch.from_numpy(Q0).to(d)
