@@ -324,7 +324,8 @@ def run_ours(args, world, rank, local):
     torch.cuda.empty_cache()
     if args.kernel == "qband":
         bucket_qbands(grid, k, tile_bytes=tile_bytes, elem_bytes=2 if precision == "f16" else 4,
-                      impl=5 if args.split else None, split=args.split or None)
+                      impl=5 if args.split else None, split=args.split or None,
+                      max_tile_rows=args.tile_rows)
     stream_epoch = None
     if not args.no_e2e and args.kernel == "qband" and world == 1:
         # e2e streams the same layout from pinned host memory, tile by tile
@@ -721,6 +722,8 @@ def main():
                     help="Zipf exponent of item popularity (0 = the synthetic law's uniform cells)")
     ap.add_argument("--split", type=int, default=0,
                     help="implementation 5 with this many parts per item run (0 = default layout)")
+    ap.add_argument("--tile-rows", type=int, default=None,
+                    help="cap on users per row tile (default data.QBAND_MAX_TILE_ROWS; 0 = none)")
     ap.add_argument("--tile-mb", type=float, default=None,
                     help="P rows per Q-band row tile in MiB (default data.QBAND_TILE_BYTES; 0 = no tiling)")
     ap.add_argument("--sim-world", type=int, default=0,

@@ -483,17 +483,25 @@ def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int, cap: int | None = 
 # P rows per row tile of the Q-band kernel: one tile's P rows, the Q band and
 # the triple stream share the 126 MB L2 (sweep: profiles/r02_tile_sweep*).
 QBAND_TILE_BYTES = 32 << 20
+# rows per tile cap (None = by bytes only); 65536 keeps tile-relative user ids
+# in 16 bits for the streamed layout (workers.StreamingEpoch)
+QBAND_MAX_TILE_ROWS: int | None = None
 
 
 def qband_row_tiles(n_rows: int, k: int, elem_bytes: int = 4,
-                    tile_bytes: int | None = None) -> int:
+                    tile_bytes: int | None = None, max_rows: int | None = None) -> int:
     """Row tiles for a block spanning n_rows users: the fewest equal tiles
-    whose P rows (n_rows/T x k x elem_bytes) fit tile_bytes.  tile_bytes <= 0
-    disables tiling."""
+    whose P rows (n_rows/T x k x elem_bytes) fit tile_bytes and, when
+    max_rows is set (default QBAND_MAX_TILE_ROWS), hold at most max_rows
+    rows.  tile_bytes <= 0 disables the byte bound."""
     tb = QBAND_TILE_BYTES if tile_bytes is None else int(tile_bytes)
-    if tb <= 0 or n_rows <= 0:
+    mr = QBAND_MAX_TILE_ROWS if max_rows is None else int(max_rows)
+    if n_rows <= 0:
         return 1
-    return max(1, min(n_rows, -(-(n_rows * k * elem_bytes) // tb)))
+    t = 1 if tb <= 0 else -(-(n_rows * k * elem_bytes) // tb)
+    if mr and mr > 0:
+        t = max(t, -(-n_rows // mr))
+    return max(1, min(n_rows, t))
 
 
 def qband_split_for(slots: int, items: int, block_nnz: float, n_tiles: int, k: int = 128,
@@ -530,11 +538,12 @@ def qband_split_for(slots: int, items: int, block_nnz: float, n_tiles: int, k: i
 
 def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
                   tile_bytes: int | None = None, elem_bytes: int = 4,
-                  impl: int | None = None, split: int | None = None) -> DeviceGrid:
+                  impl: int | None = None, split: int | None = None,
+                  max_tile_rows: int | None = None) -> DeviceGrid:
     """Re-bucket every block of a device grid for the Q-band kernel, in place:
     row tile major, then item (both stable), and attach sub_ptr / sub_cuts /
     sub_tiles.  Row tiles are equal user ranges of the block's row band, sized
-    by qband_row_tiles (tile_bytes <= 0: one tile).  Sorting by item inside a
+    by qband_row_tiles (tile_bytes <= 0 and no row cap: one tile).  Sorting by item inside a
     tile makes every (tile, sub-band) range contiguous and lays each item's
     ratings out as one run, so the kernel keeps the current item's Q row in
     registers.  The order of ratings within an item is the block order
@@ -569,7 +578,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         split = 1 if target is not None else qband_split_for(
             resident_warps(dev, k, f16, 5), widest,
             float(np.mean(sizes[full])) if full else 0.0,
-            qband_row_tiles(rows, k, elem_bytes, tile_bytes), k, f16)
+            qband_row_tiles(rows, k, elem_bytes, tile_bytes, max_tile_rows), k, f16)
     split = 1 if impl != 5 or not split else int(split)
     if split > 1:
         target = widest          # one item per sub-band, then its parts
@@ -592,7 +601,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         lo, hi = grid.block_range(b)
         c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
         r_lo, r_hi = grid.row_span(b // grid.n_col_bands)
-        n_tiles = qband_row_tiles(r_hi - r_lo, k, elem_bytes, tile_bytes)
+        n_tiles = qband_row_tiles(r_hi - r_lo, k, elem_bytes, tile_bytes, max_tile_rows)
         tiles = np.linspace(r_lo, r_hi, n_tiles + 1).round().astype(np.int64)
         cuts = qband_sub_cuts(c_lo, c_hi, k, target, cap)
         parts = None             # parts per item (single-item sub-bands), device int64
