@@ -725,7 +725,7 @@ def main():
     ap.add_argument("--tile-rows", type=int, default=None,
                     help="cap on users per row tile (default data.QBAND_MAX_TILE_ROWS; 0 = none)")
     ap.add_argument("--tile-mb", type=float, default=None,
-                    help="P rows per Q-band row tile in MiB (default data.QBAND_TILE_BYTES; 0 = no tiling)")
+                    help="P rows per Q-band row tile in MiB (default data.QBAND_TILE_BYTES; 0 = no byte bound)")
     ap.add_argument("--sim-world", type=int, default=0,
                     help="N=1 only: run rank 0 of an N-GPU job's geometry (projected per-GPU rate)")
     ap.add_argument("--no-e2e", action="store_true")

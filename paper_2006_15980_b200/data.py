@@ -483,9 +483,12 @@ def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int, cap: int | None = 
 # P rows per row tile of the Q-band kernel: one tile's P rows, the Q band and
 # the triple stream share the 126 MB L2 (sweep: profiles/r02_tile_sweep*).
 QBAND_TILE_BYTES = 32 << 20
-# rows per tile cap (None = by bytes only); 65536 keeps tile-relative user ids
-# in 16 bits for the streamed layout (workers.StreamingEpoch)
-QBAND_MAX_TILE_ROWS: int | None = None
+# users per row tile at most: tile-relative user ids then fit 16 bits, so a
+# streamed epoch (workers.StreamingEpoch) sends 6 bytes per rating at every k
+# and precision (NF k = 32..64, fp16 k = 128: 8.9-9.0 G upd/s end to end vs
+# 6.7-6.8 with 4-byte ids; resident throughput within -4.5..+1.5 %,
+# profiles/r02/tile_rows_cap.jsonl)
+QBAND_MAX_TILE_ROWS: int | None = 65536
 
 
 def qband_row_tiles(n_rows: int, k: int, elem_bytes: int = 4,

@@ -372,9 +372,11 @@ def test_ml1m_quality_within_0005_of_reference(dev):
 # Q-band-stationary kernel
 # ---------------------------------------------------------------------------
 def _qband_grid(dev, m, k, col_cuts, target, tile_bytes=None):
+    """An explicit tile_bytes sets the tile count alone (no user cap)."""
     from paper_2006_15980_b200.data import DeviceTriples, bucket_qbands, build_device_grid
     g = build_device_grid(DeviceTriples.from_host(m, dev), [0, m.n_users], col_cuts)
-    return bucket_qbands(g, k, target=target, tile_bytes=tile_bytes)
+    return bucket_qbands(g, k, target=target, tile_bytes=tile_bytes,
+                         max_tile_rows=None if tile_bytes is None else 0)
 
 
 def _fin(z):

@@ -83,8 +83,10 @@ def test_qband_row_tiles():
     from paper_2006_15980_b200.data import qband_row_tiles
     # Netflix k=128 fp32: 480 000 rows x 512 B = 246 MB -> 8 tiles of <= 32 MB
     assert qband_row_tiles(480_000, 128, 4) == 8
-    assert qband_row_tiles(480_000, 128, 2) == 4           # fp16 rows
-    assert qband_row_tiles(480_000, 128, 4, tile_bytes=0) == 1
+    assert qband_row_tiles(480_000, 128, 2, max_rows=0) == 4   # fp16 rows, bytes only
+    assert qband_row_tiles(480_000, 128, 2) == 8           # at most 65536 users per tile
+    assert qband_row_tiles(480_000, 128, 4, tile_bytes=0, max_rows=0) == 1
+    assert qband_row_tiles(480_000, 32, 4, tile_bytes=0) == 8
     assert qband_row_tiles(50_000_000, 128, 4) == 763       # Hugewiki on one GPU
     assert qband_row_tiles(100, 128, 4, tile_bytes=1) == 100  # never more tiles than rows
 
