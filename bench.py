@@ -283,6 +283,7 @@ def run_ours(args, world, rank, local):
     if args.chain_lockstep is not None:
         _lib.check(_lib.load().hmf_qband_set_chain_lockstep(args.chain_lockstep),
                    "hmf_qband_set_chain_lockstep")
+    _lib.check(_lib.load().hmf_qband_set_pstore(args.pstore), "hmf_qband_set_pstore")
     dev = torch.device("cuda", local)
     n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
     k = args.k or k0
@@ -454,6 +455,9 @@ def run_ours(args, world, rank, local):
                        "chain_cfg": (args.chain_cfg if (getattr(grid, "sub_impl", None) or 0) >= 4
                                      else None),
                        "item_run_split": getattr(grid, "sub_split", None),
+                       "p_writeback": ({-1: "auto: stores for fp32 k>=128, else reductions",
+                                        0: "vector reductions", 1: "stores"}[args.pstore]
+                                       if (getattr(grid, "sub_impl", None) or 0) >= 4 else None),
                        "item_skew": args.item_skew or None,
                        "row_tiles": (list(grid.sub_tiles) if getattr(grid, "sub_tiles", None)
                                      else None),
@@ -706,6 +710,8 @@ def main():
     ap.add_argument("--chain-cfg", type=int, choices=list(range(-1, 7)), default=-1,
                     help="configuration of Q-band implementation 4 (qchain.cuh ChainCfg)")
     ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)
+    ap.add_argument("--pstore", type=int, choices=[-1, 0, 1], default=-1,
+                    help="chained kernel P write-back: -1 auto, 0 reductions, 1 stores")
     ap.add_argument("--stream-buffers", type=int, default=3,
                     help="e2e: device staging buffers (ring)")
     ap.add_argument("--stream-tiles", type=int, default=4,

@@ -62,6 +62,8 @@ SIGNATURES = {
     "hmf_qband_chain_lanes": (_i32, [_i64]),
     "hmf_qband_chain_lanes_for": (_i32, [_i64, _i32]),
     "hmf_qband_set_chain_lockstep": (C.c_int, [_i32]),
+    "hmf_qband_set_pstore": (C.c_int, [_i32]),
+    "hmf_qband_get_pstore": (_i32, []),
     "hmf_sgd_block_qband_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i32, _f64,
                                        _f64, _f64, _u64, _i64, _i64, _p]),
     "hmf_sgd_block_qband_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i32, _f64,

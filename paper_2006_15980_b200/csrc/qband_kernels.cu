@@ -935,6 +935,14 @@ int hmf_qband_set_chain_lockstep(int32_t bits) {
   return HMF_OK;
 }
 
+int hmf_qband_set_pstore(int32_t mode) {
+  if (mode < -1 || mode > 1) return int(hmf::set_error(HMF_ERR_ARG, "pstore must be -1..1"));
+  hmf::qs::g_chain_pstore = mode;
+  return HMF_OK;
+}
+
+int32_t hmf_qband_get_pstore(void) { return hmf::qs::g_chain_pstore; }
+
 int32_t hmf_qband_get_chain_cfg(void) { return hmf::qs::g_chain_cfg; }
 
 int hmf_qband_set_qsync(int32_t steps) {

@@ -155,7 +155,7 @@ __device__ inline void st_release_u32(unsigned* p, unsigned v) {
 // release/acquire, and load balance no longer depends on the number of
 // sub-bands being a multiple of the number of chains.
 template <int K, typename S, int LPC, int PD, int WPB, int MINB, bool DYN,
-          typename RowT = int32_t>
+          typename RowT = int32_t, bool PST = false>
 __global__ void __launch_bounds__(WPB * 32, MINB)
     qchain_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const RowT* __restrict__ rows,
                   const int32_t* __restrict__ cols, const float* __restrict__ vals,
@@ -344,13 +344,26 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     for (int o = LPC / 2; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
     if (act) {
       const float a = lr * (r - d);
+      if constexpr (PST) {
+        // the new row stored over the old, as the reference's racing lanes
+        // write it (workers.py:222-266): no read-modify-write at L2; a
+        // concurrent update of the same user by another chain may be lost
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const float pu = pc[e], qv = q[e];
-        pc[e] = fmaf(a, qv, -a_ru * pu);
-        q[e] = fmaf(a, pu, keep_q * qv);
+        for (int e = 0; e < E; ++e) {
+          const float pu = pc[e], qv = q[e];
+          pc[e] = pu + fmaf(a, qv, -a_ru * pu);
+          q[e] = fmaf(a, pu, keep_q * qv);
+        }
+        L::stg(Pb + int64_t(u) * K, l, pc);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const float pu = pc[e], qv = q[e];
+          pc[e] = fmaf(a, qv, -a_ru * pu);
+          q[e] = fmaf(a, pu, keep_q * qv);
+        }
+        L::red(Pb + int64_t(u) * K, l, pc);
       }
-      L::red(Pb + int64_t(u) * K, l, pc);
       if (j + 1 < cnt) {
         ++j;
       } else {
@@ -425,6 +438,19 @@ template <int K, typename S> static int chain_cfg() {
 // bin changes in warp lockstep: bit 0 for the static, bit 1 for the dynamic
 // scheduler
 static std::atomic<int> g_chain_lockstep{3};
+// P write-back: -1 automatic (plain stores of the updated row for fp32 rows
+// of k >= 128 in chain configurations 5 and 6, +19 % at NF k = 128 and 256,
+// profiles/r02/pstore.jsonl; vector reductions of the change otherwise),
+// 0 reductions, 1 stores where available (fp32, configurations 5 and 6)
+static std::atomic<int> g_chain_pstore{-1};
+template <int K, typename S, int CFG> static bool chain_pstore() {
+  if constexpr (sizeof(S) != 4 || (CFG != 5 && CFG != 6)) {
+    return false;
+  } else {
+    const int v = g_chain_pstore.load();
+    return v < 0 ? K >= 128 : v != 0;
+  }
+}
 
 template <int K, typename S, int CFG>
 static int chain_slots_per_sm_cfg() {
@@ -482,6 +508,12 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
   constexpr int NC = 32 / C::LPC;
   auto kstat = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false, RowT>;
   auto kdyn = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, true, RowT>;
+  if constexpr (sizeof(S) == 4 && (CFG == 5 || CFG == 6)) {
+    if (chain_pstore<K, S, CFG>()) {
+      kstat = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false, RowT, true>;
+      kdyn = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, true, RowT, true>;
+    }
+  }
   static int per_sm = 0;
   if (per_sm == 0) {
     const cudaError_t e =

@@ -699,7 +699,18 @@ def test_qband_split_runs_apply_every_rating(dev, n_tiles, k, dtype):
     chain on its own Q copy, changes added back by reductions.  At a small
     step SGD is linear in the ratings, so the factor changes must equal the
     sequential reference's to first order: every rating applied once, every
-    Q delta added once (nothing lost, nothing doubled)."""
+    Q delta added once (nothing lost, nothing doubled).  Users repeat here, so
+    P goes back by reductions (hmf_qband_set_pstore(0)): stores may drop a
+    concurrent update of the same user."""
+    from paper_2006_15980_b200 import _lib
+    _lib.check(_lib.load().hmf_qband_set_pstore(0), "set_pstore")
+    try:
+        _split_runs_apply_every_rating(dev, n_tiles, k, dtype)
+    finally:
+        _lib.load().hmf_qband_set_pstore(-1)
+
+
+def _split_runs_apply_every_rating(dev, n_tiles, k, dtype):
     from paper_2006_15980_b200 import kernels
     from paper_2006_15980_b200.data import RatingMatrix
     lr = 1e-4
@@ -732,6 +743,59 @@ def test_qband_split_runs_apply_every_rating(dev, n_tiles, k, dtype):
     # round these 1e-5 changes away: covered by the quality tests instead)
     assert rel_err(dQ, Qe - Q0) < 0.03
     assert rel_err(dP, Pe - P0) < 0.03
+
+
+def test_qband_pstore_conflict_free_equals_reductions_and_trains(dev):
+    """P write-back by stores (the automatic choice for fp32, k >= 128):
+    with distinct users per launch nothing can race, so stores and
+    reductions give the same factors; with repeated users (the racing case)
+    a few epochs still train to the reductions' test RMSE within 0.005."""
+    from paper_2006_15980_b200 import _lib, kernels
+    from paper_2006_15980_b200.data import RatingMatrix
+    lib = _lib.load()
+    k = 128
+    rng = np.random.default_rng(17)
+    n_users, n_items = 120_000, 700
+    # conflict-free: every user once
+    n = 90_000
+    users = rng.permutation(n_users)[:n].astype(np.int32)
+    items = rng.integers(0, n_items, n).astype(np.int32)
+    vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
+    m = RatingMatrix(n_users, n_items, users, items, vals)
+    g = _qband_grid(dev, m, k, [0, n_items], target=None)
+    P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
+    Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
+    out = {}
+    try:
+        for mode in (0, 1):
+            _lib.check(lib.hmf_qband_set_pstore(mode), "set_pstore")
+            P, Q = to_dev(P0, dev), to_dev(Q0, dev)
+            assert kernels.launch_block_qband(P, Q, g, 0, 0.05, 0.02, 0.03, 11) == n
+            out[mode] = (P.cpu().numpy(), Q.cpu().numpy())
+        assert np.allclose(out[0][0], out[1][0], rtol=1e-6, atol=1e-7)
+        assert np.allclose(out[0][1], out[1][1], rtol=1e-5, atol=1e-6)
+        # repeated users: held-out RMSE after 4 epochs, stores vs reductions
+        n = 600_000
+        users = rng.integers(0, n_users, n).astype(np.int32)
+        items = rng.integers(0, n_items, n).astype(np.int32)
+        a = rng.uniform(0, 0.5, size=(n_users, 8))
+        b = rng.uniform(0, 0.5, size=(n_items, 8))
+        vals = np.einsum("ij,ij->i", a[users], b[items]) + rng.normal(0, 0.1, n)
+        cut = n * 19 // 20
+        m = RatingMatrix(n_users, n_items, users[:cut], items[:cut], vals[:cut])
+        g = _qband_grid(dev, m, k, [0, n_items], target=None)
+        tu, ti, tv = users[cut:], items[cut:], vals[cut:]
+        rm = {}
+        for mode in (0, 1):
+            _lib.check(lib.hmf_qband_set_pstore(mode), "set_pstore")
+            P, Q = to_dev(P0, dev), to_dev(Q0, dev)
+            for e in range(4):
+                kernels.launch_block_qband(P, Q, g, 0, 0.01, 0.01, 0.01, 100 + e)
+            Ph, Qh = P.double().cpu().numpy(), Q.double().cpu().numpy()
+            rm[mode] = float(np.sqrt(np.mean((tv - np.einsum("ij,ij->i", Ph[tu], Qh[ti])) ** 2)))
+        assert np.isfinite(rm[1]) and abs(rm[1] - rm[0]) <= 0.005, rm
+    finally:
+        lib.hmf_qband_set_pstore(-1)
 
 
 def test_qband_split_runs_ml1m_quality(dev):
