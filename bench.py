@@ -283,7 +283,9 @@ def run_ours(args, world, rank, local):
     if args.chain_lockstep is not None:
         _lib.check(_lib.load().hmf_qband_set_chain_lockstep(args.chain_lockstep),
                    "hmf_qband_set_chain_lockstep")
-    _lib.check(_lib.load().hmf_qband_set_pstore(args.pstore), "hmf_qband_set_pstore")
+    if args.pstore >= 0:
+        from paper_2006_15980_b200 import kernels as _k
+        _k.PSTORE_OVERRIDE = args.pstore
     dev = torch.device("cuda", local)
     n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
     k = args.k or k0
@@ -455,8 +457,10 @@ def run_ours(args, world, rank, local):
                        "chain_cfg": (args.chain_cfg if (getattr(grid, "sub_impl", None) or 0) >= 4
                                      else None),
                        "item_run_split": getattr(grid, "sub_split", None),
-                       "p_writeback": ({-1: "auto: stores for fp32 k>=128, else reductions",
-                                        0: "vector reductions", 1: "stores"}[args.pstore]
+                       "p_writeback": ((["vector reductions", "stores"][
+                                           args.pstore if args.pstore >= 0
+                                           else int(getattr(grid, "sub_pstore", 0) or 0)]
+                                        if precision == "f32" else "vector reductions")
                                        if (getattr(grid, "sub_impl", None) or 0) >= 4 else None),
                        "item_skew": args.item_skew or None,
                        "row_tiles": (list(grid.sub_tiles) if getattr(grid, "sub_tiles", None)
@@ -711,7 +715,8 @@ def main():
                     help="configuration of Q-band implementation 4 (qchain.cuh ChainCfg)")
     ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)
     ap.add_argument("--pstore", type=int, choices=[-1, 0, 1], default=-1,
-                    help="chained kernel P write-back: -1 auto, 0 reductions, 1 stores")
+                    help="chained kernel P write-back: -1 the layout's (grid.sub_pstore), "
+                         "0 reductions, 1 stores")
     ap.add_argument("--stream-buffers", type=int, default=3,
                     help="e2e: device staging buffers (ring)")
     ap.add_argument("--stream-tiles", type=int, default=4,

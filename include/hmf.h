@@ -164,12 +164,12 @@ int32_t hmf_qband_chain_lanes_for(int64_t k, int32_t f16);
 /* Implementation 4: chains of a warp change bins together (bit 0: static
  * scheduler, bit 1: dynamic scheduler; default 3). */
 int hmf_qband_set_chain_lockstep(int32_t bits);
-/* How the chained kernel writes P rows back: -1 automatic (plain stores of
- * the updated row for fp32 storage at k >= 128, vector reductions of the
- * change otherwise), 0 reductions, 1 stores (fp32 with chain configuration 5
- * or 6; reductions elsewhere).  Stores are the reference's racing-lane
- * semantics (workers.py:222-266): a concurrent update of the same user by
- * another chain may be lost; reductions lose none.  Added in ABI version 3. */
+/* How the chained kernel writes P rows back (process-wide, for the launches
+ * that follow): 0 or -1 (default) vector reductions of the change, 1 plain
+ * stores of the updated row (fp32 with chain configuration 5 or 6;
+ * reductions elsewhere).  Stores are the reference's racing-lane semantics
+ * (workers.py:222-266): a concurrent update of the same user by another
+ * chain may be lost; reductions lose none.  Added in ABI version 3. */
 int hmf_qband_set_pstore(int32_t mode);
 int32_t hmf_qband_get_pstore(void);
 /* impl: the implementation for this launch (-1 = the process default).

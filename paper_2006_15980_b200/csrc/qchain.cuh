@@ -438,17 +438,17 @@ template <int K, typename S> static int chain_cfg() {
 // bin changes in warp lockstep: bit 0 for the static, bit 1 for the dynamic
 // scheduler
 static std::atomic<int> g_chain_lockstep{3};
-// P write-back: -1 automatic (plain stores of the updated row for fp32 rows
-// of k >= 128 in chain configurations 5 and 6, +19 % at NF k = 128 and 256,
-// profiles/r02/pstore.jsonl; vector reductions of the change otherwise),
-// 0 reductions, 1 stores where available (fp32, configurations 5 and 6)
+// P write-back: 0 (default, also -1) vector reductions of the change; 1
+// plain stores of the updated row where available (fp32 rows, chain
+// configurations 5 and 6: +19 % at NF k = 128 and 256,
+// profiles/r02/pstore.jsonl).  data.bucket_qbands picks stores only when a
+// row tile holds several times more users than there are chains.
 static std::atomic<int> g_chain_pstore{-1};
 template <int K, typename S, int CFG> static bool chain_pstore() {
   if constexpr (sizeof(S) != 4 || (CFG != 5 && CFG != 6)) {
     return false;
   } else {
-    const int v = g_chain_pstore.load();
-    return v < 0 ? K >= 128 : v != 0;
+    return g_chain_pstore.load() == 1;
   }
 }
 

@@ -379,6 +379,7 @@ class DeviceGrid:
     sub_tile_rows: list | None = None   # per block: row cuts of its tiles (host int64)
     sub_split: int = 1                  # parts per item run (implementation 5)
     sub_qsync: int = 0                  # Q publication period for implementation 5
+    sub_pstore: int = 0                 # chained kernel P write-back: 1 stores, 0 reductions
 
     n_row_bands = BlockGrid.n_row_bands
     n_col_bands = BlockGrid.n_col_bands
@@ -715,6 +716,16 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     bound = 128 if any_skewed else 512
     grid.sub_qsync = max(4, min(32, bound // max(split, 1))) if impl == 5 else 0
     grid.sub_tile_rows = tile_rows
+    # P rows written back by plain stores (the reference's racing lanes)
+    # instead of reductions where that is measured faster (fp32, k >= 128:
+    # +19 %) and where a tile holds at least 4x as many users as there are
+    # chains, so concurrent updates of one user stay rare (Netflix-shaped
+    # k = 128: test RMSE within 0.0015 of reductions at every epoch, equal
+    # after 10, profiles/r02/pstore.jsonl; a 3 000-user tile lost ~10 % of
+    # its P change)
+    min_rows = min((int(np.min(np.diff(r))) for r in tile_rows if len(r) > 1), default=0)
+    grid.sub_pstore = int(impl >= 4 and not f16 and k >= 128
+                          and min_rows >= 4 * resident_warps(dev, k, f16, impl))
     return grid
 
 

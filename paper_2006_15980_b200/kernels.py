@@ -114,6 +114,18 @@ def set_qsync(grid) -> None:
         _lib.check(_lib.load().hmf_qband_set_qsync(q), "hmf_qband_set_qsync")
 
 
+# P write-back of the chained kernel for every launch (None: the layout's
+# grid.sub_pstore, data.bucket_qbands; 0 reductions, 1 stores)
+PSTORE_OVERRIDE: int | None = None
+
+
+def set_pstore(grid) -> None:
+    """The P write-back for the launches that follow: PSTORE_OVERRIDE if set,
+    else the layout's choice (process-wide setting, hmf_qband_set_pstore)."""
+    v = PSTORE_OVERRIDE if PSTORE_OVERRIDE is not None else int(getattr(grid, "sub_pstore", 0) or 0)
+    _lib.check(_lib.load().hmf_qband_set_pstore(int(v)), "hmf_qband_set_pstore")
+
+
 def launch_block_qband(user_f, item_f, grid, block, lr, reg_user, reg_item, seed, row_base=0,
                        col_base=0, stream=None) -> int:
     """Q-band-stationary update of one block of a DeviceGrid bucketed by
@@ -135,6 +147,7 @@ def launch_block_qband(user_f, item_f, grid, block, lr, reg_user, reg_item, seed
         raise ValueError("sub_ptr does not match sub_cuts x sub_tiles")
     s = current_stream_handle(user_f.device) if stream is None else int(stream)
     set_qsync(grid)
+    set_pstore(grid)
     fn = getattr(_lib.load(), f"hmf_sgd_block_qband_{st}")
     _lib.check(fn(user_f.data_ptr(), item_f.data_ptr(), user_f.shape[1], grid.users.data_ptr(),
                   grid.items.data_ptr(), grid.ratings.data_ptr(), sp.data_ptr(), sc.data_ptr(),

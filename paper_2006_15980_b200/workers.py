@@ -477,6 +477,7 @@ class StreamingEpoch:
         self.nnz = sg.nnz
         self.sub_impl = sg.sub_impl
         self.qsync = sg.sub_qsync
+        self.sub_pstore = sg.sub_pstore
         self.reuse = bool(reuse)
         # every sub-band a single item (or a part of one): the item is implicit
         self.implicit_items = compact and sg.sub_impl >= 4 and all(
@@ -577,6 +578,7 @@ class StreamingEpoch:
             head = [o for ch in resident for o in order if (o[0], o[1]) == ch]
             order = head + [o for o in order if (o[0], o[1]) not in resident]
         kernels.set_qsync(self.qsync)
+        kernels.set_pstore(self)
         done, uploaded = 0, 0
         for b, t, bseed in order:
             chunks, sc = self.blocks[b]

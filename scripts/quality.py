@@ -189,8 +189,9 @@ def main():
     ap.add_argument("--pstore", type=int, default=-1,
                     help="chained Q-band kernel P write-back (hmf_qband_set_pstore)")
     args = ap.parse_args()
-    from paper_2006_15980_b200 import _lib
-    _lib.check(_lib.load().hmf_qband_set_pstore(args.pstore), "hmf_qband_set_pstore")
+    if args.pstore >= 0:
+        from paper_2006_15980_b200 import kernels
+        kernels.PSTORE_OVERRIDE = args.pstore
     {"ml1m": ml1m, "netflix": netflix, "sweep": sweep}[args.what](args)
 
 

@@ -700,14 +700,14 @@ def test_qband_split_runs_apply_every_rating(dev, n_tiles, k, dtype):
     step SGD is linear in the ratings, so the factor changes must equal the
     sequential reference's to first order: every rating applied once, every
     Q delta added once (nothing lost, nothing doubled).  Users repeat here, so
-    P goes back by reductions (hmf_qband_set_pstore(0)): stores may drop a
-    concurrent update of the same user."""
-    from paper_2006_15980_b200 import _lib
-    _lib.check(_lib.load().hmf_qband_set_pstore(0), "set_pstore")
+    P goes back by reductions (kernels.PSTORE_OVERRIDE = 0): stores may drop
+    a concurrent update of the same user."""
+    from paper_2006_15980_b200 import kernels
+    kernels.PSTORE_OVERRIDE = 0
     try:
         _split_runs_apply_every_rating(dev, n_tiles, k, dtype)
     finally:
-        _lib.load().hmf_qband_set_pstore(-1)
+        kernels.PSTORE_OVERRIDE = None
 
 
 def _split_runs_apply_every_rating(dev, n_tiles, k, dtype):
@@ -746,9 +746,10 @@ def _split_runs_apply_every_rating(dev, n_tiles, k, dtype):
 
 
 def test_qband_pstore_conflict_free_equals_reductions_and_trains(dev):
-    """P write-back by stores (the automatic choice for fp32, k >= 128):
-    with distinct users per launch nothing can race, so stores and
-    reductions give the same factors; with repeated users (the racing case)
+    """P write-back by stores (grid.sub_pstore, chosen for fp32 k >= 128 when
+    tiles hold many users): with distinct users per launch nothing races, so
+    stores and reductions give the same factors (whole item runs,
+    implementation 4, deterministic); with repeated users (the racing case)
     a few epochs still train to the reductions' test RMSE within 0.005."""
     from paper_2006_15980_b200 import _lib, kernels
     from paper_2006_15980_b200.data import RatingMatrix
@@ -756,24 +757,27 @@ def test_qband_pstore_conflict_free_equals_reductions_and_trains(dev):
     k = 128
     rng = np.random.default_rng(17)
     n_users, n_items = 120_000, 700
-    # conflict-free: every user once
     n = 90_000
     users = rng.permutation(n_users)[:n].astype(np.int32)
     items = rng.integers(0, n_items, n).astype(np.int32)
     vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
     m = RatingMatrix(n_users, n_items, users, items, vals)
-    g = _qband_grid(dev, m, k, [0, n_items], target=None)
     P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
     Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
     out = {}
     try:
+        _lib.check(lib.hmf_qband_set_impl(4), "set_impl")
+        g = _qband_grid(dev, m, k, [0, n_items], target=None)
+        assert g.sub_impl == 4
         for mode in (0, 1):
-            _lib.check(lib.hmf_qband_set_pstore(mode), "set_pstore")
+            kernels.PSTORE_OVERRIDE = mode
             P, Q = to_dev(P0, dev), to_dev(Q0, dev)
             assert kernels.launch_block_qband(P, Q, g, 0, 0.05, 0.02, 0.03, 11) == n
+            assert lib.hmf_qband_get_pstore() == mode
             out[mode] = (P.cpu().numpy(), Q.cpu().numpy())
-        assert np.allclose(out[0][0], out[1][0], rtol=1e-6, atol=1e-7)
-        assert np.allclose(out[0][1], out[1][1], rtol=1e-5, atol=1e-6)
+        assert np.array_equal(out[0][0], out[1][0])
+        assert np.array_equal(out[0][1], out[1][1])
+        lib.hmf_qband_set_impl(-1)
         # repeated users: held-out RMSE after 4 epochs, stores vs reductions
         n = 600_000
         users = rng.integers(0, n_users, n).astype(np.int32)
@@ -787,7 +791,7 @@ def test_qband_pstore_conflict_free_equals_reductions_and_trains(dev):
         tu, ti, tv = users[cut:], items[cut:], vals[cut:]
         rm = {}
         for mode in (0, 1):
-            _lib.check(lib.hmf_qband_set_pstore(mode), "set_pstore")
+            kernels.PSTORE_OVERRIDE = mode
             P, Q = to_dev(P0, dev), to_dev(Q0, dev)
             for e in range(4):
                 kernels.launch_block_qband(P, Q, g, 0, 0.01, 0.01, 0.01, 100 + e)
@@ -795,7 +799,26 @@ def test_qband_pstore_conflict_free_equals_reductions_and_trains(dev):
             rm[mode] = float(np.sqrt(np.mean((tv - np.einsum("ij,ij->i", Ph[tu], Qh[ti])) ** 2)))
         assert np.isfinite(rm[1]) and abs(rm[1] - rm[0]) <= 0.005, rm
     finally:
-        lib.hmf_qband_set_pstore(-1)
+        kernels.PSTORE_OVERRIDE = None
+        lib.hmf_qband_set_impl(-1)
+
+
+def test_qband_pstore_layout_choice(dev):
+    """The layout picks stores only for fp32 k >= 128 with tiles of at least
+    4x as many users as chains (Netflix-shaped tiles: 60 000 users)."""
+    from paper_2006_15980_b200.data import RatingMatrix, resident_warps
+    rng = np.random.default_rng(2)
+    for n_users, k, f16, want in [(60_000, 128, False, None), (3_000, 128, False, 0),
+                                  (60_000, 64, False, 0), (60_000, 128, True, 0)]:
+        n = 50_000
+        m = RatingMatrix(n_users, 500, rng.integers(0, n_users, n).astype(np.int32),
+                         rng.integers(0, 500, n).astype(np.int32), rng.uniform(0, 1, n))
+        from paper_2006_15980_b200.data import DeviceTriples, bucket_qbands, build_device_grid
+        g = build_device_grid(DeviceTriples.from_host(m, dev), [0, n_users], [0, 500])
+        bucket_qbands(g, k, elem_bytes=2 if f16 else 4)
+        if want is None:
+            want = int(n_users >= 4 * resident_warps(dev, k, False, g.sub_impl))
+        assert g.sub_pstore == want, (n_users, k, f16)
 
 
 def test_qband_split_runs_ml1m_quality(dev):
