@@ -64,17 +64,19 @@ def measured_peak():
     return 6650.0, "fallback"
 
 
-def l2_ceiling(k: int, precision: str):
+def l2_ceiling(k: int, precision: str, stores: bool = False):
     """The measured ceiling of the dominant kernel's memory pattern once the
     P tile sits in L2: one random k-row load plus one vector reduction into it
-    per update, no arithmetic (scripts/l2_rowbench.cu on a B200, 32 MB
-    buffer; profiles/r02/l2_rowbench.jsonl).  Best rows/s over prefetch
-    depths and lane layouts; None when that row size was not measured."""
+    (or, with P written back by stores, one store of it) per update, no
+    arithmetic (scripts/l2_rowbench.cu on a B200, 32 MB buffer;
+    profiles/r02/l2_rowbench.jsonl).  Best rows/s over prefetch depths and
+    lane layouts; None when that row size was not measured."""
     p = ROOT / "profiles" / "r02" / "l2_rowbench.jsonl"
     if not p.exists():
         return None
     row = k * (2 if precision == "f16" else 4)
-    mode = "load+red_f16x2" if precision == "f16" else "load+red"
+    mode = ("load+red_f16x2" if precision == "f16"
+            else "load+store" if stores else "load+red")
     best, buf = None, None
     for line in p.read_text().splitlines():
         try:
@@ -394,7 +396,10 @@ def run_ours(args, world, rank, local):
     bpu = bytes_per_update(k, precision)
     achieved = mean_updates * bpu / (mean_ms / 1e3) / 1e9
     peak, peak_kind = measured_peak()
-    l2_rows = l2_ceiling(k, precision)
+    p_stores = (precision == "f32" and args.kernel == "qband"
+                and (getattr(grid, "sub_impl", None) or 0) >= 4
+                and (args.pstore == 1 or (args.pstore < 0 and getattr(grid, "sub_pstore", 0))))
+    l2_rows = l2_ceiling(k, precision, bool(p_stores))
     kernel_ups = mean_updates / (mean_ms / 1e3)
     traffic = None
     prof = ROOT / "profiles" / "traffic.json"
@@ -471,8 +476,9 @@ def run_ours(args, world, rank, local):
                          "l2_ceiling": (None if l2_rows is None else {
                              "updates_per_s": l2_rows, "kernel_updates_per_s": kernel_ups,
                              "frac": kernel_ups / l2_rows,
-                             "source": "scripts/l2_rowbench.cu: random P-row load + vector "
-                                       "reduction, L2-resident 32 MB, no arithmetic "
+                             "source": "scripts/l2_rowbench.cu: random P-row load + "
+                                       + ("store" if p_stores else "vector reduction")
+                                       + ", L2-resident 32 MB, no arithmetic "
                                        "(profiles/r02/l2_rowbench.jsonl)"}),
                          "peak_kind": peak_kind, "bytes_per_update": bpu,
                          "kernel": ("qband_kernel" if args.kernel == "qband"

@@ -18,7 +18,8 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 }
 
 // MODE 0 = load, 1 = red, 2 = load + red of the loaded values' negation,
-// 3 = f16x2 red, 4 = load + f16x2 red.
+// 3 = f16x2 red, 4 = load + f16x2 red, 5 = store, 6 = load + store of the
+// loaded values scaled (the P write-back by plain stores).
 // LPR lanes per row; lane l of a row group moves NV = ROWB/(16*LPR) 16-byte
 // vectors at byte offsets (v*LPR + l)*16 (the chain layout of qchain.cuh).
 template <int MODE, int ROWB, int DEPTH, int LPR>
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(512, 1) rowbench(float* buf, uint32_t n_rows, 
       const float4* p = reinterpret_cast<const float4*>(buf + size_t(r[d]) * (ROWB / 4));
 #pragma unroll
       for (int w = 0; w < NV; ++w)
-        if (MODE != 1 && MODE != 3) v[d][w] = __ldcg(p + w * LPR + l);
+        if (MODE != 1 && MODE != 3 && MODE != 5) v[d][w] = __ldcg(p + w * LPR + l);
     }
 #pragma unroll
     for (int d = 0; d < DEPTH; ++d) {
@@ -47,6 +48,10 @@ __global__ void __launch_bounds__(512, 1) rowbench(float* buf, uint32_t n_rows, 
         float* p = buf + size_t(r[d]) * (ROWB / 4) + 4 * (w * LPR + l);
         if (MODE == 0) {
           acc += v[d][w].x + v[d][w].y + v[d][w].z + v[d][w].w;
+        } else if (MODE >= 5) {
+          float4 o = MODE == 6 ? v[d][w] : make_float4(1e-30f, 1e-30f, 1e-30f, 1e-30f);
+          if (MODE == 6) { o.x *= 0.999f; o.y *= 0.999f; o.z *= 0.999f; o.w *= 0.999f; }
+          __stcg(reinterpret_cast<float4*>(p), o);
         } else if (MODE >= 3) {  // fp16 rows: 8 halves per 16-byte vector
           const unsigned a = MODE == 4 ? (__float_as_uint(v[d][w].x) & 0x00010001u) : 0x00010001u;
           asm volatile("red.global.add.noftz.v4.f16x2 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a),
@@ -144,7 +149,7 @@ static void run(float* buf, uint32_t n_rows, float* sink, int sms) {
   printf("{\"mode\": \"%s\", \"row_bytes\": %d, \"depth\": %d, \"lanes_per_row\": %d, "
          "\"rows_per_s\": %.4g, \"GBps_rowbytes\": %.1f}\n",
          MODE == 0 ? "load" : MODE == 1 ? "red" : MODE == 2 ? "load+red" : MODE == 3 ? "red_f16x2"
-                                                                                : "load+red_f16x2",
+                         : MODE == 4 ? "load+red_f16x2" : MODE == 5 ? "store" : "load+store",
          ROWB, DEPTH, LPR, rows / (ms * 1e-3),
          rows * ROWB / (ms * 1e-3) / 1e9);
 }
@@ -181,6 +186,14 @@ int main(int argc, char** argv) {
   run<2, 256, 16, 8>(buf, uint32_t((mb << 20) / 256), sink, sms);
   run<4, 256, 16, 8>(buf, uint32_t((mb << 20) / 256), sink, sms);
   run<2, 1024, 8, 8>(buf, uint32_t((mb << 20) / 1024), sink, sms);
+  // plain stores, alone and after the load (P write-back by stores)
+  run<5, 512, 4, 8>(buf, uint32_t((mb << 20) / 512), sink, sms);
+  run<6, 512, 4, 8>(buf, uint32_t((mb << 20) / 512), sink, sms);
+  run<6, 512, 8, 8>(buf, uint32_t((mb << 20) / 512), sink, sms);
+  run<6, 1024, 4, 8>(buf, uint32_t((mb << 20) / 1024), sink, sms);
+  run<6, 1024, 8, 8>(buf, uint32_t((mb << 20) / 1024), sink, sms);
+  run<6, 256, 4, 8>(buf, uint32_t((mb << 20) / 256), sink, sms);
+  run<6, 256, 8, 8>(buf, uint32_t((mb << 20) / 256), sink, sms);
   // TMA bulk reductions
   run_bulk<512, 4, false>(buf, uint32_t((mb << 20) / 512), sink, sms);
   run_bulk<512, 8, false>(buf, uint32_t((mb << 20) / 512), sink, sms);
