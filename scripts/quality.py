@@ -71,7 +71,7 @@ def netflix(args):
                                             synthetic_device, RatingMatrix)
     from paper_2006_15980_b200.sgd import DeviceModel, FactorModel, rmse
     dev = torch.device("cuda", 0)
-    n_users, n_items, n_train, k = 480_000, 17_700, args.nnz, 128
+    n_users, n_items, n_train, k = 480_000, 17_700, args.nnz, args.k
     lr, reg = 0.005, 0.05
     trip = synthetic_device(n_users, n_items, int(round(n_train / 0.95)), seed=0, device=dev)
     train, test = split_device(trip, 0.05)
