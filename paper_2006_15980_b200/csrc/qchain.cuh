@@ -439,12 +439,13 @@ template <int K, typename S> static int chain_cfg() {
 // scheduler
 static std::atomic<int> g_chain_lockstep{3};
 // P write-back: 0 (default, also -1) vector reductions of the change; 1
-// plain stores of the updated row where available (chain configurations 4,
-// 5 and 6: +19 % at NF k = 128 and 256 fp32, profiles/r02/pstore.jsonl).  data.bucket_qbands picks stores only when a
+// plain stores of the updated row where available (fp32 rows, chain
+// configurations 5 and 6: +19 % at NF k = 128 and 256, +4 % at k = 64;
+// fp16 rows and k = 32 were slower with stores, profiles/r02/pstore*.jsonl).  data.bucket_qbands picks stores only when a
 // row tile holds several times more users than there are chains.
 static std::atomic<int> g_chain_pstore{-1};
 template <int K, typename S, int CFG> static bool chain_pstore() {
-  if constexpr (CFG < 4) {
+  if constexpr (sizeof(S) != 4 || (CFG != 5 && CFG != 6)) {
     return false;
   } else {
     return g_chain_pstore.load() == 1;
@@ -507,7 +508,7 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
   constexpr int NC = 32 / C::LPC;
   auto kstat = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false, RowT>;
   auto kdyn = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, true, RowT>;
-  if constexpr (CFG >= 4) {
+  if constexpr (sizeof(S) == 4 && (CFG == 5 || CFG == 6)) {
     if (chain_pstore<K, S, CFG>()) {
       kstat = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false, RowT, true>;
       kdyn = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, true, RowT, true>;
