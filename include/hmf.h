@@ -188,7 +188,7 @@ int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                 double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
                                 void* stream);
 
-/* The chained kernel (implementation 4 or 5, chain configuration 5 or 6) with
+/* The chained kernel (implementation 4 or 5, chain configuration 2, 4, 5 or 6) with
  * uint16 row ids: row = rows[i] - row_base, so a row tile of at most 65536
  * rows streams 2-byte ids with row_base = -(the tile's first row).  Same
  * arguments and contract as hmf_sgd_block_qband_*. */

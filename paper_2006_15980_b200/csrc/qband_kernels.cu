@@ -843,8 +843,8 @@ static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_
     return set_error(HMF_ERR_ARG, "factor arrays must be 16-byte aligned");
   const int set = g_chain_cfg.load();
   const int cfg = set >= 0 ? set : auto_chain_cfg(int(k), sizeof(S) == 2);
-  if (cfg < 4 || cfg > 6)
-    return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need chain configuration 4, 5 or 6");
+  if (cfg != 2 && (cfg < 4 || cfg > 6))
+    return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need chain configuration 2, 4, 5 or 6");
   const int impl = resolve_impl(impl_req, k, sizeof(S) == 2);
   if (impl < 4)
     return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need implementation 4, 5 or 6");

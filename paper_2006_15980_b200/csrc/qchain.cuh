@@ -420,15 +420,17 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
 // at item and bin changes)
 static std::atomic<int> g_qsync_steps{32};
 
-// -1 = automatic (measured, profiles/r02/chain_cfg_by_k.jsonl): k = 32
-// 4 lanes per chain, 4 steps ahead (cfg 4; 28.8 / 33.6 G upd/s fp32 / fp16
-// vs 20.6 / 23.4 with 8 lanes); k = 64 fp32 8 lanes 4 ahead (cfg 6), fp16 4
-// lanes 4 ahead (cfg 4); k >= 128: 8 lanes (16 at k = 256), 2 ahead in fp32
-// (cfg 5, the register budget), 4 ahead in fp16 (cfg 6, raw fp16 slots).
+// -1 = automatic (measured on tiles of at most 65 536 users,
+// profiles/r02/small_k_cfg.jsonl, chain_cfg_by_k.jsonl): k = 32 4 lanes per
+// chain, 3 steps ahead, 24 warps per SM (cfg 2; 30.6 / 41.9 G upd/s fp32 /
+// fp16 vs 28.1 / 32.0 with 16 warps, cfg 4); k = 64 fp32 8 lanes, 3 ahead,
+// 24 warps (cfg 2; 19.7 vs 18.5), fp16 4 lanes 4 ahead (cfg 4); k >= 128:
+// 8 lanes (16 at k = 256), 2 ahead in fp32 (cfg 5, the register budget), 4
+// ahead in fp16 (cfg 6, raw fp16 slots).
 static std::atomic<int> g_chain_cfg{-1};
 static inline int auto_chain_cfg(int k, bool f16) {
-  if (k <= 32) return 4;
-  if (k <= 64) return f16 ? 4 : 6;
+  if (k <= 32) return 2;
+  if (k <= 64) return f16 ? 4 : 2;
   return f16 ? 6 : 5;
 }
 template <int K, typename S> static int chain_cfg() {
@@ -549,7 +551,7 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
 }
 
 // rows: int32 row ids, or uint16 (a row tile's ids relative to its first row:
-// 2 bytes per rating on the host stream; configurations 4, 5 and 6 only).
+// 2 bytes per rating on the host stream; configurations 2, 4, 5 and 6 only).
 // The tile's first row is tile_row0[tile] (device, n_tiles entries) or, with
 // tile_row0 == nullptr, -row_base for every tile.
 template <int K, typename S, typename RowT = int32_t>
@@ -565,6 +567,7 @@ static cudaError_t launch_chain(S* P, S* Q, const RowT* rows, const int32_t* col
                                            col_base, stream, qdelta)
   if constexpr (sizeof(RowT) == 2) {
     switch (chain_cfg<K, S>()) {
+      case 2: HMF_CHAIN_CFG(2);
       case 4: HMF_CHAIN_CFG(4);
       case 5: HMF_CHAIN_CFG(5);
       case 6: HMF_CHAIN_CFG(6);

@@ -482,7 +482,7 @@ class StreamingEpoch:
         # every sub-band a single item (or a part of one): the item is implicit
         self.implicit_items = compact and sg.sub_impl >= 4 and all(
             bool(torch.all(c[1:] - c[:-1] <= 1)) for c in sg.sub_cuts)
-        cfg_ok = int(_lib.load().hmf_qband_get_chain_cfg()) in (-1, 4, 5, 6)
+        cfg_ok = int(_lib.load().hmf_qband_get_chain_cfg()) in (-1, 2, 4, 5, 6)
         self.u16 = self.implicit_items and cfg_ok and all(
             int(np.max(np.diff(r))) <= 65536 for r in sg.sub_tile_rows)
         # chunks: G consecutive row tiles of a block -> [lo, hi) of the
