@@ -440,6 +440,20 @@ class BatchWorker(threading.Thread):
                     self.engine.close()
 
 
+def chunk_cuts(n_tiles: int, tiles_per_chunk: int, last_chunk_tiles: int = 0) -> list:
+    """Tile cuts of a block's streamed chunks: runs of tiles_per_chunk tiles,
+    the last chunk last_chunk_tiles long when 0 < last_chunk_tiles < n_tiles
+    (e.g. 8 tiles, 4 per chunk, last 1 -> [0, 4, 7, 8])."""
+    g = max(1, int(tiles_per_chunk))
+    head = n_tiles - last_chunk_tiles if 0 < last_chunk_tiles < n_tiles else n_tiles
+    cuts = [0]
+    while cuts[-1] < head:
+        cuts.append(min(head, cuts[-1] + g))
+    if head < n_tiles:
+        cuts.append(n_tiles)
+    return cuts
+
+
 class StreamingEpoch:
     """Epochs whose rating triples stream from pinned host memory.
 
@@ -498,12 +512,7 @@ class StreamingEpoch:
             sp = sg.sub_ptr[b].cpu().numpy()
             T = sg.sub_tiles[b]
             S = (len(sp) - 1) // T
-            head = T - self.last_chunk_tiles if 0 < self.last_chunk_tiles < T else T
-            cuts = [0]
-            while cuts[-1] < head:
-                cuts.append(min(head, cuts[-1] + self.tiles_per_chunk))
-            if head < T:
-                cuts.append(T)
+            cuts = chunk_cuts(T, self.tiles_per_chunk, self.last_chunk_tiles)
             chunks = []
             for t0, t1 in zip(cuts, cuts[1:]):
                 lo, hi = int(sp[t0 * S]), int(sp[t1 * S])

@@ -115,3 +115,17 @@ def test_bench_l2_ceiling_lookup():
     assert f16 is not None and f16 > 1.5 * f32           # 256-byte rows
     assert bench.bytes_per_update(128, "f32") == 2060
     assert bench.bytes_per_update(128, "f16") == 12 + 8 * 128
+    st = bench.l2_ceiling(128, "f32", stores=True)
+    assert st is not None and st > f32                   # load + store beats load + reduction
+
+
+def test_stream_chunk_cuts():
+    """workers.chunk_cuts: runs of tiles per chunk, an optional short last chunk."""
+    from paper_2006_15980_b200.workers import chunk_cuts
+    assert chunk_cuts(8, 4) == [0, 4, 8]
+    assert chunk_cuts(8, 4, 1) == [0, 4, 7, 8]
+    assert chunk_cuts(8, 3) == [0, 3, 6, 8]
+    assert chunk_cuts(3, 1) == [0, 1, 2, 3]
+    assert chunk_cuts(3, 2, 1) == [0, 2, 3]
+    assert chunk_cuts(1, 4, 1) == [0, 1]                 # one tile: no separate last chunk
+    assert chunk_cuts(15, 4) == [0, 4, 8, 12, 15]
