@@ -281,7 +281,8 @@ def run_ours(args, world, rank, local):
     _lib.check(_lib.load().hmf_qband_set_impl(args.qband_impl), "hmf_qband_set_impl")
     _lib.check(_lib.load().hmf_qband_set_chain_cfg(args.chain_cfg), "hmf_qband_set_chain_cfg")
     if args.qsync is not None:
-        _lib.check(_lib.load().hmf_qband_set_qsync(args.qsync), "hmf_qband_set_qsync")
+        from paper_2006_15980_b200 import kernels as _kq
+        _kq.QSYNC_OVERRIDE = args.qsync
     if args.chain_lockstep is not None:
         _lib.check(_lib.load().hmf_qband_set_chain_lockstep(args.chain_lockstep),
                    "hmf_qband_set_chain_lockstep")

@@ -105,11 +105,17 @@ def launch_sgd_range(user_f, item_f, rows, cols, vals, start, stop, lr, reg_user
     return _lib.check(got, f"hmf_sgd_range_{st}")
 
 
+# Q publication period for every launch (None: the layout's grid.sub_qsync)
+QSYNC_OVERRIDE: int | None = None
+
+
 def set_qsync(grid) -> None:
     """The layout's Q publication period (data.bucket_qbands; a grid or the
-    period itself) for the launches that follow (process-wide setting,
-    hmf_qband_set_qsync)."""
+    period itself), or QSYNC_OVERRIDE if set, for the launches that follow
+    (process-wide setting, hmf_qband_set_qsync)."""
     q = int(grid if isinstance(grid, int) else (getattr(grid, "sub_qsync", 0) or 0))
+    if QSYNC_OVERRIDE is not None:
+        q = int(QSYNC_OVERRIDE)
     if q > 0:
         _lib.check(_lib.load().hmf_qband_set_qsync(q), "hmf_qband_set_qsync")
 
