@@ -201,3 +201,49 @@ def test_streaming_epoch_applies_every_triple_once(dev, k, impl, tiles, last):
     for e in range(2):
         assert se_all.run(P, Q, hp, seed=3 + e) == n
         assert se_all.h2d_bytes_last() == se_all.h2d_bytes
+
+
+def test_u16_single_tile_entry_equals_tiles_entry(dev):
+    """hmf_sgd_block_qband_u16_* (one tile, row_base = -first row) and
+    hmf_sgd_block_qband_u16_tiles_* (first rows per tile) update the same
+    rows the same way: whole item runs (implementation 4), distinct users."""
+    from paper_2006_15980_b200 import _lib
+    from paper_2006_15980_b200.data import DeviceTriples, RatingMatrix, bucket_qbands, build_device_grid
+    lib = _lib.load()
+    rng = np.random.default_rng(8)
+    n_users, n_items, k = 50_000, 300, 64
+    n = 20_000
+    users = (10_000 + rng.permutation(40_000)[:n]).astype(np.int32)   # one tile: rows 10000..49999
+    items = rng.integers(0, n_items, n).astype(np.int32)
+    vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
+    d = torch.device("cuda", dev) if isinstance(dev, int) else dev
+    m = RatingMatrix(n_users, n_items, users, items, vals)
+    g = build_device_grid(DeviceTriples.from_host(m, d), [0, n_users], [0, n_items])
+    _lib.check(lib.hmf_qband_set_impl(4), "set_impl")
+    try:
+        bucket_qbands(g, k, tile_bytes=0, target=n_items)
+        assert g.sub_tiles == [1] and g.sub_impl == 4
+        sc, sp = g.sub_cuts[0], g.sub_ptr[0]
+        assert bool(torch.all(sc[1:] - sc[:-1] == 1))      # one item per sub-band: cols = NULL
+        rel16 = (g.users - 10_000).to(torch.int32).to(torch.int16)
+        first = torch.tensor([10_000], dtype=torch.int32, device=d)
+        P0 = rng.uniform(0, 0.1, size=(n_users, k)).astype(np.float32)
+        Q0 = rng.uniform(0, 0.1, size=(n_items, k)).astype(np.float32)
+        out = []
+        for tiles in (False, True):
+            P, Q = torch.from_numpy(P0).to(d), torch.from_numpy(Q0).to(d)
+            s = torch.cuda.current_stream(d).cuda_stream
+            head = (P.data_ptr(), Q.data_ptr(), k, rel16.data_ptr(), 0, g.ratings.data_ptr(),
+                    sp.data_ptr(), sc.data_ptr(), int(sc.numel()) - 1, 1)
+            if tiles:
+                got = lib.hmf_sgd_block_qband_u16_tiles_f32(*head, first.data_ptr(), 4, 0.05, 0.02,
+                                                             0.03, 5, 0, s)
+            else:
+                got = lib.hmf_sgd_block_qband_u16_f32(*head, 4, 0.05, 0.02, 0.03, 5, -10_000, 0, s)
+            _lib.check(got, "u16 entry")
+            torch.cuda.synchronize(d)
+            out.append((P.cpu().numpy(), Q.cpu().numpy()))
+        assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+        assert not np.array_equal(out[0][0], P0)
+    finally:
+        lib.hmf_qband_set_impl(-1)
