@@ -547,6 +547,7 @@ def run_ours_multi(args, world, rank, local):
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     upd0 = trainer.total_updates
+    blocks0 = int(trainer.counts.sum())
     with ClockSampler(local) as clocks:
         e0.record(band.stream)
         for _ in range(args.steps):
@@ -556,6 +557,8 @@ def run_ours_multi(args, world, rank, local):
         torch.cuda.synchronize(dev)
     ms = max_over_ranks(e0.elapsed_time(e1), world)
     updates = sum_over_ranks(float(trainer.total_updates - upd0), world)
+    # one kernel launch per granted block (CudaRowBand.compute)
+    launches = int(sum_over_ranks(float(int(trainer.counts.sum()) - blocks0), world))
     band.refresh_q(table)
     sums = residual_sums(DeviceModel(band.P, band.Q), test.users, test.items, test.ratings,
                          row_base=row_lo).to(_reduce_device())
@@ -583,7 +586,7 @@ def run_ours_multi(args, world, rank, local):
             "rmse": {"epochs": args.warmup + args.steps,
                      "test": float(np.sqrt(sums[0].item() / n_test))},
             "lease_wait_seconds_rank0": trainer.wait_seconds,
-            "gpu_launches": None, "clocks": clocks.summary(), "e2e": None,
+            "gpu_launches": launches, "clocks": clocks.summary(), "e2e": None,
         }), flush=True)
 
 
