@@ -239,6 +239,11 @@ class CudaRowBand:
         self.stream_of = {}
         self.copy_stream = torch.cuda.Stream(device=self.dev)
         self.done_events = {}
+        # host staging (stage_from_host): every granted block's triples are
+        # uploaded from pinned host copies on its stream before the launch,
+        # as BatchEngine.stage_in does per lease (workers.py:186-202)
+        self.host = None
+        self.staged_bytes = 0
         # P, Q and the grid were produced on the current stream; the band's
         # own compute / copy streams must not start before they exist
         torch.cuda.current_stream(self.dev).synchronize()
@@ -285,11 +290,26 @@ class CudaRowBand:
         ev.record(self.copy_stream)
         stream.wait_event(ev)
 
+    def stage_from_host(self, on: bool = True) -> None:
+        """Upload each granted block's triples from pinned host memory before
+        its launch (the end-to-end path); the device arrays are overwritten
+        with identical values, so training is unchanged."""
+        if on and self.host is None:
+            self.host = [a.cpu().pin_memory() for a in (self.grid.users, self.grid.items,
+                                                       self.grid.ratings)]
+        self._staging = bool(on)
+
     def compute(self, c: int, seed: int) -> int:
         from . import kernels
         b = self.block_of[c]
         lo, hi = self.grid.block_range(b)
         stream = self._stream_for(c)
+        if getattr(self, "_staging", False) and hi > lo:
+            with self.torch.cuda.stream(stream):
+                for dst, src in zip((self.grid.users, self.grid.items, self.grid.ratings),
+                                    self.host):
+                    dst[lo:hi].copy_(src[lo:hi], non_blocking=True)
+                    self.staged_bytes += (hi - lo) * dst.element_size()
         if self.kernel == "qband":
             lib = self.lib.load()
             lib.hmf_qband_set_grid_share(self.concurrency)
