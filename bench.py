@@ -586,8 +586,8 @@ def run_ours_multi(args, world, rank, local):
                "d2h_bytes_per_step": 24 * world, "steps": e2e_steps,
                "path": "distributed.RowBandTrainer lease loop with CudaRowBand.stage_from_host: "
                        "each granted block's triples (12 B/rating) uploaded from pinned host "
-                       "memory on its stream before the launch; per-rank residual sums read "
-                       "back every step"}
+                       "memory on the copy stream (the block granted ahead uploads while the "
+                       "current one trains); per-rank residual sums read back every step"}
     band.refresh_q(table)
     sums = residual_sums(DeviceModel(band.P, band.Q), test.users, test.items, test.ratings,
                          row_base=row_lo).to(_reduce_device())

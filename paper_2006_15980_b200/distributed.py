@@ -305,11 +305,18 @@ class CudaRowBand:
         lo, hi = self.grid.block_range(b)
         stream = self._stream_for(c)
         if getattr(self, "_staging", False) and hi > lo:
-            with self.torch.cuda.stream(stream):
+            # on the copy stream: a block granted ahead (the trainer's
+            # prefetch) uploads while the current block's kernel runs; its
+            # range is disjoint from every block in flight, and its previous
+            # launch finished before the lease was released
+            with self.torch.cuda.stream(self.copy_stream):
                 for dst, src in zip((self.grid.users, self.grid.items, self.grid.ratings),
                                     self.host):
                     dst[lo:hi].copy_(src[lo:hi], non_blocking=True)
                     self.staged_bytes += (hi - lo) * dst.element_size()
+                up = self.torch.cuda.Event()
+                up.record(self.copy_stream)
+            stream.wait_event(up)
         if self.kernel == "qband":
             lib = self.lib.load()
             lib.hmf_qband_set_grid_share(self.concurrency)
