@@ -585,9 +585,11 @@ def run_ours_multi(args, world, rank, local):
                                          / e2e_steps),
                "d2h_bytes_per_step": 24 * world, "steps": e2e_steps,
                "path": "distributed.RowBandTrainer lease loop with CudaRowBand.stage_from_host: "
-                       "each granted block's triples (12 B/rating) uploaded from pinned host "
-                       "memory on the copy stream (the block granted ahead uploads while the "
-                       "current one trains); per-rank residual sums read back every step"}
+                       "each granted block's ratings uploaded from pinned host memory ("
+                       + ("6 B/rating: uint16 user ids relative to the row tile, item implicit"
+                          if band.compact is not None else "12 B/rating triples")
+                       + ") on the copy stream, the block granted ahead uploading while the "
+                       "current one trains; per-rank residual sums read back every step"}
     band.refresh_q(table)
     sums = residual_sums(DeviceModel(band.P, band.Q), test.users, test.items, test.ratings,
                          row_base=row_lo).to(_reduce_device())

@@ -243,6 +243,7 @@ class CudaRowBand:
         # uploaded from pinned host copies on its stream before the launch,
         # as BatchEngine.stage_in does per lease (workers.py:186-202)
         self.host = None
+        self.compact = None      # block -> its tiles' first rows (compact stream)
         self.staged_bytes = 0
         # P, Q and the grid were produced on the current stream; the band's
         # own compute / copy streams must not start before they exist
@@ -292,31 +293,91 @@ class CudaRowBand:
 
     def stage_from_host(self, on: bool = True) -> None:
         """Upload each granted block's triples from pinned host memory before
-        its launch (the end-to-end path); the device arrays are overwritten
-        with identical values, so training is unchanged."""
+        its launch (the end-to-end path); training is unchanged.  With the
+        chained kernel on single-item sub-bands and row tiles of at most
+        65 536 users the stream is compact, as in workers.StreamingEpoch:
+        uint16 user ids relative to the tile plus the rating, 6 bytes per
+        rating (hmf_sgd_block_qband_u16_tiles_*); otherwise the triples, 12."""
+        torch = self.torch
         if on and self.host is None:
-            self.host = [a.cpu().pin_memory() for a in (self.grid.users, self.grid.items,
-                                                       self.grid.ratings)]
+            g = self.grid
+            cfg = int(self.lib.load().hmf_qband_get_chain_cfg())
+            compact = (self.kernel == "qband" and (g.sub_impl or 0) >= 4
+                       and cfg in (-1, 2, 4, 5, 6)
+                       and all(bool(torch.all(sc[1:] - sc[:-1] <= 1)) for sc in g.sub_cuts)
+                       and all(len(r) < 2 or int(np.max(np.diff(r))) <= 65536
+                               for r in g.sub_tile_rows))
+            self.compact = {} if compact else None
+            if compact:
+                rel = torch.empty(g.nnz, dtype=torch.int16, device=self.dev)
+                for c in range(self.n_cols):
+                    b = self.block_of[c]
+                    sp = g.sub_ptr[b].cpu().numpy()
+                    T = g.sub_tiles[b]
+                    S = (len(sp) - 1) // T
+                    rows0 = [int(r) for r in g.sub_tile_rows[b][:T]]
+                    for t in range(T):
+                        a, z = int(sp[t * S]), int(sp[(t + 1) * S])
+                        if z > a:
+                            rel[a:z] = (g.users[a:z] - rows0[t]).to(torch.int32).to(torch.int16)
+                    # first rows relative to this band's P (row_lo)
+                    self.compact[b] = torch.tensor([r - self.row_lo for r in rows0],
+                                                   dtype=torch.int32, device=self.dev)
+                self.host = [rel.cpu().pin_memory(), g.ratings.cpu().pin_memory()]
+                self.dev_rel = rel
+            else:
+                self.host = [a.cpu().pin_memory() for a in (g.users, g.items, g.ratings)]
         self._staging = bool(on)
+
+    def _launch_compact(self, b: int, seed: int, stream) -> int:
+        from . import kernels
+        g = self.grid
+        lo, hi = g.block_range(b)
+        sp, sc = g.sub_ptr[b], g.sub_cuts[b]
+        kernels.set_qsync(g)
+        kernels.set_pstore(g)
+        lib = self.lib.load()
+        st = "f16" if self.P.dtype == self.torch.float16 else "f32"
+        fn = getattr(lib, f"hmf_sgd_block_qband_u16_tiles_{st}")
+        self.lib.check(fn(self.P.data_ptr(), self.Q.data_ptr(), self.k, self.dev_rel.data_ptr(),
+                          0, g.ratings.data_ptr(), sp.data_ptr(), sc.data_ptr(),
+                          int(sc.numel()) - 1, int(g.sub_tiles[b]),
+                          self.compact[b].data_ptr(), int(g.sub_impl), float(self.lr),
+                          float(self.ru), float(self.ri), int(seed) & kernels._MASK64, 0,
+                          stream.cuda_stream), "hmf_sgd_block_qband_u16_tiles")
+        return hi - lo
 
     def compute(self, c: int, seed: int) -> int:
         from . import kernels
         b = self.block_of[c]
         lo, hi = self.grid.block_range(b)
         stream = self._stream_for(c)
-        if getattr(self, "_staging", False) and hi > lo:
+        staging = getattr(self, "_staging", False) and hi > lo
+        if staging:
             # on the copy stream: a block granted ahead (the trainer's
             # prefetch) uploads while the current block's kernel runs; its
             # range is disjoint from every block in flight, and its previous
             # launch finished before the lease was released
+            dsts = ((self.dev_rel, self.grid.ratings) if self.compact is not None
+                    else (self.grid.users, self.grid.items, self.grid.ratings))
             with self.torch.cuda.stream(self.copy_stream):
-                for dst, src in zip((self.grid.users, self.grid.items, self.grid.ratings),
-                                    self.host):
+                for dst, src in zip(dsts, self.host):
                     dst[lo:hi].copy_(src[lo:hi], non_blocking=True)
                     self.staged_bytes += (hi - lo) * dst.element_size()
                 up = self.torch.cuda.Event()
                 up.record(self.copy_stream)
             stream.wait_event(up)
+        if staging and self.compact is not None:
+            lib = self.lib.load()
+            lib.hmf_qband_set_grid_share(self.concurrency)
+            try:
+                n = self._launch_compact(b, seed, stream)
+            finally:
+                lib.hmf_qband_set_grid_share(1)
+            ev = self.torch.cuda.Event()
+            ev.record(stream)
+            self.done_events[c] = ev
+            return n
         if self.kernel == "qband":
             lib = self.lib.load()
             lib.hmf_qband_set_grid_share(self.concurrency)

@@ -34,7 +34,7 @@ def problem(conflict_free=False):
     return users, items, vals, P0, Q0
 
 
-def main(out_dir, kernel="exact"):
+def main(out_dir, kernel="exact", stage=False):
     import torch
     import torch.distributed as dist
     from paper_2006_15980_b200.data import DeviceTriples
@@ -59,6 +59,11 @@ def main(out_dir, kernel="exact"):
     if rank == 0:
         table.initialize()
     dist.barrier()
+    if stage:      # every block's ratings uploaded from pinned host memory per lease
+        band.stage_from_host(True)
+        if rank == 0:
+            with open(os.path.join(out_dir, "staged.txt"), "w") as fh:
+                fh.write("compact" if band.compact is not None else "triples")
     trainer = RowBandTrainer(band, table, rank, seed=SEED, record=True)
     for _ in range(EPOCHS):
         trainer.run_epoch()
@@ -75,4 +80,5 @@ def main(out_dir, kernel="exact"):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "exact")
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "exact",
+         len(sys.argv) > 3 and sys.argv[3] == "stage")

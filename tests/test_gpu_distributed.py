@@ -54,11 +54,14 @@ def test_two_ranks_ipc_lease_protocol_equals_serial_replay(tmp_path):
     assert np.array_equal(Q_final, Q)
 
 
-def test_two_ranks_qband_path_applies_every_triple(tmp_path):
+@pytest.mark.parametrize("stage", [False, True], ids=["resident", "host_staged"])
+def test_two_ranks_qband_path_applies_every_triple(tmp_path, stage):
     """The default multi-GPU kernel path (Q-band layout of each rank's band,
     narrow column bands split over the chains) on conflict-free triples:
     order-free, so after the epochs P and Q equal the reference update of
-    every triple once per epoch (oracle, f64) within fp32 rounding."""
+    every triple once per epoch (oracle, f64) within fp32 rounding — with the
+    triples resident, and uploaded from pinned host memory per lease (the
+    N>1 e2e path, CudaRowBand.stage_from_host)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import oracle
@@ -67,11 +70,15 @@ def test_two_ranks_qband_path_applies_every_triple(tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_port()}",
            str(ROOT / "tests" / "dist_gpu_worker.py"), str(tmp_path), "qband"]
+    if stage:
+        cmd.append("stage")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res, Q_final, row_cuts, col_cuts = pickle.loads((tmp_path / "result.pkl").read_bytes())
     for log, Pb, counts in res:
         assert counts == [W.EPOCHS] * (len(col_cuts) - 1)
+    if stage:
+        print("staged stream:", (tmp_path / "staged.txt").read_text())
     users, items, vals, P0, Q0 = W.problem(conflict_free=True)
     P, Q = P0.astype(np.float64), Q0.astype(np.float64)
     for e in range(W.EPOCHS):
