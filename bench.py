@@ -228,6 +228,14 @@ def cpu_sample_run(n_users, n_items, k, sample_nnz, threads, epochs, seed=SEED):
     return got / dt, got, dt
 
 
+def launch_overrides(args) -> dict:
+    """Command-line overrides of the layout's per-launch Q-band options."""
+    return {"impl": args.qband_impl if args.qband_impl >= 0 else None,
+            "chain_cfg": args.chain_cfg if args.chain_cfg >= 0 else None,
+            "pstore": args.pstore if args.pstore >= 0 else None,
+            "qsync": args.qsync, "lockstep": args.chain_lockstep}
+
+
 def host_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -278,17 +286,8 @@ def run_ours(args, world, rank, local):
     _lib.load()
     if args.variant is not None:
         _lib.set_variant(args.variant)
-    _lib.check(_lib.load().hmf_qband_set_impl(args.qband_impl), "hmf_qband_set_impl")
-    _lib.check(_lib.load().hmf_qband_set_chain_cfg(args.chain_cfg), "hmf_qband_set_chain_cfg")
-    if args.qsync is not None:
-        from paper_2006_15980_b200 import kernels as _kq
-        _kq.QSYNC_OVERRIDE = args.qsync
-    if args.chain_lockstep is not None:
-        _lib.check(_lib.load().hmf_qband_set_chain_lockstep(args.chain_lockstep),
-                   "hmf_qband_set_chain_lockstep")
-    if args.pstore >= 0:
-        from paper_2006_15980_b200 import kernels as _k
-        _k.PSTORE_OVERRIDE = args.pstore
+    # per-launch overrides of the layout's Q-band options (ABI 4)
+    overrides = launch_overrides(args)
     dev = torch.device("cuda", local)
     n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
     k = args.k or k0
@@ -330,8 +329,10 @@ def run_ours(args, world, rank, local):
     torch.cuda.empty_cache()
     if args.kernel == "qband":
         bucket_qbands(grid, k, tile_bytes=tile_bytes, elem_bytes=2 if precision == "f16" else 4,
-                      impl=5 if args.split else None, split=args.split or None,
-                      max_tile_rows=args.tile_rows)
+                      impl=(5 if args.split else (args.qband_impl if args.qband_impl >= 0
+                                                  else None)),
+                      split=args.split or None, max_tile_rows=args.tile_rows,
+                      chain_cfg=args.chain_cfg)
     stream_epoch = None
     if not args.no_e2e and args.kernel == "qband" and world == 1:
         # e2e streams the same layout from pinned host memory, tile by tile
@@ -339,7 +340,7 @@ def run_ours(args, world, rank, local):
         stream_epoch = StreamingEpoch(grid, k, n_buffers=args.stream_buffers,
                                       tiles_per_chunk=args.stream_tiles,
                                       last_chunk_tiles=args.stream_last,
-                                      reuse=args.stream_reuse)
+                                      reuse=args.stream_reuse, opts=overrides)
     model = init_device_model(n_users, n_items, k, SEED, device=dev,
                               dtype="float16" if precision == "f16" else "float32")
     torch.cuda.synchronize(dev)
@@ -361,7 +362,7 @@ def run_ours(args, world, rank, local):
                 e0.record(stream)
             if args.kernel == "qband":
                 kernels.launch_block_qband(model.P, model.Q, grid, b, LR, REG, REG, seed,
-                                           stream=stream.cuda_stream)
+                                           stream=stream.cuda_stream, opts=overrides)
             else:
                 kernels.launch_sgd_range(model.P, model.Q, grid.users, grid.items, grid.ratings,
                                          lo, hi, LR, REG, REG, seed, 0, 0, args.mode,
@@ -750,10 +751,11 @@ def main():
                     help="N>1: a workload-sized band per GPU (weak) or the workload split (strong)")
     ap.add_argument("--multi-concurrency", type=int, default=1,
                     help="N>1: column blocks in flight per GPU (each on its own stream)")
-    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 1, 2, 3, 4, 5, 6], default=-1,
-                    help="Q-band kernel: 0 = register prefetch (default), 1 = TMA pipeline")
-    ap.add_argument("--chain-cfg", type=int, choices=list(range(-1, 7)), default=-1,
-                    help="configuration of Q-band implementation 4 (qchain.cuh ChainCfg)")
+    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 4, 5, 6], default=-1,
+                    help="Q-band kernel: 0 = warp per rating, 4-6 chained item runs "
+                         "(-1: the layout's, 5 by default)")
+    ap.add_argument("--chain-cfg", type=int, choices=[-1, 2, 4, 5, 6], default=-1,
+                    help="configuration of the chained kernel (qchain.cuh ChainCfg)")
     ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)
     ap.add_argument("--pstore", type=int, choices=[-1, 0, 1], default=-1,
                     help="chained kernel P write-back: -1 the layout's (grid.sub_pstore), "

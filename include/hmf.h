@@ -14,8 +14,8 @@
  *   hmf_sgd_block_qband_u16_*     (the same, uint16 tile-relative row ids)
  *   hmf_sgd_block_qband_u16_tiles_*  (the same over several row tiles)
  *                                                              workers.py:186-255
- *   hmf_qband_set_*, _get_*       (kernel selection / configuration; no
- *                                 reference counterpart)
+ *   hmf_qband_resolve_*, _slots_per_sm, _chain_lanes, _max_items
+ *                                 (layout queries; no reference counterpart)
  *   hmf_visit_order               sgd_range's visit order      kernels.py:77-119
  *   hmf_mix64                     kernels.mix64                kernels.py:32-48
  *   hmf_residual_sums_{f32,f16,f64}
@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define HMF_ABI_VERSION 3
+#define HMF_ABI_VERSION 4
 
 #define HMF_OK 0
 #define HMF_ERR_ARG (-1)
@@ -97,134 +97,124 @@ int64_t hmf_sgd_range_f64(double* user_f, double* item_f, int64_t k, const int32
                           int64_t row_base, int64_t col_base, int32_t mode, void* stream);
 
 /*
- * Q-band-stationary update of one block (the engine's fast path): the block's
+ * Q-band-stationary update of one block (the engine's fast path,
+ * BatchEngine.compute on a staged item band, workers.py:186-266): the block's
  * triples are bucketed into n_sub column sub-bands (stable), sub-band s being
  * triples [sub_ptr[s], sub_ptr[s+1]) whose items lie in [sub_cuts[s],
- * sub_cuts[s+1]) (absolute item ids; device arrays).  One warp (or one
- * lane group, implementation 4) owns a sub-band: its Q rows stay on chip for
- * the whole launch (exact sequential SGD on Q), P deltas go back by vector
- * reductions.  Each sub-band may span at most hmf_qband_max_items_for(k, f16,
- * impl) items; k in {32, 64, 128, 256}; ratings are f32.  Triples of a
- * sub-band sorted by item (data.bucket_qbands) keep the current item's Q row
- * in registers.  Same update rule and indexing (row_base / col_base) as
- * hmf_sgd_range_*.  Returns 0 or < 0.
+ * sub_cuts[s+1]) (absolute item ids; device arrays).  A warp (implementation
+ * 0) or a lane-group chain (4-6) owns a sub-band: the current item's Q row
+ * stays on chip (exact sequential SGD on Q), P changes go back by vector
+ * reductions or plain stores.  k in {32, 64, 128, 256}; ratings are f32.
+ * Same update rule and indexing (row_base / col_base) as hmf_sgd_range_*.
+ * Returns 0 or < 0.
  *
  * Row tiles: with n_tiles > 1 the block's triples are bucketed tile-major
  * (n_tiles row tiles x n_sub sub-bands, sub_ptr holding n_tiles*n_sub + 1
  * offsets); tile t's sub-band s is [sub_ptr[t*n_sub+s], sub_ptr[t*n_sub+s+1]).
  * The launch walks the tiles in a seeded rotation so that one tile's P rows
- * stay resident in L2; sub-band s keeps the same owning warp in every tile.
- * n_tiles = 1 is the plain sub-band layout.
+ * stay resident in L2.
+ *
+ * Every launch-shaping choice is an argument (ABI version 4): `opts` (NULL =
+ * all defaults) is read during the call only.  Nothing is process-global, so
+ * threads launching different layouts concurrently do not interfere.
  */
-int32_t hmf_qband_max_items(int64_t k);
-/* The same for one storage type and implementation (impl -1: default). */
-int32_t hmf_qband_max_items_for(int64_t k, int32_t f16, int32_t impl);
-/* Sub-band slots per SM of an implementation (warps, or chains for
- * implementation 4); needs a current CUDA device.  f16 != 0 for fp16
- * storage; impl -1 = the default.  hmf_qband_warps_per_sm(k, f16) is
- * hmf_qband_slots_per_sm(k, f16, -1). */
-int32_t hmf_qband_slots_per_sm(int64_t k, int32_t f16, int32_t impl);
-int32_t hmf_qband_warps_per_sm(int64_t k, int32_t f16);
-/* Q-band implementations: 0 = register prefetch + per-lane vector reductions,
- * 1 = TMA pipeline (bulk P-row loads into a shared ring, bulk reductions of
- * P deltas), 2 = per-lane cp.async ring of P rows + vector reductions, 3 =
- * implementation 0 with one CTA per SM and twice the prefetch depth, 4 =
- * chained item runs (several lane groups per warp, each walking its own
- * sub-band with the item's Q row in registers), 5 = implementation 4 with
- * Q deltas: several sub-bands may hold runs of the same item (a narrow block's
- * item runs split over chains); each chain updates its own copy of the Q row
- * and adds the change back with vector reductions, publishing and re-reading
- * it every hmf_qband_set_qsync ratings (bounded staleness), 6 = implementation
- * 5 publishing only at item and bin changes (whole runs per sub-band, whose
- * units in consecutive row tiles may overlap).  hmf_qband_set_impl sets the
- * process default; -1 (initial) = automatic: 5 (4 when every sub-band holds
- * whole item runs).  hmf_qband_resolve_impl gives what the default resolves
- * to. */
-int hmf_qband_set_impl(int32_t impl);
-int32_t hmf_qband_get_impl(void);
+typedef struct hmf_qband_opts {
+  /* Implementation: -1 = default (5); 0 = one warp per rating on its
+   * sub-band's Q rows in shared memory (each sub-band at most
+   * hmf_qband_max_items(k, f16, 0) items); 4 = chained item runs (several
+   * lane-group chains per warp, the item's Q row in registers; whole runs
+   * per sub-band); 5 = 4 with Q deltas: runs of one item may be split over
+   * chains, each adds its change back with vector reductions and re-reads the
+   * row every `qsync` ratings (bounded staleness); 6 = 5 publishing only at
+   * item and bin changes. */
+  int32_t impl;
+  /* Chained-kernel configuration 2, 4, 5 or 6 (lanes per chain, prefetch
+   * distance, occupancy); -1 = by k and storage
+   * (hmf_qband_resolve_chain_cfg). */
+  int32_t chain_cfg;
+  /* P write-back of the chained kernel: -1/0 vector reductions of the change
+   * (no update lost), 1 plain stores of the updated row (fp32 rows with
+   * configuration 5 or 6; reductions elsewhere) — the reference's racing-lane
+   * semantics (workers.py:222-266): a concurrent update of the same user by
+   * another chain may be lost. */
+  int32_t pstore;
+  /* Implementation 5: ratings between Q-delta publications; -1 = 32, 0 =
+   * only at item and bin changes. */
+  int32_t qsync;
+  /* -1/1: the launch may fill the GPU; d in 2..64: its grid is capped at 1/d
+   * of the resident CTA slots, so d launches on separate streams (several
+   * column blocks of one row band) run side by side. */
+  int32_t grid_share;
+  /* Chains of a warp change bins together: bit 0 static, bit 1 dynamic
+   * scheduler; -1 = 3. */
+  int32_t lockstep;
+} hmf_qband_opts;
+
+/* Default implementation / chain configuration for k and storage. */
 int32_t hmf_qband_resolve_impl(int64_t k, int32_t f16);
-/* Implementation 4 configuration 0..6 (lanes per chain, prefetch distance,
- * occupancy; -1 = default by k and storage: k = 32 cfg 4 (4 lanes, 4 ahead),
- * k = 64 cfg 6 fp32 / 4 fp16, k >= 128 cfg 5 fp32 (8 lanes, 16 at k = 256, 2
- * ahead) / 6 fp16 (4 ahead)) and the lanes per
- * chain it uses for k; a chain walks full batches of that many triples in a
- * seeded rotation, then the partial batch. */
-int hmf_qband_set_chain_cfg(int32_t cfg);
-int32_t hmf_qband_get_chain_cfg(void);
-/* Cap every Q-band launch's grid at 1/div of the resident CTA slots (default
- * 1), so div launches on separate streams — several column blocks of one row
- * band — run side by side. */
-int hmf_qband_set_grid_share(int32_t div);
-/* Implementation 5: every `steps` ratings (default 32) each chain publishes
- * its Q-row change and re-reads the row, bounding how stale the copies of
- * chains sharing an item get (0 = publish only at item and bin changes). */
-int hmf_qband_set_qsync(int32_t steps);
-int32_t hmf_qband_chain_lanes(int64_t k);               /* fp32 rows */
-int32_t hmf_qband_chain_lanes_for(int64_t k, int32_t f16);
-/* Implementation 4: chains of a warp change bins together (bit 0: static
- * scheduler, bit 1: dynamic scheduler; default 3). */
-int hmf_qband_set_chain_lockstep(int32_t bits);
-/* How the chained kernel writes P rows back (process-wide, for the launches
- * that follow): 0 or -1 (default) vector reductions of the change, 1 plain
- * stores of the updated row (fp32 with chain configuration 5 or 6;
- * reductions elsewhere).  Stores are the reference's racing-lane semantics
- * (workers.py:222-266): a concurrent update of the same user by another
- * chain may be lost; reductions lose none.  Added in ABI version 3. */
-int hmf_qband_set_pstore(int32_t mode);
-int32_t hmf_qband_get_pstore(void);
-/* impl: the implementation for this launch (-1 = the process default).
- * cols may be NULL with implementation 4 when every sub-band is a single
+int32_t hmf_qband_resolve_chain_cfg(int64_t k, int32_t f16);
+/* Sub-band slots per SM of the launch `opts` describes (warps for
+ * implementation 0, chains for 4-6); needs a current CUDA device (per-device
+ * occupancy).  f16 != 0 for fp16 storage. */
+int32_t hmf_qband_slots_per_sm(int64_t k, int32_t f16, const hmf_qband_opts* opts);
+/* Lanes per chain of configuration cfg (-1: the default) at k. */
+int32_t hmf_qband_chain_lanes(int64_t k, int32_t f16, int32_t cfg);
+/* Items one sub-band may span under implementation impl (1<<30: unbounded;
+ * 0: k unsupported). */
+int32_t hmf_qband_max_items(int64_t k, int32_t f16, int32_t impl);
+
+/* cols may be NULL with implementations 4-6 when every sub-band is a single
  * item (sub_cuts[s+1] = sub_cuts[s] + 1): the item of sub-band s is then
- * sub_cuts[s] (a host->device stream of 8 instead of 12 bytes per rating). */
+ * sub_cuts[s] (8 instead of 12 bytes per rating on a host stream). */
 int64_t hmf_sgd_block_qband_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
                                 const int32_t* cols, const float* vals, const int64_t* sub_ptr,
                                 const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles,
-                                int32_t impl, double lr, double reg_user, double reg_item,
-                                uint64_t seed, int64_t row_base, int64_t col_base, void* stream);
+                                const hmf_qband_opts* opts, double lr, double reg_user,
+                                double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
+                                void* stream);
 int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                 const int32_t* rows, const int32_t* cols, const float* vals,
                                 const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
-                                int64_t n_tiles, int32_t impl, double lr, double reg_user,
-                                double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
-                                void* stream);
+                                int64_t n_tiles, const hmf_qband_opts* opts, double lr,
+                                double reg_user, double reg_item, uint64_t seed, int64_t row_base,
+                                int64_t col_base, void* stream);
 
-/* The chained kernel (implementation 4 or 5, chain configuration 2, 4, 5 or 6) with
- * uint16 row ids: row = rows[i] - row_base, so a row tile of at most 65536
- * rows streams 2-byte ids with row_base = -(the tile's first row).  Same
- * arguments and contract as hmf_sgd_block_qband_*. */
+/* The chained kernel (implementations 4-6) with uint16 row ids: row =
+ * rows[i] - row_base, so a row tile of at most 65536 rows streams 2-byte ids
+ * with row_base = -(the tile's first row).  Same contract as
+ * hmf_sgd_block_qband_*. */
 int64_t hmf_sgd_block_qband_u16_f32(float* user_f, float* item_f, int64_t k,
                                     const uint16_t* rows, const int32_t* cols, const float* vals,
                                     const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
-                                    int64_t n_tiles, int32_t impl, double lr, double reg_user,
-                                    double reg_item, uint64_t seed, int64_t row_base,
-                                    int64_t col_base, void* stream);
+                                    int64_t n_tiles, const hmf_qband_opts* opts, double lr,
+                                    double reg_user, double reg_item, uint64_t seed,
+                                    int64_t row_base, int64_t col_base, void* stream);
 int64_t hmf_sgd_block_qband_u16_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                     const uint16_t* rows, const int32_t* cols, const float* vals,
                                     const int64_t* sub_ptr, const int32_t* sub_cuts, int64_t n_sub,
-                                    int64_t n_tiles, int32_t impl, double lr, double reg_user,
-                                    double reg_item, uint64_t seed, int64_t row_base,
-                                    int64_t col_base, void* stream);
+                                    int64_t n_tiles, const hmf_qband_opts* opts, double lr,
+                                    double reg_user, double reg_item, uint64_t seed,
+                                    int64_t row_base, int64_t col_base, void* stream);
 
 /* uint16 row ids over n_tiles row tiles in one launch: a rating of tile t
  * updates row tile_row0[t] + rows[i] (tile_row0: device int32[n_tiles], the
  * tiles' first rows in user_f).  Lets a host stream stage several tiles of a
  * block as one chunk at 2 bytes per user id.  Same contract as
- * hmf_sgd_block_qband_u16_* otherwise (there is no row_base).  Added in ABI
- * version 3. */
+ * hmf_sgd_block_qband_u16_* otherwise (there is no row_base). */
 int64_t hmf_sgd_block_qband_u16_tiles_f32(float* user_f, float* item_f, int64_t k,
                                           const uint16_t* rows, const int32_t* cols,
                                           const float* vals, const int64_t* sub_ptr,
                                           const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles,
-                                          const int32_t* tile_row0, int32_t impl, double lr,
-                                          double reg_user, double reg_item, uint64_t seed,
-                                          int64_t col_base, void* stream);
+                                          const int32_t* tile_row0, const hmf_qband_opts* opts,
+                                          double lr, double reg_user, double reg_item,
+                                          uint64_t seed, int64_t col_base, void* stream);
 int64_t hmf_sgd_block_qband_u16_tiles_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                           const uint16_t* rows, const int32_t* cols,
                                           const float* vals, const int64_t* sub_ptr,
                                           const int32_t* sub_cuts, int64_t n_sub, int64_t n_tiles,
-                                          const int32_t* tile_row0, int32_t impl, double lr,
-                                          double reg_user, double reg_item, uint64_t seed,
-                                          int64_t col_base, void* stream);
+                                          const int32_t* tile_row0, const hmf_qband_opts* opts,
+                                          double lr, double reg_user, double reg_item,
+                                          uint64_t seed, int64_t col_base, void* stream);
 
 /*
  * The reference visit order of a range of n triples under `seed`

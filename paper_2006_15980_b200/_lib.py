@@ -29,6 +29,7 @@ MODES = {"hogwild": MODE_HOGWILD, "ordered": MODE_ORDERED, "exact": MODE_EXACT,
          "hogwild_lww": MODE_HOGWILD_LWW}
 
 TUNE_VARIANT = 1
+ABI_VERSION = 4
 
 _p = C.c_void_p
 _i64 = C.c_int64
@@ -48,34 +49,23 @@ SIGNATURES = {
                                  _i64, _i64, _i32, _p]),
     "hmf_sgd_range_f64": (_i64, [_p, _p, _i64, _p, _p, _p, _i64, _i64, _f64, _f64, _f64, _u64,
                                  _i64, _i64, _i32, _p]),
-    "hmf_qband_max_items": (_i32, [_i64]),
-    "hmf_qband_max_items_for": (_i32, [_i64, _i32, _i32]),
-    "hmf_qband_warps_per_sm": (_i32, [_i64, _i32]),
-    "hmf_qband_slots_per_sm": (_i32, [_i64, _i32, _i32]),
     "hmf_qband_resolve_impl": (_i32, [_i64, _i32]),
-    "hmf_qband_get_impl": (_i32, []),
-    "hmf_qband_set_impl": (C.c_int, [_i32]),
-    "hmf_qband_set_chain_cfg": (C.c_int, [_i32]),
-    "hmf_qband_get_chain_cfg": (_i32, []),
-    "hmf_qband_set_grid_share": (C.c_int, [_i32]),
-    "hmf_qband_set_qsync": (C.c_int, [_i32]),
-    "hmf_qband_chain_lanes": (_i32, [_i64]),
-    "hmf_qband_chain_lanes_for": (_i32, [_i64, _i32]),
-    "hmf_qband_set_chain_lockstep": (C.c_int, [_i32]),
-    "hmf_qband_set_pstore": (C.c_int, [_i32]),
-    "hmf_qband_get_pstore": (_i32, []),
-    "hmf_sgd_block_qband_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i32, _f64,
+    "hmf_qband_resolve_chain_cfg": (_i32, [_i64, _i32]),
+    "hmf_qband_slots_per_sm": (_i32, [_i64, _i32, _p]),
+    "hmf_qband_chain_lanes": (_i32, [_i64, _i32, _i32]),
+    "hmf_qband_max_items": (_i32, [_i64, _i32, _i32]),
+    "hmf_sgd_block_qband_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _p, _f64,
                                        _f64, _f64, _u64, _i64, _i64, _p]),
-    "hmf_sgd_block_qband_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i32, _f64,
+    "hmf_sgd_block_qband_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _p, _f64,
                                        _f64, _f64, _u64, _i64, _i64, _p]),
-    "hmf_sgd_block_qband_u16_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i32,
+    "hmf_sgd_block_qband_u16_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _p,
                                            _f64, _f64, _f64, _u64, _i64, _i64, _p]),
-    "hmf_sgd_block_qband_u16_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i32,
+    "hmf_sgd_block_qband_u16_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _p,
                                            _f64, _f64, _f64, _u64, _i64, _i64, _p]),
     "hmf_sgd_block_qband_u16_tiles_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64,
-                                                 _p, _i32, _f64, _f64, _f64, _u64, _i64, _p]),
+                                                 _p, _p, _f64, _f64, _f64, _u64, _i64, _p]),
     "hmf_sgd_block_qband_u16_tiles_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64,
-                                                 _p, _i32, _f64, _f64, _f64, _u64, _i64, _p]),
+                                                 _p, _p, _f64, _f64, _f64, _u64, _i64, _p]),
     "hmf_visit_order": (C.c_int, [_i64, _u64, _p, _p]),
     "hmf_mix64": (_u64, [C.POINTER(_u64), _i32]),
     "hmf_residual_sums_f32": (C.c_int, [_p, _p, _i64, _p, _p, _p, _i64, _i64, _i64, _i32, _p, _p]),
@@ -128,7 +118,7 @@ def load() -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.hmf_abi_version() != 3:
+        if lib.hmf_abi_version() != ABI_VERSION:
             raise HmfError("libhmf ABI version mismatch")
         _lib = lib
         return lib
@@ -149,6 +139,24 @@ def check(rc: int, what: str) -> int:
 def mix64_native(*parts: int) -> int:
     arr = (_u64 * len(parts))(*[int(p) & 0xFFFFFFFFFFFFFFFF for p in parts])
     return int(load().hmf_mix64(arr, len(parts)))
+
+
+class QbandOpts(C.Structure):
+    """hmf_qband_opts (include/hmf.h): per-launch options of the Q-band
+    kernels; -1 in a field means the library default."""
+    _fields_ = [("impl", _i32), ("chain_cfg", _i32), ("pstore", _i32), ("qsync", _i32),
+                ("grid_share", _i32), ("lockstep", _i32)]
+
+    def __init__(self, **kw):
+        vals = {name: -1 for name, _ in self._fields_}
+        vals.update({k: int(v) for k, v in kw.items() if v is not None})
+        super().__init__(**vals)
+
+    def as_dict(self) -> dict:
+        return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+    def __repr__(self):
+        return f"QbandOpts({self.as_dict()})"
 
 
 def set_variant(variant: int) -> None:

@@ -143,8 +143,13 @@ static int bucket(const int32_t* rows, const int32_t* cols, const float* vals, i
   if (warps < 1) warps = 1;
   const size_t smem = size_t(warps) * size_t(n_blocks) * 8;
   if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(bucket_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 0;  // sets the shared-memory opt-in on this device
+    cudaError_t ea = kernel_occupancy(reinterpret_cast<const void*>(bucket_count_kernel),
+                                      warps * 32, int(smem), &per_sm);
+    if (ea == cudaSuccess)
+      ea = kernel_occupancy(reinterpret_cast<const void*>(bucket_scatter_kernel), warps * 32,
+                            int(smem), &per_sm);
+    if (ea != cudaSuccess) return int(set_cuda_error(ea));
   }
   int64_t* counts = nullptr;
   const size_t cells = size_t(n_blocks) * size_t(g.n_tiles);

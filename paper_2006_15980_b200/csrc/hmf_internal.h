@@ -21,4 +21,9 @@ cudaError_t scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, cudaS
 
 int device_sm_count();
 
+// Resident CTAs per SM of `kern` on the current device with `threads` threads
+// and `smem` bytes of dynamic shared memory (>= 1).  Sets the shared-memory
+// opt-in on that device first; cached per (kernel, device, threads, smem).
+cudaError_t kernel_occupancy(const void* kern, int threads, int smem, int* per_sm);
+
 }  // namespace hmf

@@ -28,12 +28,12 @@
 // a = lr*err:  dP = a*q - (lr*reg_u)*p,  q' = (1 - lr*reg_i)*q + a*p.
 #pragma once
 
-#include <atomic>
+#include <map>
 #include <mutex>
-#include <unordered_map>
 #include <utility>
 
 #include "hmf_common.cuh"
+#include "hmf_internal.h"
 #include "lanevec.cuh"
 
 namespace hmf {
@@ -94,28 +94,19 @@ template <int K, typename S, int LPC> struct ChainLay {
   }
 };
 
-// Configurations (hmf_qband_set_chain_cfg): lanes per chain (about 16 or 8
-// fp32 elements per lane, 4..32 lanes), prefetch distance PD in steps,
-// warps per CTA and CTAs per SM (register budget).
+// Configurations (hmf_qband_opts.chain_cfg): lanes per chain (about 8 or 16
+// fp32 elements per lane, 4..32 lanes), prefetch distance PD in steps, warps
+// per CTA and CTAs per SM (register budget).  Configurations 0, 1 and 3 of
+// round 1 (16 elements per lane with 1-2 steps ahead; 8 elements with 2
+// ahead at 24 warps) were never the fastest at any k and are gone
+// (profiles/r02/chain_cfg_by_k.jsonl).
 template <int K, int CFG> struct ChainCfg;
-template <int K> struct ChainCfg<K, 0> {  // 16 elements/lane, 1 step ahead
-  static constexpr int LPC = (K / 16) < 4 ? 4 : ((K / 16) > 32 ? 32 : (K / 16));
-  static constexpr int PD = 1, WPB = 16, MINB = 1;
-};
-template <int K> struct ChainCfg<K, 1> {  // 16 elements/lane, 2 steps ahead
-  static constexpr int LPC = ChainCfg<K, 0>::LPC;
-  static constexpr int PD = 2, WPB = 16, MINB = 1;
-};
 template <int K> struct ChainCfg<K, 2> {  // 8 elements/lane, 3 steps ahead, 24 warps/SM
   static constexpr int LPC = (K / 8) < 4 ? 4 : ((K / 8) > 32 ? 32 : (K / 8));
   static constexpr int PD = 3, WPB = 8, MINB = 3;
 };
-template <int K> struct ChainCfg<K, 3> {  // 8 elements/lane, 2 steps ahead, 24 warps/SM
-  static constexpr int LPC = ChainCfg<K, 2>::LPC;
-  static constexpr int PD = 2, WPB = 8, MINB = 3;
-};
 template <int K> struct ChainCfg<K, 4> {  // 16 elements/lane, 4 steps ahead (fp16 rows)
-  static constexpr int LPC = ChainCfg<K, 0>::LPC;
+  static constexpr int LPC = (K / 16) < 4 ? 4 : ((K / 16) > 32 ? 32 : (K / 16));
   static constexpr int PD = LPC > 4 ? 4 : LPC - 1, WPB = 16, MINB = 1;
 };
 template <int K> struct ChainCfg<K, 5> {  // 8 lanes per chain (4 chains), 2 steps ahead
@@ -126,16 +117,6 @@ template <int K> struct ChainCfg<K, 6> {  // 8 lanes per chain (4 chains), 4 ste
   static constexpr int LPC = K >= 256 ? 16 : 8;
   static constexpr int PD = 4, WPB = 16, MINB = 1;
 };
-constexpr int kChainCfgs = 7;
-
-// Share of the GPU one Q-band launch may fill: its grid is capped at
-// 1/g_grid_div of the resident CTA slots, so g_grid_div launches on separate
-// streams (several column blocks of one row band) run side by side.
-static std::atomic<int> g_grid_div{1};
-static inline int grid_share(int cap) {
-  const int c = (cap + g_grid_div - 1) / g_grid_div;
-  return c < 1 ? 1 : c;
-}
 
 __device__ inline unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -416,82 +397,82 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
   }
 }
 
-// implementation 5: steps between Q-delta publications of a chain (0 = only
-// at item and bin changes)
-static std::atomic<int> g_qsync_steps{32};
+// Per-launch options after defaults (hmf_qband_opts, resolved in
+// qband_kernels.cu): nothing here is process-global, so concurrent launches
+// with different layouts on different streams or threads do not interfere.
+struct LaunchOpts {
+  int impl;      // 0 (warp per rating), 4, 5 or 6 (chained)
+  int cfg;       // chain configuration 2, 4, 5 or 6
+  int pstore;    // 1: P rows written back by plain stores (fp32, cfg 5 / 6)
+  int qsync;     // implementation 5: ratings between Q publications (0 = item/bin changes)
+  int share;     // grid capped at 1/share of the resident CTA slots
+  int lockstep;  // chains change bins together: bit 0 static, bit 1 dynamic scheduler
+};
 
-// -1 = automatic (measured on tiles of at most 65 536 users,
-// profiles/r02/small_k_cfg.jsonl, chain_cfg_by_k.jsonl): k = 32 4 lanes per
-// chain, 3 steps ahead, 24 warps per SM (cfg 2; 30.6 / 41.9 G upd/s fp32 /
-// fp16 vs 28.1 / 32.0 with 16 warps, cfg 4); k = 64 fp32 8 lanes, 3 ahead,
-// 24 warps (cfg 2; 19.7 vs 18.5), fp16 4 lanes 4 ahead (cfg 4); k >= 128:
-// 8 lanes (16 at k = 256), 2 ahead in fp32 (cfg 5, the register budget), 4
-// ahead in fp16 (cfg 6, raw fp16 slots).
-static std::atomic<int> g_chain_cfg{-1};
+static inline int grid_share(int cap, int share) {
+  const int c = (cap + share - 1) / (share < 1 ? 1 : share);
+  return c < 1 ? 1 : c;
+}
+
+// Default configuration by k and storage (measured on tiles of at most
+// 65 536 users, profiles/r02/small_k_cfg.jsonl, chain_cfg_by_k.jsonl): k = 32
+// 4 lanes per chain, 3 steps ahead, 24 warps per SM (cfg 2; 30.6 / 41.9 G
+// upd/s fp32 / fp16 vs 28.1 / 32.0 with 16 warps, cfg 4); k = 64 fp32 8
+// lanes, 3 ahead, 24 warps (cfg 2; 19.7 vs 18.5), fp16 4 lanes 4 ahead (cfg
+// 4); k >= 128: 8 lanes (16 at k = 256), 2 ahead in fp32 (cfg 5, the
+// register budget), 4 ahead in fp16 (cfg 6, raw fp16 slots).
 static inline int auto_chain_cfg(int k, bool f16) {
   if (k <= 32) return 2;
   if (k <= 64) return f16 ? 4 : 2;
   return f16 ? 6 : 5;
 }
-template <int K, typename S> static int chain_cfg() {
-  const int set = g_chain_cfg.load();
-  return set >= 0 ? set : auto_chain_cfg(K, sizeof(S) == 2);
-}
-// bin changes in warp lockstep: bit 0 for the static, bit 1 for the dynamic
-// scheduler
-static std::atomic<int> g_chain_lockstep{3};
-// P write-back: 0 (default, also -1) vector reductions of the change; 1
-// plain stores of the updated row where available (fp32 rows, chain
-// configurations 5 and 6: +19 % at NF k = 128 and 256, +4 % at k = 64;
-// fp16 rows and k = 32 were slower with stores, profiles/r02/pstore*.jsonl).  data.bucket_qbands picks stores only when a
-// row tile holds several times more users than there are chains.
-static std::atomic<int> g_chain_pstore{-1};
-template <int K, typename S, int CFG> static bool chain_pstore() {
-  if constexpr (sizeof(S) != 4 || (CFG != 5 && CFG != 6)) {
-    return false;
-  } else {
-    return g_chain_pstore.load() == 1;
-  }
+static inline bool chain_cfg_ok(int cfg) { return cfg == 2 || (cfg >= 4 && cfg <= 6); }
+static inline int chain_lanes(int k, int cfg) {
+  if (cfg == 5 || cfg == 6) return k >= 256 ? 16 : 8;
+  const int lpc = k / (cfg == 2 ? 8 : 16);
+  return lpc < 4 ? 4 : (lpc > 32 ? 32 : lpc);
 }
 
 template <int K, typename S, int CFG>
-static int chain_slots_per_sm_cfg() {
+static cudaError_t chain_slots_per_sm_cfg(int* out) {
   using C = ChainCfg<K, CFG>;
   auto kern = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false>;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPB * 32, 0);
-  return per_sm * C::WPB * (32 / C::LPC);
+  const cudaError_t e =
+      kernel_occupancy(reinterpret_cast<const void*>(kern), C::WPB * 32, 0, &per_sm);
+  *out = per_sm * C::WPB * (32 / C::LPC);
+  return e;
 }
 
 template <int K, typename S>
-static int chain_slots_per_sm() {
-  switch (chain_cfg<K, S>()) {
-    case 0: return chain_slots_per_sm_cfg<K, S, 0>();
-    case 2: return chain_slots_per_sm_cfg<K, S, 2>();
-    case 3: return chain_slots_per_sm_cfg<K, S, 3>();
-    case 4: return chain_slots_per_sm_cfg<K, S, 4>();
-    case 5: return chain_slots_per_sm_cfg<K, S, 5>();
-    case 6: return chain_slots_per_sm_cfg<K, S, 6>();
-    default: return chain_slots_per_sm_cfg<K, S, 1>();
+static cudaError_t chain_slots_per_sm(int cfg, int* out) {
+  switch (cfg) {
+    case 2: return chain_slots_per_sm_cfg<K, S, 2>(out);
+    case 4: return chain_slots_per_sm_cfg<K, S, 4>(out);
+    case 5: return chain_slots_per_sm_cfg<K, S, 5>(out);
+    default: return chain_slots_per_sm_cfg<K, S, 6>(out);
   }
 }
 
-// Per-stream scratch for the dynamic scheduler ({counter, done[n_sub]});
-// launches on one stream are ordered, so they can share it.
+// Scratch of the dynamic scheduler ({counter, done[n_sub]}) per (device,
+// stream): launches on one stream are ordered, so they can share it.
 static cudaError_t chain_work(cudaStream_t stream, size_t words, unsigned** out) {
   static std::mutex mu;
-  static std::unordered_map<cudaStream_t, std::pair<unsigned*, size_t>> bufs;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<unsigned*, size_t>> bufs;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lock(mu);
-  auto& b = bufs[stream];
+  auto& b = bufs[{dev, stream}];
   if (b.second < words) {
     if (b.first) {
-      cudaError_t e = cudaStreamSynchronize(stream);
+      e = cudaStreamSynchronize(stream);
       if (e != cudaSuccess) return e;
       cudaFree(b.first);
       b.first = nullptr;
       b.second = 0;
     }
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&b.first), words * sizeof(unsigned));
+    e = cudaMalloc(reinterpret_cast<void**>(&b.first), words * sizeof(unsigned));
     if (e != cudaSuccess) return e;
     b.second = words;
   }
@@ -502,30 +483,36 @@ static cudaError_t chain_work(cudaStream_t stream, size_t words, unsigned** out)
 template <int K, typename S, int CFG, typename RowT>
 static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t* cols,
                                     const float* vals, const int64_t* sub_ptr,
-                                    const int32_t* sub_cuts, int n_sub,
-                                    int n_tiles, const int32_t* tile_row0, double lr, double ru,
-                                    double ri, uint64_t seed, int64_t row_base, int64_t col_base,
-                                    cudaStream_t stream, int qdelta) {
+                                    const int32_t* sub_cuts, int n_sub, int n_tiles,
+                                    const int32_t* tile_row0, double lr, double ru, double ri,
+                                    uint64_t seed, int64_t row_base, int64_t col_base,
+                                    cudaStream_t stream, const LaunchOpts& o) {
   using C = ChainCfg<K, CFG>;
   constexpr int NC = 32 / C::LPC;
+  // qdelta 0: whole item runs per sub-band (plain Q stores); 1: bounded
+  // staleness (publish and re-read every o.qsync ratings); 2: publish at item
+  // and bin changes only (whole runs per sub-band)
+  const int qdelta = o.impl == 4 ? 0 : (o.impl == 5 ? 1 : 2);
   auto kstat = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false, RowT>;
   auto kdyn = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, true, RowT>;
+  // P write-back by plain stores (the reference's racing lanes): fp32 rows
+  // with configurations 5 and 6 only (+19 % at NF k = 128 and 256, +4 % at
+  // k = 64; fp16 rows and k = 32 were slower, profiles/r02/pstore*.jsonl);
+  // reductions elsewhere
   if constexpr (sizeof(S) == 4 && (CFG == 5 || CFG == 6)) {
-    if (chain_pstore<K, S, CFG>()) {
+    if (o.pstore == 1) {
       kstat = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, false, RowT, true>;
       kdyn = qchain_kernel<K, S, C::LPC, C::PD, C::WPB, C::MINB, true, RowT, true>;
     }
   }
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    const cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kstat, C::WPB * 32, 0);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-  }
+  const int smem = qdelta ? C::WPB * NC * K * int(sizeof(float)) : 0;
+  int per_sm = 0;
+  cudaError_t e =
+      kernel_occupancy(reinterpret_cast<const void*>(kstat), C::WPB * 32, smem, &per_sm);
+  if (e != cudaSuccess) return e;
   // a full grid (chains are spread CTA-minor, so even a block with few
   // sub-bands uses every SM); blocks with fewer sub-bands than CTAs need fewer
-  const int cap = grid_share(device_sm_count() * per_sm);
+  const int cap = grid_share(device_sm_count() * per_sm, o.share);
   const int grid = n_sub < cap ? n_sub : cap;
   if (grid <= 0) return cudaSuccess;
   // more sub-bands than chains: units are handed out dynamically (a static
@@ -534,15 +521,14 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
   const bool dyn = int64_t(n_sub) > int64_t(grid) * C::WPB * NC;
   unsigned* work = nullptr;
   if (dyn) {
-    const cudaError_t e = chain_work(stream, size_t(n_sub) + 1, &work);
+    e = chain_work(stream, size_t(n_sub) + 1, &work);
+    if (e != cudaSuccess) return e;
+    e = kernel_occupancy(reinterpret_cast<const void*>(kdyn), C::WPB * 32, smem, &per_sm);
     if (e != cudaSuccess) return e;
   }
   auto kern = dyn ? kdyn : kstat;
-  const int lockstep = dyn ? (g_chain_lockstep & 2) != 0 : (g_chain_lockstep & 1) != 0;
-  const int smem = qdelta ? C::WPB * NC * K * int(sizeof(float)) : 0;
-  // qdelta 1: bounded staleness (publish and re-read every g_qsync_steps);
-  // 2: publish at item and bin changes only (whole runs per sub-band)
-  const int qsync = qdelta == 1 && g_qsync_steps > 0 ? (g_qsync_steps + C::PD) / (C::PD + 1) : 0;
+  const int lockstep = dyn ? (o.lockstep & 2) != 0 : (o.lockstep & 1) != 0;
+  const int qsync = qdelta == 1 && o.qsync > 0 ? (o.qsync + C::PD) / (C::PD + 1) : 0;
   kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
                                          sub_ptr, sub_cuts, n_sub, n_tiles, tile_row0, float(lr),
                                          float(ru), float(ri), seed, work, lockstep, qdelta,
@@ -551,38 +537,26 @@ static cudaError_t launch_chain_cfg(S* P, S* Q, const RowT* rows, const int32_t*
 }
 
 // rows: int32 row ids, or uint16 (a row tile's ids relative to its first row:
-// 2 bytes per rating on the host stream; configurations 2, 4, 5 and 6 only).
-// The tile's first row is tile_row0[tile] (device, n_tiles entries) or, with
-// tile_row0 == nullptr, -row_base for every tile.
+// 2 bytes per rating on the host stream).  The tile's first row is
+// tile_row0[tile] (device, n_tiles entries) or, with tile_row0 == nullptr,
+// -row_base for every tile.
 template <int K, typename S, typename RowT = int32_t>
 static cudaError_t launch_chain(S* P, S* Q, const RowT* rows, const int32_t* cols,
                                 const float* vals, const int64_t* sub_ptr,
-                                const int32_t* sub_cuts, int n_sub, int n_tiles,
-                                double lr, double ru, double ri, uint64_t seed, int64_t row_base,
-                                int64_t col_base, cudaStream_t stream, int qdelta = 0,
+                                const int32_t* sub_cuts, int n_sub, int n_tiles, double lr,
+                                double ru, double ri, uint64_t seed, int64_t row_base,
+                                int64_t col_base, cudaStream_t stream, const LaunchOpts& o,
                                 const int32_t* tile_row0 = nullptr) {
 #define HMF_CHAIN_CFG(CFG)                                                                     \
   return launch_chain_cfg<K, S, CFG, RowT>(P, Q, rows, cols, vals, sub_ptr, sub_cuts, n_sub,  \
                                            n_tiles, tile_row0, lr, ru, ri, seed, row_base,     \
-                                           col_base, stream, qdelta)
-  if constexpr (sizeof(RowT) == 2) {
-    switch (chain_cfg<K, S>()) {
-      case 2: HMF_CHAIN_CFG(2);
-      case 4: HMF_CHAIN_CFG(4);
-      case 5: HMF_CHAIN_CFG(5);
-      case 6: HMF_CHAIN_CFG(6);
-      default: return cudaErrorNotSupported;
-    }
-  } else {
-    switch (chain_cfg<K, S>()) {
-      case 0: HMF_CHAIN_CFG(0);
-      case 2: HMF_CHAIN_CFG(2);
-      case 3: HMF_CHAIN_CFG(3);
-      case 4: HMF_CHAIN_CFG(4);
-      case 5: HMF_CHAIN_CFG(5);
-      case 6: HMF_CHAIN_CFG(6);
-      default: HMF_CHAIN_CFG(1);
-    }
+                                           col_base, stream, o)
+  switch (o.cfg) {
+    case 2: HMF_CHAIN_CFG(2);
+    case 4: HMF_CHAIN_CFG(4);
+    case 5: HMF_CHAIN_CFG(5);
+    case 6: HMF_CHAIN_CFG(6);
+    default: return cudaErrorInvalidValue;
   }
 #undef HMF_CHAIN_CFG
 }

@@ -420,16 +420,7 @@ __global__ void __launch_bounds__(32)
 // ---------------------------------------------------------------------------
 // Host-side launchers.
 // ---------------------------------------------------------------------------
-static int sm_count() {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    if (cached <= 0) cached = 148;
-  }
-  return cached;
-}
+static int sm_count() { return device_sm_count(); }
 
 static uint64_t gcd_u64(uint64_t a, uint64_t b) {
   while (b) {
@@ -451,13 +442,11 @@ static cudaError_t launch_hogwild_v(S* P, S* Q, const int32_t* rows, const int32
   constexpr int CH = ChunkOf<S>::CH;
   auto kern = sgd_hogwild_kernel<K, S, U, WPB, MINB, ATOMIC>;
   const int smem = WPB * warp_smem_bytes<S>();
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 0;
+  {
+    const cudaError_t e =
+        kernel_occupancy(reinterpret_cast<const void*>(kern), WPB * 32, smem, &per_sm);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
   }
   const int64_t a0 = start & ~int64_t(3);
   const int64_t n_chunks = (stop - a0 + CH - 1) / CH;
@@ -586,8 +575,9 @@ static cudaError_t launch_exact(S* P, S* Q, int k, const int32_t* rows, const in
                                 int64_t row_base, int64_t col_base, cudaStream_t stream) {
   const size_t smem = size_t(2) * size_t(k) * sizeof(S);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(sgd_exact_kernel<S>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 0;  // sets the shared-memory opt-in on this device
+    const cudaError_t e = kernel_occupancy(reinterpret_cast<const void*>(sgd_exact_kernel<S>), 32,
+                                           int(smem), &per_sm);
     if (e != cudaSuccess) return e;
   }
   sgd_exact_kernel<S><<<1, 32, smem, stream>>>(P, Q, rows, cols, vals, perm, start, n, k, lr, ru,

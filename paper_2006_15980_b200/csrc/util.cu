@@ -1,6 +1,9 @@
 // Error reporting, mix64, device/peer/IPC utilities and a device int64 scan.
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "hmf_common.cuh"
 #include "hmf_internal.h"
@@ -25,6 +28,34 @@ int device_sm_count() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   return n > 0 ? n : 148;
+}
+
+// Function attributes (the dynamic shared-memory opt-in above 48 KB) are per
+// device: set them and query the occupancy once per (kernel, device, shape).
+cudaError_t kernel_occupancy(const void* kern, int threads, int smem, int* per_sm) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, int>, int> cache;
+  const auto key = std::make_tuple(kern, dev, threads, smem);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *per_sm = it->second;
+    return cudaSuccess;
+  }
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  int n = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, size_t(smem));
+  if (e != cudaSuccess) return e;
+  if (n < 1) n = 1;
+  cache[key] = n;
+  *per_sm = n;
+  return cudaSuccess;
 }
 
 // ---------------------------------------------------------------------------

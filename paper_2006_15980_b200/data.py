@@ -17,6 +17,7 @@ Device side is the B200 layout the hot path reads:
 
 from __future__ import annotations
 
+import ctypes
 import struct
 from dataclasses import dataclass, field
 
@@ -376,6 +377,7 @@ class DeviceGrid:
     # sub_tiles[b] * S + 1 offsets, tile-major
     sub_tiles: list | None = None
     sub_impl: int = -1          # Q-band implementation the layout is for
+    sub_cfg: int = -1           # chain configuration it is for (-1: by k and storage)
     sub_tile_rows: list | None = None   # per block: row cuts of its tiles (host int64)
     sub_split: int = 1                  # parts per item run (implementation 5)
     sub_qsync: int = 0                  # Q publication period for implementation 5
@@ -444,26 +446,25 @@ def build_device_grid(triples: DeviceTriples, row_cuts, col_cuts, region_of_row=
                       sub_row_parent, out_u, out_i, out_r, ptr)
 
 
-def resident_warps(device, k: int = 128, f16: bool = False, impl: int = -1) -> int:
-    """Sub-band slots the Q-band kernel keeps resident on `device` (warps, or
-    lane-group chains for implementation 4): SMs x slots per SM."""
+def resident_warps(device, k: int = 128, f16: bool = False, impl: int = -1,
+                   chain_cfg: int = -1) -> int:
+    """Sub-band slots the Q-band kernel keeps resident on `device` (warps for
+    implementation 0, lane-group chains for 4-6): SMs x slots per SM of that
+    launch shape (hmf_qband_slots_per_sm, per-device occupancy)."""
     torch = _torch()
+    opts = _lib.QbandOpts(impl=int(impl), chain_cfg=int(chain_cfg))
     with torch.cuda.device(device):
-        per_sm = int(_lib.load().hmf_qband_slots_per_sm(int(k), 1 if f16 else 0, int(impl)))
+        per_sm = int(_lib.load().hmf_qband_slots_per_sm(int(k), 1 if f16 else 0,
+                                                         ctypes.byref(opts)))
     return int(torch.cuda.get_device_properties(device).multi_processor_count) * max(per_sm, 1)
 
 
 def qband_impl_for(device, k: int, f16: bool, n_items: int) -> int:
-    """The Q-band implementation a grid is laid out and launched for: the
-    process default (hmf_qband_set_impl) when one is set, else the library's
-    automatic choice (hmf_qband_resolve_impl): the chained kernel with Q
-    deltas (5), whose layout splits item runs only when a block has fewer
-    items than chains (bucket_qbands)."""
-    lib = _lib.load()
-    impl = int(lib.hmf_qband_get_impl())
-    if impl >= 0:
-        return impl
-    return int(lib.hmf_qband_resolve_impl(int(k), 1 if f16 else 0))
+    """The Q-band implementation a grid is laid out and launched for when the
+    caller names none: the library's default (hmf_qband_resolve_impl), the
+    chained kernel with Q deltas (5), whose layout splits item runs only when
+    a block has fewer items than chains (bucket_qbands)."""
+    return int(_lib.load().hmf_qband_resolve_impl(int(k), 1 if f16 else 0))
 
 
 def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int, cap: int | None = None) -> np.ndarray:
@@ -471,7 +472,7 @@ def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int, cap: int | None = 
     (one per resident warp or chain), never more than the items, and at most
     `cap` items wide (the kernel's Q-slice bound; default hmf_qband_max_items)."""
     items = c_hi - c_lo
-    cap = int(_lib.load().hmf_qband_max_items(k)) if cap is None else int(cap)
+    cap = int(_lib.load().hmf_qband_max_items(int(k), 0, -1)) if cap is None else int(cap)
     if cap <= 0:
         raise ValueError(f"Q-band kernel does not support k={k}")
     n_sub = min(items, max(target, -(-items // cap)))
@@ -543,7 +544,7 @@ def qband_split_for(slots: int, items: int, block_nnz: float, n_tiles: int, k: i
 def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
                   tile_bytes: int | None = None, elem_bytes: int = 4,
                   impl: int | None = None, split: int | None = None,
-                  max_tile_rows: int | None = None) -> DeviceGrid:
+                  max_tile_rows: int | None = None, chain_cfg: int = -1) -> DeviceGrid:
     """Re-bucket every block of a device grid for the Q-band kernel, in place:
     row tile major, then item (both stable), and attach sub_ptr / sub_cuts /
     sub_tiles.  Row tiles are equal user ranges of the block's row band, sized
@@ -564,9 +565,12 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     lib = _lib.load()
     s = _stream(dev)
     f16 = elem_bytes == 2
-    # an implementation asked for (argument or process default) keeps its
-    # layout rules; the automatic choice also splits hot items' runs
-    auto = impl is None and int(lib.hmf_qband_get_impl()) < 0
+    # an implementation asked for keeps its layout rules; the automatic
+    # choice (None or -1) also splits hot items' runs
+    if impl is not None and int(impl) < 0:
+        impl = None
+    auto = impl is None
+    chain_cfg = int(chain_cfg)
     split_given = split is not None
     if impl is None:
         impl = qband_impl_for(dev, k, f16, max((grid.col_span(c)[1] - grid.col_span(c)[0]
@@ -580,7 +584,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         rows = max((grid.row_span(b // grid.n_col_bands)[1] - grid.row_span(b // grid.n_col_bands)[0]
                     for b in full), default=1)
         split = 1 if target is not None else qband_split_for(
-            resident_warps(dev, k, f16, 5), widest,
+            resident_warps(dev, k, f16, 5, chain_cfg), widest,
             float(np.mean(sizes[full])) if full else 0.0,
             qband_row_tiles(rows, k, elem_bytes, tile_bytes, max_tile_rows), k, f16)
     split = 1 if impl != 5 or not split else int(split)
@@ -590,11 +594,11 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         # one sub-band per resident slot; for the chained kernel with at least
         # twice as many items as chains, narrower sub-bands (up to 4 per
         # chain) that its dynamic scheduler balances (qchain.cuh)
-        target = resident_warps(dev, k, f16, impl)
+        target = resident_warps(dev, k, f16, impl, chain_cfg)
         if impl >= 4 and widest >= 2 * target:
             target = min(widest, 4 * target)
     target = int(target)
-    cap = int(lib.hmf_qband_max_items_for(int(k), 1 if f16 else 0, impl))
+    cap = int(lib.hmf_qband_max_items(int(k), 1 if f16 else 0, impl))
     out_u = torch.empty_like(grid.users)
     out_i = torch.empty_like(grid.items)
     out_r = torch.empty_like(grid.ratings)
@@ -703,9 +707,10 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         # side by side on Q deltas without hand-off waits, published at item
         # changes only (implementation 6; Yahoo 9.7 vs 9.1 G upd/s with the
         # 16-rating publication, RMSE equal)
-        slots = resident_warps(dev, k, f16, 4)
+        slots = resident_warps(dev, k, f16, 4, chain_cfg)
         impl = 4 if all(len(c) - 1 <= slots for c in sub_cuts) else 6
     grid.sub_impl = impl
+    grid.sub_cfg = chain_cfg
     grid.sub_split = split
     # Q publication period for split runs, bounding an item's steps in
     # flight across its parts (parts x period): ~128 when hot items are split
@@ -725,7 +730,7 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     # its P change)
     min_rows = min((int(np.min(np.diff(r))) for r in tile_rows if len(r) > 1), default=0)
     grid.sub_pstore = int(impl >= 4 and not f16 and k >= 128
-                          and min_rows >= 4 * resident_warps(dev, k, f16, impl))
+                          and min_rows >= 4 * resident_warps(dev, k, f16, impl, chain_cfg))
     return grid
 
 

@@ -29,6 +29,7 @@ CPU transport over gloo (world size 2).
 
 from __future__ import annotations
 
+import ctypes
 import time
 import uuid
 
@@ -301,9 +302,7 @@ class CudaRowBand:
         torch = self.torch
         if on and self.host is None:
             g = self.grid
-            cfg = int(self.lib.load().hmf_qband_get_chain_cfg())
             compact = (self.kernel == "qband" and (g.sub_impl or 0) >= 4
-                       and cfg in (-1, 2, 4, 5, 6)
                        and all(bool(torch.all(sc[1:] - sc[:-1] <= 1)) for sc in g.sub_cuts)
                        and all(len(r) < 2 or int(np.max(np.diff(r))) <= 65536
                                for r in g.sub_tile_rows))
@@ -334,15 +333,14 @@ class CudaRowBand:
         g = self.grid
         lo, hi = g.block_range(b)
         sp, sc = g.sub_ptr[b], g.sub_cuts[b]
-        kernels.set_qsync(g)
-        kernels.set_pstore(g)
+        opts = kernels.qband_opts(g, grid_share=self.concurrency)
         lib = self.lib.load()
         st = "f16" if self.P.dtype == self.torch.float16 else "f32"
         fn = getattr(lib, f"hmf_sgd_block_qband_u16_tiles_{st}")
         self.lib.check(fn(self.P.data_ptr(), self.Q.data_ptr(), self.k, self.dev_rel.data_ptr(),
                           0, g.ratings.data_ptr(), sp.data_ptr(), sc.data_ptr(),
                           int(sc.numel()) - 1, int(g.sub_tiles[b]),
-                          self.compact[b].data_ptr(), int(g.sub_impl), float(self.lr),
+                          self.compact[b].data_ptr(), ctypes.byref(opts), float(self.lr),
                           float(self.ru), float(self.ri), int(seed) & kernels._MASK64, 0,
                           stream.cuda_stream), "hmf_sgd_block_qband_u16_tiles")
         return hi - lo
@@ -368,25 +366,18 @@ class CudaRowBand:
                 up.record(self.copy_stream)
             stream.wait_event(up)
         if staging and self.compact is not None:
-            lib = self.lib.load()
-            lib.hmf_qband_set_grid_share(self.concurrency)
-            try:
-                n = self._launch_compact(b, seed, stream)
-            finally:
-                lib.hmf_qband_set_grid_share(1)
+            n = self._launch_compact(b, seed, stream)
             ev = self.torch.cuda.Event()
             ev.record(stream)
             self.done_events[c] = ev
             return n
         if self.kernel == "qband":
-            lib = self.lib.load()
-            lib.hmf_qband_set_grid_share(self.concurrency)
-            try:
-                n = kernels.launch_block_qband(self.P, self.Q, self.grid, b, self.lr, self.ru,
-                                               self.ri, seed, row_base=self.row_lo,
-                                               stream=stream.cuda_stream)
-            finally:
-                lib.hmf_qband_set_grid_share(1)
+            # several column blocks in flight: each launch fills 1/concurrency
+            # of the GPU (a per-launch option, ABI 4)
+            n = kernels.launch_block_qband(self.P, self.Q, self.grid, b, self.lr, self.ru,
+                                           self.ri, seed, row_base=self.row_lo,
+                                           stream=stream.cuda_stream,
+                                           opts={"grid_share": self.concurrency})
         else:   # "range" (HOGWILD) or "exact" (reference order and arithmetic)
             n = kernels.launch_sgd_range(self.P, self.Q, self.grid.users, self.grid.items,
                                          self.grid.ratings, lo, hi, self.lr, self.ru, self.ri,

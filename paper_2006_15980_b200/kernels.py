@@ -20,6 +20,9 @@ There is no CPU path: without the CUDA library every call raises.
 
 from __future__ import annotations
 
+import ctypes
+import threading
+
 import numpy as np
 
 from . import _lib
@@ -105,37 +108,43 @@ def launch_sgd_range(user_f, item_f, rows, cols, vals, start, stop, lr, reg_user
     return _lib.check(got, f"hmf_sgd_range_{st}")
 
 
-# Q publication period for every launch (None: the layout's grid.sub_qsync)
-QSYNC_OVERRIDE: int | None = None
+QbandOpts = _lib.QbandOpts
 
 
-def set_qsync(grid) -> None:
-    """The layout's Q publication period (data.bucket_qbands; a grid or the
-    period itself), or QSYNC_OVERRIDE if set, for the launches that follow
-    (process-wide setting, hmf_qband_set_qsync)."""
-    q = int(grid if isinstance(grid, int) else (getattr(grid, "sub_qsync", 0) or 0))
-    if QSYNC_OVERRIDE is not None:
-        q = int(QSYNC_OVERRIDE)
-    if q > 0:
-        _lib.check(_lib.load().hmf_qband_set_qsync(q), "hmf_qband_set_qsync")
+def qband_opts(grid=None, **overrides) -> "QbandOpts":
+    """The per-launch options (hmf_qband_opts, ABI 4) of a layout: what
+    data.bucket_qbands chose for `grid` (sub_impl, sub_cfg, sub_pstore,
+    sub_qsync), then every override that is not None (impl, chain_cfg,
+    pstore, qsync, grid_share, lockstep).  Options travel with each launch;
+    nothing is process-wide, so threads launching different layouts at once
+    do not interfere."""
+    vals = {}
+    if grid is not None:
+        impl = getattr(grid, "sub_impl", None)
+        vals["impl"] = -1 if impl is None else int(impl)
+        cfg = getattr(grid, "sub_cfg", None)
+        vals["chain_cfg"] = -1 if cfg is None else int(cfg)
+        vals["pstore"] = int(getattr(grid, "sub_pstore", 0) or 0)
+        q = int(getattr(grid, "sub_qsync", 0) or 0)
+        vals["qsync"] = q if q > 0 else -1
+    vals.update({k: v for k, v in overrides.items() if v is not None})
+    return QbandOpts(**vals)
 
 
-# P write-back of the chained kernel for every launch (None: the layout's
-# grid.sub_pstore, data.bucket_qbands; 0 reductions, 1 stores)
-PSTORE_OVERRIDE: int | None = None
-
-
-def set_pstore(grid) -> None:
-    """The P write-back for the launches that follow: PSTORE_OVERRIDE if set,
-    else the layout's choice (process-wide setting, hmf_qband_set_pstore)."""
-    v = PSTORE_OVERRIDE if PSTORE_OVERRIDE is not None else int(getattr(grid, "sub_pstore", 0) or 0)
-    _lib.check(_lib.load().hmf_qband_set_pstore(int(v)), "hmf_qband_set_pstore")
+def _as_opts(grid, opts) -> "QbandOpts":
+    if opts is None:
+        return qband_opts(grid)
+    if isinstance(opts, QbandOpts):
+        return opts
+    return qband_opts(grid, **dict(opts))
 
 
 def launch_block_qband(user_f, item_f, grid, block, lr, reg_user, reg_item, seed, row_base=0,
-                       col_base=0, stream=None) -> int:
+                       col_base=0, stream=None, opts=None) -> int:
     """Q-band-stationary update of one block of a DeviceGrid bucketed by
-    data.bucket_qbands (the engine fast path).  Returns triples processed."""
+    data.bucket_qbands (the engine fast path).  `opts`: a QbandOpts, a dict
+    of overrides of the layout's options, or None (the layout's).  Returns
+    triples processed."""
     _check_factor(user_f, "user_f")
     _check_factor(item_f, "item_f")
     if grid.sub_ptr is None:
@@ -152,14 +161,12 @@ def launch_block_qband(user_f, item_f, grid, block, lr, reg_user, reg_item, seed
     if int(sp.numel()) != n_tiles * n_sub + 1:
         raise ValueError("sub_ptr does not match sub_cuts x sub_tiles")
     s = current_stream_handle(user_f.device) if stream is None else int(stream)
-    set_qsync(grid)
-    set_pstore(grid)
+    o = _as_opts(grid, opts)
     fn = getattr(_lib.load(), f"hmf_sgd_block_qband_{st}")
     _lib.check(fn(user_f.data_ptr(), item_f.data_ptr(), user_f.shape[1], grid.users.data_ptr(),
                   grid.items.data_ptr(), grid.ratings.data_ptr(), sp.data_ptr(), sc.data_ptr(),
-                  n_sub, n_tiles, int(grid.sub_impl), float(lr), float(reg_user),
-                  float(reg_item),
-                  int(seed) & _MASK64, int(row_base), int(col_base), s),
+                  n_sub, n_tiles, ctypes.byref(o), float(lr), float(reg_user),
+                  float(reg_item), int(seed) & _MASK64, int(row_base), int(col_base), s),
                f"hmf_sgd_block_qband_{st}")
     return hi - lo
 
@@ -185,6 +192,32 @@ def sgd_range(user_f, item_f, rows, cols, vals, start, stop, lr, reg_user, reg_i
     if stop - start <= 0:
         return 0
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    # One call at a time per pair of host factor arrays: each call uploads
+    # both arrays whole and writes them back whole, so two concurrent calls
+    # on the same arrays (the reference's BatchEngine lanes, workers.py:
+    # 244-255) would otherwise overwrite each other's updates.  Serialised,
+    # every call sees all updates of the calls before it.
+    with _host_lock(user_f, item_f):
+        return _sgd_range_host(user_f, item_f, rows, cols, vals, start, stop, lr, reg_user,
+                               reg_item, seed, row_base, col_base, mode, stream, dev)
+
+
+_host_locks: dict = {}
+_host_locks_guard = threading.Lock()
+
+
+def _host_lock(user_f, item_f):
+    key = (user_f.__array_interface__["data"][0], item_f.__array_interface__["data"][0])
+    with _host_locks_guard:
+        lock = _host_locks.get(key)
+        if lock is None:
+            lock = _host_locks[key] = threading.Lock()
+        return lock
+
+
+def _sgd_range_host(user_f, item_f, rows, cols, vals, start, stop, lr, reg_user, reg_item, seed,
+                    row_base, col_base, mode, stream, dev) -> int:
+    torch = _torch()
     st = _storage_of(user_f.dtype)
     vdt = np.float64 if st == "f64" else np.float32
     lo = start & ~3  # keep the device triple arrays 16-byte aligned at `lo`
@@ -195,6 +228,8 @@ def sgd_range(user_f, item_f, rows, cols, vals, start, stop, lr, reg_user, reg_i
     d_q = torch.from_numpy(item_f).to(dev, non_blocking=True)
     got = launch_sgd_range(d_p, d_q, d_rows, d_cols, d_vals, start - lo, stop - lo, lr, reg_user,
                            reg_item, seed, row_base, col_base, mode, stream)
+    if stream is not None:
+        torch.cuda.synchronize(dev)
     torch.from_numpy(user_f).copy_(d_p, non_blocking=False)
     torch.from_numpy(item_f).copy_(d_q, non_blocking=False)
     return got

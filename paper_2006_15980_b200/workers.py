@@ -31,6 +31,7 @@ GPU with sleeps and CPU lanes; here:
 
 from __future__ import annotations
 
+import ctypes
 import threading
 import time
 from dataclasses import dataclass, field
@@ -173,6 +174,11 @@ class FactorStore:
         moved = 0
         with self.lock:
             runs = self._runs(home, lo, hi)
+            mine = self.events.get(dev)
+        # work already recorded on dev's rows (a gather on the copy stream,
+        # another engine's compute) completes before `stream` touches them
+        if mine is not None:
+            stream.wait_event(mine)
         for a, b, h in runs:
             if h == dev:
                 continue
@@ -222,6 +228,13 @@ class FactorStore:
         s = self.copy_stream(dev)
         self.bring("p", dev, 0, self.model.n_users, s)
         self.bring("q", dev, 0, self.model.n_items, s)
+        # every row is now homed on dev and complete at this event: other
+        # devices' pulls from dev and dev's own engine stream order on it
+        # (through events[dev]), not only the caller's current stream
+        ev = torch.cuda.Event()
+        ev.record(s)
+        with self.lock:
+            self.events[dev] = ev
         torch.cuda.current_stream(dev).wait_stream(s)
         return self.replicas[dev]
 
@@ -481,23 +494,25 @@ class StreamingEpoch:
 
     def __init__(self, grid: DeviceGrid, k: int, tile_bytes=None, n_buffers: int = 3,
                  elem_bytes: int = 4, compact: bool = True, tiles_per_chunk: int = 4,
-                 last_chunk_tiles: int = 0, reuse: bool = False):
+                 last_chunk_tiles: int = 0, reuse: bool = False, opts=None, impl=None):
         torch = _torch()
         self.dev = grid.device
         # a grid the caller already laid out for the Q-band kernel is used as is
         sg = grid if grid.sub_ptr is not None else bucket_qbands(
-            grid, k, tile_bytes=tile_bytes, elem_bytes=elem_bytes)
+            grid, k, tile_bytes=tile_bytes, elem_bytes=elem_bytes, impl=impl)
         self.k = k
         self.nnz = sg.nnz
         self.sub_impl = sg.sub_impl
         self.qsync = sg.sub_qsync
         self.sub_pstore = sg.sub_pstore
+        # the launch options of this layout (plus explicit overrides), passed
+        # with every launch (ABI 4: nothing process-wide)
+        self.opts = kernels.qband_opts(sg, **dict(opts or {}))
         self.reuse = bool(reuse)
         # every sub-band a single item (or a part of one): the item is implicit
         self.implicit_items = compact and sg.sub_impl >= 4 and all(
             bool(torch.all(c[1:] - c[:-1] <= 1)) for c in sg.sub_cuts)
-        cfg_ok = int(_lib.load().hmf_qband_get_chain_cfg()) in (-1, 2, 4, 5, 6)
-        self.u16 = self.implicit_items and cfg_ok and all(
+        self.u16 = self.implicit_items and all(
             int(np.max(np.diff(r))) <= 65536 for r in sg.sub_tile_rows)
         # chunks: G consecutive row tiles of a block -> [lo, hi) of the
         # bucketed arrays, the number of tiles, their sub-band offsets relative
@@ -586,8 +601,6 @@ class StreamingEpoch:
             resident = [ch for ch in reversed(self.lru) if ch is not None]
             head = [o for ch in resident for o in order if (o[0], o[1]) == ch]
             order = head + [o for o in order if (o[0], o[1]) not in resident]
-        kernels.set_qsync(self.qsync)
-        kernels.set_pstore(self)
         done, uploaded = 0, 0
         for b, t, bseed in order:
             chunks, sc = self.blocks[b]
@@ -625,10 +638,10 @@ class StreamingEpoch:
                     buf[-1].data_ptr(), rel.data_ptr(), sc.data_ptr(), int(sc.numel()) - 1,
                     n_tiles)
             if self.u16:        # tile-relative uint16 ids, first rows per tile
-                args += (trow.data_ptr(), self.sub_impl, hparams.learning_rate,
+                args += (trow.data_ptr(), ctypes.byref(self.opts), hparams.learning_rate,
                          hparams.reg_user, hparams.reg_item, tseed, 0, comp.cuda_stream)
             else:
-                args += (self.sub_impl, hparams.learning_rate, hparams.reg_user,
+                args += (ctypes.byref(self.opts), hparams.learning_rate, hparams.reg_user,
                          hparams.reg_item, tseed, 0, 0, comp.cuda_stream)
             if tr is not None:
                 tr["k0"] = torch.cuda.Event(enable_timing=True)

@@ -41,17 +41,26 @@ def test_binding_matches_header():
 def test_host_only_entry_points():
     from paper_2006_15980_b200 import _lib, kernels
     lib = _lib.load()
-    assert lib.hmf_abi_version() == 3
+    assert lib.hmf_abi_version() == _lib.ABI_VERSION == 4
     for parts in [(0,), (7, 3, 1), (2 ** 63 - 1, 5), (123456789, 42, 17, 3)]:
         assert _lib.mix64_native(*parts) == kernels.mix64(*parts)
     # argument validation happens before any device work
     assert lib.hmf_visit_order(-1, 0, None, None) == _lib.HMF_ERR_ARG
     assert "out of range" in _lib.last_error()
     assert lib.hmf_set_tuning(99, 0) == _lib.HMF_ERR_ARG
-    assert lib.hmf_qband_set_pstore(2) == _lib.HMF_ERR_ARG
-    assert lib.hmf_qband_get_pstore() in (-1, 0)
-    assert lib.hmf_qband_set_pstore(0) == 0 and lib.hmf_qband_get_pstore() == 0
-    assert lib.hmf_qband_set_pstore(-1) == 0
+    # per-launch options are validated before any device work (ABI 4)
+    import ctypes
+    args = (None, None, 128, None, None, None, None, None, 4, 1)
+    tail = (0.01, 0.0, 0.0, 0, 0, 0, None)
+    for bad in ({"pstore": 2}, {"impl": 1}, {"impl": 3}, {"chain_cfg": 0}, {"chain_cfg": 3},
+                {"grid_share": 0}, {"grid_share": 65}, {"lockstep": 4}, {"qsync": -2}):
+        o = _lib.QbandOpts(**bad)
+        assert lib.hmf_sgd_block_qband_f32(*args, ctypes.byref(o), *tail) == _lib.HMF_ERR_ARG, bad
+    assert lib.hmf_qband_resolve_impl(128, 0) == 5
+    assert [lib.hmf_qband_resolve_chain_cfg(k, f) for k in (32, 64, 128, 256) for f in (0, 1)] \
+        == [2, 2, 2, 4, 5, 6, 5, 6]
+    assert [lib.hmf_qband_chain_lanes(k, 0, -1) for k in (32, 64, 128, 256)] == [4, 8, 8, 16]
+    assert lib.hmf_qband_max_items(128, 0, 0) == 8 and lib.hmf_qband_max_items(128, 0, 5) == 1 << 30
     assert lib.hmf_sgd_range_f32(None, None, 4, None, None, None, 0, 0, 0.1, 0, 0, 0, 0, 0, 0,
                                  None) == 0  # empty range: nothing to do, no error
 

@@ -3,6 +3,8 @@ modelled on the reference's tests/test_workers.py and test_acceptance.py."""
 
 import json
 
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -164,16 +166,11 @@ def test_streaming_epoch_applies_every_triple_once(dev, k, impl, tiles, last):
     m = RatingMatrix(9000, 7000, users, items, vals)
     d = torch.device("cuda", dev)
     g = build_device_grid(DeviceTriples.from_host(m, d), [0, 9000], [0, 3500, 7000])
-    from paper_2006_15980_b200 import _lib
-    _lib.check(_lib.load().hmf_qband_set_impl(impl), "set_impl")
-    try:
-        se = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1,   # 3 row tiles per block
-                            tiles_per_chunk=tiles, last_chunk_tiles=last, n_buffers=2,
-                            reuse=True)
-        se_all = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1, tiles_per_chunk=tiles,
-                                last_chunk_tiles=last, reuse=False)
-    finally:
-        _lib.load().hmf_qband_set_impl(-1)
+    se = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1,   # 3 row tiles per block
+                        tiles_per_chunk=tiles, last_chunk_tiles=last, n_buffers=2,
+                        reuse=True, impl=impl)
+    se_all = StreamingEpoch(g, k, tile_bytes=9000 * k * 4 // 3 + 1, tiles_per_chunk=tiles,
+                            last_chunk_tiles=last, reuse=False, impl=impl)
     assert se.n_chunks == 2 * ((1 + -(-2 // tiles)) if last else -(-3 // tiles))
     P0 = rng.uniform(0, 0.1, size=(9000, k)).astype(np.float32)
     Q0 = rng.uniform(0, 0.1, size=(7000, k)).astype(np.float32)
@@ -219,31 +216,82 @@ def test_u16_single_tile_entry_equals_tiles_entry(dev):
     d = torch.device("cuda", dev) if isinstance(dev, int) else dev
     m = RatingMatrix(n_users, n_items, users, items, vals)
     g = build_device_grid(DeviceTriples.from_host(m, d), [0, n_users], [0, n_items])
-    _lib.check(lib.hmf_qband_set_impl(4), "set_impl")
-    try:
-        bucket_qbands(g, k, tile_bytes=0, target=n_items)
-        assert g.sub_tiles == [1] and g.sub_impl == 4
-        sc, sp = g.sub_cuts[0], g.sub_ptr[0]
-        assert bool(torch.all(sc[1:] - sc[:-1] == 1))      # one item per sub-band: cols = NULL
-        rel16 = (g.users - 10_000).to(torch.int32).to(torch.int16)
-        first = torch.tensor([10_000], dtype=torch.int32, device=d)
+    bucket_qbands(g, k, tile_bytes=0, target=n_items, impl=4)
+    assert g.sub_tiles == [1] and g.sub_impl == 4
+    sc, sp = g.sub_cuts[0], g.sub_ptr[0]
+    assert bool(torch.all(sc[1:] - sc[:-1] == 1))      # one item per sub-band: cols = NULL
+    rel16 = (g.users - 10_000).to(torch.int32).to(torch.int16)
+    first = torch.tensor([10_000], dtype=torch.int32, device=d)
+    P0 = rng.uniform(0, 0.1, size=(n_users, k)).astype(np.float32)
+    Q0 = rng.uniform(0, 0.1, size=(n_items, k)).astype(np.float32)
+    opts = _lib.QbandOpts(impl=4)
+    out = []
+    for tiles in (False, True):
+        P, Q = torch.from_numpy(P0).to(d), torch.from_numpy(Q0).to(d)
+        s = torch.cuda.current_stream(d).cuda_stream
+        head = (P.data_ptr(), Q.data_ptr(), k, rel16.data_ptr(), 0, g.ratings.data_ptr(),
+                sp.data_ptr(), sc.data_ptr(), int(sc.numel()) - 1, 1)
+        if tiles:
+            got = lib.hmf_sgd_block_qband_u16_tiles_f32(*head, first.data_ptr(),
+                                                         ctypes.byref(opts), 0.05, 0.02, 0.03, 5,
+                                                         0, s)
+        else:
+            got = lib.hmf_sgd_block_qband_u16_f32(*head, ctypes.byref(opts), 0.05, 0.02, 0.03, 5,
+                                                   -10_000, 0, s)
+        _lib.check(got, "u16 entry")
+        torch.cuda.synchronize(d)
+        out.append((P.cpu().numpy(), Q.cpu().numpy()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert not np.array_equal(out[0][0], P0)
+
+
+def test_concurrent_layouts_equal_serial(dev):
+    """ABI 4: launch options are per call.  Two threads launch two different
+    layouts at once (implementation 4 with P by stores, configuration 5;
+    implementation 0, warp per rating), each on its own stream and factors.
+    With distinct users and whole item runs both kernels are deterministic, so
+    the concurrent results equal the serial ones bit for bit — impossible
+    when options were process-wide (one thread's settings leaked into the
+    other's launches)."""
+    import threading
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import (DeviceTriples, RatingMatrix, bucket_qbands,
+                                            build_device_grid)
+    d = torch.device("cuda", dev) if isinstance(dev, int) else dev
+    rng = np.random.default_rng(31)
+    k, n_users, n_items, n = 128, 60_000, 400, 30_000
+    cases = []
+    for impl, opts in ((4, {"pstore": 1, "chain_cfg": 5}), (0, {})):
+        users = rng.permutation(n_users)[:n].astype(np.int32)
+        items = rng.integers(0, n_items, n).astype(np.int32)
+        vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
+        m = RatingMatrix(n_users, n_items, users, items, vals)
+        g = build_device_grid(DeviceTriples.from_host(m, d), [0, n_users], [0, n_items])
+        bucket_qbands(g, k, impl=impl, target=n_items if impl else 50, tile_bytes=0)
+        assert g.sub_impl == impl
         P0 = rng.uniform(0, 0.1, size=(n_users, k)).astype(np.float32)
         Q0 = rng.uniform(0, 0.1, size=(n_items, k)).astype(np.float32)
-        out = []
-        for tiles in (False, True):
+        cases.append((g, opts, P0, Q0))
+
+    def run(case, stream, out, i, reps=20):
+        g, opts, P0, Q0 = case
+        with torch.cuda.stream(stream):
             P, Q = torch.from_numpy(P0).to(d), torch.from_numpy(Q0).to(d)
-            s = torch.cuda.current_stream(d).cuda_stream
-            head = (P.data_ptr(), Q.data_ptr(), k, rel16.data_ptr(), 0, g.ratings.data_ptr(),
-                    sp.data_ptr(), sc.data_ptr(), int(sc.numel()) - 1, 1)
-            if tiles:
-                got = lib.hmf_sgd_block_qband_u16_tiles_f32(*head, first.data_ptr(), 4, 0.05, 0.02,
-                                                             0.03, 5, 0, s)
-            else:
-                got = lib.hmf_sgd_block_qband_u16_f32(*head, 4, 0.05, 0.02, 0.03, 5, -10_000, 0, s)
-            _lib.check(got, "u16 entry")
-            torch.cuda.synchronize(d)
-            out.append((P.cpu().numpy(), Q.cpu().numpy()))
-        assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
-        assert not np.array_equal(out[0][0], P0)
-    finally:
-        lib.hmf_qband_set_impl(-1)
+            for r in range(reps):
+                kernels.launch_block_qband(P, Q, g, 0, 0.01, 0.02, 0.03, 50 + r,
+                                           stream=stream.cuda_stream, opts=opts)
+            stream.synchronize()
+            out[i] = (P.cpu().numpy(), Q.cpu().numpy())
+
+    streams = [torch.cuda.Stream(device=d) for _ in cases]
+    serial = [None, None]
+    for i, c in enumerate(cases):
+        run(c, streams[i], serial, i)
+    conc = [None, None]
+    ts = [threading.Thread(target=run, args=(c, streams[i], conc, i)) for i, c in enumerate(cases)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for a, b in zip(serial, conc):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])

@@ -11,6 +11,7 @@ Bars (north star, BASELINE.json):
   * residual sums match the oracle; bucketing equals build_grid bit for bit.
 """
 
+import contextlib
 import json
 
 import numpy as np
@@ -371,12 +372,29 @@ def test_ml1m_quality_within_0005_of_reference(dev):
 # ---------------------------------------------------------------------------
 # Q-band-stationary kernel
 # ---------------------------------------------------------------------------
+# The Q-band implementation / chain configuration the helpers lay grids out
+# for (None / -1: the library's defaults).  Launches take the layout's
+# options from the grid (ABI 4: per-launch, nothing process-wide).
+_LAYOUT = {"impl": None, "cfg": -1}
+
+
+@contextlib.contextmanager
+def layout(impl=None, cfg=-1):
+    old = dict(_LAYOUT)
+    _LAYOUT.update(impl=impl, cfg=cfg)
+    try:
+        yield
+    finally:
+        _LAYOUT.update(old)
+
+
 def _qband_grid(dev, m, k, col_cuts, target, tile_bytes=None):
     """An explicit tile_bytes sets the tile count alone (no user cap)."""
     from paper_2006_15980_b200.data import DeviceTriples, bucket_qbands, build_device_grid
     g = build_device_grid(DeviceTriples.from_host(m, dev), [0, m.n_users], col_cuts)
     return bucket_qbands(g, k, target=target, tile_bytes=tile_bytes,
-                         max_tile_rows=None if tile_bytes is None else 0)
+                         max_tile_rows=None if tile_bytes is None else 0,
+                         impl=_LAYOUT["impl"], chain_cfg=_LAYOUT["cfg"])
 
 
 def _fin(z):
@@ -387,9 +405,10 @@ def _fin(z):
 
 
 def _chain_lanes(k):
-    """Lanes per chain of Q-band implementation 4 (qchain.cuh ChainCfg)."""
+    """Lanes per chain of the chained kernel (qchain.cuh ChainCfg) in the
+    current layout's configuration."""
     from paper_2006_15980_b200 import _lib
-    return int(_lib.load().hmf_qband_chain_lanes(k))
+    return int(_lib.load().hmf_qband_chain_lanes(k, 0, _LAYOUT["cfg"]))
 
 
 def _bin_visit(impl, k, beg, end, seed, bin_index):
@@ -468,23 +487,18 @@ def test_qband_bucketing_contract(dev, k):
         lo, hi = g.block_range(b)
         assert ptr[0] == lo and ptr[-1] == hi
         from paper_2006_15980_b200 import _lib
-        assert np.max(np.diff(cuts)) <= _lib.load().hmf_qband_max_items(k)
+        assert np.max(np.diff(cuts)) <= _lib.load().hmf_qband_max_items(k, 0, -1)
         for s in range(len(cuts) - 1):
             seg = items[ptr[s]:ptr[s + 1]]
             assert np.all((seg >= cuts[s]) & (seg < cuts[s + 1]))
 
 
-@pytest.fixture(params=[(4, -1), (4, 1), (4, 2), (3, -1), (2, -1), (1, -1), (0, -1)],
-                ids=["chains", "chains_cfg1", "chains_cfg2", "regs_deep", "cpasync", "tma",
-                     "regs"])
+@pytest.fixture(params=[(4, -1), (4, 2), (4, 4), (4, 6), (0, -1)],
+                ids=["chains", "chains_cfg2", "chains_cfg4", "chains_cfg6", "regs"])
 def qband_impl(request):
-    from paper_2006_15980_b200 import _lib
     impl, cfg = request.param
-    _lib.check(_lib.load().hmf_qband_set_impl(impl), "set_impl")
-    _lib.check(_lib.load().hmf_qband_set_chain_cfg(cfg), "set_chain_cfg")
-    yield impl
-    _lib.load().hmf_qband_set_impl(-1)
-    _lib.load().hmf_qband_set_chain_cfg(-1)
+    with layout(impl, cfg):
+        yield impl
 
 
 @pytest.mark.parametrize("k", [32, 64, 128, 256])
@@ -539,7 +553,7 @@ def test_qband_ml1m_quality_within_0005_of_reference(dev, qband_impl, tile_bytes
     hp = Hyperparams(n_factors=32, reg_user=0.01, reg_item=0.01, learning_rate=0.01)
     grid = DeviceGrid.from_host(build_grid(shuffle_triples(train, 0), [0, 6040], [0, 1853, 3706]),
                                 dev)
-    bucket_qbands(grid, 32, tile_bytes=tile_bytes)
+    bucket_qbands(grid, 32, tile_bytes=tile_bytes, impl=_LAYOUT["impl"], chain_cfg=_LAYOUT["cfg"])
     assert grid.sub_tiles == ([1, 1] if tile_bytes is None else [8, 8])
     model = DeviceModel.from_host(init_model(6040, 3706, hp, 0), dev)
     got = {}
@@ -607,8 +621,7 @@ def test_qband_chains_dynamic_matches_sequential(dev, n_tiles):
     from paper_2006_15980_b200.data import RatingMatrix, resident_warps
     from paper_2006_15980_b200.kernels import _MASK64
     k = 128
-    _lib.check(_lib.load().hmf_qband_set_impl(4), "set_impl")
-    try:
+    with layout(4):
         slots = resident_warps(dev, k, False, 4)
         rng = np.random.default_rng(99)
         n_items = 2 * slots + 777
@@ -641,8 +654,6 @@ def test_qband_chains_dynamic_matches_sequential(dev, n_tiles):
             Qe[v] = qv + 0.05 * (e * pu - 0.03 * qv)
         assert rel_err(Q.double().cpu().numpy(), Qe) < 1e-5
         assert rel_err(P.double().cpu().numpy(), Pe) < 1e-5
-    finally:
-        _lib.load().hmf_qband_set_impl(-1)
 
 
 @pytest.mark.parametrize("n_items,impl", [(300, 0), (300, 4), (40_000, 4)],
@@ -655,8 +666,7 @@ def test_qband_skewed_items_match_sequential(dev, n_items, impl):
     from paper_2006_15980_b200 import _lib, kernels
     from paper_2006_15980_b200.data import RatingMatrix
     k, n_tiles, seed = 64, 3, 777
-    _lib.check(_lib.load().hmf_qband_set_impl(impl), "set_impl")
-    try:
+    with layout(impl):
         rng = np.random.default_rng(n_items + impl)
         n_users, n = 300_000, 60_000
         users = rng.permutation(n_users)[:n].astype(np.int32)
@@ -687,8 +697,6 @@ def test_qband_skewed_items_match_sequential(dev, n_items, impl):
             Qe[v] = qv + 0.05 * (e * pu - 0.03 * qv)
         assert rel_err(Q.double().cpu().numpy(), Qe) < 1e-5
         assert rel_err(P.double().cpu().numpy(), Pe) < 1e-5
-    finally:
-        _lib.load().hmf_qband_set_impl(-1)
 
 
 @pytest.mark.parametrize("k,dtype", [(128, torch.float32), (64, torch.float32),
@@ -700,14 +708,9 @@ def test_qband_split_runs_apply_every_rating(dev, n_tiles, k, dtype):
     step SGD is linear in the ratings, so the factor changes must equal the
     sequential reference's to first order: every rating applied once, every
     Q delta added once (nothing lost, nothing doubled).  Users repeat here, so
-    P goes back by reductions (kernels.PSTORE_OVERRIDE = 0): stores may drop
-    a concurrent update of the same user."""
-    from paper_2006_15980_b200 import kernels
-    kernels.PSTORE_OVERRIDE = 0
-    try:
-        _split_runs_apply_every_rating(dev, n_tiles, k, dtype)
-    finally:
-        kernels.PSTORE_OVERRIDE = None
+    P goes back by reductions (opts pstore = 0): stores may drop a concurrent
+    update of the same user."""
+    _split_runs_apply_every_rating(dev, n_tiles, k, dtype)
 
 
 def _split_runs_apply_every_rating(dev, n_tiles, k, dtype):
@@ -730,7 +733,7 @@ def _split_runs_apply_every_rating(dev, n_tiles, k, dtype):
     P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
     Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
     P, Q = to_dev(P0, dev, dtype), to_dev(Q0, dev, dtype)
-    assert kernels.launch_block_qband(P, Q, g, 0, lr, 0.02, 0.03, 3) == n
+    assert kernels.launch_block_qband(P, Q, g, 0, lr, 0.02, 0.03, 3, opts={"pstore": 0}) == n
     Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
     for u, v, r in zip(users, items, vals):
         pu, qv = Pe[u].copy(), Qe[v].copy()
@@ -751,9 +754,8 @@ def test_qband_pstore_conflict_free_equals_reductions_and_trains(dev):
     stores and reductions give the same factors (whole item runs,
     implementation 4, deterministic); with repeated users (the racing case)
     a few epochs still train to the reductions' test RMSE within 0.005."""
-    from paper_2006_15980_b200 import _lib, kernels
+    from paper_2006_15980_b200 import kernels
     from paper_2006_15980_b200.data import RatingMatrix
-    lib = _lib.load()
     k = 128
     rng = np.random.default_rng(17)
     n_users, n_items = 120_000, 700
@@ -765,42 +767,36 @@ def test_qband_pstore_conflict_free_equals_reductions_and_trains(dev):
     P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
     Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
     out = {}
-    try:
-        _lib.check(lib.hmf_qband_set_impl(4), "set_impl")
+    with layout(4):
         g = _qband_grid(dev, m, k, [0, n_items], target=None)
-        assert g.sub_impl == 4
-        for mode in (0, 1):
-            kernels.PSTORE_OVERRIDE = mode
-            P, Q = to_dev(P0, dev), to_dev(Q0, dev)
-            assert kernels.launch_block_qband(P, Q, g, 0, 0.05, 0.02, 0.03, 11) == n
-            assert lib.hmf_qband_get_pstore() == mode
-            out[mode] = (P.cpu().numpy(), Q.cpu().numpy())
-        assert np.array_equal(out[0][0], out[1][0])
-        assert np.array_equal(out[0][1], out[1][1])
-        lib.hmf_qband_set_impl(-1)
-        # repeated users: held-out RMSE after 4 epochs, stores vs reductions
-        n = 600_000
-        users = rng.integers(0, n_users, n).astype(np.int32)
-        items = rng.integers(0, n_items, n).astype(np.int32)
-        a = rng.uniform(0, 0.5, size=(n_users, 8))
-        b = rng.uniform(0, 0.5, size=(n_items, 8))
-        vals = np.einsum("ij,ij->i", a[users], b[items]) + rng.normal(0, 0.1, n)
-        cut = n * 19 // 20
-        m = RatingMatrix(n_users, n_items, users[:cut], items[:cut], vals[:cut])
-        g = _qband_grid(dev, m, k, [0, n_items], target=None)
-        tu, ti, tv = users[cut:], items[cut:], vals[cut:]
-        rm = {}
-        for mode in (0, 1):
-            kernels.PSTORE_OVERRIDE = mode
-            P, Q = to_dev(P0, dev), to_dev(Q0, dev)
-            for e in range(4):
-                kernels.launch_block_qband(P, Q, g, 0, 0.01, 0.01, 0.01, 100 + e)
-            Ph, Qh = P.double().cpu().numpy(), Q.double().cpu().numpy()
-            rm[mode] = float(np.sqrt(np.mean((tv - np.einsum("ij,ij->i", Ph[tu], Qh[ti])) ** 2)))
-        assert np.isfinite(rm[1]) and abs(rm[1] - rm[0]) <= 0.005, rm
-    finally:
-        kernels.PSTORE_OVERRIDE = None
-        lib.hmf_qband_set_impl(-1)
+    assert g.sub_impl == 4
+    for mode in (0, 1):
+        P, Q = to_dev(P0, dev), to_dev(Q0, dev)
+        assert kernels.launch_block_qband(P, Q, g, 0, 0.05, 0.02, 0.03, 11,
+                                          opts={"pstore": mode}) == n
+        out[mode] = (P.cpu().numpy(), Q.cpu().numpy())
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    # repeated users: held-out RMSE after 4 epochs, stores vs reductions
+    n = 600_000
+    users = rng.integers(0, n_users, n).astype(np.int32)
+    items = rng.integers(0, n_items, n).astype(np.int32)
+    a = rng.uniform(0, 0.5, size=(n_users, 8))
+    b = rng.uniform(0, 0.5, size=(n_items, 8))
+    vals = np.einsum("ij,ij->i", a[users], b[items]) + rng.normal(0, 0.1, n)
+    cut = n * 19 // 20
+    m = RatingMatrix(n_users, n_items, users[:cut], items[:cut], vals[:cut])
+    g = _qband_grid(dev, m, k, [0, n_items], target=None)
+    tu, ti, tv = users[cut:], items[cut:], vals[cut:]
+    rm = {}
+    for mode in (0, 1):
+        P, Q = to_dev(P0, dev), to_dev(Q0, dev)
+        for e in range(4):
+            kernels.launch_block_qband(P, Q, g, 0, 0.01, 0.01, 0.01, 100 + e,
+                                       opts={"pstore": mode})
+        Ph, Qh = P.double().cpu().numpy(), Q.double().cpu().numpy()
+        rm[mode] = float(np.sqrt(np.mean((tv - np.einsum("ij,ij->i", Ph[tu], Qh[ti])) ** 2)))
+    assert np.isfinite(rm[1]) and abs(rm[1] - rm[0]) <= 0.005, rm
 
 
 def test_qband_pstore_layout_choice(dev):
