@@ -156,6 +156,9 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
+        # NCCL init lines (nranks, transports) in the log, for the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         n_dev = torch.cuda.device_count()
         local = local % n_dev            # several ranks may share a GPU (testing)
         torch.cuda.set_device(local)
@@ -279,8 +282,7 @@ def run_reference_arm(args, world, rank):
 def run_ours(args, world, rank, local):
     import torch
     from paper_2006_15980_b200 import _lib, kernels
-    from paper_2006_15980_b200.data import (bucket_qbands, build_device_grid, split_device,
-                                            synthetic_device)
+    from paper_2006_15980_b200.data import bucket_qbands, build_device_grid, synthetic_band
     from paper_2006_15980_b200.sgd import init_device_model, rmse
 
     _lib.load()
@@ -293,10 +295,11 @@ def run_ours(args, world, rank, local):
     k = args.k or k0
     precision = args.precision
     n_total = int(round(n_train / (1.0 - TEST_FRACTION)))
-    # every rank holds the same-shaped workload: a replica per GPU (weak scaling)
+    # the whole matrix on one GPU: synthetic_band over every row (the same
+    # generator the N > 1 ranks use for their bands of one matrix)
     t0 = time.perf_counter()
-    trip = synthetic_device(n_users, n_items, n_total, rank=8, noise=0.1, seed=SEED + rank,
-                            device=dev)
+    train, test = synthetic_band(n_users, n_items, n_total, 0, n_users, rank=8, noise=0.1,
+                                 seed=SEED, test_fraction=TEST_FRACTION, device=dev)
     if args.item_skew > 0:
         # Zipf-like item popularity (p(item of rank r) ~ r^-alpha), for the
         # layout's handling of hot items; ratings keep the law's values
@@ -304,12 +307,12 @@ def run_ours(args, world, rank, local):
         g.manual_seed(SEED + 17)
         w = torch.arange(1, n_items + 1, device=dev, dtype=torch.float64).pow(-args.item_skew)
         perm = torch.randperm(n_items, device=dev, generator=g)
-        for a in range(0, trip.nnz, 1 << 24):
-            z = min(trip.nnz, a + (1 << 24))
-            trip.items[a:z] = perm[torch.multinomial(w, z - a, replacement=True,
-                                                     generator=g)].to(torch.int32)
+        for part in (train, test):
+            for a in range(0, part.nnz, 1 << 24):
+                z = min(part.nnz, a + (1 << 24))
+                part.items[a:z] = perm[torch.multinomial(w, z - a, replacement=True,
+                                                         generator=g)].to(torch.int32)
         del w, perm
-    train, test = split_device(trip, TEST_FRACTION)
     nnz = train.nnz
     # 1-GPU batch-only uniform plan: 1 row band x 2 column bands
     row_cuts = np.array([0, n_users], dtype=np.int64)
@@ -325,7 +328,7 @@ def run_ours(args, world, rank, local):
     test = DeviceTriples(test.n_users, test.n_items, test.users[order].contiguous(),
                          test.items[order].contiguous(), test.ratings[order].contiguous())
     del order
-    del trip, train
+    del train
     torch.cuda.empty_cache()
     if args.kernel == "qband":
         bucket_qbands(grid, k, tile_bytes=tile_bytes, elem_bytes=2 if precision == "f16" else 4,
@@ -498,15 +501,20 @@ def run_ours(args, world, rank, local):
 
 
 def run_ours_multi(args, world, rank, local):
-    """N > 1: one process per GPU, weak scaling.  Every rank owns a Netflix-
-    shaped row band (480 000 users, 100 M training ratings) of one matrix with
-    shared items (17 700); Q column bands (2N+1) move between GPUs through the
-    lease table (distributed.LeaseTable) and CUDA IPC peer pulls; P bands stay
-    resident.  A step is one quota epoch of every GPU's blocks + a barrier."""
+    """N > 1: one process per GPU over ONE synthetic matrix (data.synthetic_band:
+    every rank generates its own row band, keyed by global ids, so the bands
+    are pieces of the same matrix with the same held-out cells).
+    * weak scaling (default): the matrix is N x the workload's users (each
+      rank's band Netflix-shaped: 480 000 users, 100 M training ratings),
+      items shared (17 700);
+    * strong scaling: the workload's matrix itself, split into N row bands.
+    P bands stay resident; Q column bands (2N+1) move between GPUs through
+    the lease table and CUDA IPC peer pulls.  A step is one quota epoch of
+    every GPU's blocks + a barrier."""
     import torch
     import torch.distributed as dist
     from paper_2006_15980_b200 import _lib
-    from paper_2006_15980_b200.data import split_device, synthetic_device
+    from paper_2006_15980_b200.data import synthetic_band
     from paper_2006_15980_b200.distributed import CudaRowBand, LeaseTable, RowBandTrainer
     from paper_2006_15980_b200.sgd import DeviceModel, residual_sums
 
@@ -517,24 +525,23 @@ def run_ours_multi(args, world, rank, local):
     n_total = int(round(n_train / (1.0 - TEST_FRACTION)))
     geo = args.sim_world or world      # --sim-world: rank 0's share of a larger job
     if args.scaling == "strong":
-        # the workload itself split into row bands (same law, same density)
-        band = -(-n_users // geo)
-        row_lo, row_hi = rank * band, min(n_users, (rank + 1) * band)
-        n_rank = int(round(n_total * (row_hi - row_lo) / n_users))
-        trip = synthetic_device(row_hi - row_lo, n_items, n_rank, rank=8, noise=0.1,
-                                seed=SEED + rank, device=dev)
+        m_users, m_total = n_users, n_total            # the workload's matrix, split
+        band_rows = -(-n_users // geo)
     else:
-        # weak scaling: a workload-sized row band per GPU, items shared
-        row_lo, row_hi = rank * n_users, (rank + 1) * n_users
-        trip = synthetic_device(n_users, n_items, n_total, rank=8, noise=0.1, seed=SEED + rank,
-                                device=dev)
-    trip.users += row_lo                       # global user ids of this rank's band
-    train, test = split_device(trip, TEST_FRACTION)
+        m_users, m_total = n_users * geo, n_total * geo  # a workload-sized band per GPU
+        band_rows = n_users
+    row_lo, row_hi = rank * band_rows, min(m_users, (rank + 1) * band_rows)
+    t0 = time.perf_counter()
+    train, test = synthetic_band(m_users, n_items, m_total, row_lo, row_hi, rank=8, noise=0.1,
+                                 seed=SEED, test_fraction=TEST_FRACTION, device=dev)
     n_cols = 2 * geo + 1
     col_cuts = np.linspace(0, n_items, n_cols + 1).astype(np.int64)
     band = CudaRowBand(dist, rank, world, dev, train, row_lo, row_hi, col_cuts, k, LR, REG, REG,
                        init_seed=SEED, kernel=args.multi_kernel,
                        concurrency=args.multi_concurrency, split=args.split or None)
+    del train
+    torch.cuda.synchronize(dev)
+    setup_s = time.perf_counter() - t0
     table = LeaseTable(dist.distributed_c10d._get_default_store(), n_cols, rank,
                        f"bench{os.getpid() if world == 1 else 0}")
     if rank == 0:
@@ -560,6 +567,15 @@ def run_ours_multi(args, world, rank, local):
     updates = sum_over_ranks(float(trainer.total_updates - upd0), world)
     # one kernel launch per granted block (CudaRowBand.compute)
     launches = int(sum_over_ranks(float(int(trainer.counts.sum()) - blocks0), world))
+    # test RMSE after exactly warmup + steps epochs (the N = 1 line's count)
+    band.refresh_q(table)
+    dist.barrier()
+    sums = residual_sums(DeviceModel(band.P, band.Q), test.users, test.items, test.ratings,
+                         row_base=row_lo).to(_reduce_device())
+    dist.all_reduce(sums)
+    n_test = sum_over_ranks(float(test.nnz), world)
+    test_rmse = float(np.sqrt(sums[0].item() / n_test))
+    n_train = sum_over_ranks(float(band.grid.nnz), world)
     e2e = None
     if not args.no_e2e:
         # end to end through the same lease loop: every granted block's
@@ -590,12 +606,10 @@ def run_ours_multi(args, world, rank, local):
                        + ("6 B/rating: uint16 user ids relative to the row tile, item implicit"
                           if band.compact is not None else "12 B/rating triples")
                        + ") on the copy stream, the block granted ahead uploading while the "
-                       "current one trains; per-rank residual sums read back every step"}
-    band.refresh_q(table)
-    sums = residual_sums(DeviceModel(band.P, band.Q), test.users, test.items, test.ratings,
-                         row_base=row_lo).to(_reduce_device())
-    dist.all_reduce(sums)
-    n_test = sum_over_ranks(float(test.nnz), world)
+                       "current one trains; per-rank residual sums read back every step. The "
+                       "device copy of the band's ratings stays allocated (each lease "
+                       "overwrites its block from the host): a data-off-device run is the N=1 "
+                       "workers.StreamingEpoch path"}
     if rank == 0:
         print(json.dumps({
             "metric": "sgd_updates_per_sec", "value": updates / (ms / 1e3), "unit": "updates/s",
@@ -603,9 +617,13 @@ def run_ours_multi(args, world, rank, local):
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synthetic_ratings law, device generator)",
-            "config": {"workload": (f"{desc} row band per GPU (weak scaling), k={k}"
+            "config": {"workload": (f"{desc} row band per GPU of one {m_users}x{n_items} "
+                                    f"matrix (weak scaling), k={k}"
                                     if args.scaling == "weak" else
                                     f"{desc} split into {geo} row bands (strong scaling), k={k}"),
+                       "train_ratings": int(n_train), "test_ratings": int(n_test),
+                       "matrix": "one matrix: each rank generates its row band of it "
+                                 "(data.synthetic_band, keyed by global ids)",
                        "grid": f"{geo} row bands x {n_cols} column bands",
                        "simulated": (None if not args.sim_world else
                                      f"one process with rank 0's band and column geometry of "
@@ -615,9 +633,9 @@ def run_ours_multi(args, world, rank, local):
                        "kernel": band.kernel, "qband_impl": getattr(band.grid, "sub_impl", None),
                        "item_run_split": getattr(band.grid, "sub_split", None),
                        "blocks_in_flight": band.concurrency, "lr": LR, "reg": REG},
-            "rmse": {"epochs": args.warmup + args.steps + (e2e["steps"] if e2e else 0),
-                     "test": float(np.sqrt(sums[0].item() / n_test))},
+            "rmse": {"epochs": args.warmup + args.steps, "test": test_rmse},
             "lease_wait_seconds_rank0": trainer.wait_seconds,
+            "setup_seconds": setup_s,
             "gpu_launches": launches, "clocks": clocks.summary(), "e2e": e2e,
         }), flush=True)
 
@@ -732,6 +750,28 @@ def run_e2e(args, grid, model, k, precision, dev, world):
             "path": "kernels.sgd_range(numpy pinned host arrays) per block"}
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        return int(sock.getsockname()[1])
+
+
+def self_launch(n: int, argv: list) -> int:
+    """Re-run this script under torch.distributed.run with n ranks on this
+    node (rendezvous on 127.0.0.1); rank 0 prints the JSON line.  NCCL's init
+    log is on so every rank's communicator (nranks) shows in the output."""
+    import subprocess
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), str(Path(__file__).resolve()), *argv]
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -784,11 +824,21 @@ def main():
                     help="N=1 only: run rank 0 of an N-GPU job's geometry (projected per-GPU rate)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--spawn-probe", action="store_true",
+                    help="print each rank's RANK/WORLD_SIZE and exit (tests the self-launch)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # `python bench.py --gpus N`: one process per GPU, launched here
+        sys.exit(self_launch(args.gpus, sys.argv[1:]))
+    if args.spawn_probe:
+        print(json.dumps({"rank": int(os.environ.get("RANK", "0")),
+                          "world": int(os.environ.get("WORLD_SIZE", "1")),
+                          "local_rank": int(os.environ.get("LOCAL_RANK", "0"))}), flush=True)
+        return
     if args.impl == "reference":
-        world = int(os.environ.get("WORLD_SIZE", "1"))
+        world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
         rank = int(os.environ.get("RANK", "0"))
         run_reference_arm(args, world, rank)
         return

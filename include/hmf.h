@@ -265,21 +265,24 @@ int hmf_bucket_triples(const int32_t* rows, const int32_t* cols, const float* va
 /*
  * Synthetic instance generator with the synthetic_ratings law
  * (data.py:311-336), for shapes the reference generator cannot reach.
- * Cells: each of the n_rows x n_cols cells is selected independently with
- * probability p (geometric skipping along each row, counter-based RNG keyed by
- * seed), so the selected set is uniform given its size.
+ * Cells: each cell of rows [row_base, row_base + n_rows) x [0, n_cols) is
+ * selected independently with probability p (geometric skipping along each
+ * row, counter-based RNG keyed by seed and the GLOBAL row id), so the
+ * selected set is uniform given its size, and a row band generated alone is
+ * exactly that band of the whole matrix (one matrix across ranks).
  *   hmf_synthetic_count: row_ptr (device int64[n_rows + 1]) <- CSR offsets of
- *     the selected cells; returns the total count (synchronises `stream`).
- *   hmf_synthetic_cells: writes the selected (row, col) pairs, row-major.
+ *     the selected cells of the band; returns the total count (synchronises
+ *     `stream`).
+ *   hmf_synthetic_cells: writes the selected (global row, col) pairs, row-major.
  * Values: vals[i] = sum_{r<rank} A[rows[i], r] * B[cols[i], r] + N(0, noise),
  * A, B entries U[0, factor_scale/sqrt(rank)] from a hash of (seed, row/col, r),
- * the noise from a hash of (seed, i).
+ * the noise from a hash of (seed, row, col): a function of the cell only.
  */
 int64_t hmf_synthetic_count(int64_t n_rows, int64_t n_cols, double p, uint64_t seed,
-                            int64_t* row_ptr, void* stream);
+                            int64_t row_base, int64_t* row_ptr, void* stream);
 int hmf_synthetic_cells(int64_t n_rows, int64_t n_cols, double p, uint64_t seed,
-                        const int64_t* row_ptr, int32_t* out_rows, int32_t* out_cols,
-                        void* stream);
+                        int64_t row_base, const int64_t* row_ptr, int32_t* out_rows,
+                        int32_t* out_cols, void* stream);
 /* out[i] = in[pi(i)] for i < n_out, pi a keyed pseudo-random permutation of
  * [0, n_in) (Feistel network with cycle walking): the reference's
  * permutation(chosen)[:target] without a sort or an index array. */
@@ -289,6 +292,11 @@ int hmf_permute_cells(const int32_t* in_rows, const int32_t* in_cols, int64_t n_
 int hmf_synthetic_fill(const int32_t* rows, const int32_t* cols, int64_t n, int32_t rank,
                        double noise, double factor_scale, uint64_t seed, float* vals,
                        void* stream);
+/* Held-out split keyed by the cell: mask[i] = 1 iff a hash of (seed, rows[i],
+ * cols[i]) falls below `fraction` (device uint8[n]), so every row band agrees
+ * with the whole matrix on its test cells. */
+int hmf_cell_mask(const int32_t* rows, const int32_t* cols, int64_t n, double fraction,
+                  uint64_t seed, uint8_t* mask, void* stream);
 
 /* Device / peer utilities for the multi-GPU item-band hand-off. */
 int hmf_device_count(int32_t* n);

@@ -72,8 +72,9 @@ SIGNATURES = {
     "hmf_residual_sums_f16": (C.c_int, [_p, _p, _i64, _p, _p, _p, _i64, _i64, _i64, _i32, _p, _p]),
     "hmf_residual_sums_f64": (C.c_int, [_p, _p, _i64, _p, _p, _p, _i64, _i64, _i64, _i32, _p, _p]),
     "hmf_bucket_triples": (C.c_int, [_p, _p, _p, _i64, _p, _i32, _p, _i32, _p, _p, _p, _p, _p]),
-    "hmf_synthetic_count": (_i64, [_i64, _i64, _f64, _u64, _p, _p]),
-    "hmf_synthetic_cells": (C.c_int, [_i64, _i64, _f64, _u64, _p, _p, _p, _p]),
+    "hmf_synthetic_count": (_i64, [_i64, _i64, _f64, _u64, _i64, _p, _p]),
+    "hmf_synthetic_cells": (C.c_int, [_i64, _i64, _f64, _u64, _i64, _p, _p, _p, _p]),
+    "hmf_cell_mask": (C.c_int, [_p, _p, _i64, _f64, _u64, _p, _p]),
     "hmf_synthetic_fill": (C.c_int, [_p, _p, _i64, _i32, _f64, _f64, _u64, _p, _p]),
     "hmf_permute_cells": (C.c_int, [_p, _p, _i64, _p, _p, _i64, _u64, _p]),
     "hmf_device_count": (C.c_int, [C.POINTER(_i32)]),

@@ -36,13 +36,13 @@ __device__ inline int64_t next_cell(int64_t col, double log_q, uint64_t seed, in
 }
 
 __global__ void synth_count_kernel(int64_t n_rows, int64_t n_cols, double log_q, uint64_t seed,
-                                   int64_t* row_cnt) {
+                                   int64_t row_base, int64_t* row_cnt) {
   for (int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < n_rows;
        row += int64_t(gridDim.x) * blockDim.x) {
     int64_t col = -1, cnt = 0;
     uint64_t j = 0;
     while (true) {
-      col = next_cell(col, log_q, seed, row, j++);
+      col = next_cell(col, log_q, seed, row_base + row, j++);
       if (col >= n_cols) break;
       ++cnt;
     }
@@ -52,16 +52,16 @@ __global__ void synth_count_kernel(int64_t n_rows, int64_t n_cols, double log_q,
 }
 
 __global__ void synth_cells_kernel(int64_t n_rows, int64_t n_cols, double log_q, uint64_t seed,
-                                   const int64_t* __restrict__ row_ptr, int32_t* out_rows,
-                                   int32_t* out_cols) {
+                                   int64_t row_base, const int64_t* __restrict__ row_ptr,
+                                   int32_t* out_rows, int32_t* out_cols) {
   for (int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < n_rows;
        row += int64_t(gridDim.x) * blockDim.x) {
     int64_t col = -1, pos = row_ptr[row];
     uint64_t j = 0;
     while (true) {
-      col = next_cell(col, log_q, seed, row, j++);
+      col = next_cell(col, log_q, seed, row_base + row, j++);
       if (col >= n_cols) break;
-      out_rows[pos] = int32_t(row);
+      out_rows[pos] = int32_t(row_base + row);
       out_cols[pos] = int32_t(col);
       ++pos;
     }
@@ -83,8 +83,11 @@ __global__ void synth_fill_kernel(const int32_t* __restrict__ rows,
       acc += a * b;
     }
     if (noise > 0.0) {
-      const double u1 = unit_open(hash3(seed_n, uint64_t(i), 0));
-      const double u2 = unit_open(hash3(seed_n, uint64_t(i), 1));
+      // keyed by the cell, not its position: a row band generated alone
+      // (hmf_synthetic_count with row_base) gets the same values as the
+      // whole matrix
+      const double u1 = unit_open(hash3(seed_n, u, v));
+      const double u2 = unit_open(hash3(seed_n ^ kMixB, u, v));
       acc += noise * sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
     }
     vals[i] = float(acc);
@@ -128,6 +131,17 @@ __global__ void permute_cells_kernel(const int32_t* __restrict__ in_rows,
   }
 }
 
+// Held-out split keyed by the cell: mask[i] = 1 iff hash(seed, row, col) <
+// fraction, so every row band of a matrix agrees with the whole on which
+// cells are test cells.
+__global__ void cell_mask_kernel(const int32_t* __restrict__ rows,
+                                 const int32_t* __restrict__ cols, int64_t n, double fraction,
+                                 uint64_t seed, uint8_t* __restrict__ mask) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    mask[i] = unit_open(hash3(seed, uint64_t(rows[i]), uint64_t(cols[i]))) <= fraction ? 1 : 0;
+}
+
 static double log_keep(double p) {
   if (p >= 1.0) return 0.0;
   return log1p(-p);
@@ -138,13 +152,13 @@ static double log_keep(double p) {
 extern "C" {
 
 int64_t hmf_synthetic_count(int64_t n_rows, int64_t n_cols, double p, uint64_t seed,
-                            int64_t* row_ptr, void* stream_) {
+                            int64_t row_base, int64_t* row_ptr, void* stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  if (n_rows < 0 || n_cols < 0 || !(p > 0.0) || !row_ptr)
+  if (n_rows < 0 || n_cols < 0 || row_base < 0 || !(p > 0.0) || !row_ptr)
     return hmf::set_error(HMF_ERR_ARG, "bad generator arguments");
   const int64_t blocks = n_rows > 0 ? (n_rows + 255) / 256 : 1;
   hmf::synth_count_kernel<<<unsigned(blocks < 65535 * 16 ? blocks : 65535 * 16), 256, 0, stream>>>(
-      n_rows, n_cols, hmf::log_keep(p), seed, row_ptr);
+      n_rows, n_cols, hmf::log_keep(p), seed, row_base, row_ptr);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = hmf::scan_exclusive_i64(row_ptr, row_ptr, n_rows + 1, stream);
   int64_t total = 0;
@@ -156,16 +170,16 @@ int64_t hmf_synthetic_count(int64_t n_rows, int64_t n_cols, double p, uint64_t s
 }
 
 int hmf_synthetic_cells(int64_t n_rows, int64_t n_cols, double p, uint64_t seed,
-                        const int64_t* row_ptr, int32_t* out_rows, int32_t* out_cols,
-                        void* stream_) {
+                        int64_t row_base, const int64_t* row_ptr, int32_t* out_rows,
+                        int32_t* out_cols, void* stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  if (n_rows < 0 || n_cols < 0 || !(p > 0.0) || !row_ptr)
+  if (n_rows < 0 || n_cols < 0 || row_base < 0 || !(p > 0.0) || !row_ptr)
     return int(hmf::set_error(HMF_ERR_ARG, "bad generator arguments"));
-  if (n_rows > INT32_MAX || n_cols > INT32_MAX)
+  if (row_base + n_rows > INT32_MAX || n_cols > INT32_MAX)
     return int(hmf::set_error(HMF_ERR_ARG, "indices must fit int32"));
   const int64_t blocks = n_rows > 0 ? (n_rows + 255) / 256 : 1;
   hmf::synth_cells_kernel<<<unsigned(blocks < 65535 * 16 ? blocks : 65535 * 16), 256, 0, stream>>>(
-      n_rows, n_cols, hmf::log_keep(p), seed, row_ptr, out_rows, out_cols);
+      n_rows, n_cols, hmf::log_keep(p), seed, row_base, row_ptr, out_rows, out_cols);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? HMF_OK : int(hmf::set_cuda_error(e));
 }
@@ -203,6 +217,19 @@ int hmf_synthetic_fill(const int32_t* rows, const int32_t* cols, int64_t n, int3
   if (blocks > int64_t(hmf::device_sm_count()) * 32) blocks = int64_t(hmf::device_sm_count()) * 32;
   hmf::synth_fill_kernel<<<unsigned(blocks), 256, 0, stream>>>(rows, cols, n, rank, noise, hi, seed,
                                                                vals);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HMF_OK : int(hmf::set_cuda_error(e));
+}
+
+int hmf_cell_mask(const int32_t* rows, const int32_t* cols, int64_t n, double fraction,
+                  uint64_t seed, uint8_t* mask, void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (n < 0 || !(fraction >= 0.0) || fraction > 1.0)
+    return int(hmf::set_error(HMF_ERR_ARG, "bad mask arguments"));
+  if (n == 0) return HMF_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > int64_t(hmf::device_sm_count()) * 32) blocks = int64_t(hmf::device_sm_count()) * 32;
+  hmf::cell_mask_kernel<<<unsigned(blocks), 256, 0, stream>>>(rows, cols, n, fraction, seed, mask);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? HMF_OK : int(hmf::set_cuda_error(e));
 }

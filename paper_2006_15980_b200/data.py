@@ -756,8 +756,8 @@ def synthetic_device(n_users: int, n_items: int, nnz: int, rank: int = 8, noise:
     for attempt in range(8):
         gseed = (seed * 0x9E3779B1 + attempt * 0x85EBCA77 + 1) & 0xFFFFFFFFFFFFFFFF
         row_ptr = torch.empty(n_users + 1, dtype=torch.int64, device=dev)
-        got = _lib.check(lib.hmf_synthetic_count(n_users, n_items, p, gseed, row_ptr.data_ptr(), s),
-                         "hmf_synthetic_count")
+        got = _lib.check(lib.hmf_synthetic_count(n_users, n_items, p, gseed, 0, row_ptr.data_ptr(),
+                                                 s), "hmf_synthetic_count")
         if got >= nnz:
             break
         p = min(1.0, p * 1.01 + 1.0 / total)
@@ -765,7 +765,7 @@ def synthetic_device(n_users: int, n_items: int, nnz: int, rank: int = 8, noise:
         raise DataError("generator could not reach the requested count")
     users = torch.empty(got, dtype=torch.int32, device=dev)
     items = torch.empty(got, dtype=torch.int32, device=dev)
-    _lib.check(lib.hmf_synthetic_cells(n_users, n_items, p, gseed, row_ptr.data_ptr(),
+    _lib.check(lib.hmf_synthetic_cells(n_users, n_items, p, gseed, 0, row_ptr.data_ptr(),
                                        users.data_ptr(), items.data_ptr(), s), "hmf_synthetic_cells")
     del row_ptr
     # random order, first nnz kept (a keyed permutation: no sort, no index array)
@@ -780,6 +780,91 @@ def synthetic_device(n_users: int, n_items: int, nnz: int, rank: int = 8, noise:
                                       factor_scale, (seed + 0x5EED) & 0xFFFFFFFFFFFFFFFF,
                                       vals.data_ptr(), s), "hmf_synthetic_fill")
     return DeviceTriples(n_users, n_items, users, items, vals)
+
+
+def synthetic_band(n_users: int, n_items: int, nnz: float, row_lo: int = 0,
+                   row_hi: int | None = None, rank: int = 8, noise: float = 0.1, seed: int = 0,
+                   test_fraction: float = 0.05, factor_scale: float = 1.0, device=None):
+    """Rows [row_lo, row_hi) of ONE synthetic matrix (the synthetic_ratings
+    law, data.py:311-336), generated in HBM, split into (train, test).
+
+    Every decision is keyed by the global cell, so the bands of any row
+    partition are exactly the pieces of the whole matrix — N ranks each
+    generating their own band train on the same matrix as one GPU, with the
+    same held-out cells and the same ground truth (latent factors hashed from
+    the global user and item ids, noise from the cell):
+    * a cell is present with probability nnz / cells (geometric skipping per
+      global row), so the matrix holds nnz ratings in expectation (not
+      exactly: there is no global truncation step);
+    * a cell is a test cell iff a hash of it falls below test_fraction
+      (hmf_cell_mask);
+    * each band's cells are then put in a keyed random order (the
+      reference's shuffle_triples, data.py:99-102), train and test kept in it.
+    User ids are global.  Returns (train, test) DeviceTriples with n_users
+    the whole matrix's."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    row_hi = n_users if row_hi is None else int(row_hi)
+    row_lo = int(row_lo)
+    if not 0 <= row_lo <= row_hi <= n_users:
+        raise DataError("bad row band")
+    total = float(n_users) * float(n_items)
+    if nnz > total:
+        raise DataError("more ratings than cells")
+    p = min(1.0, float(nnz) / total)
+    lib = _lib.load()
+    s = _stream(dev)
+    gseed = (seed * 0x9E3779B1 + 1) & 0xFFFFFFFFFFFFFFFF
+    n_rows = row_hi - row_lo
+    row_ptr = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
+    got = _lib.check(lib.hmf_synthetic_count(n_rows, n_items, p, gseed, row_lo,
+                                             row_ptr.data_ptr(), s), "hmf_synthetic_count")
+    users = torch.empty(got, dtype=torch.int32, device=dev)
+    items = torch.empty(got, dtype=torch.int32, device=dev)
+    _lib.check(lib.hmf_synthetic_cells(n_rows, n_items, p, gseed, row_lo, row_ptr.data_ptr(),
+                                       users.data_ptr(), items.data_ptr(), s), "hmf_synthetic_cells")
+    del row_ptr
+    # keyed random order of the band's cells (a permutation of all of them)
+    out_u = torch.empty_like(users)
+    out_i = torch.empty_like(items)
+    _lib.check(lib.hmf_permute_cells(users.data_ptr(), items.data_ptr(), got, out_u.data_ptr(),
+                                     out_i.data_ptr(), got,
+                                     (seed * 0x2545F491 + 7 + row_lo * 0x9E3779B97F4A7C15)
+                                     & 0xFFFFFFFFFFFFFFFF, s), "hmf_permute_cells")
+    users, items = out_u, out_i
+    del out_u, out_i
+    vals = torch.empty(got, dtype=torch.float32, device=dev)
+    _lib.check(lib.hmf_synthetic_fill(users.data_ptr(), items.data_ptr(), got, rank, noise,
+                                      factor_scale, (seed + 0x5EED) & 0xFFFFFFFFFFFFFFFF,
+                                      vals.data_ptr(), s), "hmf_synthetic_fill")
+    mask = torch.empty(got, dtype=torch.uint8, device=dev)
+    _lib.check(lib.hmf_cell_mask(users.data_ptr(), items.data_ptr(), got, float(test_fraction),
+                                 (seed * 0x632BE59BD9B4E019 + 0x7E57) & 0xFFFFFFFFFFFFFFFF,
+                                 mask.data_ptr(), s), "hmf_cell_mask")
+    # stable split, chunk by chunk (no nnz-long index array at Hugewiki scale)
+    n_test = int(mask.sum(dtype=torch.int64))
+    out = [(torch.empty(got - n_test, dtype=torch.int32, device=dev),
+            torch.empty(got - n_test, dtype=torch.int32, device=dev),
+            torch.empty(got - n_test, dtype=torch.float32, device=dev)),
+           (torch.empty(n_test, dtype=torch.int32, device=dev),
+            torch.empty(n_test, dtype=torch.int32, device=dev),
+            torch.empty(n_test, dtype=torch.float32, device=dev))]
+    at = [0, 0]
+    chunk = 1 << 27
+    for a in range(0, got, chunk):
+        z = min(got, a + chunk)
+        sel = mask[a:z].bool()
+        for which, m in ((1, sel), (0, ~sel)):
+            idx = torch.nonzero(m).squeeze(1)
+            n = int(idx.numel())
+            for dst, src in zip(out[which], (users, items, vals)):
+                dst[at[which]:at[which] + n] = src[a:z][idx]
+            at[which] += n
+        del sel
+    del mask, users, items, vals
+    train = DeviceTriples(n_users, n_items, *out[0])
+    test = DeviceTriples(n_users, n_items, *out[1])
+    return train, test
 
 
 def split_device(triples: DeviceTriples, test_fraction: float, seed: int = 1):

@@ -61,6 +61,15 @@ def main(out_dir, kernel="exact", stage=False):
     dist.barrier()
     if stage:      # every block's ratings uploaded from pinned host memory per lease
         band.stage_from_host(True)
+        # poison the device copies: only the per-lease uploads can make the
+        # result right (a broken or skipped upload trains on zeros / NaNs)
+        if band.compact is not None:
+            band.dev_rel.zero_()
+        else:
+            band.grid.users.fill_(lo)
+            band.grid.items.zero_()
+        band.grid.ratings.fill_(float("nan"))
+        torch.cuda.synchronize()
         if rank == 0:
             with open(os.path.join(out_dir, "staged.txt"), "w") as fh:
                 fh.write("compact" if band.compact is not None else "triples")

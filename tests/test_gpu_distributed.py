@@ -78,7 +78,8 @@ def test_two_ranks_qband_path_applies_every_triple(tmp_path, stage):
     for log, Pb, counts in res:
         assert counts == [W.EPOCHS] * (len(col_cuts) - 1)
     if stage:
-        print("staged stream:", (tmp_path / "staged.txt").read_text())
+        # the compact 6-byte stream (uint16 tile-relative ids, implicit items) ran
+        assert (tmp_path / "staged.txt").read_text() == "compact"
     users, items, vals, P0, Q0 = W.problem(conflict_free=True)
     P, Q = P0.astype(np.float64), Q0.astype(np.float64)
     for e in range(W.EPOCHS):
