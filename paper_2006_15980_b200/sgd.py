@@ -182,8 +182,10 @@ def sgd_update(model: FactorModel, user: int, item: int, rating: float,
     kernel in EXACT mode (f64, both sides from pre-update vectors)."""
     pu0 = model.user_factors[user].copy()
     qv0 = model.item_factors[item].copy()
-    P = np.ascontiguousarray(pu0[None, :])
-    Q = np.ascontiguousarray(qv0[None, :])
+    # fresh arrays: the kernel updates them in place, pu0 / qv0 stay the
+    # pre-update vectors the trace is computed from
+    P = pu0[None, :].copy()
+    Q = qv0[None, :].copy()
     kernels.sgd_range(P, Q, np.zeros(1, np.int32), np.zeros(1, np.int32),
                       np.array([rating], dtype=np.float64), 0, 1, hparams.learning_rate,
                       hparams.reg_user, hparams.reg_item, 0, 0, 0, mode="exact")

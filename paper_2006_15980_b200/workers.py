@@ -259,6 +259,13 @@ class BatchEngine:
     def __init__(self, config: BatchWorkerConfig, model: FactorModel, hparams: Hyperparams,
                  store: FactorStore | None = None):
         torch = _torch()
+        if not isinstance(config, BatchWorkerConfig):
+            # the reference's BatchWorkerConfig (lanes, launch_overhead,
+            # bandwidth; workers.py:45-58): the drop-in binding
+            # `hetmf.workers.BatchEngine = paper_2006_15980_b200.workers.BatchEngine`
+            # hands those to the reference's own BatchWorker (workers.py:315)
+            config = BatchWorkerConfig(lanes=config.lanes, launch_overhead=config.launch_overhead,
+                                       bandwidth=config.bandwidth)
         config.validate()
         _lib.load()
         if not torch.cuda.is_available():

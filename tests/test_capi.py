@@ -72,3 +72,15 @@ def test_product_path_has_no_oracle_dependency():
         src = p.read_text()
         assert "import oracle" not in src and "from oracle" not in src, p
         assert "hmf_oracle" not in src, p
+
+
+def test_package_reexports_reference_names():
+    """Every public name of the reference (hetmf/__init__.py:31-44) is
+    importable from the package, except the two documented out-of-scope ones."""
+    import paper_2006_15980_b200 as pkg
+    from oracle import reference
+    if reference.installed():
+        ref_all = set(reference.hetmf().__all__)
+        assert ref_all - set(pkg.REFERENCE_NAMES) == set(pkg.NOT_EXPORTED)
+    for name in pkg.__all__:
+        assert hasattr(pkg, name), name
