@@ -203,23 +203,62 @@ def sum_over_ranks(x: float, world: int) -> float:
 
 
 # ---------------------------------------------------------------------------
-# CPU arm (oracle port of the reference's stream-only path)
+# CPU arm: the reference's own stream-only path on the host cores
 # ---------------------------------------------------------------------------
-def cpu_sample_run(n_users, n_items, k, sample_nnz, threads, epochs, seed=SEED):
-    """Time the reference CPU algorithm (oracle C port, `threads` workers on
-    the uniform threads x (threads+1) grid) on a sample of the workload:
-    full-size P and Q (f64, the reference's layout), `sample_nnz` ratings drawn
-    with the same law.  Returns (updates/s, updates, seconds)."""
+def reference_module():
+    """The unmodified reference package installed under oracle/_ref (test and
+    baseline infrastructure, oracle/reference.py), or None."""
+    try:
+        from oracle import reference
+        return reference.hetmf() if reference.installed() else None
+    except Exception:
+        return None
+
+
+def workload_sample(n_users, n_items, sample_nnz, seed=SEED):
+    """A bounded sample of the workload under its law (synthetic_ratings,
+    data.py:311-336: rank 8, factors U[0, 1/sqrt 8], noise N(0, 0.1)) over
+    the FULL user x item space: cells uniform (duplicates are ~nnz^2/cells,
+    negligible at these sizes), so the timed run touches full-size P and Q."""
+    rng = np.random.default_rng(seed)
+    users = rng.integers(0, n_users, sample_nnz, dtype=np.int32)
+    items = rng.integers(0, n_items, sample_nnz, dtype=np.int32)
+    top = 1.0 / np.sqrt(8.0)
+    A = rng.uniform(0.0, top, size=(n_users, 8))
+    B = rng.uniform(0.0, top, size=(n_items, 8))
+    vals = np.einsum("ij,ij->i", A[users], B[items]) + rng.normal(0.0, 0.1, sample_nnz)
+    return users, items, vals
+
+
+def cpu_reference_run(n_users, n_items, k, sample_nnz, threads, epochs, seed=SEED):
+    """The reference's CPU path on a sample: hetmf.run_training(RunConfig(
+    schedule="stream-only", n_stream=threads, ...)) (engine.py:190-268), its
+    numba sgd_range on `threads` stream workers, log_train_loss off.  Returns
+    (updates/s, updates, seconds) from the reference's own TrainResult
+    (scheduler.total_updates / wall_seconds: the training loop, not setup)."""
+    ref = reference_module()
+    users, items, vals = workload_sample(n_users, n_items, sample_nnz, seed)
+    m = ref.RatingMatrix(n_users, n_items, users, items, vals)
+    cfg = ref.RunConfig(schedule="stream-only", n_stream=threads, n_factors=k, learning_rate=LR,
+                        reg_user=REG, reg_item=REG, epochs=epochs, seed=seed,
+                        log_train_loss=False)
+    res = ref.run_training(cfg, matrix=m)
+    got = int(res.scheduler.total_updates)
+    return got / res.wall_seconds, got, res.wall_seconds
+
+
+def cpu_port_run(n_users, n_items, k, sample_nnz, threads, epochs, seed=SEED):
+    """The oracle's C port of the same stream-only path (threads x (threads+1)
+    uniform grid, f64 P/Q) on the same sample: used when the reference is not
+    installed, and to state the port / reference speed ratio."""
     import oracle
     from paper_2006_15980_b200.data import build_grid, RatingMatrix
-    rng = np.random.default_rng(seed)
-    users = rng.integers(0, n_users, sample_nnz).astype(np.int32)
-    items = rng.integers(0, n_items, sample_nnz).astype(np.int32)
-    vals = rng.uniform(0.0, 0.5, sample_nnz)
+    users, items, vals = workload_sample(n_users, n_items, sample_nnz, seed)
     m = RatingMatrix(n_users, n_items, users, items, vals)
     rows_cut = np.linspace(0, n_users, threads + 1).astype(np.int64)
     cols_cut = np.linspace(0, n_items, threads + 2).astype(np.int64)
     g = build_grid(m, rows_cut, cols_cut)
+    rng = np.random.default_rng(seed)
     top = 1.0 / np.sqrt(k)
     P = rng.uniform(0, top, size=(n_users, k))
     Q = rng.uniform(0, top, size=(n_items, k))
@@ -231,12 +270,13 @@ def cpu_sample_run(n_users, n_items, k, sample_nnz, threads, epochs, seed=SEED):
     return got / dt, got, dt
 
 
-def launch_overrides(args) -> dict:
-    """Command-line overrides of the layout's per-launch Q-band options."""
-    return {"impl": args.qband_impl if args.qband_impl >= 0 else None,
-            "chain_cfg": args.chain_cfg if args.chain_cfg >= 0 else None,
-            "pstore": args.pstore if args.pstore >= 0 else None,
-            "qsync": args.qsync, "lockstep": args.chain_lockstep}
+def cpu_run(n_users, n_items, k, sample_nnz, threads, epochs, seed=SEED):
+    """(kind, updates/s, updates, seconds): the reference when installed,
+    else the port."""
+    if reference_module() is not None:
+        return ("reference",) + cpu_reference_run(n_users, n_items, k, sample_nnz, threads,
+                                                  epochs, seed)
+    return ("port",) + cpu_port_run(n_users, n_items, k, sample_nnz, threads, epochs, seed)
 
 
 def host_threads() -> int:
@@ -246,34 +286,147 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
+def workload_config(args) -> dict:
+    """The workload description both arms print (deterministic, no data-
+    dependent counts: those are top-level keys)."""
+    n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
+    k = args.k or k0
+    return {"workload": f"{desc}, k={k}, {args.precision} storage", "k": k,
+            "lr": LR, "reg": REG, "test_fraction": TEST_FRACTION, "seed": SEED,
+            "scaling": args.scaling if args.gpus > 1 or "WORLD_SIZE" in os.environ else "weak",
+            "l2": ("inputs larger than L2 (triples alone > 126 MB); no flush"
+                   if n_train * 12 > (126 << 20) else
+                   "inputs fit in the 126 MB L2 (not a headline configuration); no flush")}
+
+
 def run_reference_arm(args, world, rank):
     n_users, n_items, n_train, k0, desc = WORKLOADS[args.workload]
     k = args.k or k0
     if rank != 0:
         return
     threads = host_threads()
-    sample = int(min(n_train, 1_500_000 * threads))
-    times = []
+    sample = int(min(n_train, 1_000_000 * threads))
+    times, kind = [], None
     for step in range(args.warmup + args.steps):
-        rate, got, dt = cpu_sample_run(n_users, n_items, k, sample, threads, 1, seed=step)
+        kind, rate, got, dt = cpu_run(n_users, n_items, k, sample, threads, 1, seed=SEED + step)
         if step >= args.warmup:
             times.append((got, dt))
     ups = sum(g for g, _ in times) / sum(d for _, d in times)
     ms = 1e3 * sum(d for _, d in times) / len(times)
+    what = ("hetmf.run_training(stream-only, numba sgd_range), unmodified reference from "
+            "oracle/_ref" if kind == "reference" else "oracle C port of the stream-only path")
     line = {
         "impl": "reference", "metric": "sgd_updates_per_sec", "value": ups, "unit": "updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference law, host)",
-        "config": {"workload": f"{desc}, k={k}; CPU sample of {sample} ratings per step "
-                               f"(full-size P/Q), stream-only uniform grid"},
-        "cpu_baseline": {"value": ups, "unit": "updates/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} ratings x 1 epoch per step, full {n_users}x"
-                                   f"{n_items} P/Q at k={k}, {threads} threads"},
+        "data": "synthetic (the workload's law, host sample)",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": ups, "unit": "updates/s", "cores": threads, "kind": kind,
+                         "sample": f"{sample} ratings of the workload's law over the full "
+                                   f"{n_users}x{n_items} matrix, 1 epoch per step, {threads} "
+                                   f"stream workers: {what}"},
         "e2e": {"value": ups, "unit": "updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def ncu_summary(key: str):
+    """The committed ncu --set full summary of the dominant kernel for this
+    workload (profiles/round2/ncu_summary.json, scripts/ncu_summary.py), or
+    None."""
+    p = ROOT / "profiles" / "round2" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(key)
+    except ValueError:
+        return None
+
+
+def roofline_fields(args, achieved, peak, peak_kind, bpu, mean_ms, mean_updates, compulsory,
+                    l2_rows, kernel_ups, p_stores) -> dict:
+    """The dominant kernel against its bounds.
+
+    frac (the contract's roofline): ALGORITHMIC bytes per launch (12 + 16k per
+    update in fp32: the rating, p_u and q_v read and written) over
+    the live CUDA-event launch time, over the measured HBM copy bandwidth —
+    the north star's "% of HBM roofline".  It exceeds 1 because the row-tile
+    layout keeps each tile's P rows in the 126 MB L2: the P traffic is served
+    on chip.  What the kernel does to DRAM and to the on-chip units comes from
+    the committed ncu capture: `dram` (measured DRAM bytes per launch over the
+    live launch time, over the same peak), `compulsory` (the bytes that must
+    cross HBM once per launch) and `binding_unit` (the busiest unit)."""
+    k = args.k or WORKLOADS[args.workload][3]
+    ncu = ncu_summary(f"{args.workload}_k{k}_{args.precision}_{args.kernel}")
+    dram = None
+    if ncu:
+        gbs = ncu["dram_bytes"] / (mean_ms / 1e3) / 1e9
+        dram = {"bytes_per_launch": ncu["dram_bytes"], "achieved_gbs": gbs, "frac": gbs / peak,
+                "ncu_launch_ms": 1e3 * ncu["duration"], "source": ncu["source"]}
+    out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+           "frac": achieved / peak, "traffic": ncu["dram_bytes"] if ncu else None,
+           "peak_kind": peak_kind, "bytes_per_update": bpu,
+           "frac_meaning": "north-star ratio: algorithmic bytes (rating + p_u, q_v read and "
+                           "written) per launch / live launch time / measured HBM copy BW; > 1 "
+                           "because P rows are served from L2 (row tiles); see dram, "
+                           "compulsory, binding_unit for the measured picture",
+           "kernel": ncu["kernel"] if ncu else ("qchain_kernel" if args.kernel == "qband"
+                                                else "sgd_hogwild_kernel"),
+           "mean_launch_ms": mean_ms, "updates_per_launch": mean_updates,
+           "dram": dram,
+           "compulsory": (None if compulsory is None else {
+               "bytes_per_launch": compulsory,
+               "what": "triples once + one read and one write of the block's P band and Q band",
+               "dram_over_compulsory": (ncu["dram_bytes"] / compulsory) if ncu else None}),
+           "binding_unit": (None if not ncu else {
+               "unit": "L1TEX (LSU request path: P-row loads and stores/reductions)",
+               "l1tex_pct": ncu["l1tex_pct"], "lts_pct": ncu["lts_pct"],
+               "dram_pct": ncu["dram_pct"], "sm_pct": ncu["sm_pct"],
+               "l2_hit_pct": ncu["l2_hit_pct"], "source": ncu["source"]}),
+           "l2_ceiling": (None if l2_rows is None else {
+               "updates_per_s": l2_rows, "kernel_updates_per_s": kernel_ups,
+               "frac": kernel_ups / l2_rows,
+               "source": "scripts/l2_rowbench.cu: random P-row load + "
+                         + ("store" if p_stores else "vector reduction")
+                         + ", L2-resident 32 MB, no arithmetic (profiles/r02/l2_rowbench.jsonl)"})}
+    return out
+
+
+def cpu_baseline(n_users, n_items, k, nnz) -> dict:
+    """~10-30 s of the reference's CPU path on the host cores (all threads):
+    the reference itself (oracle/_ref) when installed, else the C port; plus
+    the port on the same sample, so the line states the port / reference
+    speed ratio measured on this host."""
+    threads = host_threads()
+    sample = int(min(nnz, 1_000_000 * threads))
+    kind, rate, got, dt = cpu_run(n_users, n_items, k, sample, threads, 1)
+    epochs = 1
+    if dt < 10.0:
+        more = max(1, int(round((10.0 - dt) / max(dt, 1e-3))))
+        _, _, got2, dt2 = cpu_run(n_users, n_items, k, sample, threads, more, seed=SEED + 1)
+        got, dt, epochs = got + got2, dt + dt2, 1 + more
+        rate = got / dt
+    out = {"value": rate, "unit": "updates/s", "cores": threads, "kind": kind,
+           "sample": f"{sample} ratings of the workload's law over the full {n_users}x{n_items}"
+                     f" matrix (f64 P/Q, k={k}), {epochs} epochs, {threads} stream workers, "
+                     f"{dt:.1f} s: " + ("hetmf.run_training(stream-only), the unmodified "
+                                        "reference (numba sgd_range) from oracle/_ref"
+                                        if kind == "reference" else
+                                        "oracle C port of the stream-only path")}
+    if kind == "reference":
+        prate, _, _ = cpu_port_run(n_users, n_items, k, sample, threads, 1)
+        out["port_vs_reference"] = {"port_updates_per_s": prate, "ratio": prate / rate,
+                                    "note": "oracle C port on the same sample, 1 epoch"}
+    return out
+
+
+def launch_overrides(args) -> dict:
+    """Command-line overrides of the layout's per-launch Q-band options."""
+    return {"impl": args.qband_impl if args.qband_impl >= 0 else None,
+            "chain_cfg": args.chain_cfg if args.chain_cfg >= 0 else None,
+            "pstore": args.pstore if args.pstore >= 0 else None,
+            "qsync": args.qsync, "lockstep": args.chain_lockstep}
 
 
 # ---------------------------------------------------------------------------
@@ -406,16 +559,19 @@ def run_ours(args, world, rank, local):
                 and (args.pstore == 1 or (args.pstore < 0 and getattr(grid, "sub_pstore", 0))))
     l2_rows = l2_ceiling(k, precision, bool(p_stores))
     kernel_ups = mean_updates / (mean_ms / 1e3)
-    traffic = None
-    prof = ROOT / "profiles" / "traffic.json"
-    if prof.exists():
-        try:
-            tr = json.loads(prof.read_text()).get(
-                f"{args.workload}_k{k}_{precision}_{args.kernel}")
-            if tr:
-                traffic = tr["dram_bytes_per_launch"]
-        except Exception:
-            traffic = None
+    # compulsory DRAM bytes of one launch: its triples once, one read and one
+    # write of every P row of its row band and of every Q row of its column
+    # band (what must cross HBM if nothing stayed in L2 between launches)
+    s_el = 2 if precision == "f16" else 4
+    comp = []
+    for b in range(grid.n_blocks):
+        lo, hi = grid.block_range(b)
+        if hi <= lo:
+            continue
+        r0, r1 = grid.row_span(b // grid.n_col_bands)
+        c0, c1 = grid.col_span(b % grid.n_col_bands)
+        comp.append((hi - lo) * 12 + 2 * ((r1 - r0) + (c1 - c0)) * k * s_el)
+    compulsory = float(np.mean(comp)) if comp else None
 
     # test RMSE after the epochs run (not timed)
     test_rmse = rmse(test, model).value
@@ -434,21 +590,7 @@ def run_ours(args, world, rank, local):
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        threads = host_threads()
-        sample = int(min(nnz, 1_000_000 * threads))
-        # about 10 s of CPU work: one epoch over the sample, then as many
-        # more as that takes to reach ~10 s
-        rate, got, dt = cpu_sample_run(n_users, n_items, k, sample, threads, 1)
-        epochs = 1
-        if dt < 10.0:
-            more = max(1, int(round((10.0 - dt) / max(dt, 1e-3))))
-            _, got2, dt2 = cpu_sample_run(n_users, n_items, k, sample, threads, more, seed=SEED + 1)
-            got, dt, epochs = got + got2, dt + dt2, 1 + more
-            rate = got / dt
-        cpu = {"value": rate, "unit": "updates/s", "cores": threads, "kind": "port",
-               "sample": f"{sample} ratings x {epochs} epochs, full {n_users}x{n_items} P/Q "
-                         f"(f64) at k={k}, stream-only uniform {threads}x{threads + 1} grid, "
-                         f"{dt:.1f} s"}
+        cpu = cpu_baseline(n_users, n_items, k, nnz)
 
     if rank == 0:
         line = {
@@ -457,11 +599,10 @@ def run_ours(args, world, rank, local):
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": precision,
             "data": "synthetic (synthetic_ratings law, device generator)",
-            "config": {"workload": f"{desc}, k={k}, {precision} storage",
-                       "train_ratings": nnz, "test_ratings": test.nnz,
-                       "grid": "uniform 1x2 (1 batch worker per GPU)",
-                       "parallelism": f"replica x{world}" if world > 1 else "single GPU",
-                       "lr": LR, "reg": REG, "mode": args.mode, "kernel": args.kernel,
+            "config": workload_config(args),
+            "counts": {"train_ratings": nnz, "test_ratings": test.nnz},
+            "layout": {"grid": "uniform 1x2 (1 batch worker per GPU, partition.py:89-107)",
+                       "parallelism": "single GPU", "mode": args.mode, "kernel": args.kernel,
                        "variant": args.variant,
                        "qband_impl": getattr(grid, "sub_impl", None),
                        "chain_cfg": (args.chain_cfg if (getattr(grid, "sub_impl", None) or 0) >= 4
@@ -474,22 +615,9 @@ def run_ours(args, world, rank, local):
                                        if (getattr(grid, "sub_impl", None) or 0) >= 4 else None),
                        "item_skew": args.item_skew or None,
                        "row_tiles": (list(grid.sub_tiles) if getattr(grid, "sub_tiles", None)
-                                     else None),
-                       "l2": "inputs larger than L2 (P + triples >> 126 MB); no flush"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "l2_ceiling": (None if l2_rows is None else {
-                             "updates_per_s": l2_rows, "kernel_updates_per_s": kernel_ups,
-                             "frac": kernel_ups / l2_rows,
-                             "source": "scripts/l2_rowbench.cu: random P-row load + "
-                                       + ("store" if p_stores else "vector reduction")
-                                       + ", L2-resident 32 MB, no arithmetic "
-                                       "(profiles/r02/l2_rowbench.jsonl)"}),
-                         "peak_kind": peak_kind, "bytes_per_update": bpu,
-                         "kernel": ("qband_kernel" if args.kernel == "qband"
-                                    else "sgd_hogwild_kernel"),
-                         "mean_launch_ms": mean_ms,
-                         "updates_per_launch": mean_updates},
+                                     else None)},
+            "roofline": roofline_fields(args, achieved, peak, peak_kind, bpu, mean_ms,
+                                        mean_updates, compulsory, l2_rows, kernel_ups, p_stores),
             "rmse": {"epochs": epochs_run, "test": test_rmse},
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -617,14 +745,15 @@ def run_ours_multi(args, world, rank, local):
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synthetic_ratings law, device generator)",
-            "config": {"workload": (f"{desc} row band per GPU of one {m_users}x{n_items} "
-                                    f"matrix (weak scaling), k={k}"
-                                    if args.scaling == "weak" else
-                                    f"{desc} split into {geo} row bands (strong scaling), k={k}"),
-                       "train_ratings": int(n_train), "test_ratings": int(n_test),
-                       "matrix": "one matrix: each rank generates its row band of it "
-                                 "(data.synthetic_band, keyed by global ids)",
+            "config": workload_config(args),
+            "counts": {"train_ratings": int(n_train), "test_ratings": int(n_test)},
+            "layout": {"matrix": (f"{desc} row band per GPU of one {m_users}x{n_items} matrix "
+                                  "(weak scaling)" if args.scaling == "weak" else
+                                  f"{desc} split into {geo} row bands (strong scaling)")
+                                 + ": each rank generates its row band of it "
+                                   "(data.synthetic_band, keyed by global ids)",
                        "grid": f"{geo} row bands x {n_cols} column bands",
+                       "devices": int(torch.cuda.device_count()),
                        "simulated": (None if not args.sim_world else
                                      f"one process with rank 0's band and column geometry of "
                                      f"a {geo}-GPU job (per-GPU throughput; peer pulls of Q "
@@ -632,7 +761,7 @@ def run_ours_multi(args, world, rank, local):
                        "parallelism": f"dp{world} row bands, Q bands leased and pulled peer-to-peer",
                        "kernel": band.kernel, "qband_impl": getattr(band.grid, "sub_impl", None),
                        "item_run_split": getattr(band.grid, "sub_split", None),
-                       "blocks_in_flight": band.concurrency, "lr": LR, "reg": REG},
+                       "blocks_in_flight": band.concurrency},
             "rmse": {"epochs": args.warmup + args.steps, "test": test_rmse},
             "lease_wait_seconds_rank0": trainer.wait_seconds,
             "setup_seconds": setup_s,

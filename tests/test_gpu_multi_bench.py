@@ -77,8 +77,8 @@ def test_two_ranks_strong_yahoo_matches_one_rank_rmse():
     two, err = _bench("--gpus", "2", "--scaling", "strong", *common)
     assert one["n_gpus"] == 1 and two["n_gpus"] == 2
     # the same matrix: same training and test cells
-    assert two["config"]["train_ratings"] == one["config"]["train_ratings"]
-    assert two["config"]["test_ratings"] == one["config"]["test_ratings"]
+    assert two["counts"]["train_ratings"] == one["counts"]["train_ratings"]
+    assert two["counts"]["test_ratings"] == one["counts"]["test_ratings"]
     assert one["rmse"]["epochs"] == two["rmse"]["epochs"] == 7
     assert abs(two["rmse"]["test"] - one["rmse"]["test"]) <= 0.005, (one["rmse"], two["rmse"])
     assert two["value"] > 0 and two["gpu_launches"] == 2 * 5 * 4   # 2 ranks x 5 columns x steps
