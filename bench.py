@@ -920,9 +920,9 @@ def main():
                     help="N>1: a workload-sized band per GPU (weak) or the workload split (strong)")
     ap.add_argument("--multi-concurrency", type=int, default=1,
                     help="N>1: column blocks in flight per GPU (each on its own stream)")
-    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 4, 5, 6], default=-1,
-                    help="Q-band kernel: 0 = warp per rating, 4-6 chained item runs "
-                         "(-1: the layout's, 5 by default)")
+    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 4, 5, 6, 7], default=-1,
+                    help="Q-band kernel: 0 = warp per rating, 4-6 chained item runs, 7 "
+                         "tile-resident P (-1: the layout's, 5 by default)")
     ap.add_argument("--chain-cfg", type=int, choices=[-1, 2, 4, 5, 6], default=-1,
                     help="configuration of the chained kernel (qchain.cuh ChainCfg)")
     ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)

@@ -126,7 +126,7 @@ typedef struct hmf_qband_opts {
    * per sub-band); 5 = 4 with Q deltas: runs of one item may be split over
    * chains, each adds its change back with vector reductions and re-reads the
    * row every `qsync` ratings (bounded staleness); 6 = 5 publishing only at
-   * item and bin changes. */
+   * item and bin changes; 7 = tile-resident P (hmf_sgd_block_ptile_* only). */
   int32_t impl;
   /* Chained-kernel configuration 2, 4, 5 or 6 (lanes per chain, prefetch
    * distance, occupancy); -1 = by k and storage
@@ -215,6 +215,36 @@ int64_t hmf_sgd_block_qband_u16_tiles_f16(uint16_t* user_f, uint16_t* item_f, in
                                           const int32_t* tile_row0, const hmf_qband_opts* opts,
                                           double lr, double reg_user, double reg_item,
                                           uint64_t seed, int64_t col_base, void* stream);
+
+/*
+ * Tile-resident P (implementation 7, ABI 4): the block's users are cut into
+ * n_tiles row tiles, tile t being rows [tile_cut[t], tile_cut[t+1]) of
+ * user_f (absolute indices, i.e. rows[i] - row_base; device int32[n_tiles +
+ * 1]) of at most max_tile_rows rows <= hmf_ptile_max_rows(k, f16); triples
+ * bucketed tile-major into n_sub item sub-bands per tile (sub_ptr: n_tiles *
+ * n_sub + 1 offsets, item-sorted inside a tile; data.bucket_qbands with
+ * impl 7), cols required.  A persistent CTA per SM holds one tile's P rows
+ * in shared memory at a time; chains walk item runs with the Q row in
+ * registers and add Q changes back by vector reductions.  opts.impl must be
+ * -1 or 7; grid_share applies.  Same update rule and return convention as
+ * hmf_sgd_block_qband_*.
+ */
+int32_t hmf_ptile_max_rows(int64_t k, int32_t f16);
+/* Sub-bands per tile the layout should cut (chains per CTA x 4). */
+int32_t hmf_ptile_bins_per_tile(int64_t k);
+int64_t hmf_sgd_block_ptile_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
+                                const int32_t* cols, const float* vals, const int64_t* sub_ptr,
+                                int64_t n_sub, int64_t n_tiles, const int32_t* tile_cut,
+                                int32_t max_tile_rows, const hmf_qband_opts* opts, double lr,
+                                double reg_user, double reg_item, uint64_t seed, int64_t row_base,
+                                int64_t col_base, void* stream);
+int64_t hmf_sgd_block_ptile_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                                const int32_t* rows, const int32_t* cols, const float* vals,
+                                const int64_t* sub_ptr, int64_t n_sub, int64_t n_tiles,
+                                const int32_t* tile_cut, int32_t max_tile_rows,
+                                const hmf_qband_opts* opts, double lr, double reg_user,
+                                double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
+                                void* stream);
 
 /*
  * The reference visit order of a range of n triples under `seed`

@@ -64,6 +64,15 @@ template <int K, typename S, int LPC> struct ChainLay {
 #pragma unroll
     for (int v = 0; v < NV; ++v) V::red(row + off(v, l), d + v * W);
   }
+  // the same row in shared memory (storage type, same element interleave)
+  __device__ static void lds(const S* row, int l, float* o) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) V::lds(row + off(v, l), o + v * W);
+  }
+  __device__ static void sts(S* row, int l, const float* i) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) V::sts(row + off(v, l), i + v * W);
+  }
   // storage-typed row kept raw in registers (RW 32-bit words per lane), so a
   // prefetched fp16 row costs half the registers of its fp32 expansion
   static constexpr int VW = W * int(sizeof(S)) / 4;

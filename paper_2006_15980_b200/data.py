@@ -382,6 +382,8 @@ class DeviceGrid:
     sub_split: int = 1                  # parts per item run (implementation 5)
     sub_qsync: int = 0                  # Q publication period for implementation 5
     sub_pstore: int = 0                 # chained kernel P write-back: 1 stores, 0 reductions
+    sub_tile_cuts: list | None = None   # implementation 7: per block, device int32 tile cuts
+    sub_max_rows: int = 0               # implementation 7: rows of the largest tile
 
     n_row_bands = BlockGrid.n_row_bands
     n_col_bands = BlockGrid.n_col_bands
@@ -576,6 +578,8 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
         impl = qband_impl_for(dev, k, f16, max((grid.col_span(c)[1] - grid.col_span(c)[0]
                                                 for c in range(grid.n_col_bands)), default=0))
     impl = int(impl)
+    if impl == 7:
+        return _bucket_ptile(grid, k, f16, max_tile_rows)
     widest = max((grid.col_span(c)[1] - grid.col_span(c)[0]
                   for c in range(grid.n_col_bands)), default=0)
     if impl == 5 and split is None:
@@ -731,6 +735,74 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     min_rows = min((int(np.min(np.diff(r))) for r in tile_rows if len(r) > 1), default=0)
     grid.sub_pstore = int(impl >= 4 and not f16 and k >= 128
                           and min_rows >= 4 * resident_warps(dev, k, f16, impl, chain_cfg))
+    return grid
+
+
+def ptile_row_cuts(r_lo: int, r_hi: int, k: int, f16: bool, n_sm: int,
+                   max_rows: int | None = None) -> np.ndarray:
+    """Row tiles of implementation 7 (tile-resident P): the fewest equal
+    tiles whose P rows fit one CTA's shared memory (hmf_ptile_max_rows) —
+    rounded up to a multiple of the SM count, so the persistent CTAs finish
+    their last tiles together."""
+    n = r_hi - r_lo
+    cap = int(_lib.load().hmf_ptile_max_rows(int(k), 1 if f16 else 0))
+    if max_rows:
+        cap = min(cap, int(max_rows))
+    t = max(1, -(-n // cap))
+    if t > n_sm // 2:
+        t = -(-t // n_sm) * n_sm
+    t = max(1, min(n, t))
+    return np.linspace(r_lo, r_hi, t + 1).round().astype(np.int64)
+
+
+def _bucket_ptile(grid: DeviceGrid, k: int, f16: bool, max_rows: int | None) -> DeviceGrid:
+    """The layout of implementation 7 (csrc/ptile.cuh): per block, row tiles
+    that fit shared memory (ptile_row_cuts) and, inside each tile, the
+    block's items cut into hmf_ptile_bins_per_tile equal sub-bands, triples
+    sorted by (tile, item) — stable, so each item's ratings keep the block's
+    shuffled order (data.py:242-244, 264).  One stable device sort per block."""
+    torch = _torch()
+    dev = grid.device
+    lib = _lib.load()
+    n_sm = int(torch.cuda.get_device_properties(dev).multi_processor_count)
+    bins = int(lib.hmf_ptile_bins_per_tile(int(k)))
+    sub_ptrs, sub_cuts, sub_tiles, tile_rows, tile_cuts = [], [], [], [], []
+    for b in range(grid.n_blocks):
+        lo, hi = grid.block_range(b)
+        c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
+        r_lo, r_hi = grid.row_span(b // grid.n_col_bands)
+        tiles = ptile_row_cuts(r_lo, r_hi, k, f16, n_sm, max_rows)
+        T = len(tiles) - 1
+        cuts = qband_sub_cuts(c_lo, c_hi, k, bins, 1 << 30)
+        S = len(cuts) - 1
+        ptr = torch.full((T * S + 1,), hi, dtype=torch.int64, device=dev)
+        if hi > lo:
+            d_tiles = torch.from_numpy(tiles[1:-1]).to(dev, torch.int32)
+            d_cuts = torch.from_numpy(cuts[1:-1]).to(dev, torch.int32)
+            tile_of = torch.bucketize(grid.users[lo:hi], d_tiles, right=True)
+            sub_of = torch.bucketize(grid.items[lo:hi], d_cuts, right=True)
+            key = (tile_of.to(torch.int64) * (c_hi - c_lo)
+                   + (grid.items[lo:hi] - c_lo).to(torch.int64))
+            order = torch.sort(key, stable=True).indices
+            grid.users[lo:hi] = grid.users[lo:hi][order]
+            grid.items[lo:hi] = grid.items[lo:hi][order]
+            grid.ratings[lo:hi] = grid.ratings[lo:hi][order]
+            bin_of = tile_of.to(torch.int64) * S + sub_of
+            cnt = torch.bincount(bin_of, minlength=T * S)
+            ptr[0] = lo
+            ptr[1:] = lo + torch.cumsum(cnt, 0)
+            del tile_of, sub_of, key, order, bin_of, cnt
+        sub_ptrs.append(ptr)
+        sub_cuts.append(torch.from_numpy(cuts).to(device=dev, dtype=torch.int32))
+        sub_tiles.append(T)
+        tile_rows.append(tiles)
+        tile_cuts.append(torch.from_numpy(tiles).to(device=dev, dtype=torch.int32))
+    grid.sub_ptr, grid.sub_cuts, grid.sub_tiles = sub_ptrs, sub_cuts, sub_tiles
+    grid.sub_impl, grid.sub_cfg, grid.sub_split, grid.sub_qsync, grid.sub_pstore = 7, -1, 1, 0, 0
+    grid.sub_tile_rows = tile_rows
+    grid.sub_tile_cuts = tile_cuts
+    grid.sub_max_rows = max((int(np.max(np.diff(t))) for t in tile_rows if len(t) > 1),
+                            default=1)
     return grid
 
 

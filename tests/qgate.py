@@ -50,7 +50,7 @@ def reference_rmse(hetmf, n_users, n_items, k, tr, te, epochs, seed=0, threads=N
     return [m.test_rmse for m in res.metrics], init
 
 
-def ours_rmse(train, test, init, k, precision, epochs, seed=0, opts=None):
+def ours_rmse(train, test, init, k, precision, epochs, seed=0, opts=None, impl=None):
     """Per-epoch test RMSE of the bench's GPU path; returns (rmses, grid)."""
     import torch
     from paper_2006_15980_b200 import kernels
@@ -60,7 +60,7 @@ def ours_rmse(train, test, init, k, precision, epochs, seed=0, opts=None):
     n_users, n_items = train.n_users, train.n_items
     grid = build_device_grid(train, np.array([0, n_users]),
                              np.array([0, (n_items + 1) // 2, n_items]))
-    bucket_qbands(grid, k, elem_bytes=2 if precision == "f16" else 4)
+    bucket_qbands(grid, k, elem_bytes=2 if precision == "f16" else 4, impl=impl)
     dt = torch.float16 if precision == "f16" else torch.float32
     model = DeviceModel(torch.from_numpy(init.user_factors).to(dev, dt).contiguous(),
                         torch.from_numpy(init.item_factors).to(dev, dt).contiguous())

@@ -948,3 +948,40 @@ def test_qband_bucketing_many_subbands(dev):
     # stable item runs: inside an item the original (block) order is preserved
     order = np.argsort(m.items, kind="stable")
     assert np.array_equal(users, m.users[order]) and np.array_equal(items, m.items[order])
+
+
+@pytest.mark.parametrize("k,dtype", [(128, torch.float32), (32, torch.float32),
+                                     (64, torch.float16), (256, torch.float32)])
+def test_ptile_conflict_free_equals_oracle(dev, k, dtype):
+    """Implementation 7 (tile-resident P): with distinct users AND distinct
+    items nothing races and nothing is stale, so the result is every triple
+    applied once from the initial factors — the reference update (oracle,
+    f64) within storage rounding — across many row tiles and both blocks."""
+    import oracle
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import (DeviceTriples, RatingMatrix, bucket_qbands,
+                                            build_device_grid)
+    rng = np.random.default_rng(k)
+    n_users, n_items = 200_000, 30_000
+    n = 25_000
+    users = rng.permutation(n_users)[:n].astype(np.int32)
+    items = rng.permutation(n_items)[:n].astype(np.int32)
+    vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
+    m = RatingMatrix(n_users, n_items, users, items, vals)
+    g = build_device_grid(DeviceTriples.from_host(m, dev), [0, n_users],
+                          [0, n_items // 2, n_items])
+    bucket_qbands(g, k, impl=7, elem_bytes=2 if dtype == torch.float16 else 4)
+    assert g.sub_impl == 7 and g.sub_tiles[0] > 1
+    P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
+    Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
+    if dtype == torch.float16:
+        P0, Q0 = P0.astype(np.float16).astype(np.float32), Q0.astype(np.float16).astype(np.float32)
+    P, Q = to_dev(P0, dev, dtype), to_dev(Q0, dev, dtype)
+    got = sum(kernels.launch_block_qband(P, Q, g, b, 0.05, 0.02, 0.03, 7 + b)
+              for b in range(g.n_blocks))
+    assert got == n
+    Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
+    oracle.sgd_range(Pe, Qe, users, items, vals, 0, n, 0.05, 0.02, 0.03, 1, 0, 0)
+    tol = 2e-3 if dtype == torch.float16 else 1e-5
+    assert rel_err(P.double().cpu().numpy(), Pe) < tol
+    assert rel_err(Q.double().cpu().numpy(), Qe) < tol

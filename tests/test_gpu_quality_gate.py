@@ -41,6 +41,13 @@ def data():
 _REF = {}
 
 
+def _fresh(t):
+    """A copy of the training triples (bucketing reorders a grid in place)."""
+    from paper_2006_15980_b200.data import DeviceTriples
+    return DeviceTriples(t.n_users, t.n_items, t.users.clone(), t.items.clone(),
+                         t.ratings.clone())
+
+
 def _reference(hetmf, data, k):
     if k not in _REF:
         _, _, tr, te = data
@@ -53,7 +60,7 @@ def _reference(hetmf, data, k):
 def test_headline_path_rmse_within_0005_of_reference(hetmf, data, k, precision):
     train, test, _, _ = data
     ref, init = _reference(hetmf, data, k)
-    ours, grid = qgate.ours_rmse(train, test, init, k, precision, EPOCHS)
+    ours, grid = qgate.ours_rmse(_fresh(train), test, init, k, precision, EPOCHS)
     print(f"k={k} {precision}: layout impl {grid.sub_impl} split {grid.sub_split} pstore "
           f"{grid.sub_pstore} tiles {grid.sub_tiles}; ours {np.round(ours, 5).tolist()} "
           f"reference {np.round(ref, 5).tolist()}")
@@ -69,3 +76,17 @@ def test_headline_path_rmse_within_0005_of_reference(hetmf, data, k, precision):
     assert np.all(gaps <= 0.005), (ours, ref)
     if precision == "f32":
         assert gaps[0] <= 0.003, (ours[0], ref[0])
+
+
+@pytest.mark.parametrize("precision", ["f32", "f16"])
+@pytest.mark.parametrize("k", [128, 32, 64, 256])
+def test_tile_resident_p_rmse_within_0005_of_reference(hetmf, data, k, precision):
+    """Implementation 7 (tile-resident P, csrc/ptile.cuh) on the same gate."""
+    train, test, _, _ = data
+    ref, init = _reference(hetmf, data, k)
+    ours, grid = qgate.ours_rmse(_fresh(train), test, init, k, precision, EPOCHS, impl=7)
+    print(f"impl 7 k={k} {precision}: tiles {grid.sub_tiles} rows <= {grid.sub_max_rows}; "
+          f"ours {np.round(ours, 5).tolist()} reference {np.round(ref, 5).tolist()}")
+    assert grid.sub_impl == 7
+    gaps = np.abs(np.asarray(ours) - np.asarray(ref))
+    assert np.all(gaps <= 0.005), (ours, ref)
