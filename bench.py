@@ -643,7 +643,7 @@ def run_ours_multi(args, world, rank, local):
     import torch.distributed as dist
     from paper_2006_15980_b200 import _lib
     from paper_2006_15980_b200.data import synthetic_band
-    from paper_2006_15980_b200.distributed import CudaRowBand, LeaseTable, RowBandTrainer
+    from paper_2006_15980_b200.distributed import CudaRowBand, RowBandTrainer, make_lease_table
     from paper_2006_15980_b200.sgd import DeviceModel, residual_sums
 
     _lib.load()
@@ -670,8 +670,10 @@ def run_ours_multi(args, world, rank, local):
     del train
     torch.cuda.synchronize(dev)
     setup_s = time.perf_counter() - t0
-    table = LeaseTable(dist.distributed_c10d._get_default_store(), n_cols, rank,
-                       f"bench{os.getpid() if world == 1 else 0}")
+    run_id = [f"bench{os.getpid()}"]
+    dist.broadcast_object_list(run_id, src=0)
+    table = make_lease_table(args.lease, dist.distributed_c10d._get_default_store(), n_cols,
+                             rank, run_id[0])
     if rank == 0:
         table.initialize()
     dist.barrier()
@@ -693,6 +695,14 @@ def run_ours_multi(args, world, rank, local):
         torch.cuda.synchronize(dev)
     ms = max_over_ranks(e0.elapsed_time(e1), world)
     updates = sum_over_ranks(float(trainer.total_updates - upd0), world)
+    # lease-table cost (all epochs so far), worst rank, against the timed step
+    st = trainer.lease_stats()
+    lease_stats = {"table": st["table"], "leases_rank0": st["leases"],
+                   "ops_per_lease": st["ops_per_lease"],
+                   "us_per_lease_max_rank": max_over_ranks(st["us_per_lease"], world),
+                   "share_of_step_max_rank": max_over_ranks(
+                       st["seconds"] / max(1, args.warmup + args.steps) / (ms / args.steps / 1e3),
+                       world)}
     # one kernel launch per granted block (CudaRowBand.compute)
     launches = int(sum_over_ranks(float(int(trainer.counts.sum()) - blocks0), world))
     # test RMSE after exactly warmup + steps epochs (the N = 1 line's count)
@@ -764,9 +774,12 @@ def run_ours_multi(args, world, rank, local):
                        "blocks_in_flight": band.concurrency},
             "rmse": {"epochs": args.warmup + args.steps, "test": test_rmse},
             "lease_wait_seconds_rank0": trainer.wait_seconds,
+            "leases": lease_stats,
             "setup_seconds": setup_s,
             "gpu_launches": launches, "clocks": clocks.summary(), "e2e": e2e,
         }), flush=True)
+    dist.barrier()
+    table.close(unlink=rank == 0)
 
 
 def run_e2e_stream(args, se, model, test, dev):
@@ -918,6 +931,9 @@ def main():
     ap.add_argument("--multi-kernel", choices=["auto", "qband", "range"], default="auto")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="N>1: a workload-sized band per GPU (weak) or the workload split (strong)")
+    ap.add_argument("--lease", choices=["shm", "store"], default="shm",
+                    help="N>1: column-lease table: node-local shared memory (csrc/lease.cu) "
+                         "or the torch.distributed store")
     ap.add_argument("--multi-concurrency", type=int, default=1,
                     help="N>1: column blocks in flight per GPU (each on its own stream)")
     ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 4, 5, 6, 7], default=-1,

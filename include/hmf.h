@@ -341,6 +341,36 @@ int hmf_ipc_get_handle(const void* dptr, uint8_t* handle64, int64_t* offset);
 int hmf_ipc_open_handle(const uint8_t* handle64, void** dptr);
 int hmf_ipc_close_handle(void* dptr);
 
+/*
+ * Node-local column-lease table of the multi-GPU engine (replaces the
+ * reference's in-process GridScheduler.acquire/release for column units,
+ * scheduler.py:333-409; the torch.distributed TCPStore compare-and-set in
+ * distributed.LeaseTable is the portable alternative).  A POSIX shared-memory
+ * segment `name` ("/..."): per column band its holder (-1 free) and last
+ * owner (-1 none), and a ticket counter; every operation is one lock-free
+ * atomic (host code, no GPU needed).
+ *   hmf_lease_open: create != 0 (one process, before the others open it)
+ *     makes a fresh segment with every column free; otherwise maps the
+ *     existing one (n_cols must match).  *table is an opaque handle.
+ *   hmf_lease_try_acquire: 1 granted, 0 held by someone, < 0 error.
+ *   hmf_lease_acquire_first: tries cands[0..n) in order; *got = the first
+ *     granted column, or -1 if every candidate is held.
+ *   hmf_lease_release: records rank as the column's owner, then frees it;
+ *     error if rank does not hold it.
+ *   hmf_lease_ticket: a global sequence number (1, 2, ...).
+ *   hmf_lease_ops: atomic operations served so far (all processes).
+ */
+int hmf_lease_open(const char* name, int32_t n_cols, int32_t create, void** table);
+int hmf_lease_close(void* table, int32_t unlink_segment);
+int32_t hmf_lease_try_acquire(void* table, int32_t c, int32_t rank);
+int hmf_lease_acquire_first(void* table, const int32_t* cands, int32_t n, int32_t rank,
+                            int32_t* got);
+int32_t hmf_lease_release(void* table, int32_t c, int32_t rank);
+int hmf_lease_owner(void* table, int32_t c, int32_t* owner);
+int hmf_lease_holder(void* table, int32_t c, int32_t* holder);
+int64_t hmf_lease_ticket(void* table);
+int64_t hmf_lease_ops(void* table);
+
 #ifdef __cplusplus
 }
 #endif

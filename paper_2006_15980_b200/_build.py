@@ -41,20 +41,39 @@ def needs_rebuild() -> bool:
     return any(p.stat().st_mtime > mtime for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_rebuild():
-        return LIB_PATH
-    LIB_DIR.mkdir(parents=True, exist_ok=True)
-    tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(INCLUDE), "-o", str(tmp), *map(str, sources())]
+def _compile(src: Path, obj: Path, verbose: bool) -> str:
+    cmd = [nvcc(), *NVCC_FLAGS[:-3], "-I", str(INCLUDE), "-c",
+           "-o", str(obj), str(src)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed building {LIB_PATH.name}")
+        raise RuntimeError(f"nvcc failed on {src.name}:\n{res.stdout}{res.stderr}")
+    return res.stderr
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    """One object per translation unit, compiled in parallel (the Q-band
+    kernels dominate), then one link with the static CUDA runtime."""
+    if not force and not needs_rebuild():
+        return LIB_PATH
+    from concurrent.futures import ThreadPoolExecutor
+    LIB_DIR.mkdir(parents=True, exist_ok=True)
+    obj_dir = PKG.parent / "build" / "obj"
+    obj_dir.mkdir(parents=True, exist_ok=True)
+    srcs = sources()
+    objs = [obj_dir / (s.stem + ".o") for s in srcs]
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        logs = list(ex.map(lambda so: _compile(so[0], so[1], verbose), zip(srcs, objs)))
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("".join(logs))
+    tmp = LIB_PATH.with_suffix(".so.tmp")
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+           "-Xcompiler", "-fPIC", "-o", str(tmp), *map(str, objs), "-lrt"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"nvcc failed linking {LIB_PATH.name}")
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

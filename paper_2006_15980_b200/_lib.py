@@ -91,6 +91,15 @@ SIGNATURES = {
     "hmf_ipc_get_handle": (C.c_int, [_p, C.POINTER(C.c_uint8), C.POINTER(_i64)]),
     "hmf_ipc_open_handle": (C.c_int, [C.POINTER(C.c_uint8), C.POINTER(_p)]),
     "hmf_ipc_close_handle": (C.c_int, [_p]),
+    "hmf_lease_open": (C.c_int, [C.c_char_p, _i32, _i32, C.POINTER(_p)]),
+    "hmf_lease_close": (C.c_int, [_p, _i32]),
+    "hmf_lease_try_acquire": (_i32, [_p, _i32, _i32]),
+    "hmf_lease_acquire_first": (C.c_int, [_p, C.POINTER(_i32), _i32, _i32, C.POINTER(_i32)]),
+    "hmf_lease_release": (_i32, [_p, _i32, _i32]),
+    "hmf_lease_owner": (C.c_int, [_p, _i32, C.POINTER(_i32)]),
+    "hmf_lease_holder": (C.c_int, [_p, _i32, C.POINTER(_i32)]),
+    "hmf_lease_ticket": (_i64, [_p]),
+    "hmf_lease_ops": (_i64, [_p]),
 }
 
 

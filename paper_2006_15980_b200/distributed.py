@@ -9,9 +9,11 @@ The reference runs its workers as threads around one GridScheduler
   the reference's P-band residency (workers.py:13-17, 324-328);
 * columns are 2*N+1 bands (a primary and a staged-ahead column per GPU plus a
   spare, the reference's column rule for batch workers);
-* a column lease is a compare-and-set on a key of the torch.distributed store
-  (LeaseTable): at most one GPU holds a column band, so Q bands have a single
-  owner at a time, exactly the scheduler's independence rule;
+* a column lease is a compare-and-set on a lock-free table in node-local
+  shared memory (ShmLeaseTable, csrc/lease.cu; or, portably, on a key of the
+  torch.distributed store, LeaseTable): at most one GPU holds a column band,
+  so Q bands have a single owner at a time, exactly the scheduler's
+  independence rule;
 * each GPU pulls (RowBandTrainer) its undone blocks dynamically, least-updated
   first with a seeded tie break, and keeps a staged-ahead column: while the
   kernel runs on column c it tries to lease the next column and starts
@@ -41,7 +43,12 @@ FREE = b"free"
 
 
 class LeaseTable:
-    """Column-band leases over a torch.distributed Store (compare-and-set)."""
+    """Column-band leases over a torch.distributed Store (compare-and-set):
+    portable (any backend, any number of nodes), one TCP round trip per
+    operation.  `ops` / `seconds` count the store operations and the host
+    time spent in them."""
+
+    kind = "store"
 
     def __init__(self, store, n_cols: int, rank: int, run_id: str):
         self.store = store
@@ -49,6 +56,8 @@ class LeaseTable:
         self.rank = rank
         self.prefix = f"hmf/{run_id}"
         self._me = str(rank).encode()
+        self.ops = 0
+        self.seconds = 0.0
 
     def _key(self, kind: str, c: int) -> str:
         return f"{self.prefix}/{kind}/{c}"
@@ -61,22 +70,161 @@ class LeaseTable:
             self.store.set(self._key("owner", c), b"-1")
 
     def try_acquire(self, c: int) -> bool:
+        t0 = time.perf_counter()
         got = self.store.compare_set(self._key("lease", c), FREE, self._me)
+        self.ops += 1
+        self.seconds += time.perf_counter() - t0
         return bytes(got) == self._me
 
     def owner(self, c: int) -> int:
-        return int(bytes(self.store.get(self._key("owner", c))))
+        t0 = time.perf_counter()
+        o = int(bytes(self.store.get(self._key("owner", c))))
+        self.ops += 1
+        self.seconds += time.perf_counter() - t0
+        return o
 
     def release(self, c: int) -> None:
+        t0 = time.perf_counter()
         # publish the new owner first: whoever leases c next pulls from us
         self.store.set(self._key("owner", c), self._me)
         got = self.store.compare_set(self._key("lease", c), self._me, FREE)
+        self.ops += 2
+        self.seconds += time.perf_counter() - t0
         if bytes(got) != FREE:
             raise RuntimeError(f"rank {self.rank} released column {c} it did not hold")
 
     def ticket(self) -> int:
         """A global sequence number (lease order, for traces and tests)."""
-        return int(self.store.add(f"{self.prefix}/seq", 1))
+        t0 = time.perf_counter()
+        n = int(self.store.add(f"{self.prefix}/seq", 1))
+        self.ops += 1
+        self.seconds += time.perf_counter() - t0
+        return n
+
+    def close(self, unlink: bool = False) -> None:
+        pass
+
+
+class ShmLeaseTable:
+    """Column-band leases in node-local shared memory (csrc/lease.cu): the
+    same protocol as LeaseTable — holder compare-and-set, owner published
+    before the release — as lock-free atomics on a POSIX shared-memory
+    segment that every GPU process of the node maps.  An operation costs
+    ~0.1-1 us instead of a TCP round trip, and acquire_first tries a whole
+    candidate list in one call.  Rank 0 creates the segment in initialize()
+    (before the first barrier, as LeaseTable); the others map it on first
+    use.  Host code only: works without a GPU (the gloo tests)."""
+
+    kind = "shm"
+
+    def __init__(self, n_cols: int, rank: int, run_id: str):
+        self.n_cols = n_cols
+        self.rank = rank
+        self.name = f"/hmf_lease_{run_id}".encode()
+        self._t = None
+        self._lib = None
+        self.ops = 0
+        self.seconds = 0.0
+
+    def _open(self, create: bool) -> None:
+        from . import _lib
+        lib = _lib.load()
+        h = ctypes.c_void_p()
+        _lib.check(lib.hmf_lease_open(self.name, self.n_cols, 1 if create else 0,
+                                      ctypes.byref(h)), "hmf_lease_open")
+        self._t, self._lib = h, lib
+
+    def _table(self):
+        if self._t is None:
+            self._open(create=False)
+        return self._t
+
+    def initialize(self) -> None:
+        self._open(create=True)
+
+    def _check(self, rc: int, what: str) -> int:
+        if rc < 0:
+            from . import _lib
+            raise _lib.HmfError(f"{what} failed ({rc}): {_lib.last_error()}")
+        return rc
+
+    def try_acquire(self, c: int) -> bool:
+        t = self._table()
+        t0 = time.perf_counter()
+        rc = self._lib.hmf_lease_try_acquire(t, int(c), self.rank)
+        self.ops += 1
+        self.seconds += time.perf_counter() - t0
+        return self._check(rc, "hmf_lease_try_acquire") == 1
+
+    def acquire_first(self, cands) -> int | None:
+        """The first candidate column granted (in list order), or None."""
+        t = self._table()
+        arr = (ctypes.c_int32 * len(cands))(*[int(c) for c in cands])
+        got = ctypes.c_int32(-1)
+        t0 = time.perf_counter()
+        rc = self._lib.hmf_lease_acquire_first(t, arr, len(cands), self.rank, ctypes.byref(got))
+        self.ops += 1
+        self.seconds += time.perf_counter() - t0
+        self._check(rc, "hmf_lease_acquire_first")
+        return None if got.value < 0 else int(got.value)
+
+    def owner(self, c: int) -> int:
+        t = self._table()
+        o = ctypes.c_int32()
+        t0 = time.perf_counter()
+        rc = self._lib.hmf_lease_owner(t, int(c), ctypes.byref(o))
+        self.ops += 1
+        self.seconds += time.perf_counter() - t0
+        self._check(rc, "hmf_lease_owner")
+        return int(o.value)
+
+    def holder(self, c: int) -> int:
+        o = ctypes.c_int32()
+        self._check(self._lib.hmf_lease_holder(self._table(), int(c), ctypes.byref(o)),
+                    "hmf_lease_holder")
+        return int(o.value)
+
+    def release(self, c: int) -> None:
+        t = self._table()
+        t0 = time.perf_counter()
+        rc = self._lib.hmf_lease_release(t, int(c), self.rank)
+        self.ops += 1
+        self.seconds += time.perf_counter() - t0
+        if rc < 0:
+            raise RuntimeError(f"rank {self.rank} released column {c} it did not hold")
+
+    def ticket(self) -> int:
+        t = self._table()
+        t0 = time.perf_counter()
+        n = self._lib.hmf_lease_ticket(t)
+        self.ops += 1
+        self.seconds += time.perf_counter() - t0
+        return int(self._check(n, "hmf_lease_ticket"))
+
+    def total_ops(self) -> int:
+        """Operations served by the segment, all processes."""
+        return int(self._lib.hmf_lease_ops(self._table()))
+
+    def close(self, unlink: bool = False) -> None:
+        if self._t is not None:
+            self._lib.hmf_lease_close(self._t, 1 if unlink else 0)
+            self._t = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def make_lease_table(kind: str, store, n_cols: int, rank: int, run_id: str):
+    """kind "shm" (one node, the default) or "store" (the torch.distributed
+    store: portable across nodes)."""
+    if kind == "shm":
+        return ShmLeaseTable(n_cols, rank, run_id)
+    if kind == "store":
+        return LeaseTable(store, n_cols, rank, run_id)
+    raise ValueError(f"lease table kind must be 'shm' or 'store', not {kind!r}")
 
 
 def new_run_id() -> str:
@@ -115,18 +263,35 @@ class RowBandTrainer:
         return [c for _, _, c in sorted(zip((self.counts[c] for c in cols), ties, cols))]
 
     def _grab(self, todo: set, blocking: bool):
-        delay = 2e-5
+        delay = 2e-6 if hasattr(self.table, "acquire_first") else 2e-5
         t0 = time.perf_counter()
         while todo:
-            for c in self._candidates(todo):
-                if self.table.try_acquire(c):
+            cands = self._candidates(todo)
+            if hasattr(self.table, "acquire_first"):
+                c = self.table.acquire_first(cands)
+                if c is not None:
                     self.wait_seconds += time.perf_counter() - t0
                     return c
+            else:
+                for c in cands:
+                    if self.table.try_acquire(c):
+                        self.wait_seconds += time.perf_counter() - t0
+                        return c
             if not blocking:
                 return None
             time.sleep(delay)
             delay = min(delay * 2, 1e-3)
         return None
+
+    def lease_stats(self) -> dict:
+        """Lease-table cost on this rank: operations and host seconds spent
+        in them, per granted lease."""
+        n = max(1, int(self.counts.sum()))
+        return {"table": getattr(self.table, "kind", "?"), "leases": int(self.counts.sum()),
+                "ops": int(self.table.ops), "ops_per_lease": self.table.ops / n,
+                "seconds": float(self.table.seconds),
+                "us_per_lease": 1e6 * self.table.seconds / n,
+                "wait_seconds": float(self.wait_seconds)}
 
     def _start(self, c: int) -> None:
         """Lease granted: stamp the seed, pull the band, enqueue compute."""

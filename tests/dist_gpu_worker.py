@@ -38,7 +38,7 @@ def main(out_dir, kernel="exact", stage=False):
     import torch
     import torch.distributed as dist
     from paper_2006_15980_b200.data import DeviceTriples
-    from paper_2006_15980_b200.distributed import CudaRowBand, LeaseTable, RowBandTrainer
+    from paper_2006_15980_b200.distributed import CudaRowBand, RowBandTrainer, make_lease_table
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"]) % torch.cuda.device_count()
@@ -55,7 +55,10 @@ def main(out_dir, kernel="exact", stage=False):
                          torch.from_numpy(vals[keep].astype(np.float32)).to(dev))
     band = CudaRowBand(dist, rank, world, dev, trip, lo, hi, col_cuts, K, LR, REG, REG,
                        kernel=kernel, init=(P0[lo:hi], Q0))
-    table = LeaseTable(dist.distributed_c10d._get_default_store(), band.n_cols, rank, "gputest")
+    run_id = [f"gputest{os.getpid()}"]
+    dist.broadcast_object_list(run_id, src=0)
+    table = make_lease_table("shm", dist.distributed_c10d._get_default_store(), band.n_cols,
+                             rank, run_id[0])
     if rank == 0:
         table.initialize()
     dist.barrier()
@@ -85,6 +88,7 @@ def main(out_dir, kernel="exact", stage=False):
         with open(os.path.join(out_dir, "result.pkl"), "wb") as fh:
             pickle.dump((res, band.Q.cpu().numpy(), row_cuts, col_cuts), fh)
     dist.barrier()
+    table.close(unlink=rank == 0)
     dist.destroy_process_group()
 
 

@@ -3,7 +3,8 @@
 Each process plays one GPU: a resident P row band, its own Q replica (a
 shared memory-mapped file standing in for the device allocation peers map
 with CUDA IPC), the oracle kernel as the compute.  Columns are leased
-through the torch.distributed store exactly as on the GPU path, Q bands are
+through the node-local shared-memory lease table (csrc/lease.cu) or the
+torch.distributed store, exactly as on the GPU path, Q bands are
 pulled from their last owner, and the result must equal a serial replay of
 the recorded lease order bit for bit — the reference's own check for its
 threaded workers (tests/test_workers.py:43-70).
@@ -83,9 +84,9 @@ class CpuBand:
         pass
 
 
-def _worker(rank, world, port, tmp):
+def _worker(rank, world, port, tmp, kind="store"):
     import torch.distributed as dist
-    from paper_2006_15980_b200.distributed import LeaseTable, RowBandTrainer
+    from paper_2006_15980_b200.distributed import RowBandTrainer, make_lease_table
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -94,7 +95,7 @@ def _worker(rank, world, port, tmp):
     col_cuts = np.array([0, 14, 28, 42, 56, N_ITEMS])       # 2N+1 column bands
     band = CpuBand(rank, world, tmp, row_cuts, col_cuts, users, items, vals, P0, Q0)
     store = dist.distributed_c10d._get_default_store()
-    table = LeaseTable(store, band.n_cols, rank, "test")
+    table = make_lease_table(kind, store, band.n_cols, rank, f"test{port}")
     if rank == 0:
         table.initialize()
     dist.barrier()
@@ -114,10 +115,12 @@ def _worker(rank, world, port, tmp):
         with open(os.path.join(tmp, "logs.pkl"), "wb") as fh:
             pickle.dump(logs, fh)
     dist.barrier()
+    table.close(unlink=rank == 0)
     dist.destroy_process_group()
 
 
-def test_two_rank_lease_protocol_equals_serial_replay(tmp_path):
+@pytest.mark.parametrize("kind", ["store", "shm"])
+def test_two_rank_lease_protocol_equals_serial_replay(tmp_path, kind):
     import pickle
 
     import oracle
@@ -128,7 +131,7 @@ def test_two_rank_lease_protocol_equals_serial_replay(tmp_path):
         mm = np.memmap(tmp_path / f"q{r}.bin", dtype=np.float64, mode="w+", shape=(N_ITEMS, K))
         mm[:] = Q0
         mm.flush()
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), kind), nprocs=2, join=True)
     logs = pickle.loads((tmp_path / "logs.pkl").read_bytes())
     row_cuts = np.array([0, 41, N_USERS])
     col_cuts = np.array([0, 14, 28, 42, 56, N_ITEMS])

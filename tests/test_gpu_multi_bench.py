@@ -82,3 +82,7 @@ def test_two_ranks_strong_yahoo_matches_one_rank_rmse():
     assert one["rmse"]["epochs"] == two["rmse"]["epochs"] == 7
     assert abs(two["rmse"]["test"] - one["rmse"]["test"]) <= 0.005, (one["rmse"], two["rmse"])
     assert two["value"] > 0 and two["gpu_launches"] == 2 * 5 * 4   # 2 ranks x 5 columns x steps
+    # leases through the node-local table: a few atomics per lease, a
+    # negligible share of the step (the TCPStore cost was unmeasured)
+    assert two["leases"]["table"] == "shm"
+    assert two["leases"]["share_of_step_max_rank"] < 0.02, two["leases"]
