@@ -344,8 +344,17 @@ def ncu_summary(key: str):
         return None
 
 
+def binding_unit(ncu: dict) -> str:
+    """The busiest unit of an ncu capture, named for this kernel family."""
+    units = {"L1TEX / shared-memory data pipe (P-row loads and stores, shuffles)":
+             ncu.get("l1tex_pct", 0.0),
+             "L2 (LTS)": ncu.get("lts_pct", 0.0), "DRAM": ncu.get("dram_pct", 0.0),
+             "instruction issue (latency-bound: few eligible warps)": ncu.get("issue_pct", 0.0)}
+    return max(units, key=units.get)
+
+
 def roofline_fields(args, achieved, peak, peak_kind, bpu, mean_ms, mean_updates, compulsory,
-                    l2_rows, kernel_ups, p_stores) -> dict:
+                    l2_rows, kernel_ups, p_stores, impl=None) -> dict:
     """The dominant kernel against its bounds.
 
     frac (the contract's roofline): ALGORITHMIC bytes per launch (12 + 16k per
@@ -358,7 +367,10 @@ def roofline_fields(args, achieved, peak, peak_kind, bpu, mean_ms, mean_updates,
     live launch time, over the same peak), `compulsory` (the bytes that must
     cross HBM once per launch) and `binding_unit` (the busiest unit)."""
     k = args.k or WORKLOADS[args.workload][3]
-    ncu = ncu_summary(f"{args.workload}_k{k}_{args.precision}_{args.kernel}")
+    base = f"{args.workload}_k{k}_{args.precision}_{args.kernel}"
+    ncu = ncu_summary(f"{base}_impl{impl}") if impl is not None else None
+    if ncu is None and impl in (None, 5):
+        ncu = ncu_summary(base)            # round-2 baseline capture (implementation 5)
     dram = None
     if ncu:
         gbs = ncu["dram_bytes"] / (mean_ms / 1e3) / 1e9
@@ -369,10 +381,14 @@ def roofline_fields(args, achieved, peak, peak_kind, bpu, mean_ms, mean_updates,
            "peak_kind": peak_kind, "bytes_per_update": bpu,
            "frac_meaning": "north-star ratio: algorithmic bytes (rating + p_u, q_v read and "
                            "written) per launch / live launch time / measured HBM copy BW; > 1 "
-                           "because P rows are served from L2 (row tiles); see dram, "
-                           "compulsory, binding_unit for the measured picture",
-           "kernel": ncu["kernel"] if ncu else ("qchain_kernel" if args.kernel == "qband"
-                                                else "sgd_hogwild_kernel"),
+                           "because P rows are served on chip (L2 row tiles; shared-memory "
+                           "tiles for implementations 7-8); see dram, compulsory, "
+                           "binding_unit for the measured picture",
+           "kernel": ncu["kernel"] if ncu else (
+               "sgd_hogwild_kernel" if args.kernel != "qband" else
+               {0: "qband_kernel", 7: "ptile_kernel", 8: "runs_kernel"}.get(impl,
+                                                                             "qchain_kernel")),
+           "qband_impl": impl,
            "mean_launch_ms": mean_ms, "updates_per_launch": mean_updates,
            "dram": dram,
            "compulsory": (None if compulsory is None else {
@@ -380,10 +396,14 @@ def roofline_fields(args, achieved, peak, peak_kind, bpu, mean_ms, mean_updates,
                "what": "triples once + one read and one write of the block's P band and Q band",
                "dram_over_compulsory": (ncu["dram_bytes"] / compulsory) if ncu else None}),
            "binding_unit": (None if not ncu else {
-               "unit": "L1TEX (LSU request path: P-row loads and stores/reductions)",
+               "unit": binding_unit(ncu),
                "l1tex_pct": ncu["l1tex_pct"], "lts_pct": ncu["lts_pct"],
                "dram_pct": ncu["dram_pct"], "sm_pct": ncu["sm_pct"],
-               "l2_hit_pct": ncu["l2_hit_pct"], "source": ncu["source"]}),
+               "issue_pct": ncu.get("issue_pct"),
+               "l2_hit_pct": ncu["l2_hit_pct"],
+               "instructions_per_update": (ncu["instructions"] / mean_updates
+                                           if ncu.get("instructions") else None),
+               "source": ncu["source"]}),
            "l2_ceiling": (None if l2_rows is None else {
                "updates_per_s": l2_rows, "kernel_updates_per_s": kernel_ups,
                "frac": kernel_ups / l2_rows,
@@ -495,6 +515,7 @@ def run_ours(args, world, rank, local):
         from paper_2006_15980_b200.workers import StreamingEpoch
         stream_epoch = StreamingEpoch(grid, k, n_buffers=args.stream_buffers,
                                       tiles_per_chunk=args.stream_tiles,
+                                      runs_chunks_per_block=args.stream_chunks,
                                       last_chunk_tiles=args.stream_last,
                                       reuse=args.stream_reuse, opts=overrides)
     model = init_device_model(n_users, n_items, k, SEED, device=dev,
@@ -557,7 +578,10 @@ def run_ours(args, world, rank, local):
     p_stores = (precision == "f32" and args.kernel == "qband"
                 and (getattr(grid, "sub_impl", None) or 0) >= 4
                 and (args.pstore == 1 or (args.pstore < 0 and getattr(grid, "sub_pstore", 0))))
-    l2_rows = l2_ceiling(k, precision, bool(p_stores))
+    impl_used = getattr(grid, "sub_impl", None)
+    # the L2 row-load ceiling describes the L2 row-tile kernels; 7 and 8 keep
+    # P in shared memory
+    l2_rows = None if (impl_used or 0) >= 7 else l2_ceiling(k, precision, bool(p_stores))
     kernel_ups = mean_updates / (mean_ms / 1e3)
     # compulsory DRAM bytes of one launch: its triples once, one read and one
     # write of every P row of its row band and of every Q row of its column
@@ -570,7 +594,12 @@ def run_ours(args, world, rank, local):
             continue
         r0, r1 = grid.row_span(b // grid.n_col_bands)
         c0, c1 = grid.col_span(b % grid.n_col_bands)
-        comp.append((hi - lo) * 12 + 2 * ((r1 - r0) + (c1 - c0)) * k * s_el)
+        if impl_used == 8:
+            # users + ratings (items live in the run descriptors, 16 B each)
+            n_runs = int(grid.sub_ptr[b].shape[0])
+            comp.append((hi - lo) * 8 + 16 * n_runs + 2 * ((r1 - r0) + (c1 - c0)) * k * s_el)
+        else:
+            comp.append((hi - lo) * 12 + 2 * ((r1 - r0) + (c1 - c0)) * k * s_el)
     compulsory = float(np.mean(comp)) if comp else None
 
     # test RMSE after the epochs run (not timed)
@@ -617,7 +646,8 @@ def run_ours(args, world, rank, local):
                        "row_tiles": (list(grid.sub_tiles) if getattr(grid, "sub_tiles", None)
                                      else None)},
             "roofline": roofline_fields(args, achieved, peak, peak_kind, bpu, mean_ms,
-                                        mean_updates, compulsory, l2_rows, kernel_ups, p_stores),
+                                        mean_updates, compulsory, l2_rows, kernel_ups, p_stores,
+                                        getattr(grid, "sub_impl", None)),
             "rmse": {"epochs": epochs_run, "test": test_rmse},
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -936,9 +966,10 @@ def main():
                          "or the torch.distributed store")
     ap.add_argument("--multi-concurrency", type=int, default=1,
                     help="N>1: column blocks in flight per GPU (each on its own stream)")
-    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 4, 5, 6, 7], default=-1,
+    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 4, 5, 6, 7, 8], default=-1,
                     help="Q-band kernel: 0 = warp per rating, 4-6 chained item runs, 7 "
-                         "tile-resident P (-1: the layout's, 5 by default)")
+                         "tile-resident P, 8 run groups over it (-1: the layout's choice, "
+                         "data.tile_resident_impl, else 5)")
     ap.add_argument("--chain-cfg", type=int, choices=[-1, 2, 4, 5, 6], default=-1,
                     help="configuration of the chained kernel (qchain.cuh ChainCfg)")
     ap.add_argument("--chain-lockstep", type=int, choices=[0, 1, 2, 3], default=None)
@@ -947,6 +978,9 @@ def main():
                          "0 reductions, 1 stores")
     ap.add_argument("--stream-buffers", type=int, default=3,
                     help="e2e: device staging buffers (ring)")
+    ap.add_argument("--stream-chunks", type=int, default=2,
+                    help="e2e with implementation 8: chunks per block (each a whole fraction "
+                         "of the block's row tiles)")
     ap.add_argument("--stream-tiles", type=int, default=4,
                     help="e2e: row tiles per streamed chunk (one launch each)")
     ap.add_argument("--stream-last", type=int, default=0,

@@ -13,6 +13,7 @@
  *   hmf_sgd_block_qband_{f32,f16} BatchEngine.compute on a staged item band
  *   hmf_sgd_block_qband_u16_*     (the same, uint16 tile-relative row ids)
  *   hmf_sgd_block_qband_u16_tiles_*  (the same over several row tiles)
+ *   hmf_sgd_block_ptile_*, hmf_sgd_block_runs_*  (the same, P tile in shared memory)
  *                                                              workers.py:186-255
  *   hmf_qband_resolve_*, _slots_per_sm, _chain_lanes, _max_items
  *                                 (layout queries; no reference counterpart)
@@ -126,7 +127,8 @@ typedef struct hmf_qband_opts {
    * per sub-band); 5 = 4 with Q deltas: runs of one item may be split over
    * chains, each adds its change back with vector reductions and re-reads the
    * row every `qsync` ratings (bounded staleness); 6 = 5 publishing only at
-   * item and bin changes; 7 = tile-resident P (hmf_sgd_block_ptile_* only). */
+   * item and bin changes; 7 = tile-resident P (hmf_sgd_block_ptile_* only);
+   * 8 = run groups over a tile-resident P (hmf_sgd_block_runs_* only). */
   int32_t impl;
   /* Chained-kernel configuration 2, 4, 5 or 6 (lanes per chain, prefetch
    * distance, occupancy); -1 = by k and storage
@@ -245,6 +247,54 @@ int64_t hmf_sgd_block_ptile_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                 const hmf_qband_opts* opts, double lr, double reg_user,
                                 double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
                                 void* stream);
+
+/*
+ * Run groups over a tile-resident P (implementation 8): the block's users cut
+ * into n_tiles row tiles as for implementation 7 (tile t = rows
+ * [tile_cut[t], tile_cut[t+1]) of user_f, at most max_tile_rows rows <=
+ * hmf_ptile_max_rows(k, f16)); inside a tile the ratings are grouped into
+ * runs (all ratings of one item, in the block's order), runs sorted by
+ * length, longest first.  runs: int32[n_runs][4] descriptors, 16-byte
+ * aligned; run r = {first, len, item, 0} holds ratings [first, first + len)
+ * of rows / vals (offsets relative to those pointers), all of item `item`
+ * (absolute, minus col_base); tile t's runs are [tile_run[t],
+ * tile_run[t+1]).  Device arrays; data.bucket_qbands with impl 8 builds them.  A persistent CTA per SM holds one tile's P rows in
+ * shared memory; each warp takes groups of hmf_runs_chains_per_warp(k)
+ * consecutive runs, one per lane-group chain, the item's Q row in registers,
+ * Q changes added back by vector reductions at the run's end.  rows: int32
+ * user ids (minus row_base), or with the _u16 entry points uint16 ids
+ * relative to the tile (tiles of at most 65536 rows; the streamed form:
+ * 6 bytes per rating, items implicit in the runs).  opts.impl must be -1 or
+ * 8; grid_share applies.  Same update rule and return convention as
+ * hmf_sgd_block_qband_*.
+ */
+int32_t hmf_runs_chains_per_warp(int64_t k);
+int64_t hmf_sgd_block_runs_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
+                               const float* vals, const int32_t* runs, const int32_t* tile_run,
+                               const int32_t* tile_cut, int64_t n_tiles, int32_t max_tile_rows,
+                               const hmf_qband_opts* opts, double lr, double reg_user,
+                               double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
+                               void* stream);
+int64_t hmf_sgd_block_runs_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                               const int32_t* rows, const float* vals, const int32_t* runs,
+                               const int32_t* tile_run, const int32_t* tile_cut, int64_t n_tiles,
+                               int32_t max_tile_rows, const hmf_qband_opts* opts, double lr,
+                               double reg_user, double reg_item, uint64_t seed, int64_t row_base,
+                               int64_t col_base, void* stream);
+int64_t hmf_sgd_block_runs_u16_f32(float* user_f, float* item_f, int64_t k, const uint16_t* rows,
+                                   const float* vals, const int32_t* runs,
+                                   const int32_t* tile_run, const int32_t* tile_cut,
+                                   int64_t n_tiles, int32_t max_tile_rows,
+                                   const hmf_qband_opts* opts, double lr, double reg_user,
+                                   double reg_item, uint64_t seed, int64_t row_base,
+                                   int64_t col_base, void* stream);
+int64_t hmf_sgd_block_runs_u16_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                                   const uint16_t* rows, const float* vals, const int32_t* runs,
+                                   const int32_t* tile_run, const int32_t* tile_cut,
+                                   int64_t n_tiles, int32_t max_tile_rows,
+                                   const hmf_qband_opts* opts, double lr, double reg_user,
+                                   double reg_item, uint64_t seed, int64_t row_base,
+                                   int64_t col_base, void* stream);
 
 /*
  * The reference visit order of a range of n triples under `seed`

@@ -72,6 +72,15 @@ SIGNATURES = {
                                        _f64, _f64, _f64, _u64, _i64, _i64, _p]),
     "hmf_sgd_block_ptile_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _i64, _i64, _p, _i32, _p,
                                        _f64, _f64, _f64, _u64, _i64, _i64, _p]),
+    "hmf_runs_chains_per_warp": (_i32, [_i64]),
+    "hmf_sgd_block_runs_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p, _f64,
+                                      _f64, _f64, _u64, _i64, _i64, _p]),
+    "hmf_sgd_block_runs_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p, _f64,
+                                      _f64, _f64, _u64, _i64, _i64, _p]),
+    "hmf_sgd_block_runs_u16_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p,
+                                          _f64, _f64, _f64, _u64, _i64, _i64, _p]),
+    "hmf_sgd_block_runs_u16_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p,
+                                          _f64, _f64, _f64, _u64, _i64, _i64, _p]),
     "hmf_visit_order": (C.c_int, [_i64, _u64, _p, _p]),
     "hmf_mix64": (_u64, [C.POINTER(_u64), _i32]),
     "hmf_residual_sums_f32": (C.c_int, [_p, _p, _i64, _p, _p, _p, _i64, _i64, _i64, _i32, _p, _p]),

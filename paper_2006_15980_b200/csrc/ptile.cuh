@@ -94,7 +94,10 @@ __global__ void __launch_bounds__(WPB * 32, 1)
     int len = 0, nf = 0, nb = 0, rot = 0, x = 0, cnt = 0;
     int32_t cu = -1, cv = 0, nu = -1, nv = 0;
     float cr = 0.f, nr = 0.f;
-    float qs[E], q0[E], qn[E];
+    // the row math runs on packed fp32 pairs (FFMA2 / FMUL2: two lanes of
+    // fp32 work per instruction, bit-identical to scalar fmaf / fmul)
+    constexpr int E2 = E / 2;
+    float2 qs[E2], q0[E2], qn[E2];
     float sq = 1.f, isq = 1.f;  // q = sq * qs; isq = 1 / sq
     int qcur = -1, qnext = -1;
 
@@ -118,11 +121,22 @@ __global__ void __launch_bounds__(WPB * 32, 1)
     auto flush_q = [&]() {
       if (qcur >= 0) {
         float dq[E];
+        const float2 sq2 = make_float2(sq, sq);
 #pragma unroll
-        for (int e = 0; e < E; ++e) dq[e] = fmaf(sq, qs[e], -q0[e]);
+        for (int e = 0; e < E2; ++e) {
+          const float2 d = __ffma2_rn(sq2, qs[e], make_float2(-q0[e].x, -q0[e].y));
+          dq[2 * e] = d.x;
+          dq[2 * e + 1] = d.y;
+        }
         L::red(Qb + int64_t(qcur) * K, l, dq);
       }
       qcur = -1;
+    };
+    auto ldq = [&](int32_t v, float2* o) {
+      float t[E];
+      L::ldg(Qb + int64_t(v) * K, l, t);
+#pragma unroll
+      for (int e = 0; e < E2; ++e) o[e] = make_float2(t[2 * e], t[2 * e + 1]);
     };
     // take the next bin (chain-divergent); false when the tile has none left
     auto take = [&]() -> bool {
@@ -167,12 +181,12 @@ __global__ void __launch_bounds__(WPB * 32, 1)
           flush_q();
           if (qnext == v) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) qs[e] = qn[e];
+            for (int e = 0; e < E2; ++e) qs[e] = qn[e];
           } else {
-            L::ldg(Qb + int64_t(v) * K, l, qs);
+            ldq(v, qs);
           }
 #pragma unroll
-          for (int e = 0; e < E; ++e) q0[e] = qs[e];
+          for (int e = 0; e < E2; ++e) q0[e] = qs[e];
           sq = 1.f;
           isq = 1.f;
           qcur = v;
@@ -180,21 +194,20 @@ __global__ void __launch_bounds__(WPB * 32, 1)
         }
         // the run ends after this rating: start loading the next run's row
         if (act && un >= 0 && vn != v && vn != qnext) {
-          L::ldg(Qb + int64_t(vn) * K, l, qn);
+          ldq(vn, qn);
           qnext = vn;
         }
-        float pc[E];
+        float2 pc[E2];
         S* prow = tile + int64_t(act ? u - r0 : 0) * K;
-        L::lds(prow, l, pc);
-        float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
+        L::lds(prow, l, reinterpret_cast<float*>(pc));
+        float2 da = make_float2(0.f, 0.f), db = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int e = 0; e < E; e += 4) {
-          d0 = fmaf(pc[e], qs[e], d0);
-          if (e + 1 < E) d1 = fmaf(pc[e + 1], qs[e + 1], d1);
-          if (e + 2 < E) d2 = fmaf(pc[e + 2], qs[e + 2], d2);
-          if (e + 3 < E) d3 = fmaf(pc[e + 3], qs[e + 3], d3);
+        for (int e = 0; e < E2; e += 2) {
+          da = __ffma2_rn(pc[e], qs[e], da);
+          if (e + 1 < E2) db = __ffma2_rn(pc[e + 1], qs[e + 1], db);
         }
-        float d = (d0 + d1) + (d2 + d3);
+        const float2 ds = __fadd2_rn(da, db);
+        float d = ds.x + ds.y;
 #pragma unroll
         for (int o = LPC / 2; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
         if (act) {
@@ -203,13 +216,29 @@ __global__ void __launch_bounds__(WPB * 32, 1)
           isq *= inv_keep_q;                      // sq' = keep_q sq
           sq *= keep_q;
           const float c = a * isq;                // qs' = qs + (a / sq') p
+          // in place, no temporaries: qs' first, then
+          // p' = keep_p p + (a sq) qs = (keep_p - (a sq) c) p + (a sq) qs'
+          const float2 as2 = make_float2(as, as);
+          const float kq = fmaf(-as, c, keep_p);
+          const float2 kq2 = make_float2(kq, kq), c2 = make_float2(c, c);
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const float pu = pc[e];
-            pc[e] = fmaf(as, qs[e], keep_p * pu);
-            qs[e] = fmaf(c, pu, qs[e]);
+          for (int e = 0; e < E2; ++e) {
+            qs[e] = __ffma2_rn(c2, pc[e], qs[e]);
+            pc[e] = __ffma2_rn(as2, qs[e], __fmul2_rn(kq2, pc[e]));
           }
-          L::sts(prow, l, pc);
+          if constexpr (sizeof(S) == 4 && L::W == 4) {
+            // fp32 rows: st.shared.v4 straight from the updated pairs
+            const uint32_t a0 = smem_addr(prow);
+#pragma unroll
+            for (int v = 0; v < L::NV; ++v)
+              asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                               a0 + uint32_t(L::off(v, l)) * 4u),
+                           "f"(pc[2 * v].x), "f"(pc[2 * v].y), "f"(pc[2 * v + 1].x),
+                           "f"(pc[2 * v + 1].y)
+                           : "memory");
+          } else {
+            L::sts(prow, l, reinterpret_cast<const float*>(pc));
+          }
         }
       }
       // next batch (chain-divergent from here)
@@ -221,8 +250,9 @@ __global__ void __launch_bounds__(WPB * 32, 1)
         load_batch(x + 1, nu, nv, nr);
         cnt = x < nf ? LPC : len - nf * LPC;
         if (sq < 0.25f && qcur >= 0) {  // keep the scaled row in range on long runs
+          const float2 sq2 = make_float2(sq, sq);
 #pragma unroll
-          for (int e = 0; e < E; ++e) qs[e] *= sq;
+          for (int e = 0; e < E2; ++e) qs[e] = __fmul2_rn(qs[e], sq2);
           sq = 1.f;
           isq = 1.f;
         }

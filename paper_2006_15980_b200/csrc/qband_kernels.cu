@@ -57,6 +57,7 @@ __device__ inline int tile_at(int i, int n_tiles, uint64_t seed) {
 
 #include "qchain.cuh"
 #include "ptile.cuh"
+#include "runs.cuh"
 
 namespace hmf {
 namespace qs {
@@ -288,9 +289,9 @@ constexpr int kDefaultQsync = 32;
 // HMF_OK or a negative code with the message set.
 static int64_t resolve_opts(const hmf_qband_opts* in, int64_t k, bool f16, LaunchOpts* o) {
   o->impl = in && in->impl >= 0 ? in->impl : kDefaultImpl;
-  if (in && in->impl < -1) return set_error(HMF_ERR_ARG, "impl must be -1, 0, 4, 5, 6 or 7");
-  if (o->impl != 0 && (o->impl < 4 || o->impl > 7))
-    return set_error(HMF_ERR_ARG, "impl must be -1, 0, 4, 5, 6 or 7");
+  if (in && in->impl < -1) return set_error(HMF_ERR_ARG, "impl must be -1, 0 or 4..8");
+  if (o->impl != 0 && (o->impl < 4 || o->impl > 8))
+    return set_error(HMF_ERR_ARG, "impl must be -1, 0 or 4..8");
   o->cfg = in && in->chain_cfg >= 0 ? in->chain_cfg : auto_chain_cfg(int(k), f16);
   if (!chain_cfg_ok(o->cfg) || (in && in->chain_cfg < -1))
     return set_error(HMF_ERR_ARG, "chain_cfg must be -1, 2, 4, 5 or 6");
@@ -332,8 +333,9 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
   if (n_sub <= 0 || n_tiles <= 0) return 0;
   rc = check_block_args(P, Q, rows, vals, sub_ptr, sub_cuts, n_sub, n_tiles);
   if (rc != HMF_OK) return rc;
-  if (o.impl == 7)
-    return set_error(HMF_ERR_ARG, "implementation 7 runs through hmf_sgd_block_ptile_*");
+  if (o.impl == 7 || o.impl == 8)
+    return set_error(HMF_ERR_ARG, "implementations 7 and 8 run through hmf_sgd_block_ptile_* / "
+                                  "hmf_sgd_block_runs_*");
   // cols == nullptr: every sub-band is one item, sub_cuts[s] (chained kernel only)
   if (!cols && o.impl == 0)
     return set_error(HMF_ERR_ARG, "cols may be null only for implementations 4-6");
@@ -373,7 +375,7 @@ static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_
   if (n_sub <= 0 || n_tiles <= 0) return 0;
   rc = check_block_args(P, Q, rows, vals, sub_ptr, sub_cuts, n_sub, n_tiles);
   if (rc != HMF_OK) return rc;
-  if (o.impl == 0 || o.impl == 7)
+  if (o.impl == 0 || o.impl >= 7)
     return set_error(HMF_ERR_UNSUPPORTED, "uint16 row ids need implementation 4, 5 or 6");
   cudaError_t e;
   switch (k) {
@@ -453,6 +455,72 @@ static int64_t run_ptile(S* P, S* Q, int64_t k, const int32_t* rows, const int32
   return 0;
 }
 
+// implementation 8: run groups over a tile-resident P (runs.cuh)
+template <int K, typename S, typename RowT>
+static cudaError_t launch_runs(S* P, S* Q, const RowT* rows, const float* vals,
+                               const int32_t* runs, const int32_t* tile_run,
+                               const int32_t* tile_cut, int n_tiles,
+                               int max_rows, double lr, double ru, double ri, uint64_t seed,
+                               int64_t row_base, int64_t col_base, cudaStream_t stream,
+                               const LaunchOpts& o) {
+  using C = RunsCfg<K>;
+  auto kern = runs_kernel<K, S, C::LPC, C::WPB, RowT>;
+  const int smem = max_rows * K * int(sizeof(S));
+  int per_sm = 0;
+  cudaError_t e = kernel_occupancy(reinterpret_cast<const void*>(kern), C::WPB * 32, smem, &per_sm);
+  if (e != cudaSuccess) return e;
+  const int cap = grid_share(device_sm_count() * per_sm, o.share);
+  const int grid = n_tiles < cap ? n_tiles : cap;
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, vals,
+                                            reinterpret_cast<const int4*>(runs), tile_run,
+                                            tile_cut, n_tiles, float(lr), float(ru), float(ri),
+                                            uint32_t(seed ^ (seed >> 32)));
+  return cudaGetLastError();
+}
+
+template <typename S, typename RowT>
+static int64_t run_runs(S* P, S* Q, int64_t k, const RowT* rows, const float* vals,
+                        const int32_t* runs, const int32_t* tile_run,
+                        const int32_t* tile_cut, int64_t n_tiles, int32_t max_rows,
+                        const hmf_qband_opts* opts, double lr, double ru, double ri,
+                        uint64_t seed, int64_t row_base, int64_t col_base, cudaStream_t stream) {
+  LaunchOpts o;
+  int64_t rc = resolve_opts(opts, k, sizeof(S) == 2, &o);
+  if (rc != HMF_OK) return rc;
+  if (opts && opts->impl >= 0 && opts->impl != 8)
+    return set_error(HMF_ERR_ARG, "hmf_sgd_block_runs_* runs implementation 8");
+  if (n_tiles <= 0) return 0;
+  if (!P || !Q || !rows || !vals || !runs || !tile_run || !tile_cut)
+    return set_error(HMF_ERR_ARG, "null pointer");
+  if ((reinterpret_cast<uintptr_t>(runs) & 15u) != 0)
+    return set_error(HMF_ERR_ARG, "run descriptors must be 16-byte aligned");
+  if (((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15u) != 0)
+    return set_error(HMF_ERR_ARG, "factor arrays must be 16-byte aligned");
+  if (n_tiles > (int64_t(1) << 30)) return set_error(HMF_ERR_ARG, "n_tiles too large");
+  if (max_rows <= 0 || int64_t(max_rows) * k * int64_t(sizeof(S)) > kPTileBytes)
+    return set_error(HMF_ERR_ARG, "a tile's P rows must fit hmf_ptile_max_rows(k, f16)");
+  if (sizeof(RowT) == 2 && max_rows > 65536)
+    return set_error(HMF_ERR_ARG, "uint16 row ids need tiles of at most 65536 rows");
+  cudaError_t e;
+  switch (k) {
+#define HMF_RN_CASE(KK)                                                                      \
+  case KK:                                                                                   \
+    e = launch_runs<KK, S, RowT>(P, Q, rows, vals, runs, tile_run, tile_cut,                 \
+                                 int(n_tiles), max_rows, lr, ru, ri, seed, row_base,          \
+                                 col_base, stream, o);                                        \
+    break;
+    HMF_RN_CASE(32)
+    HMF_RN_CASE(64)
+    HMF_RN_CASE(128)
+    HMF_RN_CASE(256)
+#undef HMF_RN_CASE
+    default: return set_error(HMF_ERR_UNSUPPORTED, "Q-band kernel needs k in {32,64,128,256}");
+  }
+  if (e != cudaSuccess) return set_cuda_error(e);
+  return 0;
+}
+
 template <typename S>
 static int slots_per_sm(int64_t k, const hmf_qband_opts* opts) {
   LaunchOpts o;
@@ -463,9 +531,9 @@ static int slots_per_sm(int64_t k, const hmf_qband_opts* opts) {
 #define HMF_WPS(KK)                                                                        \
   case KK:                                                                                 \
     e = o.impl == 0 ? warp_slots_per_sm<KK, S>(&n)                                         \
-                    : (o.impl == 7 ? (n = PTileCfg<KK>::WPB * 32 / PTileCfg<KK>::LPC,        \
-                                      cudaSuccess)                                           \
-                                   : chain_slots_per_sm<KK, S>(o.cfg, &n));                  \
+        : o.impl == 7 ? (n = PTileCfg<KK>::WPB * 32 / PTileCfg<KK>::LPC, cudaSuccess)         \
+        : o.impl == 8 ? (n = RunsCfg<KK>::WPB * 32 / RunsCfg<KK>::LPC, cudaSuccess)           \
+                      : chain_slots_per_sm<KK, S>(o.cfg, &n);                                \
     break;
     HMF_WPS(32)
     HMF_WPS(64)
@@ -575,6 +643,66 @@ int64_t hmf_sgd_block_ptile_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                     sub_ptr, n_sub, n_tiles, tile_cut, max_tile_rows, opts, lr,
                                     reg_user, reg_item, seed, row_base, col_base,
                                     static_cast<cudaStream_t>(stream));
+}
+
+int32_t hmf_runs_chains_per_warp(int64_t k) {
+  switch (k) {
+    case 32: return 32 / hmf::qs::RunsCfg<32>::LPC;
+    case 64: return 32 / hmf::qs::RunsCfg<64>::LPC;
+    case 128: return 32 / hmf::qs::RunsCfg<128>::LPC;
+    case 256: return 32 / hmf::qs::RunsCfg<256>::LPC;
+    default: return 0;
+  }
+}
+
+int64_t hmf_sgd_block_runs_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
+                               const float* vals, const int32_t* runs, const int32_t* tile_run,
+                               const int32_t* tile_cut, int64_t n_tiles, int32_t max_tile_rows,
+                               const hmf_qband_opts* opts, double lr, double reg_user,
+                               double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
+                               void* stream) {
+  return hmf::qs::run_runs<float, int32_t>(user_f, item_f, k, rows, vals, runs, tile_run,
+                                           tile_cut, n_tiles, max_tile_rows, opts, lr, reg_user,
+                                           reg_item, seed, row_base, col_base,
+                                           static_cast<cudaStream_t>(stream));
+}
+
+int64_t hmf_sgd_block_runs_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                               const int32_t* rows, const float* vals, const int32_t* runs,
+                               const int32_t* tile_run, const int32_t* tile_cut, int64_t n_tiles,
+                               int32_t max_tile_rows, const hmf_qband_opts* opts, double lr,
+                               double reg_user, double reg_item, uint64_t seed, int64_t row_base,
+                               int64_t col_base, void* stream) {
+  return hmf::qs::run_runs<__half, int32_t>(
+      reinterpret_cast<__half*>(user_f), reinterpret_cast<__half*>(item_f), k, rows, vals, runs,
+      tile_run, tile_cut, n_tiles, max_tile_rows, opts, lr, reg_user, reg_item, seed, row_base,
+      col_base, static_cast<cudaStream_t>(stream));
+}
+
+int64_t hmf_sgd_block_runs_u16_f32(float* user_f, float* item_f, int64_t k, const uint16_t* rows,
+                                   const float* vals, const int32_t* runs,
+                                   const int32_t* tile_run, const int32_t* tile_cut,
+                                   int64_t n_tiles, int32_t max_tile_rows,
+                                   const hmf_qband_opts* opts, double lr, double reg_user,
+                                   double reg_item, uint64_t seed, int64_t row_base,
+                                   int64_t col_base, void* stream) {
+  return hmf::qs::run_runs<float, uint16_t>(user_f, item_f, k, rows, vals, runs, tile_run,
+                                            tile_cut, n_tiles, max_tile_rows, opts, lr, reg_user,
+                                            reg_item, seed, row_base, col_base,
+                                            static_cast<cudaStream_t>(stream));
+}
+
+int64_t hmf_sgd_block_runs_u16_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                                   const uint16_t* rows, const float* vals, const int32_t* runs,
+                                   const int32_t* tile_run, const int32_t* tile_cut,
+                                   int64_t n_tiles, int32_t max_tile_rows,
+                                   const hmf_qband_opts* opts, double lr, double reg_user,
+                                   double reg_item, uint64_t seed, int64_t row_base,
+                                   int64_t col_base, void* stream) {
+  return hmf::qs::run_runs<__half, uint16_t>(
+      reinterpret_cast<__half*>(user_f), reinterpret_cast<__half*>(item_f), k, rows, vals, runs,
+      tile_run, tile_cut, n_tiles, max_tile_rows, opts, lr, reg_user, reg_item, seed, row_base,
+      col_base, static_cast<cudaStream_t>(stream));
 }
 
 int64_t hmf_sgd_block_qband_u16_f32(float* user_f, float* item_f, int64_t k,

@@ -1,0 +1,261 @@
+// Run groups over a tile-resident P (Q-band implementation 8).
+//
+// Implementation 7 (ptile.cuh) keeps a row tile's P rows in shared memory
+// and walks item runs one rating per step, four lane-group chains per warp.
+// Its profile (profiles/round2/s3_ptile_*) shows where the time goes: each
+// chain changes runs on its own, every ~4.75 ratings at Netflix density, so
+// the warp runs the run-change path (Q-delta flush, Q-row hand-over, the next
+// row's prefetch) on more than half of its steps, the next row is prefetched
+// only one step ahead of a ~600-cycle L2 load, and every step re-derives
+// "does my run end here" from shuffled look-ahead triples: 38 instructions
+// per update at 49 % issue.
+//
+// Here the layout hands the kernel whole runs in groups, one run per chain
+// of a warp:
+//   * inside a row tile the runs (the ratings of one item, in the block's
+//     shuffled order) are sorted by length, longest first, and cut into
+//     groups of NC = 32 / LPC consecutive runs, so the runs of a group have
+//     (nearly) the same length and chain 0 holds the longest; the warp takes
+//     groups from a per-tile counter (longest first: the tile's tail is
+//     short);
+//   * a group is one warp-uniform loop of (longest run) steps: no per-step
+//     run-change tests, the item is known per chain (no item ids on the
+//     rating stream), only the user id and the rating are broadcast;
+//   * groups are software-pipelined two deep: while group g trains, group
+//     g+1's Q rows and first batch of ratings load (their run descriptors
+//     arrived during g-1) and group g+2's run descriptors load, so neither
+//     the dependent descriptor -> row loads nor the L2 latency stall a step;
+//   * at a run's end each chain adds its Q change back with vector
+//     reductions (as implementation 7: no Q update is lost, concurrent runs
+//     of one item in other tiles see it at their next load);
+//   * inside a run the visit starts at a seeded rotation (fresh every epoch).
+// P rows live in shared memory exactly as in implementation 7 (chains of a
+// CTA that update one user in the same step race, the reference's racing
+// lanes, workers.py:222-266).  The update arithmetic is the reference's
+// (kernels.py:120-131) in fp32, on packed fp32 pairs (FFMA2).
+#pragma once
+
+#include "hmf_common.cuh"
+#include "lanevec.cuh"
+
+namespace hmf {
+namespace qs {
+
+template <int K> struct RunsCfg {
+  static constexpr int LPC = K >= 256 ? 16 : (K >= 64 ? 8 : 4);
+  static constexpr int WPB = 16;
+};
+
+// rows: int32 user ids (absolute, minus the tile's first row in the kernel)
+// or uint16 ids relative to the tile (the streamed form)
+template <typename RowT> __device__ inline int tile_row(RowT v, int r0) {
+  if constexpr (sizeof(RowT) == 2) {
+    return int(v);
+  } else {
+    return int(v) - r0;
+  }
+}
+
+// Rotation of run r's visit, uniform in [0, len): a 32-bit hash of (seed, r)
+// scaled by len (the high half of the product).  data.run_rotation restates it.
+__device__ __forceinline__ int run_rotation(uint32_t seed32, int r, int len) {
+  uint32_t h = uint32_t(r) * 0x9E3779B1u ^ seed32;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  h *= 0x297A2D39u;
+  h ^= h >> 15;
+  return int(__umulhi(h, uint32_t(len)));
+}
+
+// A run descriptor: {first rating (offset from rows / vals), length, item, 0}.
+template <int K, typename S, int LPC, int WPB, typename RowT>
+__global__ void __launch_bounds__(WPB * 32, 1)
+    runs_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const RowT* __restrict__ rows,
+                const float* __restrict__ vals, const int4* __restrict__ runs,
+                const int32_t* __restrict__ tile_run, const int32_t* __restrict__ tile_cut,
+                int n_tiles, float lr, float ru, float ri, uint32_t seed32) {
+  using L = ChainLay<K, S, LPC>;
+  constexpr int E = L::EPL;
+  constexpr int E2 = E / 2;
+  constexpr int NC = 32 / LPC;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char runs_smem[];
+  S* tile = reinterpret_cast<S*>(runs_smem);
+  __shared__ unsigned next_group;
+  const int lane = threadIdx.x & 31, c = lane / LPC, l = lane % LPC;
+  const float keep_p = 1.f - lr * ru, keep_q = 1.f - lr * ri;
+  const float inv_keep_q = 1.f / keep_q;
+  const float2 neg1 = make_float2(-1.f, -1.f);
+
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const int r0 = tile_cut[t], r1 = tile_cut[t + 1];
+    const int n16 = (r1 - r0) * K * int(sizeof(S)) / 16;
+    {
+      const int4* src = reinterpret_cast<const int4*>(Pb + int64_t(r0) * K);
+      int4* dst = reinterpret_cast<int4*>(tile);
+      for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldcg(src + i);
+    }
+    if (threadIdx.x == 0) next_group = 0;
+    __syncthreads();
+    const int run0 = tile_run[t], run1 = tile_run[t + 1];
+    const unsigned n_groups = unsigned((run1 - run0 + NC - 1) / NC);
+
+    // stage 0: the descriptor of chain c's run in the warp's next group
+    auto take_meta = [&](int4& m) {
+      unsigned w = 0;
+      if (lane == 0) w = atomicAdd(&next_group, 1u);
+      w = __shfl_sync(FULL, w, 0);
+      m = make_int4(0, 0, 0, -1);  // w = -1: no group
+      if (w < n_groups) {
+        m.w = int(w);
+        const int r = run0 + int(w) * NC + c;
+        if (r < run1) {
+          m = __ldg(runs + r);
+          m.w = r;
+        }
+      }
+    };
+    // stage 1: its Q row and first batch (lane l: position l of the rotated run)
+    float2 qn[E2];
+    int32_t nbu = 0;
+    float nbr = 0.f;
+    int nrot = 0;
+    auto stage_rows = [&](const int4& m) {
+      if (m.y > 0) {
+        float tq[E];
+        L::ldg(Qb + int64_t(m.z) * K, l, tq);
+#pragma unroll
+        for (int e = 0; e < E2; ++e) qn[e] = make_float2(tq[2 * e], tq[2 * e + 1]);
+        nrot = run_rotation(seed32, m.w, m.y);
+        if (l < m.y) {
+          int p = nrot + l;
+          if (p >= m.y) p -= m.y;
+          nbu = int32_t(__ldg(rows + m.x + p));
+          nbr = __ldg(vals + m.x + p);
+        }
+      }
+    };
+
+    int4 m1, m2;     // descriptors of the next two groups
+    take_meta(m1);
+    stage_rows(m1);
+    take_meta(m2);
+    // a warp's groups end together: m.w < 0 (or len 0 on every chain) marks none
+    bool more = __shfl_sync(FULL, m1.w, 0) >= 0;
+    while (more) {
+      // group m1 becomes current
+      const int beg = m1.x, len = m1.y, item = m1.z, rot = nrot;
+      const int steps = __shfl_sync(FULL, len, 0);   // chain 0 holds the longest run
+      float2 qs[E2], q0n[E2];                        // q = sq * qs; q0n = -(row as loaded)
+#pragma unroll
+      for (int e = 0; e < E2; ++e) {
+        qs[e] = qn[e];
+        q0n[e] = __fmul2_rn(qn[e], neg1);
+      }
+      int32_t cu = nbu;
+      float cr = nbr;
+      float sq = 1.f, isq = 1.f;
+      // pipeline: group m2's rows start loading, the one after it is taken
+      m1 = m2;
+      more = __shfl_sync(FULL, m1.w, 0) >= 0;
+      stage_rows(m1);
+      take_meta(m2);
+
+      for (int j0 = 0; j0 < steps; j0 += LPC) {
+        // the next batch of this run (lane l: position j0 + LPC + l)
+        int32_t xu = 0;
+        float xr = 0.f;
+        {
+          const int pos = j0 + LPC + l;
+          if (pos < len) {
+            int p = rot + pos;
+            if (p >= len) p -= len;
+            xu = int32_t(__ldg(rows + beg + p));
+            xr = __ldg(vals + beg + p);
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < LPC; ++jj) {
+          if (j0 + jj >= steps) break;  // warp-uniform
+          const bool act = j0 + jj < len;  // chain-uniform
+          const int32_t u = __shfl_sync(FULL, cu, jj, LPC);
+          const float r = __shfl_sync(FULL, cr, jj, LPC);
+          S* prow = tile + int64_t(act ? tile_row<RowT>(RowT(u), r0) : 0) * K;
+          float2 pc[E2];
+          L::lds(prow, l, reinterpret_cast<float*>(pc));
+          float2 da = make_float2(0.f, 0.f), db = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int e = 0; e < E2; e += 2) {
+            da = __ffma2_rn(pc[e], qs[e], da);
+            if (e + 1 < E2) db = __ffma2_rn(pc[e + 1], qs[e + 1], db);
+          }
+          const float2 ds = __fadd2_rn(da, db);
+          float d = ds.x + ds.y;
+#pragma unroll
+          for (int o = LPC / 2; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
+          if (act) {
+            const float a = lr * fmaf(-sq, d, r);  // lr * (r - p.q)
+            const float as = a * sq;
+            isq *= inv_keep_q;
+            sq *= keep_q;
+            const float cq = a * isq;
+            // in place: qs' = qs + (a / sq') p, then
+            // p' = keep_p p + (a sq) qs = (keep_p - (a sq) cq) p + (a sq) qs'
+            const float kq = fmaf(-as, cq, keep_p);
+            const float2 as2 = make_float2(as, as), kq2 = make_float2(kq, kq);
+            const float2 c2 = make_float2(cq, cq);
+#pragma unroll
+            for (int e = 0; e < E2; ++e) {
+              qs[e] = __ffma2_rn(c2, pc[e], qs[e]);
+              pc[e] = __ffma2_rn(as2, qs[e], __fmul2_rn(kq2, pc[e]));
+            }
+            if constexpr (sizeof(S) == 4 && L::W == 4) {
+              const uint32_t a0 = smem_addr(prow);
+#pragma unroll
+              for (int v = 0; v < L::NV; ++v)
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                 a0 + uint32_t(L::off(v, l)) * 4u),
+                             "f"(pc[2 * v].x), "f"(pc[2 * v].y), "f"(pc[2 * v + 1].x),
+                             "f"(pc[2 * v + 1].y)
+                             : "memory");
+            } else {
+              L::sts(prow, l, reinterpret_cast<const float*>(pc));
+            }
+          }
+        }
+        cu = xu;
+        cr = xr;
+        if (sq < 0.25f) {  // keep the scaled row in range on long runs
+          const float2 sq2 = make_float2(sq, sq);
+#pragma unroll
+          for (int e = 0; e < E2; ++e) qs[e] = __fmul2_rn(qs[e], sq2);
+          sq = 1.f;
+          isq = 1.f;
+        }
+      }
+      // the run's Q change back (vector reductions): q - q0 = sq * qs + q0n
+      if (len > 0) {
+        float dq[E];
+        const float2 sq2 = make_float2(sq, sq);
+#pragma unroll
+        for (int e = 0; e < E2; ++e) {
+          const float2 dd = __ffma2_rn(sq2, qs[e], q0n[e]);
+          dq[2 * e] = dd.x;
+          dq[2 * e + 1] = dd.y;
+        }
+        L::red(Qb + int64_t(item) * K, l, dq);
+      }
+    }
+    __syncthreads();
+    {
+      int4* dst = reinterpret_cast<int4*>(Pb + int64_t(r0) * K);
+      const int4* src = reinterpret_cast<const int4*>(tile);
+      for (int i = threadIdx.x; i < n16; i += blockDim.x) __stcg(dst + i, src[i]);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace qs
+}  // namespace hmf

@@ -384,6 +384,7 @@ class DeviceGrid:
     sub_pstore: int = 0                 # chained kernel P write-back: 1 stores, 0 reductions
     sub_tile_cuts: list | None = None   # implementation 7: per block, device int32 tile cuts
     sub_max_rows: int = 0               # implementation 7: rows of the largest tile
+    sub_tile_run: list | None = None    # implementation 8: per block, first run of each tile
 
     n_row_bands = BlockGrid.n_row_bands
     n_col_bands = BlockGrid.n_col_bands
@@ -467,6 +468,52 @@ def qband_impl_for(device, k: int, f16: bool, n_items: int) -> int:
     chained kernel with Q deltas (5), whose layout splits item runs only when
     a block has fewer items than chains (bucket_qbands)."""
     return int(_lib.load().hmf_qband_resolve_impl(int(k), 1 if f16 else 0))
+
+
+# mean ratings per (row tile, item) pair from which a tile-resident-P layout
+# (implementations 7, 8) beats the L2 row-tile kernels (5, 6): one B200,
+# profiles/round2/s3_layout_by_workload.jsonl — Netflix (4.8 at k = 128, 19
+# at k = 32) wins 1.3-1.8x; Hugewiki (0.65) and Yahoo-R1 (0.16) lose 10-35 %
+TILE_RESIDENT_MIN_RUN = 2.0
+
+
+def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> int | None:
+    """Implementation 8 (run groups over a shared-memory P tile) or 7 (the
+    same tile, item bins) when every non-empty block of `grid` suits them,
+    else None (the L2 row-tile kernels):
+    * k in {32, 64, 128, 256};
+    * at least one tile per SM (a CTA trains one tile at a time: ML-1M's
+      6 040 users make 4 tiles at k = 32 — 1.4 vs 16 G upd/s);
+    * item runs long enough: on average >= TILE_RESIDENT_MIN_RUN ratings per
+      (tile, item) — each run costs a Q-row load and a Q-delta reduction;
+    * no hot items (an item's ratings > 4x the block mean): one run per tile
+      would then be long and train concurrently in every tile from the same
+      Q row; the item-split kernel (5) handles that case.
+    fp32 at k = 256 picks 7 (6.8 vs 6.4 G upd/s at Netflix), otherwise 8
+    (Netflix fp32 k = 32 / 64 / 128: 51.8 / 30.7 / 17.3 G upd/s against
+    30.6 / 19.7 / 11.8 for implementation 5; fp16 75 / 34 / 21.5 / 8.7 against
+    42 / 27 / 16.4 / 8.5)."""
+    torch = _torch()
+    if k not in (32, 64, 128, 256) or grid.nnz == 0:
+        return None
+    dev = grid.device
+    n_sm = int(torch.cuda.get_device_properties(dev).multi_processor_count)
+    for b in range(grid.n_blocks):
+        lo, hi = grid.block_range(b)
+        if hi <= lo:
+            continue
+        if hi - lo >= (1 << 31):
+            return None
+        c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
+        r_lo, r_hi = grid.row_span(b // grid.n_col_bands)
+        T = len(ptile_row_cuts(r_lo, r_hi, k, f16, n_sm, max_rows)) - 1
+        W = max(1, c_hi - c_lo)
+        if T < n_sm or (hi - lo) / (T * W) < TILE_RESIDENT_MIN_RUN:
+            return None
+        cnt = torch.bincount(grid.items[lo:hi] - c_lo, minlength=W)
+        if float(cnt.max()) > 4 * (hi - lo) / W:
+            return None
+    return 7 if (k == 256 and not f16) else 8
 
 
 def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int, cap: int | None = None) -> np.ndarray:
@@ -574,12 +621,16 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     auto = impl is None
     chain_cfg = int(chain_cfg)
     split_given = split is not None
+    if impl is None and tile_bytes is None:
+        impl = tile_resident_impl(grid, k, f16, max_tile_rows)
     if impl is None:
         impl = qband_impl_for(dev, k, f16, max((grid.col_span(c)[1] - grid.col_span(c)[0]
                                                 for c in range(grid.n_col_bands)), default=0))
     impl = int(impl)
     if impl == 7:
         return _bucket_ptile(grid, k, f16, max_tile_rows)
+    if impl == 8:
+        return _bucket_runs(grid, k, f16, max_tile_rows)
     widest = max((grid.col_span(c)[1] - grid.col_span(c)[0]
                   for c in range(grid.n_col_bands)), default=0)
     if impl == 5 and split is None:
@@ -738,17 +789,23 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
     return grid
 
 
+PTILE_MIN_ROWS = 64
+
+
 def ptile_row_cuts(r_lo: int, r_hi: int, k: int, f16: bool, n_sm: int,
                    max_rows: int | None = None) -> np.ndarray:
-    """Row tiles of implementation 7 (tile-resident P): the fewest equal
-    tiles whose P rows fit one CTA's shared memory (hmf_ptile_max_rows) —
-    rounded up to a multiple of the SM count, so the persistent CTAs finish
-    their last tiles together."""
+    """Row tiles of implementations 7 and 8 (tile-resident P): the fewest
+    equal tiles whose P rows fit one CTA's shared memory (hmf_ptile_max_rows),
+    at least one per SM when that leaves PTILE_MIN_ROWS rows per tile (a CTA
+    trains one tile at a time) — rounded up to a multiple of the SM count,
+    so the persistent CTAs finish their last tiles together."""
     n = r_hi - r_lo
     cap = int(_lib.load().hmf_ptile_max_rows(int(k), 1 if f16 else 0))
     if max_rows:
         cap = min(cap, int(max_rows))
     t = max(1, -(-n // cap))
+    if t < n_sm and n >= n_sm * PTILE_MIN_ROWS:
+        t = n_sm
     if t > n_sm // 2:
         t = -(-t // n_sm) * n_sm
     t = max(1, min(n, t))
@@ -799,6 +856,107 @@ def _bucket_ptile(grid: DeviceGrid, k: int, f16: bool, max_rows: int | None) -> 
         tile_cuts.append(torch.from_numpy(tiles).to(device=dev, dtype=torch.int32))
     grid.sub_ptr, grid.sub_cuts, grid.sub_tiles = sub_ptrs, sub_cuts, sub_tiles
     grid.sub_impl, grid.sub_cfg, grid.sub_split, grid.sub_qsync, grid.sub_pstore = 7, -1, 1, 0, 0
+    grid.sub_tile_rows = tile_rows
+    grid.sub_tile_cuts = tile_cuts
+    grid.sub_max_rows = max((int(np.max(np.diff(t))) for t in tile_rows if len(t) > 1),
+                            default=1)
+    return grid
+
+
+def _coprime_multiplier(w: int) -> int:
+    """An odd multiplier near 0.618 w that is coprime with w (item
+    scrambling inside a tile is then a bijection)."""
+    import math
+    m = max(1, int(w * 0.6180339887)) | 1
+    while math.gcd(m, w) != 1:
+        m += 2
+    return m
+
+
+def run_rotation(seed: int, r: int, length: int) -> int:
+    """Where implementation 8 starts run r's visit (csrc/runs.cuh
+    run_rotation): a 32-bit hash of (seed, r) scaled to [0, length)."""
+    s32 = (int(seed) ^ (int(seed) >> 32)) & 0xFFFFFFFF
+    h = ((r * 0x9E3779B1) & 0xFFFFFFFF) ^ s32
+    h ^= h >> 15
+    h = (h * 0x2C1B3C6D) & 0xFFFFFFFF
+    h ^= h >> 12
+    h = (h * 0x297A2D39) & 0xFFFFFFFF
+    h ^= h >> 15
+    return (h * length) >> 32
+
+
+def _bucket_runs(grid: DeviceGrid, k: int, f16: bool, max_rows: int | None) -> DeviceGrid:
+    """The layout of implementation 8 (csrc/runs.cuh): per block, the row
+    tiles of implementation 7 (ptile_row_cuts); inside a tile the runs — all
+    ratings of one item, in the block's (shuffled) order, data.py:242-244,
+    264 — sorted by length, longest first, then in a per-tile scrambled item
+    order.  Two stable device sorts per block: by (tile, item) to measure the
+    runs, then by (tile, -length, scrambled item).  Attaches per block:
+    sub_ptr = the run descriptors (int32 [n_runs, 4]: first rating relative
+    to the block's first, length, item, 0), sub_cuts = their items (a view),
+    sub_tile_run (int32, first run of each tile), sub_tile_cuts (int32 row
+    cuts of the tiles)."""
+    torch = _torch()
+    dev = grid.device
+    n_sm = int(torch.cuda.get_device_properties(dev).multi_processor_count)
+    run_descs, tile_runs, tile_rows, tile_cuts, n_tiles = [], [], [], [], []
+    for b in range(grid.n_blocks):
+        lo, hi = grid.block_range(b)
+        c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
+        r_lo, r_hi = grid.row_span(b // grid.n_col_bands)
+        tiles = ptile_row_cuts(r_lo, r_hi, k, f16, n_sm, max_rows)
+        T = len(tiles) - 1
+        W = max(1, c_hi - c_lo)
+        if hi - lo >= (1 << 31):
+            raise ValueError("implementation 8 takes blocks of < 2^31 ratings")
+        if hi > lo:
+            d_tiles = torch.from_numpy(tiles[1:-1]).to(dev, torch.int32)
+            tile_of = torch.bucketize(grid.users[lo:hi], d_tiles, right=True).to(torch.int64)
+            item_rel = (grid.items[lo:hi] - c_lo).to(torch.int64)
+            key = tile_of * W + item_rel
+            v1, i1 = torch.sort(key, stable=True)
+            _, inv, counts = torch.unique_consecutive(v1, return_inverse=True,
+                                                      return_counts=True)
+            run_len = torch.empty_like(key)
+            run_len[i1] = counts[inv]
+            lmax = int(counts.max())
+            del v1, i1, inv, counts
+            # equal-length runs in a per-tile pseudo-random item order (a
+            # bijection of [0, W)), so the CTAs working on different tiles do
+            # not walk the same items at the same time (fewer concurrent Q
+            # deltas on one item)
+            mult = _coprime_multiplier(W)
+            scram = (item_rel * mult + tile_of * 0x9E3779B1) % W
+            key = tile_of * ((lmax + 1) * W) + (lmax - run_len) * W + scram
+            del run_len, item_rel, tile_of, scram
+            v2, order = torch.sort(key, stable=True)
+            grid.users[lo:hi] = grid.users[lo:hi][order]
+            grid.items[lo:hi] = grid.items[lo:hi][order]
+            grid.ratings[lo:hi] = grid.ratings[lo:hi][order]
+            del order
+            uniq, counts = torch.unique_consecutive(v2, return_counts=True)
+            del v2, key
+            runs = torch.zeros((uniq.numel(), 4), dtype=torch.int32, device=dev)
+            runs[1:, 0] = torch.cumsum(counts, 0)[:-1].to(torch.int32)
+            runs[:, 1] = counts.to(torch.int32)
+            runs[:, 2] = grid.items[lo:hi][runs[:, 0].to(torch.int64)]
+            run_tile = uniq // ((lmax + 1) * W)
+            trun = torch.searchsorted(run_tile, torch.arange(T + 1, device=dev))
+            run_descs.append(runs)
+            tile_runs.append(trun.to(torch.int32))
+            del uniq, counts, run_tile
+        else:
+            run_descs.append(torch.zeros((0, 4), dtype=torch.int32, device=dev))
+            tile_runs.append(torch.zeros(T + 1, dtype=torch.int32, device=dev))
+        tile_rows.append(tiles)
+        tile_cuts.append(torch.from_numpy(tiles).to(device=dev, dtype=torch.int32))
+        n_tiles.append(T)
+    # sub_ptr: the run descriptors; sub_cuts: their items (a view)
+    grid.sub_ptr, grid.sub_tiles = run_descs, n_tiles
+    grid.sub_cuts = [r[:, 2] for r in run_descs]
+    grid.sub_tile_run = tile_runs
+    grid.sub_impl, grid.sub_cfg, grid.sub_split, grid.sub_qsync, grid.sub_pstore = 8, -1, 1, 0, 0
     grid.sub_tile_rows = tile_rows
     grid.sub_tile_cuts = tile_cuts
     grid.sub_max_rows = max((int(np.max(np.diff(t))) for t in tile_rows if len(t) > 1),

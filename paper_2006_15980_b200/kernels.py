@@ -155,13 +155,24 @@ def launch_block_qband(user_f, item_f, grid, block, lr, reg_user, reg_item, seed
     lo, hi = grid.block_range(block)
     if hi <= lo:
         return 0
+    s = current_stream_handle(user_f.device) if stream is None else int(stream)
+    o = _as_opts(grid, opts)
+    if int(grid.sub_impl) == 8:
+        # run groups: per-block run descriptors, offsets relative to the block start
+        fn = getattr(_lib.load(), f"hmf_sgd_block_runs_{st}")
+        _lib.check(fn(user_f.data_ptr(), item_f.data_ptr(), user_f.shape[1],
+                      grid.users.data_ptr() + 4 * lo, grid.ratings.data_ptr() + 4 * lo,
+                      grid.sub_ptr[block].data_ptr(),
+                      grid.sub_tile_run[block].data_ptr(), grid.sub_tile_cuts[block].data_ptr(),
+                      grid.sub_tiles[block], int(grid.sub_max_rows), ctypes.byref(o), float(lr),
+                      float(reg_user), float(reg_item), int(seed) & _MASK64, int(row_base),
+                      int(col_base), s), f"hmf_sgd_block_runs_{st}")
+        return hi - lo
     sp, sc = grid.sub_ptr[block], grid.sub_cuts[block]
     n_tiles = grid.sub_tiles[block] if grid.sub_tiles is not None else 1
     n_sub = int(sc.numel()) - 1
     if int(sp.numel()) != n_tiles * n_sub + 1:
         raise ValueError("sub_ptr does not match sub_cuts x sub_tiles")
-    s = current_stream_handle(user_f.device) if stream is None else int(stream)
-    o = _as_opts(grid, opts)
     if int(grid.sub_impl) == 7:
         # tile-resident P: the layout's tile cuts travel with the launch
         fn = getattr(_lib.load(), f"hmf_sgd_block_ptile_{st}")

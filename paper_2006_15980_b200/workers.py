@@ -501,7 +501,8 @@ class StreamingEpoch:
 
     def __init__(self, grid: DeviceGrid, k: int, tile_bytes=None, n_buffers: int = 3,
                  elem_bytes: int = 4, compact: bool = True, tiles_per_chunk: int = 4,
-                 last_chunk_tiles: int = 0, reuse: bool = False, opts=None, impl=None):
+                 last_chunk_tiles: int = 0, reuse: bool = False, opts=None, impl=None,
+                 runs_chunks_per_block: int = 2):
         torch = _torch()
         self.dev = grid.device
         # a grid the caller already laid out for the Q-band kernel is used as is
@@ -516,9 +517,13 @@ class StreamingEpoch:
         # with every launch (ABI 4: nothing process-wide)
         self.opts = kernels.qband_opts(sg, **dict(opts or {}))
         self.reuse = bool(reuse)
+        # implementation 8 (run groups): the item of a rating is its run's,
+        # and its tiles hold at most hmf_ptile_max_rows users, so the stream
+        # is always the compact one (uint16 tile-relative user + rating)
+        self.runs = int(sg.sub_impl) == 8
         # every sub-band a single item (or a part of one): the item is implicit
-        self.implicit_items = compact and sg.sub_impl >= 4 and all(
-            bool(torch.all(c[1:] - c[:-1] <= 1)) for c in sg.sub_cuts)
+        self.implicit_items = self.runs or (compact and sg.sub_impl >= 4 and all(
+            bool(torch.all(c[1:] - c[:-1] <= 1)) for c in sg.sub_cuts))
         self.u16 = self.implicit_items and all(
             int(np.max(np.diff(r))) <= 65536 for r in sg.sub_tile_rows)
         # chunks: G consecutive row tiles of a block -> [lo, hi) of the
@@ -530,7 +535,9 @@ class StreamingEpoch:
         users = sg.users
         if self.u16:
             users = torch.empty(sg.nnz, dtype=torch.int16, device=self.dev)
-        for b in range(sg.n_blocks):
+        if self.runs:
+            self._init_runs(sg, users, runs_chunks_per_block)
+        for b in range(0 if self.runs else sg.n_blocks):
             sp = sg.sub_ptr[b].cpu().numpy()
             T = sg.sub_tiles[b]
             S = (len(sp) - 1) // T
@@ -564,6 +571,53 @@ class StreamingEpoch:
         self.last_h2d = 0
         self.trace = None     # set to a list to record per-chunk CUDA events
         del users
+
+    def _init_runs(self, sg, users, chunks_per_block: int) -> None:
+        """Chunks of implementation 8: each block's row tiles cut into
+        `chunks_per_block` runs of consecutive tiles (a launch needs at least
+        one tile per SM to fill the GPU, so chunks are whole fractions of a
+        block, not a few tiles); a chunk is the ratings of its tiles' runs,
+        contiguous in the layout.  Users go out as uint16 offsets from their
+        tile's first row; the run descriptors (items, lengths) stay resident."""
+        torch = _torch()
+        self.sg = sg
+        for b in range(sg.n_blocks):
+            blo, bhi = sg.block_range(b)
+            T = sg.sub_tiles[b]
+            trun = sg.sub_tile_run[b].cpu().numpy().astype(np.int64)
+            runs = sg.sub_ptr[b].cpu().numpy().astype(np.int64)
+            starts = np.concatenate([runs[:, 0], [bhi - blo]]) if len(runs) else \
+                np.array([bhi - blo], dtype=np.int64)
+            tiles = sg.sub_tile_rows[b]
+            if bhi > blo:
+                d_tiles = torch.from_numpy(tiles).to(self.dev)
+                tile_of = torch.bucketize(sg.users[blo:bhi], d_tiles[1:-1].to(torch.int32),
+                                          right=True)
+                users[blo:bhi] = (sg.users[blo:bhi] - d_tiles[tile_of]).to(torch.int32).to(
+                    torch.int16)
+            per = -(-T // max(1, int(chunks_per_block)))
+            cuts = list(range(0, T, per)) + [T]
+            chunks = []
+            for t0, t1 in zip(cuts, cuts[1:]):
+                off = int(starts[trun[t0]])
+                end = int(starts[trun[t1]])
+                chunks.append((blo + off, blo + end, t1 - t0, off, t0))
+            self.blocks.append((chunks, b))
+
+    def _launch_runs(self, P, Q, hparams, b, chunk, buf, tseed, stream) -> None:
+        sg = self.sg
+        lo, hi, n_tiles, off, t0 = chunk
+        st = "f16" if P.dtype == _torch().float16 else "f32"
+        fn = getattr(_lib.load(), f"hmf_sgd_block_runs_u16_{st}")
+        # run descriptors count from the block's first rating; the staging
+        # buffer starts at the chunk's
+        _lib.check(fn(P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr() - 2 * off,
+                      buf[-1].data_ptr() - 4 * off, sg.sub_ptr[b].data_ptr(),
+                      sg.sub_tile_run[b].data_ptr() + 4 * t0,
+                      sg.sub_tile_cuts[b].data_ptr() + 4 * t0, n_tiles, int(sg.sub_max_rows),
+                      ctypes.byref(self.opts), hparams.learning_rate, hparams.reg_user,
+                      hparams.reg_item, tseed, 0, 0, stream.cuda_stream),
+                   "hmf_sgd_block_runs_u16")
 
     @property
     def bytes_per_rating(self) -> int:
@@ -639,8 +693,21 @@ class StreamingEpoch:
                 uploaded += hi - lo
             self.lru_order.remove(slot)
             self.lru_order.append(slot)
-            items = 0 if self.implicit_items else buf[1].data_ptr()
             tseed = kernels.mix64(bseed, t) & 0xFFFFFFFFFFFFFFFF
+            if self.runs:
+                if tr is not None:
+                    tr["k0"] = torch.cuda.Event(enable_timing=True)
+                    tr["k0"].record(comp)
+                self._launch_runs(P, Q, hparams, sc, chunks[t], buf, tseed, comp)
+                ev = torch.cuda.Event(enable_timing=tr is not None)
+                ev.record(comp)
+                self.freed[slot] = ev
+                if tr is not None:
+                    tr["k1"] = ev
+                    self.trace.append(tr)
+                done += hi - lo
+                continue
+            items = 0 if self.implicit_items else buf[1].data_ptr()
             args = (P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr(), items,
                     buf[-1].data_ptr(), rel.data_ptr(), sc.data_ptr(), int(sc.numel()) - 1,
                     n_tiles)

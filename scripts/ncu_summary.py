@@ -26,6 +26,9 @@ METRICS = {
     "smsp__inst_executed.sum": "instructions",
     "launch__grid_size": "grid",
     "launch__block_size": "block",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_pct",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "smem_wavefronts",
+    "smsp__warps_eligible.avg.per_cycle_active": "eligible_warps",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9,
          "us": 1e-6, "ms": 1e-3, "s": 1.0,

@@ -295,3 +295,75 @@ def test_concurrent_layouts_equal_serial(dev):
         t.join()
     for a, b in zip(serial, conc):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("k,chunks", [(128, 2), (32, 3), (256, 1)])
+def test_streaming_epoch_runs_equals_resident_launches(dev, k, chunks):
+    """StreamingEpoch over an implementation-8 layout (run groups): 6 bytes
+    per rating from pinned host memory (uint16 tile-relative users + the
+    rating; items from the resident run descriptors), whole fractions of a
+    block per launch.  On triples whose runs never race or go stale it
+    equals the resident launches of the same layout under the same seeds —
+    and the first upload replaced poisoned device copies."""
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import (DeviceTriples, RatingMatrix, bucket_qbands,
+                                            build_device_grid, ptile_row_cuts)
+    from paper_2006_15980_b200.sgd import Hyperparams
+    from paper_2006_15980_b200.workers import StreamingEpoch
+    d = torch.device("cuda", dev)
+    rng = np.random.default_rng(k)
+    n_users, n_items = 90_000, 9_000
+    n_sm = torch.cuda.get_device_properties(d).multi_processor_count
+    tiles = ptile_row_cuts(0, n_users, k, False, n_sm)
+    T = len(tiles) - 1
+    free = [list(rng.permutation(np.arange(tiles[t], tiles[t + 1]))) for t in range(T)]
+    users, items = [], []
+    for v in range(n_items):
+        t = v % T
+        for _ in range(min(len(free[t]), int(rng.integers(1, 9)))):
+            users.append(free[t].pop())
+            items.append(v)
+    users, items = np.asarray(users, np.int32), np.asarray(items, np.int32)
+    vals = rng.uniform(0, 1, len(users)).astype(np.float32).astype(np.float64)
+    m = RatingMatrix(n_users, n_items, users, items, vals)
+    g = build_device_grid(DeviceTriples.from_host(m, d), [0, n_users], [0, 4_000, n_items])
+    bucket_qbands(g, k, impl=8)
+    se = StreamingEpoch(g, k, runs_chunks_per_block=chunks)
+    assert se.runs and se.u16 and se.implicit_items and se.h2d_bytes == 6 * len(users)
+    assert se.n_chunks == sum(len(range(0, t, -(-t // chunks))) for t in g.sub_tiles)
+    P0 = rng.uniform(0, 0.1, size=(n_users, k)).astype(np.float32)
+    Q0 = rng.uniform(0, 0.1, size=(n_items, k)).astype(np.float32)
+    hp = Hyperparams(n_factors=k, reg_user=0.02, reg_item=0.03, learning_rate=0.05)
+    P, Q = torch.from_numpy(P0).to(d), torch.from_numpy(Q0).to(d)
+    # the streamed epoch reads only what it uploads: poison the device arrays
+    saved = (g.users.clone(), g.ratings.clone())
+    g.users.fill_(-1)
+    g.ratings.fill_(float("nan"))
+    assert se.run(P, Q, hp, seed=7) == len(users)
+    torch.cuda.synchronize()
+    g.users.copy_(saved[0])
+    g.ratings.copy_(saved[1])
+    # the oracle replay: block b's chunk c runs under mix64(mix64(seed, b), c);
+    # with no races the order of runs does not matter, each run from its
+    # seeded rotation (data.run_rotation), one rating at a time
+    import oracle
+    from paper_2006_15980_b200.data import run_rotation
+    gu, gi = g.users.cpu().numpy(), g.items.cpu().numpy()
+    gr = g.ratings.cpu().numpy().astype(np.float64)
+    Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
+    for b, (chs, _) in enumerate(se.blocks):
+        blo, _ = g.block_range(b)
+        bseed = kernels.mix64(7, b) & 0xFFFFFFFFFFFFFFFF
+        runs = g.sub_ptr[b].cpu().numpy().astype(np.int64)
+        trun = g.sub_tile_run[b].cpu().numpy()
+        for c, (lo, hi, nt, off, t0) in enumerate(chs):
+            tseed = kernels.mix64(bseed, c) & 0xFFFFFFFFFFFFFFFF
+            for r in range(trun[t0], trun[t0 + nt]):
+                first, ln = int(runs[r, 0]), int(runs[r, 1])
+                rot = run_rotation(tseed, r, ln)
+                for p in range(ln):
+                    i = blo + first + (rot + p) % ln
+                    oracle.sgd_range(Pe, Qe, gu, gi, gr, i, i + 1, 0.05, 0.02, 0.03, 0, 0, 0)
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)  # noqa: E731
+    assert rel(P.double().cpu().numpy(), Pe) < 1e-5
+    assert rel(Q.double().cpu().numpy(), Qe) < 1e-5

@@ -1061,3 +1061,126 @@ def test_ptile_item_runs_equal_sequential_replay(dev, k, dtype):
     tol = 2e-3 if f16 else 1e-5
     assert rel_err(P.double().cpu().numpy(), Pe) < tol
     assert rel_err(Q.double().cpu().numpy(), Qe) < tol
+
+
+def _runs_problem(dev, k, f16, seed, n_users=120_000, n_items=12_000, max_run=13):
+    """Distinct users, every item inside one row tile (implementation 7/8
+    tiles): runs never race and never go stale."""
+    from paper_2006_15980_b200.data import ptile_row_cuts
+    rng = np.random.default_rng(seed)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    tiles = ptile_row_cuts(0, n_users, k, f16, n_sm)
+    T = len(tiles) - 1
+    free = [list(rng.permutation(np.arange(tiles[t], tiles[t + 1]))) for t in range(T)]
+    users, items = [], []
+    for v in range(n_items):
+        t = v % T
+        r = min(len(free[t]), int(rng.integers(1, max_run)))
+        for _ in range(r):
+            users.append(free[t].pop())
+            items.append(v)
+    users = np.asarray(users, dtype=np.int32)
+    items = np.asarray(items, dtype=np.int32)
+    perm = rng.permutation(len(users))
+    return users[perm], items[perm], tiles, rng
+
+
+def test_runs_layout_contract(dev):
+    """Implementation 8's layout: inside each row tile, runs (one item each,
+    the block's order kept) sorted by length, longest first; run / tile
+    arrays consistent; every rating present once."""
+    from paper_2006_15980_b200.data import (DeviceTriples, RatingMatrix, bucket_qbands,
+                                            build_device_grid)
+    m = random_matrix(30_000, 2_000, 600_000, 91)
+    g = build_device_grid(DeviceTriples.from_host(m, dev), [0, 30_000], [0, 900, 2_000])
+    orig = {}
+    for b in range(g.n_blocks):
+        lo, hi = g.block_range(b)
+        orig[b] = (g.users[lo:hi].cpu().numpy(), g.items[lo:hi].cpu().numpy(),
+                   g.ratings[lo:hi].cpu().numpy())
+    bucket_qbands(g, 128, impl=8)
+    assert g.sub_impl == 8
+    for b in range(g.n_blocks):
+        lo, hi = g.block_range(b)
+        u, i, r = (g.users[lo:hi].cpu().numpy(), g.items[lo:hi].cpu().numpy(),
+                   g.ratings[lo:hi].cpu().numpy())
+        runs = g.sub_ptr[b].cpu().numpy().astype(np.int64)
+        ptr = np.concatenate([runs[:, 0], [runs[-1, 0] + runs[-1, 1]]])
+        assert np.array_equal(ptr[1:-1], runs[1:, 0])        # runs tile the block
+        item = runs[:, 2]
+        trun = g.sub_tile_run[b].cpu().numpy()
+        tiles = g.sub_tile_rows[b]
+        T = g.sub_tiles[b]
+        assert len(tiles) == T + 1 and len(trun) == T + 1
+        assert ptr[0] == 0 and ptr[-1] == hi - lo and trun[0] == 0 and trun[-1] == len(item)
+        lens = np.diff(ptr)
+        assert np.all(lens > 0)
+        for t in range(T):
+            a, z = trun[t], trun[t + 1]
+            assert np.all(np.diff(lens[a:z]) <= 0)            # longest first
+            seg = slice(ptr[a], ptr[z])
+            assert np.all((u[seg] >= tiles[t]) & (u[seg] < tiles[t + 1]))
+        # each run is one item; the (tile, item) pairs are distinct
+        run_of = np.repeat(np.arange(len(item)), lens)
+        assert np.array_equal(i, item[run_of])
+        # same multiset of triples; inside a run the block order is kept
+        key_new = (u.astype(np.int64) << 20) | i
+        ou, oi, orr = orig[b]
+        key_old = (ou.astype(np.int64) << 20) | oi
+        assert np.array_equal(np.sort(key_new), np.sort(key_old))
+        pos_old = {kk: n for n, kk in enumerate(key_old)}
+        pos = np.array([pos_old[kk] for kk in key_new])
+        for rr in range(0, len(item), 97):
+            assert np.all(np.diff(pos[ptr[rr]:ptr[rr + 1]]) > 0)
+        assert np.array_equal(r, orr[pos])
+
+
+@pytest.mark.parametrize("k,dtype", [(128, torch.float32), (32, torch.float32),
+                                     (256, torch.float32), (64, torch.float16)])
+def test_runs_equal_sequential_replay(dev, k, dtype):
+    """Implementation 8 (run groups): with no P race and no concurrent Q
+    deltas (distinct users, items inside one tile) the kernel is exactly a
+    sequential replay, run by run, of its visit order — each run from its
+    seeded rotation (runs.cuh stage_group) — of the reference update (oracle,
+    f64), one rating at a time."""
+    import oracle
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import (DeviceTriples, RatingMatrix, bucket_qbands,
+                                            build_device_grid)
+    from paper_2006_15980_b200.kernels import _MASK64
+    f16 = dtype == torch.float16
+    n_users, n_items = 120_000, 12_000
+    users, items, tiles, rng = _runs_problem(dev, k, f16, 200 + k, n_users, n_items)
+    n = len(users)
+    vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
+    m = RatingMatrix(n_users, n_items, users, items, vals)
+    g = build_device_grid(DeviceTriples.from_host(m, dev), [0, n_users],
+                          [0, n_items // 2, n_items])
+    bucket_qbands(g, k, impl=8, elem_bytes=2 if f16 else 4)
+    assert g.sub_impl == 8 and all(np.array_equal(r, tiles) for r in g.sub_tile_rows)
+    P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
+    Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
+    if f16:
+        P0, Q0 = P0.astype(np.float16).astype(np.float32), Q0.astype(np.float16).astype(np.float32)
+    P, Q = to_dev(P0, dev, dtype), to_dev(Q0, dev, dtype)
+    lr, ru, ri = 0.05, 0.02, 0.03
+    seeds = [kernels.mix64(5, b) for b in range(g.n_blocks)]
+    got = sum(kernels.launch_block_qband(P, Q, g, b, lr, ru, ri, seeds[b])
+              for b in range(g.n_blocks))
+    assert got == n
+    gu, gi = g.users.cpu().numpy(), g.items.cpu().numpy()
+    gr = g.ratings.cpu().numpy().astype(np.float64)
+    Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
+    from paper_2006_15980_b200.data import run_rotation
+    for b in range(g.n_blocks):
+        lo, _ = g.block_range(b)
+        runs = g.sub_ptr[b].cpu().numpy().astype(np.int64)
+        for r in range(len(runs)):
+            first, ln, _, _ = runs[r]
+            rot = run_rotation(seeds[b], r, int(ln))
+            for p in range(ln):
+                i = lo + int(first) + (rot + p) % int(ln)
+                oracle.sgd_range(Pe, Qe, gu, gi, gr, i, i + 1, lr, ru, ri, 0, 0, 0)
+    tol = 2e-3 if f16 else 1e-5
+    assert rel_err(P.double().cpu().numpy(), Pe) < tol
+    assert rel_err(Q.double().cpu().numpy(), Qe) < tol

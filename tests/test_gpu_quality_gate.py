@@ -2,11 +2,10 @@
 test RMSE within 0.005 of the CPU reference after the same epochs).
 
 A Netflix-shaped problem scaled to the suite's budget — the full 17 700
-items, 120 000 users, ~10 M ratings — lays out exactly as the bench's
-480 000 x 17 700 / 100 M run does: 60 000-user row tiles, implementation 5
-with every item run split 4 ways, the dynamic unit scheduler (more
-sub-bands than chains) and, in fp32 at k >= 128, P written back by plain
-stores (the reference's racing-lane semantics).  Both sides train on the
+items, 120 000 users, 25 M ratings (Netflix's density) — lays out as the
+bench's 480 000 x 17 700 / 100 M run does (data.tile_resident_impl): P row
+tiles in shared memory, at least one per SM, item runs of ~4.9 ratings,
+implementation 8 (run groups), or 7 for fp32 at k = 256.  Both sides train on the
 identical triples from the identical initial factors; the reference is the
 unmodified hetmf.run_training(stream-only) on the host cores (oracle/_ref).
 Every epoch must be within 0.005, and stores may not push the fp32 epoch-1
@@ -22,7 +21,9 @@ import qgate
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-N_USERS, N_ITEMS, NNZ, EPOCHS = 120_000, 17_700, 10_500_000, 5
+# Netflix's density (1.18 %): a row tile then holds ~4.9 ratings per item, as
+# at 480 000 x 17 700 / 100 M, so the automatic layout makes the bench's choice
+N_USERS, N_ITEMS, NNZ, EPOCHS = 120_000, 17_700, 25_000_000, 5
 
 
 @pytest.fixture(scope="module")
@@ -64,29 +65,29 @@ def test_headline_path_rmse_within_0005_of_reference(hetmf, data, k, precision):
     print(f"k={k} {precision}: layout impl {grid.sub_impl} split {grid.sub_split} pstore "
           f"{grid.sub_pstore} tiles {grid.sub_tiles}; ours {np.round(ours, 5).tolist()} "
           f"reference {np.round(ref, 5).tolist()}")
-    if k == 128:
-        # the bench's layout decisions
-        from paper_2006_15980_b200.data import resident_warps
-        assert grid.sub_impl == 5 and grid.sub_split >= 4     # runs split (4, hot items more)
-        assert grid.sub_tiles == [2, 2]
-        chains = resident_warps(torch.device("cuda", 0), k, precision == "f16", 5)
-        assert all(int(c.numel()) - 1 > chains for c in grid.sub_cuts)   # dynamic units
-        assert grid.sub_pstore == (1 if precision == "f32" else 0)
+    # the bench's layout decision (data.tile_resident_impl): run groups over
+    # a shared-memory P tile, item bins for fp32 at k = 256
+    assert grid.sub_impl == (7 if (k == 256 and precision == "f32") else 8)
+    assert all(t >= 148 for t in grid.sub_tiles)
     gaps = np.abs(np.asarray(ours) - np.asarray(ref))
     assert np.all(gaps <= 0.005), (ours, ref)
     if precision == "f32":
         assert gaps[0] <= 0.003, (ours[0], ref[0])
 
 
+@pytest.mark.parametrize("impl", [5, 7, 8])
 @pytest.mark.parametrize("precision", ["f32", "f16"])
 @pytest.mark.parametrize("k", [128, 32, 64, 256])
-def test_tile_resident_p_rmse_within_0005_of_reference(hetmf, data, k, precision):
-    """Implementation 7 (tile-resident P, csrc/ptile.cuh) on the same gate."""
+def test_each_engine_kernel_rmse_within_0005_of_reference(hetmf, data, k, precision, impl):
+    """Every engine kernel on the same gate: 5 (L2 row tiles, split item runs
+    with Q deltas, csrc/qchain.cuh; P by stores in fp32 at k >= 128), 7
+    (tile-resident P, item bins, csrc/ptile.cuh) and 8 (run groups over it,
+    csrc/runs.cuh)."""
     train, test, _, _ = data
     ref, init = _reference(hetmf, data, k)
-    ours, grid = qgate.ours_rmse(_fresh(train), test, init, k, precision, EPOCHS, impl=7)
-    print(f"impl 7 k={k} {precision}: tiles {grid.sub_tiles} rows <= {grid.sub_max_rows}; "
+    ours, grid = qgate.ours_rmse(_fresh(train), test, init, k, precision, EPOCHS, impl=impl)
+    print(f"impl {impl} k={k} {precision}: tiles {grid.sub_tiles} rows <= {grid.sub_max_rows}; "
           f"ours {np.round(ours, 5).tolist()} reference {np.round(ref, 5).tolist()}")
-    assert grid.sub_impl == 7
+    assert grid.sub_impl == impl
     gaps = np.abs(np.asarray(ours) - np.asarray(ref))
     assert np.all(gaps <= 0.005), (ours, ref)
