@@ -255,7 +255,7 @@ int64_t hmf_sgd_block_ptile_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
  * hmf_ptile_max_rows(k, f16)); inside a tile the ratings are grouped into
  * runs (all ratings of one item, in the block's order), runs sorted by
  * length, longest first.  runs: int32[n_runs][4] descriptors, 16-byte
- * aligned; run r = {first, len, item, 0} holds ratings [first, first + len)
+ * aligned; run r = {first, len, item, r} holds ratings [first, first + len)
  * of rows / vals (offsets relative to those pointers), all of item `item`
  * (absolute, minus col_base); tile t's runs are [tile_run[t],
  * tile_run[t+1]).  Device arrays; data.bucket_qbands with impl 8 builds them.  A persistent CTA per SM holds one tile's P rows in

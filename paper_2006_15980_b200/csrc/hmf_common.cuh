@@ -192,6 +192,21 @@ __device__ inline void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Copy `bytes` (multiple of 16, both addresses 16-byte aligned) from shared
+// to global memory as one bulk-group operation (commit + wait below).
+__device__ inline void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_addr(src)), "r"(bytes)
+               : "memory");
+}
+__device__ inline void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the committed bulk stores have read their shared-memory source
+__device__ inline void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// the committed bulk stores are complete (globally visible)
+__device__ inline void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // Copy `bytes` (multiple of 16, both addresses 16-byte aligned) from global to
 // shared memory, completing on `bar` via complete_tx.
 __device__ inline void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

@@ -68,7 +68,8 @@ __device__ __forceinline__ int run_rotation(uint32_t seed32, int r, int len) {
   return int(__umulhi(h, uint32_t(len)));
 }
 
-// A run descriptor: {first rating (offset from rows / vals), length, item, 0}.
+// A run descriptor: {first rating (offset from rows / vals), length, item,
+// run index} — a 16-byte record, one load per chain per group.
 template <int K, typename S, int LPC, int WPB, typename RowT>
 __global__ void __launch_bounds__(WPB * 32, 1)
     runs_kernel(S* __restrict__ Pb, S* __restrict__ Qb, const RowT* __restrict__ rows,
@@ -87,33 +88,50 @@ __global__ void __launch_bounds__(WPB * 32, 1)
   const float keep_p = 1.f - lr * ru, keep_q = 1.f - lr * ri;
   const float inv_keep_q = 1.f / keep_q;
   const float2 neg1 = make_float2(-1.f, -1.f);
+  // the P tile moves between HBM/L2 and shared memory as one TMA bulk copy
+  // each way (cp.async.bulk): one thread issues it, the load completes on an
+  // mbarrier, the store drains while the next tile's load waits for it to
+  // have read shared memory
+  __shared__ __align__(8) uint64_t tile_bar;
+  uint32_t tile_phase = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&tile_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
 
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const int r0 = tile_cut[t], r1 = tile_cut[t + 1];
-    const int n16 = (r1 - r0) * K * int(sizeof(S)) / 16;
-    {
-      const int4* src = reinterpret_cast<const int4*>(Pb + int64_t(r0) * K);
-      int4* dst = reinterpret_cast<int4*>(tile);
-      for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldcg(src + i);
+    const uint32_t tile_bytes = uint32_t(r1 - r0) * uint32_t(K * sizeof(S));
+    if (threadIdx.x == 0) {
+      next_group = 0;
+      if (tile_bytes) {
+        bulk_wait_read_all();  // the previous tile's write-back has read the buffer
+        mbar_arrive_expect_tx(&tile_bar, tile_bytes);
+        bulk_g2s(tile, Pb + int64_t(r0) * K, tile_bytes, &tile_bar);
+      }
     }
-    if (threadIdx.x == 0) next_group = 0;
+    if (tile_bytes) {
+      mbar_wait(&tile_bar, tile_phase);
+      tile_phase ^= 1u;
+    }
     __syncthreads();
     const int run0 = tile_run[t], run1 = tile_run[t + 1];
     const unsigned n_groups = unsigned((run1 - run0 + NC - 1) / NC);
 
-    // stage 0: the descriptor of chain c's run in the warp's next group
+    // stage 0: the descriptor of chain c's run in the warp's next group.  All
+    // four words are used (m.w = the run's own index, for its rotation): an
+    // unused word would be a dead register the compiler reuses while the
+    // 16-byte load is still in flight, stalling on it (write-after-write).
+    // m.w < 0: no run; chain 0's m.w < 0 marks the end of the tile for the warp
     auto take_meta = [&](int4& m) {
       unsigned w = 0;
       if (lane == 0) w = atomicAdd(&next_group, 1u);
       w = __shfl_sync(FULL, w, 0);
-      m = make_int4(0, 0, 0, -1);  // w = -1: no group
+      m = make_int4(0, 0, 0, -1);
       if (w < n_groups) {
-        m.w = int(w);
         const int r = run0 + int(w) * NC + c;
-        if (r < run1) {
-          m = __ldg(runs + r);
-          m.w = r;
-        }
+        if (r < run1) m = __ldg(runs + r);
       }
     };
     // stage 1: its Q row and first batch (lane l: position l of the rotated run)
@@ -141,7 +159,6 @@ __global__ void __launch_bounds__(WPB * 32, 1)
     take_meta(m1);
     stage_rows(m1);
     take_meta(m2);
-    // a warp's groups end together: m.w < 0 (or len 0 on every chain) marks none
     bool more = __shfl_sync(FULL, m1.w, 0) >= 0;
     while (more) {
       // group m1 becomes current
@@ -156,6 +173,22 @@ __global__ void __launch_bounds__(WPB * 32, 1)
       int32_t cu = nbu;
       float cr = nbr;
       float sq = 1.f, isq = 1.f;
+      // the next batch of this run (lane l: position j0 + LPC + l); the
+      // group's second batch is requested before the next groups' loads
+      int32_t xu = 0;
+      float xr = 0.f;
+      auto load_batch = [&](int j0) {
+        xu = 0;
+        xr = 0.f;
+        const int pos = j0 + LPC + l;
+        if (pos < len) {
+          int p = rot + pos;
+          if (p >= len) p -= len;
+          xu = int32_t(__ldg(rows + beg + p));
+          xr = __ldg(vals + beg + p);
+        }
+      };
+      load_batch(0);
       // pipeline: group m2's rows start loading, the one after it is taken
       m1 = m2;
       more = __shfl_sync(FULL, m1.w, 0) >= 0;
@@ -163,18 +196,7 @@ __global__ void __launch_bounds__(WPB * 32, 1)
       take_meta(m2);
 
       for (int j0 = 0; j0 < steps; j0 += LPC) {
-        // the next batch of this run (lane l: position j0 + LPC + l)
-        int32_t xu = 0;
-        float xr = 0.f;
-        {
-          const int pos = j0 + LPC + l;
-          if (pos < len) {
-            int p = rot + pos;
-            if (p >= len) p -= len;
-            xu = int32_t(__ldg(rows + beg + p));
-            xr = __ldg(vals + beg + p);
-          }
-        }
+        if (j0 > 0) load_batch(j0);
 #pragma unroll
         for (int jj = 0; jj < LPC; ++jj) {
           if (j0 + jj >= steps) break;  // warp-uniform
@@ -247,14 +269,16 @@ __global__ void __launch_bounds__(WPB * 32, 1)
         L::red(Qb + int64_t(item) * K, l, dq);
       }
     }
+    // the chains' shared-memory writes, then the bulk write-back (async
+    // proxy) of the tile: every writer fences its generic-proxy stores first
+    fence_proxy_async();
     __syncthreads();
-    {
-      int4* dst = reinterpret_cast<int4*>(Pb + int64_t(r0) * K);
-      const int4* src = reinterpret_cast<const int4*>(tile);
-      for (int i = threadIdx.x; i < n16; i += blockDim.x) __stcg(dst + i, src[i]);
+    if (threadIdx.x == 0 && tile_bytes) {
+      bulk_s2g(Pb + int64_t(r0) * K, tile, tile_bytes);
+      bulk_commit();
     }
-    __syncthreads();
   }
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 }  // namespace qs

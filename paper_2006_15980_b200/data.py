@@ -489,10 +489,11 @@ def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> 
     * no hot items (an item's ratings > 4x the block mean): one run per tile
       would then be long and train concurrently in every tile from the same
       Q row; the item-split kernel (5) handles that case.
-    fp32 at k = 256 picks 7 (6.8 vs 6.4 G upd/s at Netflix), otherwise 8
-    (Netflix fp32 k = 32 / 64 / 128: 51.8 / 30.7 / 17.3 G upd/s against
-    30.6 / 19.7 / 11.8 for implementation 5; fp16 75 / 34 / 21.5 / 8.7 against
-    42 / 27 / 16.4 / 8.5)."""
+    Returns 8 (Netflix fp32 k = 32 / 64 / 128 / 256: 51.8 / 30.7 / 17.3 / 6.4
+    G upd/s against 30.6 / 19.7 / 11.8 / 5.9 for implementation 5; fp16 75 /
+    34 / 21.5 / 8.7 against 42 / 27 / 16.4 / 8.5; implementation 7 measured
+    34.3 / 21.2 / 14.8 / 6.8 fp32 — ahead only at k = 256, and without a
+    streamed form, so 8 serves every k)."""
     torch = _torch()
     if k not in (32, 64, 128, 256) or grid.nnz == 0:
         return None
@@ -513,7 +514,7 @@ def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> 
         cnt = torch.bincount(grid.items[lo:hi] - c_lo, minlength=W)
         if float(cnt.max()) > 4 * (hi - lo) / W:
             return None
-    return 7 if (k == 256 and not f16) else 8
+    return 8
 
 
 def qband_sub_cuts(c_lo: int, c_hi: int, k: int, target: int, cap: int | None = None) -> np.ndarray:
@@ -894,7 +895,7 @@ def _bucket_runs(grid: DeviceGrid, k: int, f16: bool, max_rows: int | None) -> D
     order.  Two stable device sorts per block: by (tile, item) to measure the
     runs, then by (tile, -length, scrambled item).  Attaches per block:
     sub_ptr = the run descriptors (int32 [n_runs, 4]: first rating relative
-    to the block's first, length, item, 0), sub_cuts = their items (a view),
+    to the block's first, length, item, run index), sub_cuts = their items (a view),
     sub_tile_run (int32, first run of each tile), sub_tile_cuts (int32 row
     cuts of the tiles)."""
     torch = _torch()
@@ -941,6 +942,7 @@ def _bucket_runs(grid: DeviceGrid, k: int, f16: bool, max_rows: int | None) -> D
             runs[1:, 0] = torch.cumsum(counts, 0)[:-1].to(torch.int32)
             runs[:, 1] = counts.to(torch.int32)
             runs[:, 2] = grid.items[lo:hi][runs[:, 0].to(torch.int64)]
+            runs[:, 3] = torch.arange(uniq.numel(), dtype=torch.int32, device=dev)
             run_tile = uniq // ((lmax + 1) * W)
             trun = torch.searchsorted(run_tile, torch.arange(T + 1, device=dev))
             run_descs.append(runs)

@@ -340,7 +340,7 @@ class CudaRowBand:
     def __init__(self, dist, rank: int, world: int, device, triples, row_lo: int, row_hi: int,
                  col_cuts, k: int, lr: float, reg_user: float, reg_item: float,
                  init_seed: int = 0, kernel: str = "auto", init=None, concurrency: int = 1,
-                 split: int | None = None):
+                 split: int | None = None, impl: int | None = None):
         import torch
         from . import _lib
         from .data import DeviceTriples, bucket_qbands, build_device_grid, resident_warps
@@ -392,7 +392,9 @@ class CudaRowBand:
                 widest = int(np.max(np.diff(self.col_cuts)))
                 bucket_qbands(self.grid, k, impl=5, split=max(1, min(16, slots // widest)))
             else:
-                bucket_qbands(self.grid, k)
+                # the automatic layout (data.tile_resident_impl: a Netflix-
+                # density band picks run groups over a shared-memory P tile)
+                bucket_qbands(self.grid, k, impl=impl)
         # column blocks in flight at once, each on its own stream with a
         # 1/concurrency share of the GPU.  Default 1: with item runs split
         # over chains (implementation 5) one narrow block fills the GPU, and
@@ -467,12 +469,30 @@ class CudaRowBand:
         torch = self.torch
         if on and self.host is None:
             g = self.grid
-            compact = (self.kernel == "qband" and (g.sub_impl or 0) >= 4
-                       and all(bool(torch.all(sc[1:] - sc[:-1] <= 1)) for sc in g.sub_cuts)
-                       and all(len(r) < 2 or int(np.max(np.diff(r))) <= 65536
-                               for r in g.sub_tile_rows))
+            runs = self.kernel == "qband" and g.sub_impl == 8
+            compact = runs or (self.kernel == "qband" and (g.sub_impl or 0) in (4, 5, 6)
+                               and all(bool(torch.all(sc[1:] - sc[:-1] <= 1))
+                                       for sc in g.sub_cuts)
+                               and all(len(r) < 2 or int(np.max(np.diff(r))) <= 65536
+                                       for r in g.sub_tile_rows))
             self.compact = {} if compact else None
-            if compact:
+            if runs:
+                # implementation 8: users relative to their (shared-memory) row
+                # tile, items in the resident run descriptors
+                rel = torch.empty(g.nnz, dtype=torch.int16, device=self.dev)
+                for c in range(self.n_cols):
+                    b = self.block_of[c]
+                    lo, hi = g.block_range(b)
+                    if hi > lo:
+                        d_tiles = torch.from_numpy(g.sub_tile_rows[b]).to(self.dev)
+                        tile_of = torch.bucketize(g.users[lo:hi],
+                                                  d_tiles[1:-1].to(torch.int32), right=True)
+                        rel[lo:hi] = (g.users[lo:hi] - d_tiles[tile_of]).to(torch.int32).to(
+                            torch.int16)
+                    self.compact[b] = None
+                self.host = [rel.cpu().pin_memory(), g.ratings.cpu().pin_memory()]
+                self.dev_rel = rel
+            elif compact:
                 rel = torch.empty(g.nnz, dtype=torch.int16, device=self.dev)
                 for c in range(self.n_cols):
                     b = self.block_of[c]
@@ -501,6 +521,16 @@ class CudaRowBand:
         opts = kernels.qband_opts(g, grid_share=self.concurrency)
         lib = self.lib.load()
         st = "f16" if self.P.dtype == self.torch.float16 else "f32"
+        if g.sub_impl == 8:
+            fn = getattr(lib, f"hmf_sgd_block_runs_u16_{st}")
+            self.lib.check(fn(self.P.data_ptr(), self.Q.data_ptr(), self.k,
+                              self.dev_rel.data_ptr() + 2 * lo, g.ratings.data_ptr() + 4 * lo,
+                              sp.data_ptr(), g.sub_tile_run[b].data_ptr(),
+                              g.sub_tile_cuts[b].data_ptr(), int(g.sub_tiles[b]),
+                              int(g.sub_max_rows), ctypes.byref(opts), float(self.lr),
+                              float(self.ru), float(self.ri), int(seed) & kernels._MASK64,
+                              self.row_lo, 0, stream.cuda_stream), "hmf_sgd_block_runs_u16")
+            return hi - lo
         fn = getattr(lib, f"hmf_sgd_block_qband_u16_tiles_{st}")
         self.lib.check(fn(self.P.data_ptr(), self.Q.data_ptr(), self.k, self.dev_rel.data_ptr(),
                           0, g.ratings.data_ptr(), sp.data_ptr(), sc.data_ptr(),

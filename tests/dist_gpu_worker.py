@@ -35,6 +35,9 @@ def problem(conflict_free=False):
 
 
 def main(out_dir, kernel="exact", stage=False):
+    impl = None
+    if kernel == "qband8":        # the tile-resident run-group layout, forced
+        kernel, impl = "qband", 8
     import torch
     import torch.distributed as dist
     from paper_2006_15980_b200.data import DeviceTriples
@@ -54,7 +57,7 @@ def main(out_dir, kernel="exact", stage=False):
                          torch.from_numpy(items[keep]).to(dev),
                          torch.from_numpy(vals[keep].astype(np.float32)).to(dev))
     band = CudaRowBand(dist, rank, world, dev, trip, lo, hi, col_cuts, K, LR, REG, REG,
-                       kernel=kernel, init=(P0[lo:hi], Q0))
+                       kernel=kernel, init=(P0[lo:hi], Q0), impl=impl)
     run_id = [f"gputest{os.getpid()}"]
     dist.broadcast_object_list(run_id, src=0)
     table = make_lease_table("shm", dist.distributed_c10d._get_default_store(), band.n_cols,

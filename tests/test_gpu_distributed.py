@@ -54,8 +54,9 @@ def test_two_ranks_ipc_lease_protocol_equals_serial_replay(tmp_path):
     assert np.array_equal(Q_final, Q)
 
 
+@pytest.mark.parametrize("layout", ["qband", "qband8"], ids=["auto", "run_groups"])
 @pytest.mark.parametrize("stage", [False, True], ids=["resident", "host_staged"])
-def test_two_ranks_qband_path_applies_every_triple(tmp_path, stage):
+def test_two_ranks_qband_path_applies_every_triple(tmp_path, stage, layout):
     """The default multi-GPU kernel path (Q-band layout of each rank's band,
     narrow column bands split over the chains) on conflict-free triples:
     order-free, so after the epochs P and Q equal the reference update of
@@ -69,7 +70,7 @@ def test_two_ranks_qband_path_applies_every_triple(tmp_path, stage):
     import dist_gpu_worker as W
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_port()}",
-           str(ROOT / "tests" / "dist_gpu_worker.py"), str(tmp_path), "qband"]
+           str(ROOT / "tests" / "dist_gpu_worker.py"), str(tmp_path), layout]
     if stage:
         cmd.append("stage")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)

@@ -852,10 +852,12 @@ def test_qband_split_runs_ml1m_quality(dev):
 
 @pytest.mark.parametrize("k,dtype", [(32, "float16"), (32, "float32"), (128, "float32")])
 def test_default_layout_quality_matches_whole_runs(dev, k, dtype):
-    """The default layout of a narrow block (600 items per block: item runs
-    split over the chains, Q deltas) must train like whole runs on one chain
-    each: same synthetic law, same init; test RMSE after 8 epochs within
-    0.005 (and both must have learned)."""
+    """Narrow blocks (600 items each) at 2 % density: the automatic layout
+    (run groups over a shared-memory P tile, implementation 8, since a tile
+    holds ~8 ratings per item) and the split-run layout (implementation 5:
+    item runs split over the chains, Q deltas) must both train like whole
+    runs on one chain each (implementation 4): same synthetic law, same init,
+    test RMSE after 8 epochs within 0.005 (and all must have learned)."""
     from paper_2006_15980_b200 import kernels
     from paper_2006_15980_b200.data import (bucket_qbands, build_device_grid, split_device,
                                             synthetic_device)
@@ -864,10 +866,9 @@ def test_default_layout_quality_matches_whole_runs(dev, k, dtype):
     trip = synthetic_device(120_000, 1_200, 3_000_000, seed=3, device=d)
     train, test = split_device(trip, 0.05)
     out = {}
-    for layout in ("default", "whole"):
+    for layout, impl in (("default", None), ("split", 5), ("whole", 4)):
         g = build_device_grid(train, [0, 120_000], [0, 600, 1_200])
-        bucket_qbands(g, k, elem_bytes=2 if dtype == "float16" else 4,
-                      impl=None if layout == "default" else 4)
+        bucket_qbands(g, k, elem_bytes=2 if dtype == "float16" else 4, impl=impl)
         model = init_device_model(120_000, 1_200, k, 0, device=d, dtype=dtype)
         first = rmse(test, model).value
         for e in range(8):
@@ -876,9 +877,11 @@ def test_default_layout_quality_matches_whole_runs(dev, k, dtype):
                                            kernels.mix64(b, e))
         out[layout] = (first, rmse(test, model).value, g.sub_impl, g.sub_split)
     print(out)
-    assert out["default"][3] > 1          # the default did split the runs
+    assert out["default"][2] == 8
+    assert out["split"][3] > 1            # implementation 5 did split the runs
     assert out["whole"][1] < out["whole"][0] - 0.005
-    assert abs(out["default"][1] - out["whole"][1]) <= 0.005
+    for layout in ("default", "split"):
+        assert abs(out[layout][1] - out["whole"][1]) <= 0.005, out
 
 
 @pytest.mark.parametrize("k", [32, 128])

@@ -5,7 +5,7 @@ A Netflix-shaped problem scaled to the suite's budget — the full 17 700
 items, 120 000 users, 25 M ratings (Netflix's density) — lays out as the
 bench's 480 000 x 17 700 / 100 M run does (data.tile_resident_impl): P row
 tiles in shared memory, at least one per SM, item runs of ~4.9 ratings,
-implementation 8 (run groups), or 7 for fp32 at k = 256.  Both sides train on the
+implementation 8 (run groups).  Both sides train on the
 identical triples from the identical initial factors; the reference is the
 unmodified hetmf.run_training(stream-only) on the host cores (oracle/_ref).
 Every epoch must be within 0.005, and stores may not push the fp32 epoch-1
@@ -66,8 +66,8 @@ def test_headline_path_rmse_within_0005_of_reference(hetmf, data, k, precision):
           f"{grid.sub_pstore} tiles {grid.sub_tiles}; ours {np.round(ours, 5).tolist()} "
           f"reference {np.round(ref, 5).tolist()}")
     # the bench's layout decision (data.tile_resident_impl): run groups over
-    # a shared-memory P tile, item bins for fp32 at k = 256
-    assert grid.sub_impl == (7 if (k == 256 and precision == "f32") else 8)
+    # a shared-memory P tile
+    assert grid.sub_impl == 8
     assert all(t >= 148 for t in grid.sub_tiles)
     gaps = np.abs(np.asarray(ours) - np.asarray(ref))
     assert np.all(gaps <= 0.005), (ours, ref)
