@@ -410,7 +410,39 @@ def roofline_fields(args, achieved, peak, peak_kind, bpu, mean_ms, mean_updates,
                "source": "scripts/l2_rowbench.cu: random P-row load + "
                          + ("store" if p_stores else "vector reduction")
                          + ", L2-resident 32 MB, no arithmetic (profiles/r02/l2_rowbench.jsonl)"})}
+    if ncu and ncu.get("smem_wavefronts") and impl in (7, 8):
+        # P rows live in shared memory: the bound is the SM's L1/shared data
+        # pipe, one 128-byte wavefront per cycle per SM (P-row loads and
+        # stores, 8 per update at fp32 k=128, plus shuffles and the global
+        # loads that pass through L1)
+        n_sm, mhz = sm_geometry()
+        wpu = ncu["smem_wavefronts"] / mean_updates
+        peak_w = n_sm * mhz * 1e6
+        out["smem_pipe"] = {
+            "shared_wavefronts_per_update": wpu,
+            "peak_wavefronts_per_s": peak_w, "sm_count": n_sm, "sm_max_mhz": mhz,
+            "ceiling_updates_per_s": peak_w / wpu, "kernel_updates_per_s": kernel_ups,
+            "frac": kernel_ups / (peak_w / wpu),
+            "lsu_data_pipe_pct": ncu.get("l1tex_pct"),
+            "source": ncu["source"] + " (l1tex__data_pipe_lsu_wavefronts_mem_shared.sum)"}
     return out
+
+
+def sm_geometry():
+    """(SM count, max SM clock in MHz) of device 0 (148, 1965 on B200)."""
+    try:
+        import torch
+        n = int(torch.cuda.get_device_properties(0).multi_processor_count)
+    except Exception:
+        n = 148
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(pynvml.nvmlDeviceGetHandleByIndex(0),
+                                                     pynvml.NVML_CLOCK_SM))
+    except Exception:
+        mhz = 1965.0
+    return n, mhz
 
 
 def cpu_baseline(n_users, n_items, k, nnz) -> dict:
