@@ -129,3 +129,43 @@ def test_stream_chunk_cuts():
     assert chunk_cuts(3, 2, 1) == [0, 2, 3]
     assert chunk_cuts(1, 4, 1) == [0, 1]                 # one tile: no separate last chunk
     assert chunk_cuts(15, 4) == [0, 4, 8, 12, 15]
+
+
+def test_ptile_row_cuts():
+    """Row tiles of the shared-memory P tile (implementations 7 and 8): every
+    tile fits hmf_ptile_max_rows, tiles are equal to within one row, at least
+    one per SM once that leaves >= PTILE_MIN_ROWS rows each, and a multiple of
+    the SM count when more than half the SMs get one."""
+    from paper_2006_15980_b200 import _lib
+    from paper_2006_15980_b200.data import PTILE_MIN_ROWS, ptile_row_cuts
+    lib = _lib.load()
+    for k, f16 in ((128, False), (32, False), (256, False), (64, True)):
+        cap = lib.hmf_ptile_max_rows(k, 1 if f16 else 0)
+        assert cap == 208 * 1024 // (k * (2 if f16 else 4))
+        for lo, hi in ((0, 480_000), (1000, 121_000), (0, 6040), (5, 9_000)):
+            cuts = ptile_row_cuts(lo, hi, k, f16, 148)
+            sizes = np.diff(cuts)
+            T = len(sizes)
+            assert cuts[0] == lo and cuts[-1] == hi and np.all(sizes > 0)
+            assert sizes.max() <= cap and sizes.max() - sizes.min() <= 1
+            if hi - lo >= 148 * PTILE_MIN_ROWS:
+                assert T >= 148 and T % 148 == 0
+    # NF at k=128 fp32: 1 184 tiles of ~405 users per block
+    assert len(ptile_row_cuts(0, 480_000, 128, False, 148)) - 1 == 1184
+
+
+def test_run_rotation_range_and_spread():
+    """Implementation 8's per-run start rotation (csrc/runs.cuh run_rotation,
+    restated in data.run_rotation): always inside the run, spread over it,
+    and a function of (seed, run) only."""
+    from paper_2006_15980_b200.data import run_rotation
+    for length in (1, 2, 5, 17, 416):
+        rots = [run_rotation(123456789, r, length) for r in range(4000)]
+        assert min(rots) >= 0 and max(rots) < length
+        counts = np.bincount(rots, minlength=length)
+        if 1 < length <= 17:
+            assert counts.min() > 0.5 * 4000 / length
+        elif length > 17:
+            assert (counts > 0).mean() > 0.95
+    assert run_rotation(7, 3, 10) == run_rotation(7, 3, 10)
+    assert [run_rotation(s, 3, 1000) for s in range(5)] != [run_rotation(0, 3, 1000)] * 5
