@@ -56,6 +56,43 @@ template <typename RowT> __device__ inline int tile_row(RowT v, int r0) {
   }
 }
 
+// Row layout of a chain (ChainLay: lane l of the chain holds NV vectors of W
+// elements, vector v at element (v * LPC + l) * W) with the vector order
+// rotated by the chain index c.  One LDS/STS instruction of a warp touches
+// vector v of every chain's row; when a chain's part of it is under 128 bytes
+// (fp32 k = 32: 4 lanes x 16 B), unrotated chains would all hit the same half
+// of their (128-byte aligned) rows — the same 16 banks, two wavefronts where
+// one suffices.  Rotated, chains alternate halves.  P and Q rows use the same
+// permutation, so the dot product and the update are unchanged.
+template <int K, typename S, int LPC> struct RotLay {
+  using B = ChainLay<K, S, LPC>;
+  using V = typename B::V;
+  static constexpr int EPL = B::EPL, W = B::W, NV = B::NV;
+  static_assert((NV & (NV - 1)) == 0, "NV must be a power of two");
+  // rotate only where a chain's vector is under a 128-byte line (elsewhere
+  // the unrotated offsets are compile-time immediates off one base register)
+  static constexpr bool ROT = NV > 1 && LPC * W * int(sizeof(S)) < 128;
+  __device__ static int off(int v, int l, int c) {
+    return ((ROT ? ((v + c) & (NV - 1)) : v) * LPC + l) * W;
+  }
+  __device__ static void ldg(const S* row, int l, int c, float* o) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) V::ldg(row + off(v, l, c), o + v * W);
+  }
+  __device__ static void red(S* row, int l, int c, const float* d) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) V::red(row + off(v, l, c), d + v * W);
+  }
+  __device__ static void lds(const S* row, int l, int c, float* o) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) V::lds(row + off(v, l, c), o + v * W);
+  }
+  __device__ static void sts(S* row, int l, int c, const float* i) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) V::sts(row + off(v, l, c), i + v * W);
+  }
+};
+
 // Rotation of run r's visit, uniform in [0, len): a 32-bit hash of (seed, r)
 // scaled by len (the high half of the product).  data.run_rotation restates it.
 __device__ __forceinline__ int run_rotation(uint32_t seed32, int r, int len) {
@@ -76,7 +113,7 @@ __global__ void __launch_bounds__(WPB * 32, 1)
                 const float* __restrict__ vals, const int4* __restrict__ runs,
                 const int32_t* __restrict__ tile_run, const int32_t* __restrict__ tile_cut,
                 int n_tiles, float lr, float ru, float ri, uint32_t seed32) {
-  using L = ChainLay<K, S, LPC>;
+  using L = RotLay<K, S, LPC>;
   constexpr int E = L::EPL;
   constexpr int E2 = E / 2;
   constexpr int NC = 32 / LPC;
@@ -142,7 +179,7 @@ __global__ void __launch_bounds__(WPB * 32, 1)
     auto stage_rows = [&](const int4& m) {
       if (m.y > 0) {
         float tq[E];
-        L::ldg(Qb + int64_t(m.z) * K, l, tq);
+        L::ldg(Qb + int64_t(m.z) * K, l, c, tq);
 #pragma unroll
         for (int e = 0; e < E2; ++e) qn[e] = make_float2(tq[2 * e], tq[2 * e + 1]);
         nrot = run_rotation(seed32, m.w, m.y);
@@ -205,7 +242,7 @@ __global__ void __launch_bounds__(WPB * 32, 1)
           const float r = __shfl_sync(FULL, cr, jj, LPC);
           S* prow = tile + int64_t(act ? tile_row<RowT>(RowT(u), r0) : 0) * K;
           float2 pc[E2];
-          L::lds(prow, l, reinterpret_cast<float*>(pc));
+          L::lds(prow, l, c, reinterpret_cast<float*>(pc));
           float2 da = make_float2(0.f, 0.f), db = make_float2(0.f, 0.f);
 #pragma unroll
           for (int e = 0; e < E2; e += 2) {
@@ -237,12 +274,12 @@ __global__ void __launch_bounds__(WPB * 32, 1)
 #pragma unroll
               for (int v = 0; v < L::NV; ++v)
                 asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
-                                 a0 + uint32_t(L::off(v, l)) * 4u),
+                                 a0 + uint32_t(L::off(v, l, c)) * 4u),
                              "f"(pc[2 * v].x), "f"(pc[2 * v].y), "f"(pc[2 * v + 1].x),
                              "f"(pc[2 * v + 1].y)
                              : "memory");
             } else {
-              L::sts(prow, l, reinterpret_cast<const float*>(pc));
+              L::sts(prow, l, c, reinterpret_cast<const float*>(pc));
             }
           }
         }
@@ -266,7 +303,7 @@ __global__ void __launch_bounds__(WPB * 32, 1)
           dq[2 * e] = dd.x;
           dq[2 * e + 1] = dd.y;
         }
-        L::red(Qb + int64_t(item) * K, l, dq);
+        L::red(Qb + int64_t(item) * K, l, c, dq);
       }
     }
     // the chains' shared-memory writes, then the bulk write-back (async
