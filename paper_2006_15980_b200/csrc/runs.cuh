@@ -239,7 +239,6 @@ __global__ void __launch_bounds__(WPB * 32, 1)
           if (j0 + jj >= steps) break;  // warp-uniform
           const bool act = j0 + jj < len;  // chain-uniform
           const int32_t u = __shfl_sync(FULL, cu, jj, LPC);
-          const float r = __shfl_sync(FULL, cr, jj, LPC);
           S* prow = tile + int64_t(act ? tile_row<RowT>(RowT(u), r0) : 0) * K;
           float2 pc[E2];
           L::lds(prow, l, c, reinterpret_cast<float*>(pc));
@@ -250,11 +249,13 @@ __global__ void __launch_bounds__(WPB * 32, 1)
             if (e + 1 < E2) db = __ffma2_rn(pc[e + 1], qs[e + 1], db);
           }
           const float2 ds = __fadd2_rn(da, db);
-          float d = ds.x + ds.y;
+          // the rating joins the reduction instead of being broadcast: lane jj
+          // of the chain holds it, so the chain's sum is p.q - r (q = sq qs)
+          float d = fmaf(sq, ds.x + ds.y, l == jj ? -cr : 0.f);
 #pragma unroll
           for (int o = LPC / 2; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
           if (act) {
-            const float a = lr * fmaf(-sq, d, r);  // lr * (r - p.q)
+            const float a = -lr * d;  // lr * (r - p.q)
             const float as = a * sq;
             isq *= inv_keep_q;
             sq *= keep_q;
