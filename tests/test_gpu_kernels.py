@@ -1187,3 +1187,27 @@ def test_runs_equal_sequential_replay(dev, k, dtype):
     tol = 2e-3 if f16 else 1e-5
     assert rel_err(P.double().cpu().numpy(), Pe) < tol
     assert rel_err(Q.double().cpu().numpy(), Qe) < tol
+
+
+def test_tile_resident_policy(dev):
+    """data.tile_resident_impl picks run groups (8) exactly where they win
+    (profiles/round2/s3_default_layout_sweep.jsonl): Netflix density (~4.9
+    ratings per tile-item), but not a small matrix (fewer tiles than SMs),
+    a sparse one (< 2 ratings per tile-item) or one with hot items."""
+    from paper_2006_15980_b200.data import (build_device_grid, synthetic_band,
+                                            tile_resident_impl)
+    d = dev
+
+    def grid(n_users, n_items, nnz, skew=False):
+        tr, _ = synthetic_band(n_users, n_items, nnz, seed=5, device=d)
+        if skew:   # one item takes a fifth of the ratings
+            tr.items[: tr.nnz // 5] = 7
+        return build_device_grid(tr, [0, n_users], [0, n_items // 2, n_items])
+
+    assert tile_resident_impl(grid(120_000, 17_700, 25_000_000), 128, False) == 8
+    assert tile_resident_impl(grid(120_000, 17_700, 25_000_000), 32, True) == 8
+    assert tile_resident_impl(grid(6_040, 3_706, 1_000_000), 32, False) is None      # 4 tiles
+    assert tile_resident_impl(grid(200_000, 60_000, 4_000_000), 128, False) is None  # sparse
+    assert tile_resident_impl(grid(120_000, 17_700, 25_000_000, skew=True), 128,
+                              False) is None                                         # hot item
+    assert tile_resident_impl(grid(120_000, 17_700, 25_000_000), 96, False) is None  # k
