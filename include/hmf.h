@@ -50,6 +50,7 @@ extern "C" {
 #define HMF_ERR_ARG (-1)
 #define HMF_ERR_CUDA (-2)
 #define HMF_ERR_UNSUPPORTED (-3)
+#define HMF_ERR_ABORTED (-4) /* the multi-GPU run was aborted (hmf_lease_abort) */
 
 /* Visit-order modes of hmf_sgd_range_*. */
 #define HMF_MODE_HOGWILD 0     /* throughput: many warps, lock-free delta reductions */
@@ -409,6 +410,10 @@ int hmf_ipc_close_handle(void* dptr);
  *     error if rank does not hold it.
  *   hmf_lease_ticket: a global sequence number (1, 2, ...).
  *   hmf_lease_ops: atomic operations served so far (all processes).
+ *   hmf_lease_abort: marks the run aborted by `rank` (the first abort wins);
+ *     every later acquire returns HMF_ERR_ABORTED (scheduler.abort,
+ *     scheduler.py:415-423; workers.py:300-302).  hmf_lease_aborted: the
+ *     aborting rank, or -1.
  */
 int hmf_lease_open(const char* name, int32_t n_cols, int32_t create, void** table);
 int hmf_lease_close(void* table, int32_t unlink_segment);
@@ -420,6 +425,8 @@ int hmf_lease_owner(void* table, int32_t c, int32_t* owner);
 int hmf_lease_holder(void* table, int32_t c, int32_t* holder);
 int64_t hmf_lease_ticket(void* table);
 int64_t hmf_lease_ops(void* table);
+int hmf_lease_abort(void* table, int32_t rank);
+int32_t hmf_lease_aborted(void* table);
 
 #ifdef __cplusplus
 }

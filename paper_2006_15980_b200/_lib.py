@@ -20,6 +20,7 @@ HMF_OK = 0
 HMF_ERR_ARG = -1
 HMF_ERR_CUDA = -2
 HMF_ERR_UNSUPPORTED = -3
+HMF_ERR_ABORTED = -4
 
 MODE_HOGWILD = 0
 MODE_ORDERED = 1
@@ -109,6 +110,8 @@ SIGNATURES = {
     "hmf_lease_holder": (C.c_int, [_p, _i32, C.POINTER(_i32)]),
     "hmf_lease_ticket": (_i64, [_p]),
     "hmf_lease_ops": (_i64, [_p]),
+    "hmf_lease_abort": (C.c_int, [_p, _i32]),
+    "hmf_lease_aborted": (_i32, [_p]),
 }
 
 

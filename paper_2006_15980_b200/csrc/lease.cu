@@ -42,6 +42,9 @@ struct alignas(64) Header {
   int32_t pad;
   alignas(64) std::atomic<int64_t> seq;
   alignas(64) std::atomic<int64_t> ops;  // atomic operations served (all ranks)
+  // 0, or 1 + the rank that aborted the run (scheduler.abort,
+  // scheduler.py:415-423 / workers.py:300-302): acquires fail from then on
+  alignas(64) std::atomic<int32_t> aborted;
 };
 
 static_assert(std::atomic<int32_t>::is_always_lock_free, "address-free atomics needed");
@@ -69,6 +72,16 @@ static Table* checked(void* t, int32_t c) {
     return nullptr;
   }
   return tb;
+}
+
+// HMF_ERR_ABORTED with the aborting rank in the message once the run is aborted
+static bool aborted_error(Table* t) {
+  const int32_t a = t->h->aborted.load(std::memory_order_acquire);
+  if (!a) return false;
+  char msg[96];
+  std::snprintf(msg, sizeof(msg), "the run was aborted by rank %d", a - 1);
+  set_error(HMF_ERR_ABORTED, msg);
+  return true;
 }
 
 }  // namespace lease
@@ -117,6 +130,7 @@ int hmf_lease_open(const char* name, int32_t n_cols, int32_t create, void** out)
     t->h->n_cols = n_cols;
     t->h->seq.store(0, std::memory_order_relaxed);
     t->h->ops.store(0, std::memory_order_relaxed);
+    t->h->aborted.store(0, std::memory_order_relaxed);
     for (int32_t c = 0; c < n_cols; ++c) {
       t->slots[c].holder.store(-1, std::memory_order_relaxed);
       t->slots[c].owner.store(-1, std::memory_order_relaxed);
@@ -146,6 +160,7 @@ int32_t hmf_lease_try_acquire(void* table, int32_t c, int32_t rank) {
   Table* t = checked(table, c);
   if (!t) return HMF_ERR_ARG;
   if (rank < 0) return int32_t(hmf::set_error(HMF_ERR_ARG, "rank must be >= 0"));
+  if (aborted_error(t)) return HMF_ERR_ABORTED;
   t->h->ops.fetch_add(1, std::memory_order_relaxed);
   int32_t expect = -1;
   return t->slots[c].holder.compare_exchange_strong(expect, rank, std::memory_order_acq_rel,
@@ -161,6 +176,7 @@ int hmf_lease_acquire_first(void* table, const int32_t* cands, int32_t n, int32_
   if (!t || !got || (!cands && n > 0)) return int(hmf::set_error(HMF_ERR_ARG, "null argument"));
   if (rank < 0) return int(hmf::set_error(HMF_ERR_ARG, "rank must be >= 0"));
   *got = -1;
+  if (aborted_error(t)) return HMF_ERR_ABORTED;
   for (int32_t i = 0; i < n; ++i)
     if (cands[i] < 0 || cands[i] >= t->h->n_cols)
       return int(hmf::set_error(HMF_ERR_ARG, "column out of range"));
@@ -223,6 +239,22 @@ int64_t hmf_lease_ticket(void* table) {
   if (!t) return hmf::set_error(HMF_ERR_ARG, "null lease table");
   t->h->ops.fetch_add(1, std::memory_order_relaxed);
   return t->h->seq.fetch_add(1, std::memory_order_acq_rel) + 1;
+}
+
+int hmf_lease_abort(void* table, int32_t rank) {
+  using namespace hmf::lease;
+  Table* t = static_cast<Table*>(table);
+  if (!t) return int(hmf::set_error(HMF_ERR_ARG, "null lease table"));
+  int32_t expect = 0;
+  t->h->aborted.compare_exchange_strong(expect, rank + 1, std::memory_order_acq_rel);
+  return HMF_OK;
+}
+
+int32_t hmf_lease_aborted(void* table) {
+  using namespace hmf::lease;
+  Table* t = static_cast<Table*>(table);
+  if (!t) return int32_t(hmf::set_error(HMF_ERR_ARG, "null lease table"));
+  return t->h->aborted.load(std::memory_order_acquire) - 1;
 }
 
 int64_t hmf_lease_ops(void* table) {

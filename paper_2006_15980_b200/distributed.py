@@ -101,8 +101,23 @@ class LeaseTable:
         self.seconds += time.perf_counter() - t0
         return n
 
+    def abort(self) -> None:
+        """Mark the run aborted by this rank (a store key every acquire checks)."""
+        self.store.compare_set(f"{self.prefix}/aborted", b"", str(self.rank).encode())
+
+    def aborted_by(self) -> int:
+        if not self.store.check([f"{self.prefix}/aborted"]):
+            return -1
+        return int(bytes(self.store.get(f"{self.prefix}/aborted")))
+
     def close(self, unlink: bool = False) -> None:
         pass
+
+
+class LeaseAborted(RuntimeError):
+    """Another rank aborted the run (its lease loop raised); the reference
+    re-raises a worker's exception after scheduler.abort (workers.py:300-302,
+    engine.py:255-258)."""
 
 
 class ShmLeaseTable:
@@ -142,12 +157,6 @@ class ShmLeaseTable:
     def initialize(self) -> None:
         self._open(create=True)
 
-    def _check(self, rc: int, what: str) -> int:
-        if rc < 0:
-            from . import _lib
-            raise _lib.HmfError(f"{what} failed ({rc}): {_lib.last_error()}")
-        return rc
-
     def try_acquire(self, c: int) -> bool:
         t = self._table()
         t0 = time.perf_counter()
@@ -180,8 +189,8 @@ class ShmLeaseTable:
 
     def holder(self, c: int) -> int:
         o = ctypes.c_int32()
-        self._check(self._lib.hmf_lease_holder(self._table(), int(c), ctypes.byref(o)),
-                    "hmf_lease_holder")
+        t = self._table()
+        self._check(self._lib.hmf_lease_holder(t, int(c), ctypes.byref(o)), "hmf_lease_holder")
         return int(o.value)
 
     def release(self, c: int) -> None:
@@ -203,7 +212,27 @@ class ShmLeaseTable:
 
     def total_ops(self) -> int:
         """Operations served by the segment, all processes."""
-        return int(self._lib.hmf_lease_ops(self._table()))
+        t = self._table()            # maps the segment (and binds the library) first
+        return int(self._lib.hmf_lease_ops(t))
+
+    def abort(self) -> None:
+        """Mark the run aborted by this rank: every later acquire, on every
+        rank, raises LeaseAborted (scheduler.abort, scheduler.py:415-423)."""
+        t = self._table()
+        self._check(self._lib.hmf_lease_abort(t, self.rank), "hmf_lease_abort")
+
+    def aborted_by(self) -> int:
+        """The rank that aborted the run, or -1."""
+        t = self._table()
+        return int(self._lib.hmf_lease_aborted(t))
+
+    def _check(self, rc: int, what: str) -> int:
+        from . import _lib
+        if rc == _lib.HMF_ERR_ABORTED:
+            raise LeaseAborted(_lib.last_error())
+        if rc < 0:
+            raise _lib.HmfError(f"{what} failed ({rc}): {_lib.last_error()}")
+        return rc
 
     def close(self, unlink: bool = False) -> None:
         if self._t is not None:
@@ -279,6 +308,8 @@ class RowBandTrainer:
                         return c
             if not blocking:
                 return None
+            if not hasattr(self.table, "acquire_first") and self.table.aborted_by() >= 0:
+                raise LeaseAborted(f"the run was aborted by rank {self.table.aborted_by()}")
             time.sleep(delay)
             delay = min(delay * 2, 1e-3)
         return None
@@ -303,6 +334,21 @@ class RowBandTrainer:
         self.total_updates += self.backend.compute(c, mix64(unit_seed, 0))
 
     def run_epoch(self) -> None:
+        """One quota epoch of this rank's blocks.  A failure here aborts the
+        whole run: the lease table is marked, every other rank's next acquire
+        raises LeaseAborted instead of waiting for a column this rank may
+        hold (workers.py:300-302)."""
+        try:
+            self._run_epoch()
+        except LeaseAborted:
+            raise
+        except BaseException:
+            try:
+                self.table.abort()
+            finally:
+                raise
+
+    def _run_epoch(self) -> None:
         todo = set(range(self.n_cols))
         cur = self._grab(todo, blocking=True)
         todo.discard(cur)

@@ -153,3 +153,28 @@ def test_two_rank_lease_protocol_equals_serial_replay(tmp_path, kind):
     got_P = np.concatenate([logs[0][1], logs[1][1]])
     assert np.array_equal(got_P, P)
     assert np.array_equal(np.load(tmp_path / "Q_final.npy"), Q)
+
+
+def test_store_table_abort():
+    """The portable (TCPStore) table aborts like the shared-memory one: the
+    first abort wins and a blocked acquire raises LeaseAborted."""
+    import datetime
+
+    import torch.distributed as dist
+    from paper_2006_15980_b200.distributed import LeaseAborted, LeaseTable, RowBandTrainer
+    store = dist.TCPStore("127.0.0.1", _free_port(), 1, True,
+                          timeout=datetime.timedelta(seconds=30))
+    a = LeaseTable(store, 2, 0, "abort")
+    a.initialize()
+    b = LeaseTable(store, 2, 1, "abort")
+    assert a.aborted_by() == -1
+    assert a.try_acquire(0) and a.try_acquire(1)        # rank 0 holds everything
+    b.abort()
+    a.abort()                                           # the first abort wins
+    assert a.aborted_by() == b.aborted_by() == 1
+
+    class Band:
+        n_cols = 2
+
+    with pytest.raises(LeaseAborted, match="rank 1"):
+        RowBandTrainer(Band(), b, 1)._grab({0, 1}, blocking=True)

@@ -150,3 +150,72 @@ def test_operation_cost_is_microseconds():
         assert per_lease < 200e-6, per_lease
     finally:
         t.close(unlink=True)
+
+
+def _abort_rank(rank, run_id, n_cols, out_path):
+    """Rank 1 holds a column and fails; rank 0 waits for that column and
+    must get LeaseAborted instead of waiting forever."""
+    import time as _t
+
+    from paper_2006_15980_b200.distributed import LeaseAborted, RowBandTrainer, ShmLeaseTable
+
+    class Band:
+        def __init__(self):
+            self.n_cols = n_cols
+
+        def pull(self, c, owner):
+            pass
+
+        def compute(self, c, seed):
+            if rank == 1:
+                _t.sleep(0.5)
+                raise RuntimeError("device failure on rank 1")
+            return 1
+
+        def finish(self, c):
+            pass
+
+    table = ShmLeaseTable(n_cols, rank, run_id)
+    trainer = RowBandTrainer(Band(), table, rank, seed=0)
+    try:
+        if rank == 0:              # start once rank 1 holds column 0
+            deadline = _t.time() + 30
+            while table.holder(0) != 1 and _t.time() < deadline:
+                _t.sleep(0.005)
+        trainer.run_epoch()
+        result = "finished"
+    except LeaseAborted as exc:
+        result = f"aborted: {exc}"
+    except RuntimeError as exc:
+        result = f"failed: {exc}"
+    with open(out_path + f".{rank}", "w") as fh:
+        fh.write(result)
+    table.close()
+
+
+def test_abort_releases_waiting_ranks(tmp_path):
+    """A rank whose lease loop raises marks the run aborted (hmf_lease_abort,
+    the reference's scheduler.abort on a worker error, workers.py:300-302):
+    a rank blocked waiting for a column gets LeaseAborted, and nobody hangs."""
+    run = uuid.uuid4().hex[:10]
+    n_cols = 1                           # both ranks need the same column
+    owner = _table(n_cols, 0, run)
+    owner.initialize()
+    try:
+        ctx = mp.get_context("spawn")
+        out = str(tmp_path / "res")
+        procs = [ctx.Process(target=_abort_rank, args=(r, run, n_cols, out)) for r in (1, 0)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(60)
+            assert p.exitcode == 0
+        assert open(out + ".1").read() == "failed: device failure on rank 1"
+        r0 = open(out + ".0").read()
+        assert r0.startswith("aborted") and "rank 1" in r0, r0
+        assert owner.aborted_by() == 1
+        from paper_2006_15980_b200.distributed import LeaseAborted
+        with pytest.raises(LeaseAborted):
+            owner.try_acquire(0)
+    finally:
+        owner.close(unlink=True)
