@@ -724,7 +724,7 @@ def run_ours_multi(args, world, rank, local):
     t0 = time.perf_counter()
     train, test = synthetic_band(m_users, n_items, m_total, row_lo, row_hi, rank=8, noise=0.1,
                                  seed=SEED, test_fraction=TEST_FRACTION, device=dev)
-    n_cols = 2 * geo + 1
+    n_cols = args.cols_per_gpu * geo + 1
     col_cuts = np.linspace(0, n_items, n_cols + 1).astype(np.int64)
     band = CudaRowBand(dist, rank, world, dev, train, row_lo, row_hi, col_cuts, k, LR, REG, REG,
                        init_seed=SEED, kernel=args.multi_kernel,
@@ -993,6 +993,9 @@ def main():
     ap.add_argument("--multi-kernel", choices=["auto", "qband", "range"], default="auto")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="N>1: a workload-sized band per GPU (weak) or the workload split (strong)")
+    ap.add_argument("--cols-per-gpu", type=int, default=2,
+                    help="N>1: column bands = this x N + 1 (2: a primary and a staged-ahead "
+                         "band per GPU plus a spare)")
     ap.add_argument("--lease", choices=["shm", "store"], default="shm",
                     help="N>1: column-lease table: node-local shared memory (csrc/lease.cu) "
                          "or the torch.distributed store")

@@ -200,6 +200,10 @@ __device__ inline void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
                : "memory");
 }
 __device__ inline void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Prefetch `bytes` (multiple of 16, 16-byte aligned) of global memory into L2.
+__device__ inline void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // the committed bulk stores have read their shared-memory source
 __device__ inline void bulk_wait_read_all() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
