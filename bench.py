@@ -543,9 +543,21 @@ def run_ours(args, world, rank, local):
                       chain_cfg=args.chain_cfg)
     stream_epoch = None
     if not args.no_e2e and args.kernel == "qband" and world == 1:
-        # e2e streams the same layout from pinned host memory, tile by tile
+        # e2e streams the same kind of layout from pinned host memory, tile by
+        # tile; run groups over tiles of at most --stream-tile-rows users, so
+        # each user id crosses PCIe as one byte (5 B per rating, not 6)
         from paper_2006_15980_b200.workers import StreamingEpoch
-        stream_epoch = StreamingEpoch(grid, k, n_buffers=args.stream_buffers,
+        sgrid = grid
+        if (getattr(grid, "sub_impl", None) == 8 and args.stream_tile_rows
+                and int(grid.sub_max_rows) > args.stream_tile_rows):
+            from paper_2006_15980_b200.data import DeviceGrid
+            sgrid = DeviceGrid(grid.n_rows, grid.n_cols, grid.row_cuts, grid.col_cuts,
+                               grid.region_of_row, grid.sub_row_parent, grid.users.clone(),
+                               grid.items.clone(), grid.ratings.clone(),
+                               np.asarray(grid.block_ptr).copy())
+            bucket_qbands(sgrid, k, elem_bytes=2 if precision == "f16" else 4, impl=8,
+                          max_tile_rows=args.stream_tile_rows)
+        stream_epoch = StreamingEpoch(sgrid, k, n_buffers=args.stream_buffers,
                                       tiles_per_chunk=args.stream_tiles,
                                       runs_chunks_per_block=args.stream_chunks,
                                       last_chunk_tiles=args.stream_last,
@@ -903,11 +915,15 @@ def run_e2e_stream(args, se, model, test, dev):
             "test_rmse_after": float(np.sqrt(sq / test.nnz)),
             "path": "workers.StreamingEpoch (pinned host triples streamed per epoch, "
                     + (f"{se.bytes_per_rating} B/rating: "
-                       + ("2-byte user ids relative to the row tile, " if se.u16 else "")
-                       + ("item implicit in its sub-band; " if se.implicit_items else "triples; "))
-                    + f"{se.n_chunks} chunks of {se.tiles_per_chunk} row tile(s)"
+                       + (f"{1 if se.u8 else 2}-byte user ids relative to the row tile, "
+                          if se.u16 else "")
+                       + ("item from its run descriptor (resident); " if se.runs else
+                          "item implicit in its sub-band; " if se.implicit_items else "triples; "))
+                    + (f"run groups (implementation 8), tiles of <= {se.sg.sub_max_rows} users, "
+                       f"{se.n_chunks} chunks" if se.runs else
+                       f"{se.n_chunks} chunks of {se.tiles_per_chunk} row tile(s)")
                     + (f" (each block's last {se.last_chunk_tiles})" if se.last_chunk_tiles
-                       else "") + ", "
+                       and not se.runs else "") + ", "
                     f"{se.n_buffers} staging buffers, H2D overlapped with the Q-band kernel; "
                     + ("chunks still staged from the previous epoch are not uploaded again"
                        if se.reuse else "every chunk uploaded every epoch")
@@ -1013,6 +1029,10 @@ def main():
                          "0 reductions, 1 stores")
     ap.add_argument("--stream-buffers", type=int, default=3,
                     help="e2e: device staging buffers (ring)")
+    ap.add_argument("--stream-tile-rows", type=int, default=256,
+                    help="e2e with implementation 8: row tiles of at most this many users "
+                         "(256: one-byte user ids, 5 B per streamed rating; 0: the resident "
+                         "layout's tiles)")
     ap.add_argument("--stream-chunks", type=int, default=2,
                     help="e2e with implementation 8: chunks per block (each a whole fraction "
                          "of the block's row tiles)")

@@ -296,6 +296,21 @@ int64_t hmf_sgd_block_runs_u16_f16(uint16_t* user_f, uint16_t* item_f, int64_t k
                                    const hmf_qband_opts* opts, double lr, double reg_user,
                                    double reg_item, uint64_t seed, int64_t row_base,
                                    int64_t col_base, void* stream);
+/* uint8 ids relative to tiles of at most 256 rows: 5 bytes per streamed
+ * rating (the user's byte + the fp32 rating). */
+int64_t hmf_sgd_block_runs_u8_f32(float* user_f, float* item_f, int64_t k, const uint8_t* rows,
+                                  const float* vals, const int32_t* runs, const int32_t* tile_run,
+                                  const int32_t* tile_cut, int64_t n_tiles, int32_t max_tile_rows,
+                                  const hmf_qband_opts* opts, double lr, double reg_user,
+                                  double reg_item, uint64_t seed, int64_t row_base,
+                                  int64_t col_base, void* stream);
+int64_t hmf_sgd_block_runs_u8_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                                  const uint8_t* rows, const float* vals, const int32_t* runs,
+                                  const int32_t* tile_run, const int32_t* tile_cut,
+                                  int64_t n_tiles, int32_t max_tile_rows,
+                                  const hmf_qband_opts* opts, double lr, double reg_user,
+                                  double reg_item, uint64_t seed, int64_t row_base,
+                                  int64_t col_base, void* stream);
 
 /*
  * The reference visit order of a range of n triples under `seed`

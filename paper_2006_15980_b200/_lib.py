@@ -82,6 +82,10 @@ SIGNATURES = {
                                           _f64, _f64, _f64, _u64, _i64, _i64, _p]),
     "hmf_sgd_block_runs_u16_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p,
                                           _f64, _f64, _f64, _u64, _i64, _i64, _p]),
+    "hmf_sgd_block_runs_u8_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p,
+                                         _f64, _f64, _f64, _u64, _i64, _i64, _p]),
+    "hmf_sgd_block_runs_u8_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p,
+                                         _f64, _f64, _f64, _u64, _i64, _i64, _p]),
     "hmf_visit_order": (C.c_int, [_i64, _u64, _p, _p]),
     "hmf_mix64": (_u64, [C.POINTER(_u64), _i32]),
     "hmf_residual_sums_f32": (C.c_int, [_p, _p, _i64, _p, _p, _p, _i64, _i64, _i64, _i32, _p, _p]),

@@ -502,6 +502,8 @@ static int64_t run_runs(S* P, S* Q, int64_t k, const RowT* rows, const float* va
     return set_error(HMF_ERR_ARG, "a tile's P rows must fit hmf_ptile_max_rows(k, f16)");
   if (sizeof(RowT) == 2 && max_rows > 65536)
     return set_error(HMF_ERR_ARG, "uint16 row ids need tiles of at most 65536 rows");
+  if (sizeof(RowT) == 1 && max_rows > 256)
+    return set_error(HMF_ERR_ARG, "uint8 row ids need tiles of at most 256 rows");
   cudaError_t e;
   switch (k) {
 #define HMF_RN_CASE(KK)                                                                      \
@@ -700,6 +702,31 @@ int64_t hmf_sgd_block_runs_u16_f16(uint16_t* user_f, uint16_t* item_f, int64_t k
                                    double reg_item, uint64_t seed, int64_t row_base,
                                    int64_t col_base, void* stream) {
   return hmf::qs::run_runs<__half, uint16_t>(
+      reinterpret_cast<__half*>(user_f), reinterpret_cast<__half*>(item_f), k, rows, vals, runs,
+      tile_run, tile_cut, n_tiles, max_tile_rows, opts, lr, reg_user, reg_item, seed, row_base,
+      col_base, static_cast<cudaStream_t>(stream));
+}
+
+int64_t hmf_sgd_block_runs_u8_f32(float* user_f, float* item_f, int64_t k, const uint8_t* rows,
+                                  const float* vals, const int32_t* runs, const int32_t* tile_run,
+                                  const int32_t* tile_cut, int64_t n_tiles, int32_t max_tile_rows,
+                                  const hmf_qband_opts* opts, double lr, double reg_user,
+                                  double reg_item, uint64_t seed, int64_t row_base,
+                                  int64_t col_base, void* stream) {
+  return hmf::qs::run_runs<float, uint8_t>(user_f, item_f, k, rows, vals, runs, tile_run,
+                                           tile_cut, n_tiles, max_tile_rows, opts, lr, reg_user,
+                                           reg_item, seed, row_base, col_base,
+                                           static_cast<cudaStream_t>(stream));
+}
+
+int64_t hmf_sgd_block_runs_u8_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
+                                  const uint8_t* rows, const float* vals, const int32_t* runs,
+                                  const int32_t* tile_run, const int32_t* tile_cut,
+                                  int64_t n_tiles, int32_t max_tile_rows,
+                                  const hmf_qband_opts* opts, double lr, double reg_user,
+                                  double reg_item, uint64_t seed, int64_t row_base,
+                                  int64_t col_base, void* stream) {
+  return hmf::qs::run_runs<__half, uint8_t>(
       reinterpret_cast<__half*>(user_f), reinterpret_cast<__half*>(item_f), k, rows, vals, runs,
       tile_run, tile_cut, n_tiles, max_tile_rows, opts, lr, reg_user, reg_item, seed, row_base,
       col_base, static_cast<cudaStream_t>(stream));

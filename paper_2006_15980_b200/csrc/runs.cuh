@@ -47,9 +47,9 @@ template <int K> struct RunsCfg {
 };
 
 // rows: int32 user ids (absolute, minus the tile's first row in the kernel)
-// or uint16 ids relative to the tile (the streamed form)
+// or uint16 / uint8 ids relative to the tile (the streamed forms)
 template <typename RowT> __device__ inline int tile_row(RowT v, int r0) {
-  if constexpr (sizeof(RowT) == 2) {
+  if constexpr (sizeof(RowT) <= 2) {
     return int(v);
   } else {
     return int(v) - r0;

@@ -529,6 +529,8 @@ class StreamingEpoch:
             bool(torch.all(c[1:] - c[:-1] <= 1)) for c in sg.sub_cuts))
         self.u16 = self.implicit_items and all(
             int(np.max(np.diff(r))) <= 65536 for r in sg.sub_tile_rows)
+        # run groups over tiles of at most 256 rows: one byte per user id
+        self.u8 = self.runs and int(sg.sub_max_rows) <= 256
         # chunks: G consecutive row tiles of a block -> [lo, hi) of the
         # bucketed arrays, the number of tiles, their sub-band offsets relative
         # to lo, their first rows (device int32, uint16 ids only)
@@ -537,7 +539,8 @@ class StreamingEpoch:
         self.blocks = []
         users = sg.users
         if self.u16:
-            users = torch.empty(sg.nnz, dtype=torch.int16, device=self.dev)
+            users = torch.empty(sg.nnz, dtype=torch.uint8 if self.u8 else torch.int16,
+                                device=self.dev)
         if self.runs:
             self._init_runs(sg, users, runs_chunks_per_block)
         for b in range(0 if self.runs else sg.n_blocks):
@@ -597,7 +600,7 @@ class StreamingEpoch:
                 tile_of = torch.bucketize(sg.users[blo:bhi], d_tiles[1:-1].to(torch.int32),
                                           right=True)
                 users[blo:bhi] = (sg.users[blo:bhi] - d_tiles[tile_of]).to(torch.int32).to(
-                    torch.int16)
+                    users.dtype)
             per = -(-T // max(1, int(chunks_per_block)))
             cuts = list(range(0, T, per)) + [T]
             chunks = []
@@ -611,19 +614,22 @@ class StreamingEpoch:
         sg = self.sg
         lo, hi, n_tiles, off, t0 = chunk
         st = "f16" if P.dtype == _torch().float16 else "f32"
-        fn = getattr(_lib.load(), f"hmf_sgd_block_runs_u16_{st}")
+        idb = 1 if self.u8 else 2           # bytes per user id
+        fn = getattr(_lib.load(), f"hmf_sgd_block_runs_u{8 * idb}_{st}")
         # run descriptors count from the block's first rating; the staging
         # buffer starts at the chunk's
-        _lib.check(fn(P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr() - 2 * off,
+        _lib.check(fn(P.data_ptr(), Q.data_ptr(), self.k, buf[0].data_ptr() - idb * off,
                       buf[-1].data_ptr() - 4 * off, sg.sub_ptr[b].data_ptr(),
                       sg.sub_tile_run[b].data_ptr() + 4 * t0,
                       sg.sub_tile_cuts[b].data_ptr() + 4 * t0, n_tiles, int(sg.sub_max_rows),
                       ctypes.byref(self.opts), hparams.learning_rate, hparams.reg_user,
                       hparams.reg_item, tseed, 0, 0, stream.cuda_stream),
-                   "hmf_sgd_block_runs_u16")
+                   "hmf_sgd_block_runs_u8/u16")
 
     @property
     def bytes_per_rating(self) -> int:
+        if self.u8:
+            return 5
         return 6 if self.u16 else (8 if self.implicit_items else 12)
 
     @property

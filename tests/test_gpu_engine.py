@@ -297,12 +297,14 @@ def test_concurrent_layouts_equal_serial(dev):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
-@pytest.mark.parametrize("k,chunks", [(128, 2), (32, 3), (256, 1)])
-def test_streaming_epoch_runs_equals_resident_launches(dev, k, chunks):
+@pytest.mark.parametrize("k,chunks,max_rows", [(128, 2, None), (32, 3, None), (256, 1, None),
+                                              (128, 2, 256)])
+def test_streaming_epoch_runs_equals_resident_launches(dev, k, chunks, max_rows):
     """StreamingEpoch over an implementation-8 layout (run groups): 6 bytes
     per rating from pinned host memory (uint16 tile-relative users + the
-    rating; items from the resident run descriptors), whole fractions of a
-    block per launch.  On triples whose runs never race or go stale it
+    rating; items from the resident run descriptors) — 5 when the tiles hold
+    at most 256 users (one-byte ids: k=256, or tiles capped at 256) — whole
+    fractions of a block per launch.  On triples whose runs never race or go stale it
     equals the resident launches of the same layout under the same seeds —
     and the first upload replaced poisoned device copies."""
     from paper_2006_15980_b200 import kernels
@@ -314,7 +316,7 @@ def test_streaming_epoch_runs_equals_resident_launches(dev, k, chunks):
     rng = np.random.default_rng(k)
     n_users, n_items = 90_000, 9_000
     n_sm = torch.cuda.get_device_properties(d).multi_processor_count
-    tiles = ptile_row_cuts(0, n_users, k, False, n_sm)
+    tiles = ptile_row_cuts(0, n_users, k, False, n_sm, max_rows)
     T = len(tiles) - 1
     free = [list(rng.permutation(np.arange(tiles[t], tiles[t + 1]))) for t in range(T)]
     users, items = [], []
@@ -327,9 +329,11 @@ def test_streaming_epoch_runs_equals_resident_launches(dev, k, chunks):
     vals = rng.uniform(0, 1, len(users)).astype(np.float32).astype(np.float64)
     m = RatingMatrix(n_users, n_items, users, items, vals)
     g = build_device_grid(DeviceTriples.from_host(m, d), [0, n_users], [0, 4_000, n_items])
-    bucket_qbands(g, k, impl=8)
+    bucket_qbands(g, k, impl=8, max_tile_rows=max_rows)
     se = StreamingEpoch(g, k, runs_chunks_per_block=chunks)
-    assert se.runs and se.u16 and se.implicit_items and se.h2d_bytes == 6 * len(users)
+    one_byte = int(g.sub_max_rows) <= 256
+    assert se.runs and se.u16 and se.implicit_items and se.u8 == one_byte
+    assert se.h2d_bytes == (5 if one_byte else 6) * len(users)
     assert se.n_chunks == sum(len(range(0, t, -(-t // chunks))) for t in g.sub_tiles)
     P0 = rng.uniform(0, 0.1, size=(n_users, k)).astype(np.float32)
     Q0 = rng.uniform(0, 0.1, size=(n_items, k)).astype(np.float32)
