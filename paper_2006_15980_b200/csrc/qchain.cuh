@@ -309,7 +309,6 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
     const bool act = !done && !pend && x < nb;  // chain-uniform
     const int32_t u = __shfl_sync(FULL, cu, j, LPC);
     const int32_t v = __shfl_sync(FULL, cv, j, LPC);
-    const float r = __shfl_sync(FULL, cr, j, LPC);
     const bool ahead_in = j + PD < cnt;
     const int32_t un =
         __shfl_sync(FULL, ahead_in ? cu : nu, ahead_in ? j + PD : j + PD - cnt, LPC);
@@ -329,11 +328,13 @@ __global__ void __launch_bounds__(WPB * 32, MINB)
       if (e + 2 < E) d2 = fmaf(pc[e + 2], q[e + 2], d2);
       if (e + 3 < E) d3 = fmaf(pc[e + 3], q[e + 3], d3);
     }
-    float d = (d0 + d1) + (d2 + d3);
+    // the rating joins the reduction (lane j of the chain holds it) instead
+    // of a broadcast shuffle: the chain's sum is p.q - r
+    float d = (d0 + d1) + (d2 + d3) - (l == j ? cr : 0.f);
 #pragma unroll
     for (int o = LPC / 2; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
     if (act) {
-      const float a = lr * (r - d);
+      const float a = -lr * d;  // lr * (r - p.q)
       if constexpr (PST) {
         // the new row stored over the old, as the reference's racing lanes
         // write it (workers.py:222-266): no read-modify-write at L2; a
