@@ -13,8 +13,12 @@
  *   hmf_sgd_block_qband_{f32,f16} BatchEngine.compute on a staged item band
  *   hmf_sgd_block_qband_u16_*     (the same, uint16 tile-relative row ids)
  *   hmf_sgd_block_qband_u16_tiles_*  (the same over several row tiles)
- *   hmf_sgd_block_ptile_*, hmf_sgd_block_runs_*  (the same, P tile in shared memory)
+ *   hmf_sgd_block_ptile_*, hmf_sgd_block_runs_{,u16_,u8_}*
+ *                                 (the same, P tile in shared memory)
  *                                                              workers.py:186-255
+ *   hmf_lease_*                   GridScheduler.acquire / release / abort for
+ *                                 column units across GPU processes
+ *                                                              scheduler.py:333-423
  *   hmf_qband_resolve_*, _slots_per_sm, _chain_lanes, _max_items
  *                                 (layout queries; no reference counterpart)
  *   hmf_visit_order               sgd_range's visit order      kernels.py:77-119
