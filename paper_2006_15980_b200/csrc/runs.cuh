@@ -41,6 +41,10 @@
 namespace hmf {
 namespace qs {
 
+#ifndef RUNS_SMEM_REDUCE
+#define RUNS_SMEM_REDUCE 1
+#endif
+
 template <int K> struct RunsCfg {
   static constexpr int LPC = K >= 256 ? 16 : (K >= 64 ? 8 : 4);
   static constexpr int WPB = 16;
@@ -121,7 +125,12 @@ __global__ void __launch_bounds__(WPB * 32, 1)
   extern __shared__ __align__(16) unsigned char runs_smem[];
   S* tile = reinterpret_cast<S*>(runs_smem);
   __shared__ unsigned next_group;
+  // per-warp scratch for the dot-product reduction (kSmemReduce)
+  // (measured: +2-4 % for fp32 at k = 32-128; slower at k = 256 and for fp16)
+  constexpr bool kSmemReduce = RUNS_SMEM_REDUCE && LPC >= 4 && LPC <= 8 && sizeof(S) == 4;
+  __shared__ __align__(16) float red_all[kSmemReduce ? WPB * 32 : 4];
   const int lane = threadIdx.x & 31, c = lane / LPC, l = lane % LPC;
+  float* red = red_all + (kSmemReduce ? (threadIdx.x >> 5) * 32 : 0);
   const float keep_p = 1.f - lr * ru, keep_q = 1.f - lr * ri;
   const float inv_keep_q = 1.f / keep_q;
   const float2 neg1 = make_float2(-1.f, -1.f);
@@ -252,8 +261,29 @@ __global__ void __launch_bounds__(WPB * 32, 1)
           // the rating joins the reduction instead of being broadcast: lane jj
           // of the chain holds it, so the chain's sum is p.q - r (q = sq qs)
           float d = fmaf(sq, ds.x + ds.y, l == jj ? -cr : 0.f);
+          if constexpr (kSmemReduce) {
+            // the chain's LPC partials through shared memory: one 128-byte
+            // store for the warp and LPC/4 16-byte broadcast loads per lane
+            // (3 wavefronts at LPC = 8, against 3 shuffles of ~1.5); every
+            // lane sums them in the same order
+            __syncwarp();
+            red[lane] = d;
+            __syncwarp();
+            const float4* src = reinterpret_cast<const float4*>(red + c * LPC);
+            float4 s = src[0];
 #pragma unroll
-          for (int o = LPC / 2; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
+            for (int i = 1; i < LPC / 4; ++i) {
+              const float4 t = src[i];
+              s.x += t.x;
+              s.y += t.y;
+              s.z += t.z;
+              s.w += t.w;
+            }
+            d = (s.x + s.y) + (s.z + s.w);
+          } else {
+#pragma unroll
+            for (int o = LPC / 2; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
+          }
           if (act) {
             const float a = -lr * d;  // lr * (r - p.q)
             const float as = a * sq;
