@@ -751,7 +751,7 @@ def run_ours_multi(args, world, rank, local):
     if rank == 0:
         table.initialize()
     dist.barrier()
-    trainer = RowBandTrainer(band, table, rank, seed=SEED)
+    trainer = RowBandTrainer(band, table, rank, seed=SEED, policy=args.policy, world=world)
     for _ in range(args.warmup):
         trainer.run_epoch()
         dist.barrier()
@@ -848,7 +848,7 @@ def run_ours_multi(args, world, rank, local):
                        "blocks_in_flight": band.concurrency},
             "rmse": {"epochs": args.warmup + args.steps, "test": test_rmse},
             "lease_wait_seconds_rank0": trainer.wait_seconds,
-            "leases": lease_stats,
+            "leases": lease_stats, "policy": args.policy,
             "setup_seconds": setup_s,
             "gpu_launches": launches, "clocks": clocks.summary(), "e2e": e2e,
         }), flush=True)
@@ -1015,6 +1015,11 @@ def main():
     ap.add_argument("--lease", choices=["shm", "store"], default="shm",
                     help="N>1: column-lease table: node-local shared memory (csrc/lease.cu) "
                          "or the torch.distributed store")
+    ap.add_argument("--policy", choices=["free", "quota"], default="free",
+                    help="N>1 lease policy: free = any free column band, an epoch being "
+                         "N x bands block updates claimed job-wide (the reference's POLICY_FREE, "
+                         "scheduler.py:411-429); quota = each GPU trains each of its blocks once "
+                         "per epoch")
     ap.add_argument("--multi-concurrency", type=int, default=1,
                     help="N>1: column blocks in flight per GPU (each on its own stream)")
     ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 4, 5, 6, 7, 8], default=-1,

@@ -444,6 +444,11 @@ int hmf_lease_owner(void* table, int32_t c, int32_t* owner);
 int hmf_lease_holder(void* table, int32_t c, int32_t* holder);
 int64_t hmf_lease_ticket(void* table);
 int64_t hmf_lease_ops(void* table);
+/* The free policy's job-wide work counter (scheduler.py:411-429, POLICY_FREE:
+ * an epoch is n_blocks block updates, taken by whoever is free): claims the
+ * next block update if fewer than `target` were claimed — returns its ordinal
+ * (1, 2, ...) — else 0; HMF_ERR_ABORTED once the run is aborted. */
+int64_t hmf_lease_claim(void* table, int64_t target);
 int hmf_lease_abort(void* table, int32_t rank);
 int32_t hmf_lease_aborted(void* table);
 

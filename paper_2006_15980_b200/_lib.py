@@ -114,6 +114,7 @@ SIGNATURES = {
     "hmf_lease_holder": (C.c_int, [_p, _i32, C.POINTER(_i32)]),
     "hmf_lease_ticket": (_i64, [_p]),
     "hmf_lease_ops": (_i64, [_p]),
+    "hmf_lease_claim": (_i64, [_p, _i64]),
     "hmf_lease_abort": (C.c_int, [_p, _i32]),
     "hmf_lease_aborted": (_i32, [_p]),
 }

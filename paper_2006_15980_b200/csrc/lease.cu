@@ -45,6 +45,8 @@ struct alignas(64) Header {
   // 0, or 1 + the rank that aborted the run (scheduler.abort,
   // scheduler.py:415-423 / workers.py:300-302): acquires fail from then on
   alignas(64) std::atomic<int32_t> aborted;
+  // block updates claimed so far (the free policy's job-wide epoch counter)
+  alignas(64) std::atomic<int64_t> work;
 };
 
 static_assert(std::atomic<int32_t>::is_always_lock_free, "address-free atomics needed");
@@ -131,6 +133,7 @@ int hmf_lease_open(const char* name, int32_t n_cols, int32_t create, void** out)
     t->h->seq.store(0, std::memory_order_relaxed);
     t->h->ops.store(0, std::memory_order_relaxed);
     t->h->aborted.store(0, std::memory_order_relaxed);
+    t->h->work.store(0, std::memory_order_relaxed);
     for (int32_t c = 0; c < n_cols; ++c) {
       t->slots[c].holder.store(-1, std::memory_order_relaxed);
       t->slots[c].owner.store(-1, std::memory_order_relaxed);
@@ -239,6 +242,21 @@ int64_t hmf_lease_ticket(void* table) {
   if (!t) return hmf::set_error(HMF_ERR_ARG, "null lease table");
   t->h->ops.fetch_add(1, std::memory_order_relaxed);
   return t->h->seq.fetch_add(1, std::memory_order_acq_rel) + 1;
+}
+
+int64_t hmf_lease_claim(void* table, int64_t target) {
+  using namespace hmf::lease;
+  Table* t = static_cast<Table*>(table);
+  if (!t) return hmf::set_error(HMF_ERR_ARG, "null lease table");
+  if (aborted_error(t)) return HMF_ERR_ABORTED;
+  t->h->ops.fetch_add(1, std::memory_order_relaxed);
+  int64_t old = t->h->work.load(std::memory_order_acquire);
+  while (old < target) {
+    if (t->h->work.compare_exchange_weak(old, old + 1, std::memory_order_acq_rel,
+                                         std::memory_order_acquire))
+      return old + 1;
+  }
+  return 0;
 }
 
 int hmf_lease_abort(void* table, int32_t rank) {

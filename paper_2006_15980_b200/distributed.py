@@ -105,6 +105,20 @@ class LeaseTable:
         """Mark the run aborted by this rank (a store key every acquire checks)."""
         self.store.compare_set(f"{self.prefix}/aborted", b"", str(self.rank).encode())
 
+    def claim(self, target: int) -> int:
+        """The free policy's job-wide block count: the ordinal of the claimed
+        block update, or 0 once `target` are claimed (an over-claim is given
+        back, so the count stops at the target)."""
+        t0 = time.perf_counter()
+        n = int(self.store.add(f"{self.prefix}/work", 1))
+        self.ops += 1
+        if n > target:
+            self.store.add(f"{self.prefix}/work", -1)
+            self.ops += 1
+            n = 0
+        self.seconds += time.perf_counter() - t0
+        return n
+
     def aborted_by(self) -> int:
         if not self.store.check([f"{self.prefix}/aborted"]):
             return -1
@@ -226,6 +240,16 @@ class ShmLeaseTable:
         t = self._table()
         return int(self._lib.hmf_lease_aborted(t))
 
+    def claim(self, target: int) -> int:
+        """The free policy's job-wide block count (hmf_lease_claim): the
+        ordinal of the claimed block update, or 0 once `target` are claimed."""
+        t = self._table()
+        t0 = time.perf_counter()
+        n = self._lib.hmf_lease_claim(t, int(target))
+        self.ops += 1
+        self.seconds += time.perf_counter() - t0
+        return int(self._check(n, "hmf_lease_claim"))
+
     def _check(self, rc: int, what: str) -> int:
         from . import _lib
         if rc == _lib.HMF_ERR_ABORTED:
@@ -272,7 +296,8 @@ class RowBandTrainer:
     """
 
     def __init__(self, backend, table: LeaseTable, rank: int, seed: int = 0,
-                 prefetch: bool = True, record: bool = False):
+                 prefetch: bool = True, record: bool = False, policy: str = "quota",
+                 world: int = 1):
         self.backend = backend
         self.table = table
         self.rank = rank
@@ -285,6 +310,16 @@ class RowBandTrainer:
         self.log = []            # (ticket, column, seed) per granted block
         self.total_updates = 0
         self.wait_seconds = 0.0
+        # the reference's scheduling policies (scheduler.py:41-43, 255-304,
+        # 411-429): "quota" — every rank trains each of its blocks once per
+        # epoch (batch-only, stream-only); "free" — any free column, least
+        # updated first, an epoch being world x n_cols block updates claimed
+        # job-wide by whoever is free (the hsgd schedule's POLICY_FREE)
+        if policy not in ("quota", "free"):
+            raise ValueError(f"policy must be 'quota' or 'free', not {policy!r}")
+        self.policy = policy
+        self.world = max(1, int(world))
+        self.epochs_done = 0
 
     def _candidates(self, todo: set) -> list:
         cols = sorted(todo)
@@ -349,6 +384,50 @@ class RowBandTrainer:
                 raise
 
     def _run_epoch(self) -> None:
+        if self.policy == "free":
+            self._run_epoch_free()
+        else:
+            self._run_epoch_quota()
+        self.epochs_done += 1
+
+    def _run_epoch_free(self) -> None:
+        """POLICY_FREE: lease any column this rank does not hold, least
+        updated first; a block runs only if it claims one of the epoch's
+        world x n_cols job-wide block updates (hmf_lease_claim), so ranks that
+        are free keep working until the epoch's quota is spent, with no rank
+        waiting on a particular column at the epoch's end."""
+        target = (self.epochs_done + 1) * self.world * self.n_cols
+        everything = set(range(self.n_cols))
+        pending = False          # an update claimed but not yet bound to a column
+
+        def take(held, blocking):
+            # claim first, lease second: a lease taken and handed back unused
+            # would publish this rank as the band's owner without its update
+            nonlocal pending
+            if not pending:
+                if self.table.claim(target) <= 0:     # the epoch's updates are spent
+                    return None, True
+                pending = True
+            c = self._grab(everything - held, blocking)
+            if c is None:        # keep the claim for the blocking grab after finish
+                return None, False
+            pending = False
+            self._start(c)
+            return c, False
+
+        cur, spent = take(set(), True)
+        while cur is not None:
+            nxt = None
+            if self.prefetch and not spent:
+                nxt, spent = take({cur}, False)
+            self.backend.finish(cur)
+            self.table.release(cur)
+            self.counts[cur] += 1
+            if nxt is None and not spent:
+                nxt, spent = take(set(), True)
+            cur = nxt
+
+    def _run_epoch_quota(self) -> None:
         todo = set(range(self.n_cols))
         cur = self._grab(todo, blocking=True)
         todo.discard(cur)

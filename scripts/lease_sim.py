@@ -43,6 +43,7 @@ class SimBand:
         self.busy_until = time.perf_counter()
         self.ends = {}
         self.pulls = 0
+        self.busy = 0.0                         # device seconds of block compute
 
     def pull(self, c, owner):
         if owner >= 0:
@@ -52,6 +53,7 @@ class SimBand:
     def compute(self, c, seed):
         start = max(self.busy_until, time.perf_counter())
         self.busy_until = start + self.block_seconds[c]
+        self.busy += self.block_seconds[c]
         self.ends[c] = self.busy_until
         return 1
 
@@ -64,7 +66,7 @@ class SimBand:
             time.sleep(min(left, 2e-4) if left > 3e-4 else 0)
 
 
-def rank_main(rank, world, run_id, n_cols, block_seconds, pull_seconds, epochs, out):
+def rank_main(rank, world, run_id, n_cols, block_seconds, pull_seconds, epochs, out, policy, barrier):
     from paper_2006_15980_b200.distributed import RowBandTrainer, ShmLeaseTable
     table = ShmLeaseTable(n_cols, rank, run_id)
     while True:                     # rank 0 of the parent created the segment
@@ -74,7 +76,9 @@ def rank_main(rank, world, run_id, n_cols, block_seconds, pull_seconds, epochs, 
         except Exception:
             time.sleep(0.01)
     band = SimBand(n_cols, block_seconds, pull_seconds)
-    trainer = RowBandTrainer(band, table, rank, seed=rank)
+    trainer = RowBandTrainer(band, table, rank, seed=rank, policy=policy, world=world)
+    barrier.wait()                  # every rank starts together
+    band.busy_until = time.perf_counter()
     t0 = time.perf_counter()
     per_epoch = []
     for _ in range(epochs):
@@ -84,7 +88,8 @@ def rank_main(rank, world, run_id, n_cols, block_seconds, pull_seconds, epochs, 
     st = trainer.lease_stats()
     with open(f"{out}.{rank}", "w") as fh:
         json.dump({"rank": rank, "epoch_seconds": per_epoch, "total": time.perf_counter() - t0,
-                   "pulls": band.pulls, "lease": st}, fh)
+                   "pulls": band.pulls, "busy": band.busy, "blocks": int(trainer.counts.sum()),
+                   "lease": st}, fh)
     table.close()
 
 
@@ -97,6 +102,10 @@ def main():
     ap.add_argument("--rate", type=float, default=14.1e9, help="per-GPU updates/s (sim-world)")
     ap.add_argument("--q-band-mb", type=float, default=9.0 / 17, help="Q band size per column")
     ap.add_argument("--nvlink-gbs", type=float, default=700.0)
+    ap.add_argument("--policy", choices=["quota", "free"], default="quota",
+                    help="RowBandTrainer policy (the reference's batch-only quota or hsgd free)")
+    ap.add_argument("--slow", type=float, default=1.0,
+                    help="rank N-1 runs at rate / slow (a heterogeneous or throttled GPU)")
     ap.add_argument("--scale", type=float, default=20.0,
                     help="time dilation: block durations x scale, so host jitter is small")
     args = ap.parse_args()
@@ -113,8 +122,12 @@ def main():
     owner.initialize()
     out = f"/tmp/lease_sim_{run}"
     ctx = mp.get_context("spawn")
-    procs = [ctx.Process(target=rank_main, args=(r, n, run, n_cols, block_seconds, pull_seconds,
-                                                 args.epochs, out)) for r in range(n)]
+    barrier = ctx.Barrier(n)
+    def blocks_of(r):
+        return [b * (args.slow if r == n - 1 else 1.0) for b in block_seconds]
+    procs = [ctx.Process(target=rank_main, args=(r, n, run, n_cols, blocks_of(r), pull_seconds,
+                                                 args.epochs, out, args.policy, barrier))
+             for r in range(n)]
     for p in procs:
         p.start()
     for p in procs:
@@ -125,7 +138,17 @@ def main():
     # epochs end at different times per rank; the job's epoch is the slowest rank's
     epoch = [max(r["epoch_seconds"][e] for r in res) for e in range(args.epochs)]
     steady = float(np.median(epoch[1:])) if len(epoch) > 1 else epoch[0]
-    line = {"gpus": n, "column_bands": n_cols, "epochs": args.epochs,
+    # device utilisation over the whole run: block compute seconds of all
+    # ranks over N x the slowest rank's wall time (the free policy's epochs
+    # end at different times per rank, so per-epoch times do not compare)
+    wall = max(r["total"] for r in res)
+    util = sum(r["busy"] for r in res) / (n * wall)
+    # block updates per second against every rank running its blocks back to back
+    ideal_rate = sum(n_cols / sum(blocks_of(r)) for r in range(n))
+    thru = sum(r["blocks"] for r in res) / wall / ideal_rate
+    line = {"gpus": n, "column_bands": n_cols, "epochs": args.epochs, "policy": args.policy,
+            "slow": args.slow, "device_utilisation": util, "throughput_efficiency": thru,
+            "blocks_per_rank": [r["blocks"] for r in res],
             "ideal_epoch_s": ideal / args.scale, "median_epoch_s": steady / args.scale,
             "protocol_efficiency": ideal / steady,
             "lease_us_per_lease_max": max(r["lease"]["us_per_lease"] for r in res),

@@ -34,7 +34,7 @@ def problem(conflict_free=False):
     return users, items, vals, P0, Q0
 
 
-def main(out_dir, kernel="exact", stage=False):
+def main(out_dir, kernel="exact", stage=False, policy="quota"):
     impl = None
     if kernel == "qband8":        # the tile-resident run-group layout, forced
         kernel, impl = "qband", 8
@@ -79,7 +79,8 @@ def main(out_dir, kernel="exact", stage=False):
         if rank == 0:
             with open(os.path.join(out_dir, "staged.txt"), "w") as fh:
                 fh.write("compact" if band.compact is not None else "triples")
-    trainer = RowBandTrainer(band, table, rank, seed=SEED, record=True)
+    trainer = RowBandTrainer(band, table, rank, seed=SEED, record=True, policy=policy,
+                             world=world)
     for _ in range(EPOCHS):
         trainer.run_epoch()
         dist.barrier()
@@ -96,5 +97,5 @@ def main(out_dir, kernel="exact", stage=False):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "exact",
-         len(sys.argv) > 3 and sys.argv[3] == "stage")
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "exact", "stage" in sys.argv[3:],
+         "free" if "free" in sys.argv[3:] else "quota")

@@ -84,7 +84,7 @@ class CpuBand:
         pass
 
 
-def _worker(rank, world, port, tmp, kind="store"):
+def _worker(rank, world, port, tmp, kind="store", policy="quota"):
     import torch.distributed as dist
     from paper_2006_15980_b200.distributed import RowBandTrainer, make_lease_table
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -99,7 +99,8 @@ def _worker(rank, world, port, tmp, kind="store"):
     if rank == 0:
         table.initialize()
     dist.barrier()
-    trainer = RowBandTrainer(band, table, rank, seed=SEED, record=True)
+    trainer = RowBandTrainer(band, table, rank, seed=SEED, record=True, policy=policy,
+                             world=world)
     for _ in range(EPOCHS):
         trainer.run_epoch()
         dist.barrier()
@@ -119,8 +120,9 @@ def _worker(rank, world, port, tmp, kind="store"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["store", "shm"])
-def test_two_rank_lease_protocol_equals_serial_replay(tmp_path, kind):
+@pytest.mark.parametrize("kind,policy", [("store", "quota"), ("shm", "quota"),
+                                         ("store", "free"), ("shm", "free")])
+def test_two_rank_lease_protocol_equals_serial_replay(tmp_path, kind, policy):
     import pickle
 
     import oracle
@@ -131,16 +133,25 @@ def test_two_rank_lease_protocol_equals_serial_replay(tmp_path, kind):
         mm = np.memmap(tmp_path / f"q{r}.bin", dtype=np.float64, mode="w+", shape=(N_ITEMS, K))
         mm[:] = Q0
         mm.flush()
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), kind), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), kind, policy), nprocs=2, join=True)
     logs = pickle.loads((tmp_path / "logs.pkl").read_bytes())
     row_cuts = np.array([0, 41, N_USERS])
     col_cuts = np.array([0, 14, 28, 42, 56, N_ITEMS])
-    # every rank did every block of its band once per epoch
-    for rank, (log, Pb, pulls, updates, counts) in enumerate(logs):
-        assert counts == [EPOCHS] * 5
-        assert len(log) == EPOCHS * 5
+    if policy == "quota":
+        # every rank did every block of its band once per epoch
+        for rank, (log, Pb, pulls, updates, counts) in enumerate(logs):
+            assert counts == [EPOCHS] * 5
+            assert len(log) == EPOCHS * 5
+        assert sum(x[3] for x in logs) == EPOCHS * NNZ
+    else:
+        # POLICY_FREE: the job did world x n_cols block updates per epoch, by
+        # whoever was free; a rank spreads its own updates over its columns
+        # (least updated first)
+        assert sum(sum(x[4]) for x in logs) == EPOCHS * 2 * 5
+        for rank, (log, Pb, pulls, updates, counts) in enumerate(logs):
+            assert len(log) == sum(counts)
+            assert max(counts) - min(counts) <= 1 + max(counts) // 2
     assert sum(x[2] for x in logs) > 0, "no Q band ever moved between ranks"
-    assert sum(x[3] for x in logs) == EPOCHS * NNZ
     # serial replay in global lease order
     events = sorted((t, rank, c, s) for rank, (log, *_rest) in enumerate(logs) for t, c, s in log)
     m = RatingMatrix(N_USERS, N_ITEMS, users, items, vals)

@@ -26,7 +26,8 @@ def _port():
     return p
 
 
-def test_two_ranks_ipc_lease_protocol_equals_serial_replay(tmp_path):
+@pytest.mark.parametrize("policy", ["quota", "free"])
+def test_two_ranks_ipc_lease_protocol_equals_serial_replay(tmp_path, policy):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import oracle
@@ -35,13 +36,16 @@ def test_two_ranks_ipc_lease_protocol_equals_serial_replay(tmp_path):
     from paper_2006_15980_b200.data import RatingMatrix, build_grid
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_port()}",
-           str(ROOT / "tests" / "dist_gpu_worker.py"), str(tmp_path)]
+           str(ROOT / "tests" / "dist_gpu_worker.py"), str(tmp_path), "exact", policy]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res, Q_final, row_cuts, col_cuts = pickle.loads((tmp_path / "result.pkl").read_bytes())
     n_cols = len(col_cuts) - 1
-    for log, Pb, counts in res:
-        assert counts == [W.EPOCHS] * n_cols
+    if policy == "quota":
+        for log, Pb, counts in res:
+            assert counts == [W.EPOCHS] * n_cols
+    else:      # POLICY_FREE: world x n_cols block updates per epoch, job-wide
+        assert sum(sum(c) for _l, _p, c in res) == W.EPOCHS * 2 * n_cols
     users, items, vals, P0, Q0 = W.problem()
     g = build_grid(RatingMatrix(W.N_USERS, W.N_ITEMS, users, items, vals), row_cuts, col_cuts)
     events = sorted((t, rank, c, s) for rank, (log, *_r) in enumerate(res) for t, c, s in log)

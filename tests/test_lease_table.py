@@ -65,6 +65,42 @@ def test_single_process_contract():
         a.close(unlink=True)
 
 
+def test_claim_counts_to_the_target():
+    """hmf_lease_claim, the free policy's job-wide update counter: ordinals
+    1..target across processes' tables, then 0 (never past the target); the
+    next epoch raises the target; an aborted run raises."""
+    from paper_2006_15980_b200.distributed import LeaseAborted
+    run = uuid.uuid4().hex[:10]
+    a = _table(3, 0, run)
+    a.initialize()
+    b = _table(3, 1, run)
+    try:
+        got = [a.claim(5), b.claim(5), a.claim(5), b.claim(5), a.claim(5)]
+        assert got == [1, 2, 3, 4, 5]
+        assert a.claim(5) == 0 and b.claim(5) == 0 and a.claim(5) == 0
+        assert b.claim(10) == 6
+        b.abort()
+        with pytest.raises(LeaseAborted, match="rank 1"):
+            a.claim(10)
+    finally:
+        b.close()
+        a.close(unlink=True)
+
+
+def test_store_claim_counts_to_the_target():
+    import datetime
+
+    import torch.distributed as dist
+    from paper_2006_15980_b200.distributed import LeaseTable
+    from test_distributed import _free_port
+    store = dist.TCPStore("127.0.0.1", _free_port(), 1, True,
+                          timeout=datetime.timedelta(seconds=30))
+    a, b = LeaseTable(store, 3, 0, "claim"), LeaseTable(store, 3, 1, "claim")
+    a.initialize()
+    assert [a.claim(3), b.claim(3), a.claim(3), b.claim(3), a.claim(3)] == [1, 2, 3, 0, 0]
+    assert b.claim(6) == 4                 # over-claims were given back
+
+
 def test_open_errors():
     from paper_2006_15980_b200 import _lib
     run = uuid.uuid4().hex[:10]
