@@ -264,7 +264,7 @@ int64_t hmf_sgd_block_ptile_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
  * of rows / vals (offsets relative to those pointers), all of item `item`
  * (absolute, minus col_base); tile t's runs are [tile_run[t],
  * tile_run[t+1]).  Device arrays; data.bucket_qbands with impl 8 builds them.  A persistent CTA per SM holds one tile's P rows in
- * shared memory; each warp takes groups of hmf_runs_chains_per_warp(k)
+ * shared memory; each warp takes groups of hmf_runs_chains_per_warp(k, f16)
  * consecutive runs, one per lane-group chain, the item's Q row in registers,
  * Q changes added back by vector reductions at the run's end.  rows: int32
  * user ids (minus row_base), or with the _u16 entry points uint16 ids
@@ -273,7 +273,7 @@ int64_t hmf_sgd_block_ptile_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
  * 8; grid_share applies.  Same update rule and return convention as
  * hmf_sgd_block_qband_*.
  */
-int32_t hmf_runs_chains_per_warp(int64_t k);
+int32_t hmf_runs_chains_per_warp(int64_t k, int32_t f16);
 int64_t hmf_sgd_block_runs_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
                                const float* vals, const int32_t* runs, const int32_t* tile_run,
                                const int32_t* tile_cut, int64_t n_tiles, int32_t max_tile_rows,

@@ -73,7 +73,7 @@ SIGNATURES = {
                                        _f64, _f64, _f64, _u64, _i64, _i64, _p]),
     "hmf_sgd_block_ptile_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _i64, _i64, _p, _i32, _p,
                                        _f64, _f64, _f64, _u64, _i64, _i64, _p]),
-    "hmf_runs_chains_per_warp": (_i32, [_i64]),
+    "hmf_runs_chains_per_warp": (_i32, [_i64, _i32]),
     "hmf_sgd_block_runs_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p, _f64,
                                       _f64, _f64, _u64, _i64, _i64, _p]),
     "hmf_sgd_block_runs_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p, _f64,

@@ -463,7 +463,7 @@ static cudaError_t launch_runs(S* P, S* Q, const RowT* rows, const float* vals,
                                int max_rows, double lr, double ru, double ri, uint64_t seed,
                                int64_t row_base, int64_t col_base, cudaStream_t stream,
                                const LaunchOpts& o) {
-  using C = RunsCfg<K>;
+  using C = RunsCfg<K, S>;
   auto kern = runs_kernel<K, S, C::LPC, C::WPB, RowT>;
   const int smem = max_rows * K * int(sizeof(S));
   int per_sm = 0;
@@ -534,7 +534,7 @@ static int slots_per_sm(int64_t k, const hmf_qband_opts* opts) {
   case KK:                                                                                 \
     e = o.impl == 0 ? warp_slots_per_sm<KK, S>(&n)                                         \
         : o.impl == 7 ? (n = PTileCfg<KK>::WPB * 32 / PTileCfg<KK>::LPC, cudaSuccess)         \
-        : o.impl == 8 ? (n = RunsCfg<KK>::WPB * 32 / RunsCfg<KK>::LPC, cudaSuccess)           \
+        : o.impl == 8 ? (n = RunsCfg<KK, S>::WPB * 32 / RunsCfg<KK, S>::LPC, cudaSuccess)         \
                       : chain_slots_per_sm<KK, S>(o.cfg, &n);                                \
     break;
     HMF_WPS(32)
@@ -647,14 +647,18 @@ int64_t hmf_sgd_block_ptile_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
                                     static_cast<cudaStream_t>(stream));
 }
 
-int32_t hmf_runs_chains_per_warp(int64_t k) {
+int32_t hmf_runs_chains_per_warp(int64_t k, int32_t f16) {
+  using hmf::qs::RunsCfg;
+#define HMF_RUNS_NC(KK) \
+  case KK: return 32 / (f16 ? RunsCfg<KK, __half>::LPC : RunsCfg<KK, float>::LPC);
   switch (k) {
-    case 32: return 32 / hmf::qs::RunsCfg<32>::LPC;
-    case 64: return 32 / hmf::qs::RunsCfg<64>::LPC;
-    case 128: return 32 / hmf::qs::RunsCfg<128>::LPC;
-    case 256: return 32 / hmf::qs::RunsCfg<256>::LPC;
+    HMF_RUNS_NC(32)
+    HMF_RUNS_NC(64)
+    HMF_RUNS_NC(128)
+    HMF_RUNS_NC(256)
     default: return 0;
   }
+#undef HMF_RUNS_NC
 }
 
 int64_t hmf_sgd_block_runs_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,

@@ -45,9 +45,31 @@ namespace qs {
 #define RUNS_SMEM_REDUCE 1
 #endif
 
-template <int K> struct RunsCfg {
-  static constexpr int LPC = K >= 256 ? 16 : (K >= 64 ? 8 : 4);
-  static constexpr int WPB = 16;
+// Lanes per chain (LPC) and warps per CTA, measured per (k, element size)
+// (profiles/round2/s4_k256_cfg.jsonl, s4_chain_cfg.jsonl, s4_ksweep.jsonl):
+// 16 elements per lane (k / 16 lanes) for k = 64-256 fp16 and k = 64-128
+// fp32 (fp16 k = 64 at 4 lanes: +37 % over 8; fp32 k = 64: +14 %); k = 32
+// at 4 lanes; fp32 k = 256 at 8 lanes (32 values per lane, ~190 registers)
+// in 8 warps: the reduction is one shared-memory round instead of four
+// shuffles, +5.6 % over 16 lanes.  More chains per SM than 128 is faster
+// still (k = 32: 2 lanes +12 % fp16, 20 warps +8 % fp32) but trains worse:
+// a run's Q change lands at its end, and more runs of one item in flight
+// across the CTAs' tiles make those changes staler.  On the narrow
+// 2 %-density blocks of test_default_layout_quality_matches_whole_runs
+// (fp32 k = 32) the RMSE after 8 epochs goes 0.1222 / 0.1232 / 0.138 / 0.33
+// at 16 / 17 / 18 / 20 warps (profiles/round2/s4_wpb_quality.txt).
+template <int K, typename S> struct RunsCfg {
+  static constexpr bool kWide = K >= 256 && sizeof(S) == 4;
+  static constexpr int kLPC = sizeof(S) == 2 ? (K <= 64 ? 4 : K / 16) : (K >= 128 ? 8 : 4);
+  static constexpr int kWPB = kWide ? 8 : 16;
+#ifdef RUNS_EXP_K  // A/B builds (scripts/build_variant.sh): one (k, element size) overridden
+  static constexpr bool kExp = K == RUNS_EXP_K && sizeof(S) == RUNS_EXP_S;
+  static constexpr int LPC = kExp ? RUNS_EXP_LPC : kLPC;
+  static constexpr int WPB = kExp ? RUNS_EXP_WPB : kWPB;
+#else
+  static constexpr int LPC = kLPC;
+  static constexpr int WPB = kWPB;
+#endif
 };
 
 // rows: int32 user ids (absolute, minus the tile's first row in the kernel)

@@ -475,6 +475,25 @@ def qband_impl_for(device, k: int, f16: bool, n_items: int) -> int:
 # profiles/round2/s3_layout_by_workload.jsonl — Netflix (4.8 at k = 128, 19
 # at k = 32) wins 1.3-1.8x; Hugewiki (0.65) and Yahoo-R1 (0.16) lose 10-35 %
 TILE_RESIDENT_MIN_RUN = 2.0
+# Staleness bound of implementation 8.  A run adds its Q change at its end,
+# so an item's runs training at the same time in different tiles all start
+# from the same Q row: on average chains_in_flight / items runs of L ratings,
+# S = chains_per_sm x CTAs x L / items ratings trained against one stale row.
+# Measured on narrow 2 %-density blocks (scripts/stale_margin.py, profiles/
+# round2/s4_stale_margin.jsonl): lr x S <= 2.5 trains within 0.0005 of whole
+# runs, lr x S ~ 5 loses 0.008-0.023 and 10 diverges.  Capped at 250: twice
+# the paper's learning rate (0.005) stays inside the measured-good range.
+# Netflix: S = 10.5 at N = 1, 89 per band at N = 8 (17 column bands).
+TILE_RESIDENT_MAX_STALE = 250.0
+
+
+def runs_chains_per_sm(k: int, f16: bool) -> int:
+    """Run-group chains resident per SM (implementation 8's configuration
+    for k and the element size, hmf_qband_slots_per_sm)."""
+    opts = _lib.QbandOpts(impl=8)
+    return int(_lib.check(_lib.load().hmf_qband_slots_per_sm(int(k), 1 if f16 else 0,
+                                                              ctypes.byref(opts)),
+                          "hmf_qband_slots_per_sm"))
 
 
 def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> int | None:
@@ -488,7 +507,9 @@ def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> 
       (tile, item) — each run costs a Q-row load and a Q-delta reduction;
     * no hot items (an item's ratings > 4x the block mean): one run per tile
       would then be long and train concurrently in every tile from the same
-      Q row; the item-split kernel (5) handles that case.
+      Q row; the item-split kernel (5) handles that case;
+    * Q staleness S <= TILE_RESIDENT_MAX_STALE (few items for the runs in
+      flight: narrow column blocks).
     Returns 8 (Netflix fp32 k = 32 / 64 / 128 / 256: 51.8 / 30.7 / 17.3 / 6.4
     G upd/s against 30.6 / 19.7 / 11.8 / 5.9 for implementation 5; fp16 75 /
     34 / 21.5 / 8.7 against 42 / 27 / 16.4 / 8.5; implementation 7 measured
@@ -499,6 +520,7 @@ def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> 
         return None
     dev = grid.device
     n_sm = int(torch.cuda.get_device_properties(dev).multi_processor_count)
+    chains = runs_chains_per_sm(k, f16)
     for b in range(grid.n_blocks):
         lo, hi = grid.block_range(b)
         if hi <= lo:
@@ -509,7 +531,10 @@ def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> 
         r_lo, r_hi = grid.row_span(b // grid.n_col_bands)
         T = len(ptile_row_cuts(r_lo, r_hi, k, f16, n_sm, max_rows)) - 1
         W = max(1, c_hi - c_lo)
-        if T < n_sm or (hi - lo) / (T * W) < TILE_RESIDENT_MIN_RUN:
+        run_len = (hi - lo) / (T * W)
+        if T < n_sm or run_len < TILE_RESIDENT_MIN_RUN:
+            return None
+        if chains * min(T, n_sm) * run_len / W > TILE_RESIDENT_MAX_STALE:
             return None
         cnt = torch.bincount(grid.items[lo:hi] - c_lo, minlength=W)
         if float(cnt.max()) > 4 * (hi - lo) / W:

@@ -850,14 +850,18 @@ def test_qband_split_runs_ml1m_quality(dev):
     assert abs(got["e5"] - ref["e5"]["test_rmse"]) <= 0.005
 
 
-@pytest.mark.parametrize("k,dtype", [(32, "float16"), (32, "float32"), (128, "float32")])
+@pytest.mark.parametrize("k,dtype", [(32, "float16"), (32, "float32"), (64, "float16"),
+                                     (64, "float32"), (128, "float32")])
 def test_default_layout_quality_matches_whole_runs(dev, k, dtype):
-    """Narrow blocks (600 items each) at 2 % density: the automatic layout
-    (run groups over a shared-memory P tile, implementation 8, since a tile
-    holds ~8 ratings per item) and the split-run layout (implementation 5:
-    item runs split over the chains, Q deltas) must both train like whole
-    runs on one chain each (implementation 4): same synthetic law, same init,
-    test RMSE after 8 epochs within 0.005 (and all must have learned)."""
+    """Narrow blocks (600 items each) at 2 % density: run groups over a
+    shared-memory P tile (implementation 8), the split-run layout
+    (implementation 5: item runs split over the chains, Q deltas) and the
+    automatic layout must all train like whole runs on one chain each
+    (implementation 4): same synthetic law, same init, test RMSE after 8
+    epochs within 0.005 (and all must have learned).  The automatic layout
+    picks run groups at k = 128 and, past the staleness bound
+    (data.TILE_RESIDENT_MAX_STALE: 128 chains per SM over 600 items), the
+    split runs at k = 32 / 64."""
     from paper_2006_15980_b200 import kernels
     from paper_2006_15980_b200.data import (bucket_qbands, build_device_grid, split_device,
                                             synthetic_device)
@@ -866,7 +870,7 @@ def test_default_layout_quality_matches_whole_runs(dev, k, dtype):
     trip = synthetic_device(120_000, 1_200, 3_000_000, seed=3, device=d)
     train, test = split_device(trip, 0.05)
     out = {}
-    for layout, impl in (("default", None), ("split", 5), ("whole", 4)):
+    for layout, impl in (("default", None), ("runs", 8), ("split", 5), ("whole", 4)):
         g = build_device_grid(train, [0, 120_000], [0, 600, 1_200])
         bucket_qbands(g, k, elem_bytes=2 if dtype == "float16" else 4, impl=impl)
         model = init_device_model(120_000, 1_200, k, 0, device=d, dtype=dtype)
@@ -877,11 +881,40 @@ def test_default_layout_quality_matches_whole_runs(dev, k, dtype):
                                            kernels.mix64(b, e))
         out[layout] = (first, rmse(test, model).value, g.sub_impl, g.sub_split)
     print(out)
-    assert out["default"][2] == 8
+    assert out["default"][2] == (8 if k == 128 else 5)
+    assert out["runs"][2] == 8
     assert out["split"][3] > 1            # implementation 5 did split the runs
     assert out["whole"][1] < out["whole"][0] - 0.005
-    for layout in ("default", "split"):
+    for layout in ("default", "runs", "split"):
         assert abs(out[layout][1] - out["whole"][1]) <= 0.005, out
+
+
+@pytest.mark.parametrize("k", [32, 64])
+def test_default_layout_quality_at_twice_the_paper_rate(dev, k):
+    """The staleness bound at work: at lr = 0.01 (twice the paper's) run
+    groups on these narrow blocks train 0.008 worse than whole runs (their
+    Q changes land after ~15 concurrent runs of the item, profiles/round2/
+    s4_stale_margin.jsonl); the automatic layout avoids them and stays
+    within 0.002."""
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import (bucket_qbands, build_device_grid, split_device,
+                                            synthetic_device)
+    from paper_2006_15980_b200.sgd import init_device_model, rmse
+    trip = synthetic_device(120_000, 1_200, 3_000_000, seed=3, device=dev)
+    train, test = split_device(trip, 0.05)
+    out = {}
+    for layout, impl in (("default", None), ("whole", 4)):
+        g = build_device_grid(train, [0, 120_000], [0, 600, 1_200])
+        bucket_qbands(g, k, elem_bytes=4, impl=impl)
+        model = init_device_model(120_000, 1_200, k, 0, device=dev, dtype="float32")
+        for e in range(8):
+            for b in (0, 1):
+                kernels.launch_block_qband(model.P, model.Q, g, b, 0.01, 0.05, 0.05,
+                                           kernels.mix64(b, e))
+        out[layout] = (rmse(test, model).value, g.sub_impl)
+    print(out)
+    assert out["default"][1] != 8
+    assert abs(out["default"][0] - out["whole"][0]) <= 0.002, out
 
 
 @pytest.mark.parametrize("k", [32, 128])
@@ -1193,7 +1226,8 @@ def test_tile_resident_policy(dev):
     """data.tile_resident_impl picks run groups (8) exactly where they win
     (profiles/round2/s3_default_layout_sweep.jsonl): Netflix density (~4.9
     ratings per tile-item), but not a small matrix (fewer tiles than SMs),
-    a sparse one (< 2 ratings per tile-item) or one with hot items."""
+    a sparse one (< 2 ratings per tile-item), one with hot items, or narrow
+    blocks past the staleness bound."""
     from paper_2006_15980_b200.data import (build_device_grid, synthetic_band,
                                             tile_resident_impl)
     d = dev
@@ -1211,3 +1245,8 @@ def test_tile_resident_policy(dev):
     assert tile_resident_impl(grid(120_000, 17_700, 25_000_000, skew=True), 128,
                               False) is None                                         # hot item
     assert tile_resident_impl(grid(120_000, 17_700, 25_000_000), 96, False) is None  # k
+    # narrow 600-item blocks: 128 chains per SM (k = 32) put ~15 runs of each
+    # item in flight (staleness ~500 > TILE_RESIDENT_MAX_STALE); 64 (k = 128) ~136
+    narrow = grid(120_000, 1_200, 3_000_000)
+    assert tile_resident_impl(narrow, 32, False) is None
+    assert tile_resident_impl(narrow, 128, False) == 8
