@@ -382,11 +382,11 @@ def roofline_fields(args, achieved, peak, peak_kind, bpu, mean_ms, mean_updates,
            "frac_meaning": "north-star ratio: algorithmic bytes (rating + p_u, q_v read and "
                            "written) per launch / live launch time / measured HBM copy BW; > 1 "
                            "because P rows are served on chip (L2 row tiles; shared-memory "
-                           "tiles for implementations 7-8); see dram, compulsory, "
+                           "tiles for implementation 8); see dram, compulsory, "
                            "binding_unit for the measured picture",
            "kernel": ncu["kernel"] if ncu else (
                "sgd_hogwild_kernel" if args.kernel != "qband" else
-               {0: "qband_kernel", 7: "ptile_kernel", 8: "runs_kernel"}.get(impl,
+               {0: "qband_kernel", 8: "runs_kernel"}.get(impl,
                                                                              "qchain_kernel")),
            "qband_impl": impl,
            "mean_launch_ms": mean_ms, "updates_per_launch": mean_updates,
@@ -410,7 +410,7 @@ def roofline_fields(args, achieved, peak, peak_kind, bpu, mean_ms, mean_updates,
                "source": "scripts/l2_rowbench.cu: random P-row load + "
                          + ("store" if p_stores else "vector reduction")
                          + ", L2-resident 32 MB, no arithmetic (profiles/r02/l2_rowbench.jsonl)"})}
-    if ncu and ncu.get("smem_wavefronts") and impl in (7, 8):
+    if ncu and ncu.get("smem_wavefronts") and impl == 8:
         # P rows live in shared memory: the bound is the SM's L1/shared data
         # pipe, one 128-byte wavefront per cycle per SM (P-row loads and
         # stores, 8 per update at fp32 k=128, plus shuffles and the global
@@ -625,7 +625,7 @@ def run_ours(args, world, rank, local):
     impl_used = getattr(grid, "sub_impl", None)
     # the L2 row-load ceiling describes the L2 row-tile kernels; 7 and 8 keep
     # P in shared memory
-    l2_rows = None if (impl_used or 0) >= 7 else l2_ceiling(k, precision, bool(p_stores))
+    l2_rows = None if (impl_used or 0) == 8 else l2_ceiling(k, precision, bool(p_stores))
     kernel_ups = mean_updates / (mean_ms / 1e3)
     # compulsory DRAM bytes of one launch: its triples once, one read and one
     # write of every P row of its row band and of every Q row of its column
@@ -1022,9 +1022,9 @@ def main():
                          "per epoch")
     ap.add_argument("--multi-concurrency", type=int, default=1,
                     help="N>1: column blocks in flight per GPU (each on its own stream)")
-    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 4, 5, 6, 7, 8], default=-1,
-                    help="Q-band kernel: 0 = warp per rating, 4-6 chained item runs, 7 "
-                         "tile-resident P, 8 run groups over it (-1: the layout's choice, "
+    ap.add_argument("--qband-impl", type=int, choices=[-1, 0, 4, 5, 6, 8], default=-1,
+                    help="Q-band kernel: 0 = warp per rating, 4-6 chained item runs, 8 run "
+                         "groups over a tile-resident P (-1: the layout's choice, "
                          "data.tile_resident_impl, else 5)")
     ap.add_argument("--chain-cfg", type=int, choices=[-1, 2, 4, 5, 6], default=-1,
                     help="configuration of the chained kernel (qchain.cuh ChainCfg)")

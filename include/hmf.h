@@ -13,7 +13,7 @@
  *   hmf_sgd_block_qband_{f32,f16} BatchEngine.compute on a staged item band
  *   hmf_sgd_block_qband_u16_*     (the same, uint16 tile-relative row ids)
  *   hmf_sgd_block_qband_u16_tiles_*  (the same over several row tiles)
- *   hmf_sgd_block_ptile_*, hmf_sgd_block_runs_{,u16_,u8_}*
+ *   hmf_sgd_block_runs_{,u16_,u8_}*
  *                                 (the same, P tile in shared memory)
  *                                                              workers.py:186-255
  *   hmf_lease_*                   GridScheduler.acquire / release / abort for
@@ -48,7 +48,10 @@
 extern "C" {
 #endif
 
-#define HMF_ABI_VERSION 4
+/* ABI 4: launch options per call (hmf_qband_opts).  ABI 5: implementation 7
+ * (hmf_sgd_block_ptile_*, hmf_ptile_bins_per_tile) removed;
+ * hmf_runs_chains_per_warp takes the element size; hmf_lease_claim added. */
+#define HMF_ABI_VERSION 5
 
 #define HMF_OK 0
 #define HMF_ERR_ARG (-1)
@@ -132,8 +135,9 @@ typedef struct hmf_qband_opts {
    * per sub-band); 5 = 4 with Q deltas: runs of one item may be split over
    * chains, each adds its change back with vector reductions and re-reads the
    * row every `qsync` ratings (bounded staleness); 6 = 5 publishing only at
-   * item and bin changes; 7 = tile-resident P (hmf_sgd_block_ptile_* only);
-   * 8 = run groups over a tile-resident P (hmf_sgd_block_runs_* only). */
+   * item and bin changes; 8 = run groups over a tile-resident P
+   * (hmf_sgd_block_runs_* only; 7, item bins over that tile, was removed in
+   * ABI 5: run groups beat it at every k). */
   int32_t impl;
   /* Chained-kernel configuration 2, 4, 5 or 6 (lanes per chain, prefetch
    * distance, occupancy); -1 = by k and storage
@@ -223,48 +227,23 @@ int64_t hmf_sgd_block_qband_u16_tiles_f16(uint16_t* user_f, uint16_t* item_f, in
                                           double lr, double reg_user, double reg_item,
                                           uint64_t seed, int64_t col_base, void* stream);
 
-/*
- * Tile-resident P (implementation 7, ABI 4): the block's users are cut into
- * n_tiles row tiles, tile t being rows [tile_cut[t], tile_cut[t+1]) of
- * user_f (absolute indices, i.e. rows[i] - row_base; device int32[n_tiles +
- * 1]) of at most max_tile_rows rows <= hmf_ptile_max_rows(k, f16); triples
- * bucketed tile-major into n_sub item sub-bands per tile (sub_ptr: n_tiles *
- * n_sub + 1 offsets, item-sorted inside a tile; data.bucket_qbands with
- * impl 7), cols required.  A persistent CTA per SM holds one tile's P rows
- * in shared memory at a time; chains walk item runs with the Q row in
- * registers and add Q changes back by vector reductions.  opts.impl must be
- * -1 or 7; grid_share applies.  Same update rule and return convention as
- * hmf_sgd_block_qband_*.
- */
+/* Rows of one P tile in shared memory for the run-group kernel (208 KB of
+ * P rows: 416 users at fp32 k = 128). */
 int32_t hmf_ptile_max_rows(int64_t k, int32_t f16);
-/* Sub-bands per tile the layout should cut (chains per CTA x 4). */
-int32_t hmf_ptile_bins_per_tile(int64_t k);
-int64_t hmf_sgd_block_ptile_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
-                                const int32_t* cols, const float* vals, const int64_t* sub_ptr,
-                                int64_t n_sub, int64_t n_tiles, const int32_t* tile_cut,
-                                int32_t max_tile_rows, const hmf_qband_opts* opts, double lr,
-                                double reg_user, double reg_item, uint64_t seed, int64_t row_base,
-                                int64_t col_base, void* stream);
-int64_t hmf_sgd_block_ptile_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
-                                const int32_t* rows, const int32_t* cols, const float* vals,
-                                const int64_t* sub_ptr, int64_t n_sub, int64_t n_tiles,
-                                const int32_t* tile_cut, int32_t max_tile_rows,
-                                const hmf_qband_opts* opts, double lr, double reg_user,
-                                double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
-                                void* stream);
 
 /*
  * Run groups over a tile-resident P (implementation 8): the block's users cut
- * into n_tiles row tiles as for implementation 7 (tile t = rows
- * [tile_cut[t], tile_cut[t+1]) of user_f, at most max_tile_rows rows <=
- * hmf_ptile_max_rows(k, f16)); inside a tile the ratings are grouped into
- * runs (all ratings of one item, in the block's order), runs sorted by
+ * into n_tiles row tiles (tile t = rows [tile_cut[t], tile_cut[t+1]) of
+ * user_f, absolute indices, i.e. rows[i] - row_base; device int32[n_tiles +
+ * 1]; at most max_tile_rows rows <= hmf_ptile_max_rows(k, f16)); inside a
+ * tile the ratings are grouped into runs (all ratings of one item, in the
+ * block's order), runs sorted by
  * length, longest first.  runs: int32[n_runs][4] descriptors, 16-byte
  * aligned; run r = {first, len, item, r} holds ratings [first, first + len)
  * of rows / vals (offsets relative to those pointers), all of item `item`
  * (absolute, minus col_base); tile t's runs are [tile_run[t],
- * tile_run[t+1]).  Device arrays; data.bucket_qbands with impl 8 builds them.  A persistent CTA per SM holds one tile's P rows in
- * shared memory; each warp takes groups of hmf_runs_chains_per_warp(k, f16)
+ * tile_run[t+1]).  Device arrays; data.bucket_qbands with impl 8 builds
+ * them.  A persistent CTA per SM holds one tile's P rows in shared memory; each warp takes groups of hmf_runs_chains_per_warp(k, f16)
  * consecutive runs, one per lane-group chain, the item's Q row in registers,
  * Q changes added back by vector reductions at the run's end.  rows: int32
  * user ids (minus row_base), or with the _u16 entry points uint16 ids

@@ -30,7 +30,7 @@ MODES = {"hogwild": MODE_HOGWILD, "ordered": MODE_ORDERED, "exact": MODE_EXACT,
          "hogwild_lww": MODE_HOGWILD_LWW}
 
 TUNE_VARIANT = 1
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 _p = C.c_void_p
 _i64 = C.c_int64
@@ -68,11 +68,6 @@ SIGNATURES = {
     "hmf_sgd_block_qband_u16_tiles_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64,
                                                  _p, _p, _f64, _f64, _f64, _u64, _i64, _p]),
     "hmf_ptile_max_rows": (_i32, [_i64, _i32]),
-    "hmf_ptile_bins_per_tile": (_i32, [_i64]),
-    "hmf_sgd_block_ptile_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _i64, _i64, _p, _i32, _p,
-                                       _f64, _f64, _f64, _u64, _i64, _i64, _p]),
-    "hmf_sgd_block_ptile_f16": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _i64, _i64, _p, _i32, _p,
-                                       _f64, _f64, _f64, _u64, _i64, _i64, _p]),
     "hmf_runs_chains_per_warp": (_i32, [_i64, _i32]),
     "hmf_sgd_block_runs_f32": (_i64, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p, _f64,
                                       _f64, _f64, _u64, _i64, _i64, _p]),

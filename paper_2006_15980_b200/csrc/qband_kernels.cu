@@ -56,7 +56,6 @@ __device__ inline int tile_at(int i, int n_tiles, uint64_t seed) {
 }  // namespace hmf
 
 #include "qchain.cuh"
-#include "ptile.cuh"
 #include "runs.cuh"
 
 namespace hmf {
@@ -289,9 +288,9 @@ constexpr int kDefaultQsync = 32;
 // HMF_OK or a negative code with the message set.
 static int64_t resolve_opts(const hmf_qband_opts* in, int64_t k, bool f16, LaunchOpts* o) {
   o->impl = in && in->impl >= 0 ? in->impl : kDefaultImpl;
-  if (in && in->impl < -1) return set_error(HMF_ERR_ARG, "impl must be -1, 0 or 4..8");
-  if (o->impl != 0 && (o->impl < 4 || o->impl > 8))
-    return set_error(HMF_ERR_ARG, "impl must be -1, 0 or 4..8");
+  if (in && in->impl < -1) return set_error(HMF_ERR_ARG, "impl must be -1, 0, 4..6 or 8");
+  if (o->impl != 0 && (o->impl < 4 || o->impl > 8 || o->impl == 7))
+    return set_error(HMF_ERR_ARG, "impl must be -1, 0, 4..6 or 8");
   o->cfg = in && in->chain_cfg >= 0 ? in->chain_cfg : auto_chain_cfg(int(k), f16);
   if (!chain_cfg_ok(o->cfg) || (in && in->chain_cfg < -1))
     return set_error(HMF_ERR_ARG, "chain_cfg must be -1, 2, 4, 5 or 6");
@@ -333,9 +332,8 @@ static int64_t run(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* co
   if (n_sub <= 0 || n_tiles <= 0) return 0;
   rc = check_block_args(P, Q, rows, vals, sub_ptr, sub_cuts, n_sub, n_tiles);
   if (rc != HMF_OK) return rc;
-  if (o.impl == 7 || o.impl == 8)
-    return set_error(HMF_ERR_ARG, "implementations 7 and 8 run through hmf_sgd_block_ptile_* / "
-                                  "hmf_sgd_block_runs_*");
+  if (o.impl == 8)
+    return set_error(HMF_ERR_ARG, "implementation 8 runs through hmf_sgd_block_runs_*");
   // cols == nullptr: every sub-band is one item, sub_cuts[s] (chained kernel only)
   if (!cols && o.impl == 0)
     return set_error(HMF_ERR_ARG, "cols may be null only for implementations 4-6");
@@ -390,65 +388,6 @@ static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_
     HMF_QB_CASE(128)
     HMF_QB_CASE(256)
 #undef HMF_QB_CASE
-    default: return set_error(HMF_ERR_UNSUPPORTED, "Q-band kernel needs k in {32,64,128,256}");
-  }
-  if (e != cudaSuccess) return set_cuda_error(e);
-  return 0;
-}
-
-// implementation 7: tile-resident P (ptile.cuh)
-template <int K, typename S>
-static cudaError_t launch_ptile(S* P, S* Q, const int32_t* rows, const int32_t* cols,
-                                const float* vals, const int64_t* sub_ptr, int n_sub, int n_tiles,
-                                const int32_t* tile_cut, int max_rows, double lr, double ru,
-                                double ri, uint64_t seed, int64_t row_base, int64_t col_base,
-                                cudaStream_t stream, const LaunchOpts& o) {
-  using C = PTileCfg<K>;
-  auto kern = ptile_kernel<K, S, C::LPC, C::WPB, int32_t>;
-  const int smem = max_rows * K * int(sizeof(S));
-  int per_sm = 0;
-  cudaError_t e = kernel_occupancy(reinterpret_cast<const void*>(kern), C::WPB * 32, smem, &per_sm);
-  if (e != cudaSuccess) return e;
-  const int cap = grid_share(device_sm_count() * per_sm, o.share);
-  const int grid = n_tiles < cap ? n_tiles : cap;
-  if (grid <= 0) return cudaSuccess;
-  kern<<<grid, C::WPB * 32, smem, stream>>>(P - row_base * K, Q - col_base * K, rows, cols, vals,
-                                            sub_ptr, n_sub, n_tiles, tile_cut, float(lr),
-                                            float(ru), float(ri), seed);
-  return cudaGetLastError();
-}
-
-template <typename S>
-static int64_t run_ptile(S* P, S* Q, int64_t k, const int32_t* rows, const int32_t* cols,
-                         const float* vals, const int64_t* sub_ptr, int64_t n_sub,
-                         int64_t n_tiles, const int32_t* tile_cut, int32_t max_rows,
-                         const hmf_qband_opts* opts, double lr, double ru, double ri,
-                         uint64_t seed, int64_t row_base, int64_t col_base,
-                         cudaStream_t stream) {
-  LaunchOpts o;
-  int64_t rc = resolve_opts(opts, k, sizeof(S) == 2, &o);
-  if (rc != HMF_OK) return rc;
-  if (opts && opts->impl >= 0 && opts->impl != 7)
-    return set_error(HMF_ERR_ARG, "hmf_sgd_block_ptile_* runs implementation 7");
-  if (n_sub <= 0 || n_tiles <= 0) return 0;
-  rc = check_block_args(P, Q, rows, vals, sub_ptr, cols, n_sub, n_tiles);
-  if (rc != HMF_OK) return rc;
-  if (!tile_cut) return set_error(HMF_ERR_ARG, "null pointer");
-  if (max_rows <= 0 || int64_t(max_rows) * k * int64_t(sizeof(S)) > kPTileBytes)
-    return set_error(HMF_ERR_ARG, "a tile's P rows must fit hmf_ptile_max_rows(k, f16)");
-  cudaError_t e;
-  switch (k) {
-#define HMF_PT_CASE(KK)                                                                      \
-  case KK:                                                                                   \
-    e = launch_ptile<KK, S>(P, Q, rows, cols, vals, sub_ptr, int(n_sub), int(n_tiles),       \
-                            tile_cut, max_rows, lr, ru, ri, seed, row_base, col_base, stream, \
-                            o);                                                              \
-    break;
-    HMF_PT_CASE(32)
-    HMF_PT_CASE(64)
-    HMF_PT_CASE(128)
-    HMF_PT_CASE(256)
-#undef HMF_PT_CASE
     default: return set_error(HMF_ERR_UNSUPPORTED, "Q-band kernel needs k in {32,64,128,256}");
   }
   if (e != cudaSuccess) return set_cuda_error(e);
@@ -533,7 +472,6 @@ static int slots_per_sm(int64_t k, const hmf_qband_opts* opts) {
 #define HMF_WPS(KK)                                                                        \
   case KK:                                                                                 \
     e = o.impl == 0 ? warp_slots_per_sm<KK, S>(&n)                                         \
-        : o.impl == 7 ? (n = PTileCfg<KK>::WPB * 32 / PTileCfg<KK>::LPC, cudaSuccess)         \
         : o.impl == 8 ? (n = RunsCfg<KK, S>::WPB * 32 / RunsCfg<KK, S>::LPC, cudaSuccess)         \
                       : chain_slots_per_sm<KK, S>(o.cfg, &n);                                \
     break;
@@ -606,45 +544,6 @@ int64_t hmf_sgd_block_qband_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
 int32_t hmf_ptile_max_rows(int64_t k, int32_t f16) {
   if (k != 32 && k != 64 && k != 128 && k != 256) return 0;
   return int32_t(hmf::qs::kPTileBytes / (k * (f16 ? 2 : 4)));
-}
-
-int32_t hmf_ptile_bins_per_tile(int64_t k) {
-  switch (k) {
-    case 32: return hmf::qs::PTileCfg<32>::WPB * 32 / hmf::qs::PTileCfg<32>::LPC *
-                    hmf::qs::kPTileBinsPerChain;
-    case 64: return hmf::qs::PTileCfg<64>::WPB * 32 / hmf::qs::PTileCfg<64>::LPC *
-                    hmf::qs::kPTileBinsPerChain;
-    case 128: return hmf::qs::PTileCfg<128>::WPB * 32 / hmf::qs::PTileCfg<128>::LPC *
-                     hmf::qs::kPTileBinsPerChain;
-    case 256: return hmf::qs::PTileCfg<256>::WPB * 32 / hmf::qs::PTileCfg<256>::LPC *
-                     hmf::qs::kPTileBinsPerChain;
-    default: return 0;
-  }
-}
-
-int64_t hmf_sgd_block_ptile_f32(float* user_f, float* item_f, int64_t k, const int32_t* rows,
-                                const int32_t* cols, const float* vals, const int64_t* sub_ptr,
-                                int64_t n_sub, int64_t n_tiles, const int32_t* tile_cut,
-                                int32_t max_tile_rows, const hmf_qband_opts* opts, double lr,
-                                double reg_user, double reg_item, uint64_t seed, int64_t row_base,
-                                int64_t col_base, void* stream) {
-  return hmf::qs::run_ptile<float>(user_f, item_f, k, rows, cols, vals, sub_ptr, n_sub, n_tiles,
-                                   tile_cut, max_tile_rows, opts, lr, reg_user, reg_item, seed,
-                                   row_base, col_base, static_cast<cudaStream_t>(stream));
-}
-
-int64_t hmf_sgd_block_ptile_f16(uint16_t* user_f, uint16_t* item_f, int64_t k,
-                                const int32_t* rows, const int32_t* cols, const float* vals,
-                                const int64_t* sub_ptr, int64_t n_sub, int64_t n_tiles,
-                                const int32_t* tile_cut, int32_t max_tile_rows,
-                                const hmf_qband_opts* opts, double lr, double reg_user,
-                                double reg_item, uint64_t seed, int64_t row_base, int64_t col_base,
-                                void* stream) {
-  return hmf::qs::run_ptile<__half>(reinterpret_cast<__half*>(user_f),
-                                    reinterpret_cast<__half*>(item_f), k, rows, cols, vals,
-                                    sub_ptr, n_sub, n_tiles, tile_cut, max_tile_rows, opts, lr,
-                                    reg_user, reg_item, seed, row_base, col_base,
-                                    static_cast<cudaStream_t>(stream));
 }
 
 int32_t hmf_runs_chains_per_warp(int64_t k, int32_t f16) {

@@ -1,14 +1,15 @@
 // Run groups over a tile-resident P (Q-band implementation 8).
 //
-// Implementation 7 (ptile.cuh) keeps a row tile's P rows in shared memory
-// and walks item runs one rating per step, four lane-group chains per warp.
-// Its profile (profiles/round2/s3_ptile_*) shows where the time goes: each
-// chain changes runs on its own, every ~4.75 ratings at Netflix density, so
-// the warp runs the run-change path (Q-delta flush, Q-row hand-over, the next
-// row's prefetch) on more than half of its steps, the next row is prefetched
-// only one step ahead of a ~600-cycle L2 load, and every step re-derives
-// "does my run end here" from shuffled look-ahead triples: 38 instructions
-// per update at 49 % issue.
+// The chained kernel (qchain.cuh) keeps an item's Q row in registers along
+// an item run and moves the user's P row through L2 on every rating (512 B
+// read + 512 B written per update at k = 128 fp32), binding on the SM -> L2
+// request path.  Here a row tile's P rows stay in shared memory while the
+// tile trains.  A first version (round 2's implementation 7, since removed)
+// walked item runs one rating per step, each chain changing runs on its own
+// every ~4.75 ratings at Netflix density: the warp ran the run-change path
+// on more than half of its steps and stalled on the next Q row's L2 load
+// (38 instructions per update at 49 % issue, 14.8 G upd/s; profiles/round2/
+// s3_ptile_*).
 //
 // Here the layout hands the kernel whole runs in groups, one run per chain
 // of a warp:
@@ -26,12 +27,13 @@
 //     arrived during g-1) and group g+2's run descriptors load, so neither
 //     the dependent descriptor -> row loads nor the L2 latency stall a step;
 //   * at a run's end each chain adds its Q change back with vector
-//     reductions (as implementation 7: no Q update is lost, concurrent runs
-//     of one item in other tiles see it at their next load);
+//     reductions (red.global.add.v4.f32): no Q update is lost, concurrent
+//     runs of one item in other tiles see it at their next load (bounded
+//     staleness, data.TILE_RESIDENT_MAX_STALE);
 //   * inside a run the visit starts at a seeded rotation (fresh every epoch).
-// P rows live in shared memory exactly as in implementation 7 (chains of a
-// CTA that update one user in the same step race, the reference's racing
-// lanes, workers.py:222-266).  The update arithmetic is the reference's
+// Chains of a CTA that update one user in the same step race on its P row in
+// shared memory (last store wins: the reference's racing lanes,
+// workers.py:222-266).  The update arithmetic is the reference's
 // (kernels.py:120-131) in fp32, on packed fp32 pairs (FFMA2).
 #pragma once
 
@@ -40,6 +42,10 @@
 
 namespace hmf {
 namespace qs {
+
+// shared memory for one tile's P rows (the rest of the 227 KB stays free for
+// the kernel's static shared memory)
+constexpr int kPTileBytes = 208 * 1024;
 
 #ifndef RUNS_SMEM_REDUCE
 #define RUNS_SMEM_REDUCE 1

@@ -382,8 +382,8 @@ class DeviceGrid:
     sub_split: int = 1                  # parts per item run (implementation 5)
     sub_qsync: int = 0                  # Q publication period for implementation 5
     sub_pstore: int = 0                 # chained kernel P write-back: 1 stores, 0 reductions
-    sub_tile_cuts: list | None = None   # implementation 7: per block, device int32 tile cuts
-    sub_max_rows: int = 0               # implementation 7: rows of the largest tile
+    sub_tile_cuts: list | None = None   # implementation 8: per block, device int32 tile cuts
+    sub_max_rows: int = 0               # implementation 8: rows of the largest tile
     sub_tile_run: list | None = None    # implementation 8: per block, first run of each tile
 
     n_row_bands = BlockGrid.n_row_bands
@@ -497,9 +497,8 @@ def runs_chains_per_sm(k: int, f16: bool) -> int:
 
 
 def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> int | None:
-    """Implementation 8 (run groups over a shared-memory P tile) or 7 (the
-    same tile, item bins) when every non-empty block of `grid` suits them,
-    else None (the L2 row-tile kernels):
+    """Implementation 8 (run groups over a shared-memory P tile) when every
+    non-empty block of `grid` suits it, else None (the L2 row-tile kernels):
     * k in {32, 64, 128, 256};
     * at least one tile per SM (a CTA trains one tile at a time: ML-1M's
       6 040 users make 4 tiles at k = 32 — 1.4 vs 16 G upd/s);
@@ -510,11 +509,10 @@ def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> 
       Q row; the item-split kernel (5) handles that case;
     * Q staleness S <= TILE_RESIDENT_MAX_STALE (few items for the runs in
       flight: narrow column blocks).
-    Returns 8 (Netflix fp32 k = 32 / 64 / 128 / 256: 51.8 / 30.7 / 17.3 / 6.4
-    G upd/s against 30.6 / 19.7 / 11.8 / 5.9 for implementation 5; fp16 75 /
-    34 / 21.5 / 8.7 against 42 / 27 / 16.4 / 8.5; implementation 7 measured
-    34.3 / 21.2 / 14.8 / 6.8 fp32 — ahead only at k = 256, and without a
-    streamed form, so 8 serves every k)."""
+    Returns 8 (Netflix fp32 k = 32 / 64 / 128 / 256: 68.9 / 39.7 / 19.4 / 7.5
+    G upd/s against 30.6 / 19.7 / 11.8 / 5.9 for implementation 5; fp16 72 /
+    49 / 22.2 / 9.3 against 42 / 27 / 16.4 / 8.5; profiles/round2/
+    s4_ksweep.jsonl)."""
     torch = _torch()
     if k not in (32, 64, 128, 256) or grid.nnz == 0:
         return None
@@ -654,7 +652,8 @@ def bucket_qbands(grid: DeviceGrid, k: int, target: int | None = None,
                                                 for c in range(grid.n_col_bands)), default=0))
     impl = int(impl)
     if impl == 7:
-        return _bucket_ptile(grid, k, f16, max_tile_rows)
+        raise ValueError("implementation 7 (item bins over a P tile) was removed: run groups (8) "
+                         "beat it at every k")
     if impl == 8:
         return _bucket_runs(grid, k, f16, max_tile_rows)
     widest = max((grid.col_span(c)[1] - grid.col_span(c)[0]
@@ -820,7 +819,7 @@ PTILE_MIN_ROWS = 64
 
 def ptile_row_cuts(r_lo: int, r_hi: int, k: int, f16: bool, n_sm: int,
                    max_rows: int | None = None) -> np.ndarray:
-    """Row tiles of implementations 7 and 8 (tile-resident P): the fewest
+    """Row tiles of implementation 8 (tile-resident P): the fewest
     equal tiles whose P rows fit one CTA's shared memory (hmf_ptile_max_rows),
     at least one per SM when that leaves PTILE_MIN_ROWS rows per tile (a CTA
     trains one tile at a time) — rounded up to a multiple of the SM count,
@@ -836,57 +835,6 @@ def ptile_row_cuts(r_lo: int, r_hi: int, k: int, f16: bool, n_sm: int,
         t = -(-t // n_sm) * n_sm
     t = max(1, min(n, t))
     return np.linspace(r_lo, r_hi, t + 1).round().astype(np.int64)
-
-
-def _bucket_ptile(grid: DeviceGrid, k: int, f16: bool, max_rows: int | None) -> DeviceGrid:
-    """The layout of implementation 7 (csrc/ptile.cuh): per block, row tiles
-    that fit shared memory (ptile_row_cuts) and, inside each tile, the
-    block's items cut into hmf_ptile_bins_per_tile equal sub-bands, triples
-    sorted by (tile, item) — stable, so each item's ratings keep the block's
-    shuffled order (data.py:242-244, 264).  One stable device sort per block."""
-    torch = _torch()
-    dev = grid.device
-    lib = _lib.load()
-    n_sm = int(torch.cuda.get_device_properties(dev).multi_processor_count)
-    bins = int(lib.hmf_ptile_bins_per_tile(int(k)))
-    sub_ptrs, sub_cuts, sub_tiles, tile_rows, tile_cuts = [], [], [], [], []
-    for b in range(grid.n_blocks):
-        lo, hi = grid.block_range(b)
-        c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
-        r_lo, r_hi = grid.row_span(b // grid.n_col_bands)
-        tiles = ptile_row_cuts(r_lo, r_hi, k, f16, n_sm, max_rows)
-        T = len(tiles) - 1
-        cuts = qband_sub_cuts(c_lo, c_hi, k, bins, 1 << 30)
-        S = len(cuts) - 1
-        ptr = torch.full((T * S + 1,), hi, dtype=torch.int64, device=dev)
-        if hi > lo:
-            d_tiles = torch.from_numpy(tiles[1:-1]).to(dev, torch.int32)
-            d_cuts = torch.from_numpy(cuts[1:-1]).to(dev, torch.int32)
-            tile_of = torch.bucketize(grid.users[lo:hi], d_tiles, right=True)
-            sub_of = torch.bucketize(grid.items[lo:hi], d_cuts, right=True)
-            key = (tile_of.to(torch.int64) * (c_hi - c_lo)
-                   + (grid.items[lo:hi] - c_lo).to(torch.int64))
-            order = torch.sort(key, stable=True).indices
-            grid.users[lo:hi] = grid.users[lo:hi][order]
-            grid.items[lo:hi] = grid.items[lo:hi][order]
-            grid.ratings[lo:hi] = grid.ratings[lo:hi][order]
-            bin_of = tile_of.to(torch.int64) * S + sub_of
-            cnt = torch.bincount(bin_of, minlength=T * S)
-            ptr[0] = lo
-            ptr[1:] = lo + torch.cumsum(cnt, 0)
-            del tile_of, sub_of, key, order, bin_of, cnt
-        sub_ptrs.append(ptr)
-        sub_cuts.append(torch.from_numpy(cuts).to(device=dev, dtype=torch.int32))
-        sub_tiles.append(T)
-        tile_rows.append(tiles)
-        tile_cuts.append(torch.from_numpy(tiles).to(device=dev, dtype=torch.int32))
-    grid.sub_ptr, grid.sub_cuts, grid.sub_tiles = sub_ptrs, sub_cuts, sub_tiles
-    grid.sub_impl, grid.sub_cfg, grid.sub_split, grid.sub_qsync, grid.sub_pstore = 7, -1, 1, 0, 0
-    grid.sub_tile_rows = tile_rows
-    grid.sub_tile_cuts = tile_cuts
-    grid.sub_max_rows = max((int(np.max(np.diff(t))) for t in tile_rows if len(t) > 1),
-                            default=1)
-    return grid
 
 
 def _coprime_multiplier(w: int) -> int:
@@ -913,8 +861,8 @@ def run_rotation(seed: int, r: int, length: int) -> int:
 
 
 def _bucket_runs(grid: DeviceGrid, k: int, f16: bool, max_rows: int | None) -> DeviceGrid:
-    """The layout of implementation 8 (csrc/runs.cuh): per block, the row
-    tiles of implementation 7 (ptile_row_cuts); inside a tile the runs — all
+    """The layout of implementation 8 (csrc/runs.cuh): per block, row tiles
+    whose P rows fit shared memory (ptile_row_cuts); inside a tile the runs — all
     ratings of one item, in the block's (shuffled) order, data.py:242-244,
     264 — sorted by length, longest first, then in a per-tile scrambled item
     order.  Two stable device sorts per block: by (tile, item) to measure the

@@ -173,16 +173,6 @@ def launch_block_qband(user_f, item_f, grid, block, lr, reg_user, reg_item, seed
     n_sub = int(sc.numel()) - 1
     if int(sp.numel()) != n_tiles * n_sub + 1:
         raise ValueError("sub_ptr does not match sub_cuts x sub_tiles")
-    if int(grid.sub_impl) == 7:
-        # tile-resident P: the layout's tile cuts travel with the launch
-        fn = getattr(_lib.load(), f"hmf_sgd_block_ptile_{st}")
-        _lib.check(fn(user_f.data_ptr(), item_f.data_ptr(), user_f.shape[1],
-                      grid.users.data_ptr(), grid.items.data_ptr(), grid.ratings.data_ptr(),
-                      sp.data_ptr(), n_sub, n_tiles, grid.sub_tile_cuts[block].data_ptr(),
-                      int(grid.sub_max_rows), ctypes.byref(o), float(lr), float(reg_user),
-                      float(reg_item), int(seed) & _MASK64, int(row_base), int(col_base), s),
-                   f"hmf_sgd_block_ptile_{st}")
-        return hi - lo
     fn = getattr(_lib.load(), f"hmf_sgd_block_qband_{st}")
     _lib.check(fn(user_f.data_ptr(), item_f.data_ptr(), user_f.shape[1], grid.users.data_ptr(),
                   grid.items.data_ptr(), grid.ratings.data_ptr(), sp.data_ptr(), sc.data_ptr(),

@@ -521,9 +521,6 @@ class StreamingEpoch:
         # and its tiles hold at most hmf_ptile_max_rows users, so the stream
         # is always the compact one (uint16 tile-relative user + rating)
         self.runs = int(sg.sub_impl) == 8
-        if int(sg.sub_impl) == 7:
-            raise ValueError("implementation 7 (item bins over a shared-memory P tile) has no "
-                             "streamed form; lay the grid out for implementation 8")
         # every sub-band a single item (or a part of one): the item is implicit
         self.implicit_items = self.runs or (compact and sg.sub_impl >= 4 and all(
             bool(torch.all(c[1:] - c[:-1] <= 1)) for c in sg.sub_cuts))

@@ -41,7 +41,7 @@ def test_binding_matches_header():
 def test_host_only_entry_points():
     from paper_2006_15980_b200 import _lib, kernels
     lib = _lib.load()
-    assert lib.hmf_abi_version() == _lib.ABI_VERSION == 4
+    assert lib.hmf_abi_version() == _lib.ABI_VERSION == 5
     for parts in [(0,), (7, 3, 1), (2 ** 63 - 1, 5), (123456789, 42, 17, 3)]:
         assert _lib.mix64_native(*parts) == kernels.mix64(*parts)
     # argument validation happens before any device work
@@ -52,7 +52,8 @@ def test_host_only_entry_points():
     import ctypes
     args = (None, None, 128, None, None, None, None, None, 4, 1)
     tail = (0.01, 0.0, 0.0, 0, 0, 0, None)
-    for bad in ({"pstore": 2}, {"impl": 1}, {"impl": 3}, {"chain_cfg": 0}, {"chain_cfg": 3},
+    for bad in ({"pstore": 2}, {"impl": 1}, {"impl": 3}, {"impl": 7}, {"chain_cfg": 0},
+                {"chain_cfg": 3},
                 {"grid_share": 0}, {"grid_share": 65}, {"lockstep": 4}, {"qsync": -2}):
         o = _lib.QbandOpts(**bad)
         assert lib.hmf_sgd_block_qband_f32(*args, ctypes.byref(o), *tail) == _lib.HMF_ERR_ARG, bad

@@ -988,8 +988,8 @@ def test_qband_bucketing_many_subbands(dev):
 
 @pytest.mark.parametrize("k,dtype", [(128, torch.float32), (32, torch.float32),
                                      (64, torch.float16), (256, torch.float32)])
-def test_ptile_conflict_free_equals_oracle(dev, k, dtype):
-    """Implementation 7 (tile-resident P): with distinct users AND distinct
+def test_runs_conflict_free_equals_oracle(dev, k, dtype):
+    """Implementation 8 (run groups over a tile-resident P): with distinct users AND distinct
     items nothing races and nothing is stale, so the result is every triple
     applied once from the initial factors — the reference update (oracle,
     f64) within storage rounding — across many row tiles and both blocks."""
@@ -1006,8 +1006,8 @@ def test_ptile_conflict_free_equals_oracle(dev, k, dtype):
     m = RatingMatrix(n_users, n_items, users, items, vals)
     g = build_device_grid(DeviceTriples.from_host(m, dev), [0, n_users],
                           [0, n_items // 2, n_items])
-    bucket_qbands(g, k, impl=7, elem_bytes=2 if dtype == torch.float16 else 4)
-    assert g.sub_impl == 7 and g.sub_tiles[0] > 1
+    bucket_qbands(g, k, impl=8, elem_bytes=2 if dtype == torch.float16 else 4)
+    assert g.sub_impl == 8 and g.sub_tiles[0] > 1
     P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
     Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
     if dtype == torch.float16:
@@ -1023,84 +1023,8 @@ def test_ptile_conflict_free_equals_oracle(dev, k, dtype):
     assert rel_err(Q.double().cpu().numpy(), Qe) < tol
 
 
-@pytest.mark.parametrize("k,dtype", [(128, torch.float32), (32, torch.float32),
-                                     (256, torch.float32), (64, torch.float16)])
-def test_ptile_item_runs_equal_sequential_replay(dev, k, dtype):
-    """Implementation 7 along item runs: every user rated once (no P race)
-    and every item rated inside one row tile only (no concurrent Q deltas),
-    so the kernel is exactly a sequential replay of its own visit order —
-    batches of LPC ratings rotated by the bin's seed, the partial batch last
-    (ptile.cuh take/bstart) — of the reference update (oracle, f64), one
-    rating at a time.  Pins the scaled-Q chain arithmetic (q = sq * qs, the
-    rescale, the Q delta reductions) on runs of 1-12 ratings."""
-    import oracle
-    from paper_2006_15980_b200 import _lib, kernels
-    from paper_2006_15980_b200.data import (DeviceTriples, RatingMatrix, bucket_qbands,
-                                            build_device_grid, ptile_row_cuts)
-    f16 = dtype == torch.float16
-    rng = np.random.default_rng(100 + k)
-    n_users, n_items = 120_000, 12_000
-    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    tiles = ptile_row_cuts(0, n_users, k, f16, n_sm)
-    T = len(tiles) - 1
-    free = [list(rng.permutation(np.arange(tiles[t], tiles[t + 1]))) for t in range(T)]
-    users, items = [], []
-    for v in range(n_items):
-        t = v % T
-        r = min(len(free[t]), int(rng.integers(1, 13)))
-        for _ in range(r):
-            users.append(free[t].pop())
-            items.append(v)
-    users = np.asarray(users, dtype=np.int32)
-    items = np.asarray(items, dtype=np.int32)
-    perm = rng.permutation(len(users))
-    users, items = users[perm], items[perm]
-    n = len(users)
-    vals = rng.uniform(0, 1, n).astype(np.float32).astype(np.float64)
-    m = RatingMatrix(n_users, n_items, users, items, vals)
-    g = build_device_grid(DeviceTriples.from_host(m, dev), [0, n_users],
-                          [0, n_items // 2, n_items])
-    bucket_qbands(g, k, impl=7, elem_bytes=2 if f16 else 4)
-    assert g.sub_impl == 7 and all(np.array_equal(r, tiles) for r in g.sub_tile_rows)
-    P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
-    Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
-    if f16:
-        P0, Q0 = P0.astype(np.float16).astype(np.float32), Q0.astype(np.float16).astype(np.float32)
-    P, Q = to_dev(P0, dev, dtype), to_dev(Q0, dev, dtype)
-    lr, ru, ri = 0.05, 0.02, 0.03
-    seeds = [kernels.mix64(3, b) for b in range(g.n_blocks)]
-    got = sum(kernels.launch_block_qband(P, Q, g, b, lr, ru, ri, seeds[b])
-              for b in range(g.n_blocks))
-    assert got == n
-    # the replay: per bin, the kernel's visit order, one rating at a time
-    lpc = 16 if k >= 256 else (8 if k >= 64 else 4)
-    gu, gi, gr = g.users.cpu().numpy(), g.items.cpu().numpy(), g.ratings.cpu().numpy()
-    gr = gr.astype(np.float64)
-    Pe, Qe = P0.astype(np.float64), Q0.astype(np.float64)
-    from paper_2006_15980_b200.kernels import _MASK64
-    for b in range(g.n_blocks):
-        sp = g.sub_ptr[b].cpu().numpy()
-        S = (len(sp) - 1) // g.sub_tiles[b]
-        for t in range(g.sub_tiles[b]):
-            for s_ in range(S):
-                beg, end = int(sp[t * S + s_]), int(sp[t * S + s_ + 1])
-                nf = (end - beg) // lpc
-                order = []
-                if nf:
-                    rot = _fin((seeds[b] + (t * S + s_) * 0x9E3779B97F4A7C15) & _MASK64) % nf
-                    for x in range(nf):
-                        c = (x + rot) % nf
-                        order.extend(range(beg + c * lpc, beg + (c + 1) * lpc))
-                order.extend(range(beg + nf * lpc, end))
-                for i in order:
-                    oracle.sgd_range(Pe, Qe, gu, gi, gr, i, i + 1, lr, ru, ri, 0, 0, 0)
-    tol = 2e-3 if f16 else 1e-5
-    assert rel_err(P.double().cpu().numpy(), Pe) < tol
-    assert rel_err(Q.double().cpu().numpy(), Qe) < tol
-
-
 def _runs_problem(dev, k, f16, seed, n_users=120_000, n_items=12_000, max_run=13):
-    """Distinct users, every item inside one row tile (implementation 7/8
+    """Distinct users, every item inside one row tile (implementation 8
     tiles): runs never race and never go stale."""
     from paper_2006_15980_b200.data import ptile_row_cuts
     rng = np.random.default_rng(seed)

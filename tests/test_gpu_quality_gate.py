@@ -75,14 +75,13 @@ def test_headline_path_rmse_within_0005_of_reference(hetmf, data, k, precision):
         assert gaps[0] <= 0.003, (ours[0], ref[0])
 
 
-@pytest.mark.parametrize("impl", [5, 7, 8])
+@pytest.mark.parametrize("impl", [5, 8])
 @pytest.mark.parametrize("precision", ["f32", "f16"])
 @pytest.mark.parametrize("k", [128, 32, 64, 256])
 def test_each_engine_kernel_rmse_within_0005_of_reference(hetmf, data, k, precision, impl):
     """Every engine kernel on the same gate: 5 (L2 row tiles, split item runs
-    with Q deltas, csrc/qchain.cuh; P by stores in fp32 at k >= 128), 7
-    (tile-resident P, item bins, csrc/ptile.cuh) and 8 (run groups over it,
-    csrc/runs.cuh)."""
+    with Q deltas, csrc/qchain.cuh; P by stores in fp32 at k >= 128) and 8
+    (run groups over a tile-resident P, csrc/runs.cuh)."""
     train, test, _, _ = data
     ref, init = _reference(hetmf, data, k)
     ours, grid = qgate.ours_rmse(_fresh(train), test, init, k, precision, EPOCHS, impl=impl)
