@@ -38,16 +38,24 @@ cudaError_t kernel_occupancy(const void* kern, int threads, int smem, int* per_s
   if (e != cudaSuccess) return e;
   static std::mutex mu;
   static std::map<std::tuple<const void*, int, int, int>, int> cache;
+  // the dynamic shared-memory limit set per (kernel, device): it only ever
+  // grows, so a launch with less shared memory never lowers it under one
+  // whose occupancy was cached with more
+  static std::map<std::pair<const void*, int>, int> limit;
   const auto key = std::make_tuple(kern, dev, threads, smem);
   std::lock_guard<std::mutex> lock(mu);
+  if (smem > 48 * 1024) {
+    int& lim = limit[std::make_pair(kern, dev)];
+    if (smem > lim) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      lim = smem;
+    }
+  }
   auto it = cache.find(key);
   if (it != cache.end()) {
     *per_sm = it->second;
     return cudaSuccess;
-  }
-  if (smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
   }
   int n = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, size_t(smem));

@@ -1045,6 +1045,34 @@ def _runs_problem(dev, k, f16, seed, n_users=120_000, n_items=12_000, max_run=13
     return users[perm], items[perm], tiles, rng
 
 
+def test_runs_tile_sizes_interleave(dev):
+    """One kernel launched with large, then small, then large P tiles (a
+    resident layout and a streamed 256-row one in the same process): the
+    dynamic shared-memory limit must never drop under a size launched
+    before (util.cu kernel_occupancy)."""
+    from paper_2006_15980_b200 import kernels
+    from paper_2006_15980_b200.data import (DeviceTriples, RatingMatrix, bucket_qbands,
+                                            build_device_grid)
+    rng = np.random.default_rng(5)
+    n_users, n_items, n = 120_000, 3_000, 600_000
+    cells = rng.choice(n_users * n_items, n, replace=False)
+    m = RatingMatrix(n_users, n_items, (cells // n_items).astype(np.int32),
+                     (cells % n_items).astype(np.int32), rng.uniform(0, 1, n))
+    P0 = rng.uniform(0, 0.1, size=(n_users, 128)).astype(np.float32)
+    Q0 = rng.uniform(0, 0.1, size=(n_items, 128)).astype(np.float32)
+    grids = {}
+    for rows in (None, 64):
+        g = build_device_grid(DeviceTriples.from_host(m, dev), [0, n_users], [0, n_items])
+        bucket_qbands(g, 128, impl=8, max_tile_rows=rows)
+        grids[rows] = g
+    assert grids[None].sub_max_rows > 4 * grids[64].sub_max_rows
+    P, Q = torch.from_numpy(P0).to(dev), torch.from_numpy(Q0).to(dev)
+    for rows in (None, 64, None):
+        assert kernels.launch_block_qband(P, Q, grids[rows], 0, 0.005, 0.05, 0.05, 1) == n
+    torch.cuda.synchronize(dev)
+    assert bool(torch.isfinite(P).all()) and bool(torch.isfinite(Q).all())
+
+
 def test_runs_layout_contract(dev):
     """Implementation 8's layout: inside each row tile, runs (one item each,
     the block's order kept) sorted by length, longest first; run / tile
