@@ -153,9 +153,11 @@ __global__ void __launch_bounds__(WPB * 32, 1)
   extern __shared__ __align__(16) unsigned char runs_smem[];
   S* tile = reinterpret_cast<S*>(runs_smem);
   __shared__ unsigned next_group;
-  // per-warp scratch for the dot-product reduction (kSmemReduce)
-  // (measured: +2-4 % for fp32 at k = 32-128; slower at k = 256 and for fp16)
-  constexpr bool kSmemReduce = RUNS_SMEM_REDUCE && LPC >= 4 && LPC <= 8 && sizeof(S) == 4;
+  // per-warp scratch for the dot-product reduction (kSmemReduce), at 4-8
+  // lanes per chain: +2-4 % for fp32; fp16 +1.6 % at 8 lanes (k = 128) but
+  // -3.3 % at 4 (k = 64, profiles/round2/s4_f16_reduce_ab.jsonl)
+  constexpr bool kSmemReduce =
+      RUNS_SMEM_REDUCE && LPC >= 4 && LPC <= 8 && (sizeof(S) == 4 || LPC == 8);
   __shared__ __align__(16) float red_all[kSmemReduce ? WPB * 32 : 4];
   const int lane = threadIdx.x & 31, c = lane / LPC, l = lane % LPC;
   float* red = red_all + (kSmemReduce ? (threadIdx.x >> 5) * 32 : 0);
