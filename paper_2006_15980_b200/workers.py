@@ -113,6 +113,10 @@ class FactorStore:
         self.home_q = np.full(model.n_items, HOST, dtype=np.int16)
         self.replicas: dict[int, tuple] = {}
         self.events: dict[int, object] = {}
+        # engines per device: with one, every recorded event is on that
+        # engine's stream (or a gather's), so a device's latest event covers
+        # all of its earlier work
+        self.engines_on: dict[int, int] = {}
         self.grids: dict[int, DeviceGrid] = {}
         self.host_grid = grid
         self.copy_streams: dict[int, object] = {}
@@ -279,6 +283,8 @@ class BatchEngine:
         self.resident = None
         self.staged: dict = {}
         self._owns_store = store is None
+        with self.store.lock:
+            self.store.engines_on[self.dev] = self.store.engines_on.get(self.dev, 0) + 1
 
     def close(self):
         if self._owns_store:
@@ -435,9 +441,12 @@ class BatchWorker(threading.Thread):
                 if lease.prefetch is None:
                     engine.flush_rows()
                 # the next owner of this unit's bands must see finished data:
-                # homes carry the completion event, so only the lease release
-                # (host bookkeeping) waits for the kernel here
-                engine.synchronize()
+                # homes carry the completion event (stage_out / flush_rows),
+                # and a puller's stream waits on it.  That event is the
+                # device's latest only while one engine runs there; with
+                # several on one device the release waits for the kernel.
+                if engine.store.engines_on.get(engine.dev, 0) > 1:
+                    engine.synchronize()
                 nxt = self.scheduler.release(lease, done)
                 if nxt is None:
                     engine.staged.clear()
