@@ -1059,6 +1059,8 @@ def main():
                     help="cap on users per row tile (default data.QBAND_MAX_TILE_ROWS; 0 = none)")
     ap.add_argument("--tile-mb", type=float, default=None,
                     help="P rows per Q-band row tile in MiB (default data.QBAND_TILE_BYTES; 0 = no byte bound)")
+    ap.add_argument("--tile-stagger", action="store_true",
+                    help="experimental: uneven first/last P tiles per CTA (data.PTILE_STAGGER)")
     ap.add_argument("--sim-world", type=int, default=0,
                     help="N=1 only: run rank 0 of an N-GPU job's geometry (projected per-GPU rate)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -1068,6 +1070,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.tile_stagger:
+        import paper_2006_15980_b200.data as _data
+        _data.PTILE_STAGGER = True
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
         # `python bench.py --gpus N`: one process per GPU, launched here
         sys.exit(self_launch(args.gpus, sys.argv[1:]))

@@ -818,12 +818,14 @@ PTILE_MIN_ROWS = 64
 
 
 def ptile_row_cuts(r_lo: int, r_hi: int, k: int, f16: bool, n_sm: int,
-                   max_rows: int | None = None) -> np.ndarray:
+                   max_rows: int | None = None, stagger: bool = False) -> np.ndarray:
     """Row tiles of implementation 8 (tile-resident P): the fewest
     equal tiles whose P rows fit one CTA's shared memory (hmf_ptile_max_rows),
     at least one per SM when that leaves PTILE_MIN_ROWS rows per tile (a CTA
     trains one tile at a time) — rounded up to a multiple of the SM count,
-    so the persistent CTAs finish their last tiles together."""
+    so the persistent CTAs finish their last tiles together.  With
+    `stagger` (or PTILE_STAGGER) and at least two waves, the first and last
+    tile of each CTA are uneven (_staggered_cuts)."""
     n = r_hi - r_lo
     cap = int(_lib.load().hmf_ptile_max_rows(int(k), 1 if f16 else 0))
     if max_rows:
@@ -834,7 +836,33 @@ def ptile_row_cuts(r_lo: int, r_hi: int, k: int, f16: bool, n_sm: int,
     if t > n_sm // 2:
         t = -(-t // n_sm) * n_sm
     t = max(1, min(n, t))
+    if (stagger or PTILE_STAGGER) and t % n_sm == 0 and t // n_sm >= 2:
+        return _staggered_cuts(r_lo, r_hi, t // n_sm, n_sm)
     return np.linspace(r_lo, r_hi, t + 1).round().astype(np.int64)
+
+
+# Staggered tile switches: every CTA moves its P tile at the same moments
+# when tiles are equal, and those switches are L2-throughput bound (~60 MB
+# at once, ~5 us).  Staggered, the first and last tile of CTA i are f_i and
+# 1 - f_i of a tile (f_i spread over [0, 1)), so the switches of different
+# CTAs fall at different times.  Worth it only where a tile trains briefly:
+# at the 8-GPU geometry (5 k ratings per tile) +2.9 %, at N = 1 (42 k) -4 to
+# -9 % (the partial tiles' shorter runs; profiles/round2/s4_stagger.jsonl).
+# _bucket_runs staggers resident layouts below PTILE_STAGGER_BELOW ratings
+# per tile; PTILE_STAGGER forces it everywhere (experiments, tests).
+PTILE_STAGGER = False
+PTILE_STAGGER_BELOW = 10_000
+PTILE_STAGGER_MIN_BLOCK = 1_000_000
+
+
+def _staggered_cuts(r_lo: int, r_hi: int, waves: int, n_sm: int) -> np.ndarray:
+    R = (r_hi - r_lo) / (waves * n_sm)
+    f = ((np.arange(n_sm) * 53) % n_sm) / n_sm
+    sizes = np.concatenate([f * R, np.full((waves - 1) * n_sm, R), (1 - f) * R])
+    cuts = r_lo + np.concatenate([[0.0], np.cumsum(sizes)])
+    cuts = cuts.round().astype(np.int64)
+    cuts[-1] = r_hi
+    return cuts
 
 
 def _coprime_multiplier(w: int) -> int:
@@ -880,6 +908,9 @@ def _bucket_runs(grid: DeviceGrid, k: int, f16: bool, max_rows: int | None) -> D
         c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
         r_lo, r_hi = grid.row_span(b // grid.n_col_bands)
         tiles = ptile_row_cuts(r_lo, r_hi, k, f16, n_sm, max_rows)
+        if (max_rows is None and hi - lo >= PTILE_STAGGER_MIN_BLOCK
+                and hi - lo < PTILE_STAGGER_BELOW * (len(tiles) - 1)):
+            tiles = ptile_row_cuts(r_lo, r_hi, k, f16, n_sm, max_rows, stagger=True)
         T = len(tiles) - 1
         W = max(1, c_hi - c_lo)
         if hi - lo >= (1 << 31):

@@ -1123,16 +1123,22 @@ def test_runs_layout_contract(dev):
         assert np.array_equal(r, orr[pos])
 
 
-@pytest.mark.parametrize("k,dtype", [(128, torch.float32), (32, torch.float32),
-                                     (256, torch.float32), (64, torch.float16)])
-def test_runs_equal_sequential_replay(dev, k, dtype):
+@pytest.mark.parametrize("k,dtype,stagger", [(128, torch.float32, False),
+                                             (32, torch.float32, False),
+                                             (256, torch.float32, False),
+                                             (64, torch.float16, False),
+                                             (128, torch.float32, True)])
+def test_runs_equal_sequential_replay(dev, k, dtype, stagger, monkeypatch):
     """Implementation 8 (run groups): with no P race and no concurrent Q
     deltas (distinct users, items inside one tile) the kernel is exactly a
     sequential replay, run by run, of its visit order — each run from its
     seeded rotation (runs.cuh stage_group) — of the reference update (oracle,
-    f64), one rating at a time."""
+    f64), one rating at a time.  Also with staggered tiles (uneven first
+    and last tile per CTA, an empty one among them; data._staggered_cuts)."""
     import oracle
+    from paper_2006_15980_b200 import data as hdata
     from paper_2006_15980_b200 import kernels
+    monkeypatch.setattr(hdata, "PTILE_STAGGER", stagger)
     from paper_2006_15980_b200.data import (DeviceTriples, RatingMatrix, bucket_qbands,
                                             build_device_grid)
     from paper_2006_15980_b200.kernels import _MASK64

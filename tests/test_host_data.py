@@ -169,3 +169,23 @@ def test_run_rotation_range_and_spread():
             assert (counts > 0).mean() > 0.95
     assert run_rotation(7, 3, 10) == run_rotation(7, 3, 10)
     assert [run_rotation(s, 3, 1000) for s in range(5)] != [run_rotation(0, 3, 1000)] * 5
+
+
+def test_staggered_tile_cuts():
+    """data._staggered_cuts: CTA i (tiles i, i + n_sm, ...) gets an uneven
+    first and last tile (f_i and 1 - f_i of a full one) and full tiles in
+    between, so every CTA trains the same rows and the tile switches of
+    different CTAs fall at different times; cuts are monotonic and cover
+    the band exactly."""
+    import numpy as np
+    from paper_2006_15980_b200.data import _staggered_cuts
+    n_sm, waves = 148, 8
+    cuts = _staggered_cuts(1000, 481_000, waves, n_sm)
+    sizes = np.diff(cuts)
+    assert cuts[0] == 1000 and cuts[-1] == 481_000 and np.all(sizes >= 0)
+    assert len(sizes) == (waves + 1) * n_sm
+    per_cta = sizes.reshape(waves + 1, n_sm).sum(axis=0)
+    assert per_cta.max() - per_cta.min() <= waves + 1  # rounding only
+    first = sizes[:n_sm]
+    assert len(np.unique(first)) > n_sm // 2          # switches spread out
+    assert np.all(sizes[n_sm:-n_sm] >= 405) and np.all(sizes <= 406)
