@@ -50,7 +50,8 @@ extern "C" {
 
 /* ABI 4: launch options per call (hmf_qband_opts).  ABI 5: implementation 7
  * (hmf_sgd_block_ptile_*, hmf_ptile_bins_per_tile) removed;
- * hmf_runs_chains_per_warp takes the element size; hmf_lease_claim added. */
+ * hmf_runs_chains_per_warp takes the element size; hmf_lease_claim added;
+ * hmf_qband_opts.runs_wide. */
 #define HMF_ABI_VERSION 5
 
 #define HMF_OK 0
@@ -159,6 +160,11 @@ typedef struct hmf_qband_opts {
   /* Chains of a warp change bins together: bit 0 static, bit 1 dynamic
    * scheduler; -1 = 3. */
   int32_t lockstep;
+  /* Implementation 8 at k = 32: 1 = more run-group chains per SM (fp32: 20
+   * warps; fp16: 2-lane chains), 8-12 % faster but each item's Q changes
+   * land staler — data.bucket_qbands sets it only under the staleness
+   * bound; -1 / 0 = the default 128 chains per SM.  Ignored elsewhere. */
+  int32_t runs_wide;
 } hmf_qband_opts;
 
 /* Default implementation / chain configuration for k and storage. */

@@ -173,7 +173,7 @@ class QbandOpts(C.Structure):
     """hmf_qband_opts (include/hmf.h): per-launch options of the Q-band
     kernels; -1 in a field means the library default."""
     _fields_ = [("impl", _i32), ("chain_cfg", _i32), ("pstore", _i32), ("qsync", _i32),
-                ("grid_share", _i32), ("lockstep", _i32)]
+                ("grid_share", _i32), ("lockstep", _i32), ("runs_wide", _i32)]
 
     def __init__(self, **kw):
         vals = {name: -1 for name, _ in self._fields_}

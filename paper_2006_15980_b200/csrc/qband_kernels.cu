@@ -305,6 +305,9 @@ static int64_t resolve_opts(const hmf_qband_opts* in, int64_t k, bool f16, Launc
   if (in && (in->lockstep < -1 || in->lockstep > 3))
     return set_error(HMF_ERR_ARG, "lockstep must be -1..3");
   o->lockstep = in && in->lockstep >= 0 ? in->lockstep : 3;
+  if (in && (in->runs_wide < -1 || in->runs_wide > 1))
+    return set_error(HMF_ERR_ARG, "runs_wide must be -1, 0 or 1");
+  o->wide = in && in->runs_wide == 1 ? 1 : 0;
   return HMF_OK;
 }
 
@@ -395,14 +398,20 @@ static int64_t run_u16(S* P, S* Q, int64_t k, const uint16_t* rows, const int32_
 }
 
 // implementation 8: run groups over a tile-resident P (runs.cuh)
-template <int K, typename S, typename RowT>
+template <int K, typename S, typename RowT, bool Wide = false>
 static cudaError_t launch_runs(S* P, S* Q, const RowT* rows, const float* vals,
                                const int32_t* runs, const int32_t* tile_run,
                                const int32_t* tile_cut, int n_tiles,
                                int max_rows, double lr, double ru, double ri, uint64_t seed,
                                int64_t row_base, int64_t col_base, cudaStream_t stream,
                                const LaunchOpts& o) {
-  using C = RunsCfg<K, S>;
+  if constexpr (K == 32 && !Wide) {
+    if (o.wide)
+      return launch_runs<K, S, RowT, true>(P, Q, rows, vals, runs, tile_run, tile_cut, n_tiles,
+                                           max_rows, lr, ru, ri, seed, row_base, col_base,
+                                           stream, o);
+  }
+  using C = RunsCfg<K, S, Wide>;
   auto kern = runs_kernel<K, S, C::LPC, C::WPB, RowT>;
   const int smem = max_rows * K * int(sizeof(S));
   int per_sm = 0;
@@ -472,7 +481,10 @@ static int slots_per_sm(int64_t k, const hmf_qband_opts* opts) {
 #define HMF_WPS(KK)                                                                        \
   case KK:                                                                                 \
     e = o.impl == 0 ? warp_slots_per_sm<KK, S>(&n)                                         \
-        : o.impl == 8 ? (n = RunsCfg<KK, S>::WPB * 32 / RunsCfg<KK, S>::LPC, cudaSuccess)         \
+        : o.impl == 8 ? (n = o.wide && KK == 32                                            \
+                             ? RunsCfg<KK, S, true>::WPB * 32 / RunsCfg<KK, S, true>::LPC       \
+                             : RunsCfg<KK, S>::WPB * 32 / RunsCfg<KK, S>::LPC,                  \
+                         cudaSuccess)         \
                       : chain_slots_per_sm<KK, S>(o.cfg, &n);                                \
     break;
     HMF_WPS(32)

@@ -417,6 +417,7 @@ struct LaunchOpts {
   int qsync;     // implementation 5: ratings between Q publications (0 = item/bin changes)
   int share;     // grid capped at 1/share of the resident CTA slots
   int lockstep;  // chains change bins together: bit 0 static, bit 1 dynamic scheduler
+  int wide;      // implementation 8 at k = 32: the wide run-group configuration
 };
 
 static inline int grid_share(int cap, int share) {

@@ -64,10 +64,16 @@ constexpr int kPTileBytes = 208 * 1024;
 // 2 %-density blocks of test_default_layout_quality_matches_whole_runs
 // (fp32 k = 32) the RMSE after 8 epochs goes 0.1222 / 0.1232 / 0.138 / 0.33
 // at 16 / 17 / 18 / 20 warps (profiles/round2/s4_wpb_quality.txt).
-template <int K, typename S> struct RunsCfg {
+// Wide (k = 32 only, hmf_qband_opts.runs_wide): 160 chains per SM for fp32
+// (20 warps of 4-lane chains), 256 for fp16 (2-lane chains) — the faster
+// shapes the staleness bound keeps off narrow blocks.
+template <int K, typename S, bool Wide = false> struct RunsCfg {
   static constexpr bool kWide = K >= 256 && sizeof(S) == 4;
-  static constexpr int kLPC = sizeof(S) == 2 ? (K <= 64 ? 4 : K / 16) : (K >= 128 ? 8 : 4);
-  static constexpr int kWPB = kWide ? 8 : 16;
+  static constexpr bool kMore = Wide && K == 32;
+  static constexpr int kLPC = kMore ? (sizeof(S) == 2 ? 2 : 4)
+                                    : (sizeof(S) == 2 ? (K <= 64 ? 4 : K / 16)
+                                                      : (K >= 128 ? 8 : 4));
+  static constexpr int kWPB = kWide ? 8 : (kMore && sizeof(S) == 4 ? 20 : 16);
 #ifdef RUNS_EXP_K  // A/B builds (scripts/build_variant.sh): one (k, element size) overridden
   static constexpr bool kExp = K == RUNS_EXP_K && sizeof(S) == RUNS_EXP_S;
   static constexpr int LPC = kExp ? RUNS_EXP_LPC : kLPC;

@@ -385,6 +385,7 @@ class DeviceGrid:
     sub_tile_cuts: list | None = None   # implementation 8: per block, device int32 tile cuts
     sub_max_rows: int = 0               # implementation 8: rows of the largest tile
     sub_tile_run: list | None = None    # implementation 8: per block, first run of each tile
+    sub_wide: int = 0                   # implementation 8 at k = 32: the wide configuration
 
     n_row_bands = BlockGrid.n_row_bands
     n_col_bands = BlockGrid.n_col_bands
@@ -487,10 +488,11 @@ TILE_RESIDENT_MIN_RUN = 2.0
 TILE_RESIDENT_MAX_STALE = 250.0
 
 
-def runs_chains_per_sm(k: int, f16: bool) -> int:
+def runs_chains_per_sm(k: int, f16: bool, wide: bool = False) -> int:
     """Run-group chains resident per SM (implementation 8's configuration
-    for k and the element size, hmf_qband_slots_per_sm)."""
-    opts = _lib.QbandOpts(impl=8)
+    for k and the element size, hmf_qband_slots_per_sm; `wide`: the k = 32
+    wide one)."""
+    opts = _lib.QbandOpts(impl=8, runs_wide=1 if wide else 0)
     return int(_lib.check(_lib.load().hmf_qband_slots_per_sm(int(k), 1 if f16 else 0,
                                                               ctypes.byref(opts)),
                           "hmf_qband_slots_per_sm"))
@@ -509,8 +511,8 @@ def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> 
       Q row; the item-split kernel (5) handles that case;
     * Q staleness S <= TILE_RESIDENT_MAX_STALE (few items for the runs in
       flight: narrow column blocks).
-    Returns 8 (Netflix fp32 k = 32 / 64 / 128 / 256: 68.9 / 39.7 / 19.4 / 7.5
-    G upd/s against 30.6 / 19.7 / 11.8 / 5.9 for implementation 5; fp16 72 /
+    Returns 8 (Netflix fp32 k = 32 / 64 / 128 / 256: 73.6 / 39.7 / 19.4 / 7.5
+    G upd/s against 30.6 / 19.7 / 11.8 / 5.9 for implementation 5; fp16 82 /
     49 / 22.5 / 9.3 against 42 / 27 / 16.4 / 8.5; profiles/round2/
     s4_ksweep.jsonl)."""
     torch = _torch()
@@ -967,6 +969,21 @@ def _bucket_runs(grid: DeviceGrid, k: int, f16: bool, max_rows: int | None) -> D
     grid.sub_tile_cuts = tile_cuts
     grid.sub_max_rows = max((int(np.max(np.diff(t))) for t in tile_rows if len(t) > 1),
                             default=1)
+    # k = 32: the wide configuration (more chains per SM, faster) wherever
+    # its staleness stays under the bound in every block
+    grid.sub_wide = 0
+    if k == 32:
+        wide = runs_chains_per_sm(k, f16, wide=True)
+        ok = True
+        for b in range(grid.n_blocks):
+            lo, hi = grid.block_range(b)
+            if hi <= lo:
+                continue
+            c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
+            W, T = max(1, c_hi - c_lo), max(1, n_tiles[b])
+            if wide * min(T, n_sm) * ((hi - lo) / (T * W)) / W > TILE_RESIDENT_MAX_STALE:
+                ok = False
+        grid.sub_wide = int(ok)
     return grid
 
 

@@ -127,6 +127,8 @@ def qband_opts(grid=None, **overrides) -> "QbandOpts":
         vals["pstore"] = int(getattr(grid, "sub_pstore", 0) or 0)
         q = int(getattr(grid, "sub_qsync", 0) or 0)
         vals["qsync"] = q if q > 0 else -1
+        if int(getattr(grid, "sub_wide", 0) or 0):
+            vals["runs_wide"] = 1
     vals.update({k: v for k, v in overrides.items() if v is not None})
     return QbandOpts(**vals)
 

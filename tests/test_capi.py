@@ -54,7 +54,8 @@ def test_host_only_entry_points():
     tail = (0.01, 0.0, 0.0, 0, 0, 0, None)
     for bad in ({"pstore": 2}, {"impl": 1}, {"impl": 3}, {"impl": 7}, {"chain_cfg": 0},
                 {"chain_cfg": 3},
-                {"grid_share": 0}, {"grid_share": 65}, {"lockstep": 4}, {"qsync": -2}):
+                {"grid_share": 0}, {"grid_share": 65}, {"lockstep": 4}, {"qsync": -2},
+                {"runs_wide": 2}, {"runs_wide": -2}):
         o = _lib.QbandOpts(**bad)
         assert lib.hmf_sgd_block_qband_f32(*args, ctypes.byref(o), *tail) == _lib.HMF_ERR_ARG, bad
     assert lib.hmf_qband_resolve_impl(128, 0) == 5

@@ -1123,18 +1123,21 @@ def test_runs_layout_contract(dev):
         assert np.array_equal(r, orr[pos])
 
 
-@pytest.mark.parametrize("k,dtype,stagger", [(128, torch.float32, False),
-                                             (32, torch.float32, False),
-                                             (256, torch.float32, False),
-                                             (64, torch.float16, False),
-                                             (128, torch.float32, True)])
-def test_runs_equal_sequential_replay(dev, k, dtype, stagger, monkeypatch):
+@pytest.mark.parametrize("k,dtype,stagger,wide", [(128, torch.float32, False, 0),
+                                                  (32, torch.float32, False, 0),
+                                                  (32, torch.float32, False, 1),
+                                                  (32, torch.float16, False, 1),
+                                                  (256, torch.float32, False, 0),
+                                                  (64, torch.float16, False, 0),
+                                                  (128, torch.float32, True, 0)])
+def test_runs_equal_sequential_replay(dev, k, dtype, stagger, wide, monkeypatch):
     """Implementation 8 (run groups): with no P race and no concurrent Q
     deltas (distinct users, items inside one tile) the kernel is exactly a
     sequential replay, run by run, of its visit order — each run from its
     seeded rotation (runs.cuh stage_group) — of the reference update (oracle,
     f64), one rating at a time.  Also with staggered tiles (uneven first
-    and last tile per CTA, an empty one among them; data._staggered_cuts)."""
+    and last tile per CTA, an empty one among them; data._staggered_cuts)
+    and in the k = 32 wide configuration (hmf_qband_opts.runs_wide)."""
     import oracle
     from paper_2006_15980_b200 import data as hdata
     from paper_2006_15980_b200 import kernels
@@ -1152,6 +1155,7 @@ def test_runs_equal_sequential_replay(dev, k, dtype, stagger, monkeypatch):
                           [0, n_items // 2, n_items])
     bucket_qbands(g, k, impl=8, elem_bytes=2 if f16 else 4)
     assert g.sub_impl == 8 and all(np.array_equal(r, tiles) for r in g.sub_tile_rows)
+    g.sub_wide = wide
     P0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_users, k)).astype(np.float32)
     Q0 = rng.uniform(0, 1 / np.sqrt(k), size=(n_items, k)).astype(np.float32)
     if f16:
@@ -1208,3 +1212,11 @@ def test_tile_resident_policy(dev):
     narrow = grid(120_000, 1_200, 3_000_000)
     assert tile_resident_impl(narrow, 32, False) is None
     assert tile_resident_impl(narrow, 128, False) == 8
+    # the k = 32 wide configuration (160 / 256 chains per SM) only under the
+    # same bound: on at Netflix density, off on the narrow blocks
+    from paper_2006_15980_b200.data import bucket_qbands
+    assert bucket_qbands(grid(120_000, 17_700, 25_000_000), 32, impl=8).sub_wide == 1
+    assert bucket_qbands(grid(120_000, 17_700, 25_000_000), 32, impl=8,
+                         elem_bytes=2).sub_wide == 1
+    assert bucket_qbands(narrow, 32, impl=8).sub_wide == 0
+    assert bucket_qbands(grid(120_000, 17_700, 25_000_000), 64, impl=8).sub_wide == 0
