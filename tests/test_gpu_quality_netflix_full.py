@@ -31,13 +31,19 @@ def hetmf():
     return reference.hetmf()
 
 
-def test_netflix_full_size_rmse_within_0005_of_reference(hetmf):
+@pytest.mark.parametrize("k,precision", [(K, "f32"), (32, "f32"), (32, "f16")])
+def test_netflix_full_size_rmse_within_0005_of_reference(hetmf, k, precision):
+    """Also at k = 32 (BASELINE configs[4]), where the layout picks the wide
+    run-group configuration (160 / 256 chains per SM) under the staleness
+    bound."""
     train, test, tr, te = qgate.problem(N_USERS, N_ITEMS, NNZ, seed=0,
                                         device=torch.device("cuda", 0))
-    ref, init = qgate.reference_rmse(hetmf, N_USERS, N_ITEMS, K, tr, te, EPOCHS)
-    ours, grid = qgate.ours_rmse(train, test, init, K, "f32", EPOCHS)
-    print(f"NF full size: layout impl {grid.sub_impl} tiles {grid.sub_tiles}; "
+    ref, init = qgate.reference_rmse(hetmf, N_USERS, N_ITEMS, k, tr, te, EPOCHS)
+    ours, grid = qgate.ours_rmse(train, test, init, k, precision, EPOCHS)
+    print(f"NF full size k={k} {precision}: layout impl {grid.sub_impl} wide {grid.sub_wide} "
+          f"tiles {grid.sub_tiles}; "
           f"ours {np.round(ours, 5).tolist()} reference {np.round(ref, 5).tolist()}")
     assert grid.sub_impl == 8
+    assert grid.sub_wide == (1 if k == 32 else 0)
     gaps = np.abs(np.asarray(ours) - np.asarray(ref))
     assert np.all(gaps <= 0.005), (ours, ref)
