@@ -488,6 +488,18 @@ TILE_RESIDENT_MIN_RUN = 2.0
 TILE_RESIDENT_MAX_STALE = 250.0
 
 
+def run_group_staleness(chains_per_sm: int, n_sm: int, ratings: int, tiles: int,
+                        items: int) -> float:
+    """S of TILE_RESIDENT_MAX_STALE for one block: the ratings of an item
+    training at once against one stale Q row — chains in flight (chains per
+    SM x the CTAs, one per SM up to the tiles) spread over the block's items,
+    times the mean run length (ratings per tile and item)."""
+    items = max(1, int(items))
+    tiles = max(1, int(tiles))
+    run_len = ratings / (tiles * items)
+    return chains_per_sm * min(tiles, n_sm) * run_len / items
+
+
 def runs_chains_per_sm(k: int, f16: bool, wide: bool = False) -> int:
     """Run-group chains resident per SM (implementation 8's configuration
     for k and the element size, hmf_qband_slots_per_sm; `wide`: the k = 32
@@ -534,7 +546,7 @@ def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> 
         run_len = (hi - lo) / (T * W)
         if T < n_sm or run_len < TILE_RESIDENT_MIN_RUN:
             return None
-        if chains * min(T, n_sm) * run_len / W > TILE_RESIDENT_MAX_STALE:
+        if run_group_staleness(chains, n_sm, hi - lo, T, W) > TILE_RESIDENT_MAX_STALE:
             return None
         cnt = torch.bincount(grid.items[lo:hi] - c_lo, minlength=W)
         if float(cnt.max()) > 4 * (hi - lo) / W:
@@ -981,7 +993,7 @@ def _bucket_runs(grid: DeviceGrid, k: int, f16: bool, max_rows: int | None) -> D
                 continue
             c_lo, c_hi = grid.col_span(b % grid.n_col_bands)
             W, T = max(1, c_hi - c_lo), max(1, n_tiles[b])
-            if wide * min(T, n_sm) * ((hi - lo) / (T * W)) / W > TILE_RESIDENT_MAX_STALE:
+            if run_group_staleness(wide, n_sm, hi - lo, T, W) > TILE_RESIDENT_MAX_STALE:
                 ok = False
         grid.sub_wide = int(ok)
     return grid

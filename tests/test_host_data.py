@@ -189,3 +189,20 @@ def test_staggered_tile_cuts():
     first = sizes[:n_sm]
     assert len(np.unique(first)) > n_sm // 2          # switches spread out
     assert np.all(sizes[n_sm:-n_sm] >= 405) and np.all(sizes <= 406)
+
+
+def test_run_group_staleness_bound():
+    """data.run_group_staleness against the numbers the layout policy was
+    calibrated on: Netflix at N = 1 (two 8 850-item blocks,
+    50 M ratings, 1 184 tiles, 128 chains per SM) ~10.5; one of 17 column
+    bands at N = 8 ~89; the narrow 600-item blocks at 2 % density ~500
+    (k = 32: 128 chains, 148 tiles) — over TILE_RESIDENT_MAX_STALE; and the
+    k = 32 wide configuration (160 chains) stays far under it at NF."""
+    from paper_2006_15980_b200.data import TILE_RESIDENT_MAX_STALE, run_group_staleness
+    nf = run_group_staleness(128, 148, 50_000_000, 1184, 8_850)
+    assert 9 < nf < 12
+    band8 = run_group_staleness(128, 148, 100_000_000 // 17, 1184, 17_700 // 17)
+    assert 80 < band8 < 100 < TILE_RESIDENT_MAX_STALE
+    narrow = run_group_staleness(128, 148, 1_425_000, 148, 600)
+    assert narrow > TILE_RESIDENT_MAX_STALE
+    assert run_group_staleness(160, 148, 50_000_000, 296, 8_850) < 60
