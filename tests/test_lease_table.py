@@ -255,3 +255,22 @@ def test_abort_releases_waiting_ranks(tmp_path):
             owner.try_acquire(0)
     finally:
         owner.close(unlink=True)
+
+
+@pytest.mark.parametrize("policy", ["quota", "free"])
+def test_lease_sim_runs(policy):
+    """scripts/lease_sim.py (the protocol-efficiency simulation DESIGN §6
+    quotes) runs end to end on the host: 2 simulated GPUs, both policies."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(root / "scripts" / "lease_sim.py"), "--gpus", "2",
+                          "--epochs", "2", "--policy", policy, "--ratings-per-gpu", "2e8"],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["policy"] == policy and line["gpus"] == 2 and line["column_bands"] == 5
+    assert sum(line["blocks_per_rank"]) == 2 * 2 * 5
+    assert 0.5 < line["throughput_efficiency"] <= 1.05
