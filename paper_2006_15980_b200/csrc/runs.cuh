@@ -252,7 +252,15 @@ __global__ void __launch_bounds__(WPB * 32, 1)
         qs[e] = qn[e];
         q0n[e] = __fmul2_rn(qn[e], neg1);
       }
-      int32_t cu = nbu;
+      // k = 32: the lanes hold the batch's P-row element offsets (one
+      // multiply per lane and batch instead of one per step after the
+      // broadcast): +1.9 % there, -0.8 % at k = 128 (profiles/round2/
+      // s4_rowoff_ab.jsonl)
+      constexpr bool kRowOff = K == 32;
+      auto rowoff = [&](int32_t v) {
+        return kRowOff ? tile_row<RowT>(RowT(v), r0) * K : v;
+      };
+      int32_t cu = rowoff(nbu);
       float cr = nbr;
       float sq = 1.f, isq = 1.f;
       // the next batch of this run (lane l: position j0 + LPC + l); the
@@ -284,7 +292,8 @@ __global__ void __launch_bounds__(WPB * 32, 1)
           if (j0 + jj >= steps) break;  // warp-uniform
           const bool act = j0 + jj < len;  // chain-uniform
           const int32_t u = __shfl_sync(FULL, cu, jj, LPC);
-          S* prow = tile + int64_t(act ? tile_row<RowT>(RowT(u), r0) : 0) * K;
+          S* prow = kRowOff ? tile + (act ? u : 0)
+                            : tile + int64_t(act ? tile_row<RowT>(RowT(u), r0) : 0) * K;
           float2 pc[E2];
           L::lds(prow, l, c, reinterpret_cast<float*>(pc));
           float2 da = make_float2(0.f, 0.f), db = make_float2(0.f, 0.f);
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(WPB * 32, 1)
             }
           }
         }
-        cu = xu;
+        cu = rowoff(xu);
         cr = xr;
         if (sq < 0.25f) {  // keep the scaled row in range on long runs
           const float2 sq2 = make_float2(sq, sq);
