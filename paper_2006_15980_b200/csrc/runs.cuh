@@ -252,11 +252,11 @@ __global__ void __launch_bounds__(WPB * 32, 1)
         qs[e] = qn[e];
         q0n[e] = __fmul2_rn(qn[e], neg1);
       }
-      // k = 32: the lanes hold the batch's P-row element offsets (one
-      // multiply per lane and batch instead of one per step after the
-      // broadcast): +1.9 % there, -0.8 % at k = 128 (profiles/round2/
-      // s4_rowoff_ab.jsonl)
-      constexpr bool kRowOff = K == 32;
+      // the lanes hold the batch's P-row element offsets (one multiply per
+      // lane and batch instead of one per step after the broadcast): +1-2 %
+      // at k = 32, 64, 256 and fp16 k = 128, -0.8 % at fp32 k = 128, which
+      // keeps the per-step form (profiles/round2/s4_rowoff_ab.jsonl)
+      constexpr bool kRowOff = !(K == 128 && sizeof(S) == 4);
       auto rowoff = [&](int32_t v) {
         return kRowOff ? tile_row<RowT>(RowT(v), r0) * K : v;
       };

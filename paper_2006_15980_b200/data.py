@@ -523,9 +523,9 @@ def tile_resident_impl(grid, k: int, f16: bool, max_rows: int | None = None) -> 
       Q row; the item-split kernel (5) handles that case;
     * Q staleness S <= TILE_RESIDENT_MAX_STALE (few items for the runs in
       flight: narrow column blocks).
-    Returns 8 (Netflix fp32 k = 32 / 64 / 128 / 256: 74.3 / 39.7 / 19.4 / 7.5
+    Returns 8 (Netflix fp32 k = 32 / 64 / 128 / 256: 74.7 / 40.0 / 19.4 / 7.6
     G upd/s against 30.6 / 19.7 / 11.8 / 5.9 for implementation 5; fp16 83 /
-    49 / 22.5 / 9.3 against 42 / 27 / 16.4 / 8.5; profiles/round2/
+    49 / 22.6 / 9.4 against 42 / 27 / 16.4 / 8.5; profiles/round2/
     s4_ksweep.jsonl)."""
     torch = _torch()
     if k not in (32, 64, 128, 256) or grid.nnz == 0:
